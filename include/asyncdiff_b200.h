@@ -1,0 +1,260 @@
+/*
+ * asyncdiff_b200.h -- C ABI of the B200-native AsyncDiff async denoising
+ * engine (libasyncdiff_b200.so).
+ *
+ * This is the drop-in boundary for the reference's C++ pipeline API
+ * (the headers under /root/reference/proj/include/asyncdiff/).  Every entry point cites
+ * the reference declaration it replaces.  Plain pointers and sizes only; no
+ * torch or CUDA types cross this boundary.  Errors: every function returns an
+ * adx_status; the message of the last failure on the calling thread is
+ * adx_last_error().  Status codes map 1:1 onto the reference's exception
+ * classes (std::invalid_argument, out_of_range, domain_error, runtime_error,
+ * logic_error) so a C++ facade can rethrow the same type with the same text
+ * (see include/asyncdiff_b200.hpp).
+ *
+ * Matrices crossing the boundary are row-major fp64 (element (i,j) at
+ * [i*cols + j]); latents/eps are fp64 vectors, like the reference's
+ * Eigen::VectorXd (proj/include/asyncdiff/diffusion.hpp:10-11).
+ */
+#ifndef ASYNCDIFF_B200_H
+#define ASYNCDIFF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+typedef enum {
+    ADX_OK = 0,
+    ADX_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    ADX_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range    */
+    ADX_ERR_DOMAIN = 3,           /* std::domain_error    */
+    ADX_ERR_RUNTIME = 4,          /* std::runtime_error   */
+    ADX_ERR_LOGIC = 5,            /* std::logic_error     */
+    ADX_ERR_CUDA = 6              /* CUDA / NCCL failure (runtime_error class) */
+} adx_status;
+
+const char* adx_last_error(void);
+int adx_version(void);          /* 100 * major + minor */
+int adx_device_count(void);     /* visible CUDA devices (0 without a GPU) */
+
+/* precision of the device arithmetic */
+typedef enum {
+    ADX_F64 = 0,  /* fp64 weights + activations: golden parity mode            */
+    ADX_F32 = 1,  /* fp32 weights + activations: north_star rel-L2 <= 1e-3 mode */
+    ADX_BF16 = 2  /* bf16 weights, fp32 activations/accumulation                */
+} adx_precision;
+
+/* -------------------------------------------------------------- schedule
+ * build_schedule: proj/include/asyncdiff/diffusion.hpp:36-37,
+ *                 proj/src/diffusion.cpp:39-77.  kind 0=linear 1=scaled-linear.
+ * betas/alphas: T doubles, alpha_bars: T+1 doubles (caller-owned). */
+int adx_build_schedule(int T, double beta_start, double beta_end, int kind, double* betas,
+                       double* alphas, double* alpha_bars);
+
+/* ddim_step on the GPU (device `ordinal`): proj/include/asyncdiff/diffusion.hpp:50-51,
+ * proj/src/diffusion.cpp:95-116.  alpha_bars has T+1 entries.  Non-finite eps ->
+ * ADX_ERR_DOMAIN "predict_x0: non-finite eps at t=..", t outside [1,T] ->
+ * ADX_ERR_OUT_OF_RANGE. */
+int adx_ddim_step(int ordinal, int precision, const double* x, const double* eps, int d, int t,
+                  const double* alpha_bars, int T, double* out);
+
+/* ------------------------------------------------------------------ model
+ * LayeredDenoiser: proj/include/asyncdiff/denoiser.hpp:29-72. */
+typedef struct adx_model adx_model;
+enum { ADX_SKIP_NONE = 0, ADX_SKIP_UNET_MIRROR = 1 };
+enum { ADX_T_PROJ = 0, ADX_T_W1 = 1, ADX_T_B1 = 2, ADX_T_TIN = 3, ADX_T_W2 = 4, ADX_T_B2 = 5 };
+
+/* build_toy_denoiser: denoiser.hpp:68-70, denoiser.cpp:124-142 (xavier init from Rng(seed)).
+ * widths has n_widths entries (must be L+1). */
+int adx_model_build_toy(int L, const int* widths, int n_widths, int skip_spec, uint64_t seed,
+                        int time_embed_dim, adx_model** out);
+/* make_denoiser_shell: denoiser.hpp:73-76, denoiser.cpp:75-122 (zero weights). */
+int adx_model_shell(int L, const int* widths, int n_widths, const int* link_pairs, int n_links,
+                    int time_embed_dim, adx_model** out);
+void adx_model_destroy(adx_model* m);
+int adx_model_info(const adx_model* m, int* L, int* time_embed_dim, int* n_links);
+int adx_model_widths(const adx_model* m, int* out /* L+1 */);
+int adx_model_links(const adx_model* m, int* out_pairs /* 2*n_links */);
+/* Stage::in_width/hidden_width/out_width/cost_macs (denoiser.hpp:29-43) */
+int adx_model_stage_shape(const adx_model* m, int stage, int* in, int* hidden, int* out,
+                          long long* cost_macs);
+int adx_model_set_stage_macs(adx_model* m, int stage, long long cost_macs);
+/* host fp64 row-major tensor, mutable in place (stage ignored for PROJ).
+ * Engines created afterwards see the edits. */
+int adx_model_tensor(adx_model* m, int stage, int which, double** data, int* rows, int* cols);
+/* TimeEmbedding::sinusoid (denoiser.cpp:31-41) */
+int adx_sinusoid(int t, int dim, double* out);
+
+/* -------------------------------------------------------------- partition
+ * Partition: proj/include/asyncdiff/partition.hpp:19-44. */
+typedef struct adx_partition adx_partition;
+enum { ADX_SEQUENTIAL_BALANCED = 0, ADX_FIRST_LAST_GROUPED = 1 };
+
+/* partition_balanced: partition.hpp:39-40, partition.cpp:95-198 */
+int adx_partition_balanced(const adx_model* m, int N, int strategy, adx_partition** out);
+/* explicit partition (tests' uniform_partition, plan_test.cpp:14-22):
+ * seg_sizes[n_segments], stages[sum(seg_sizes)] 1-based, devices/macs per segment */
+int adx_partition_create(int n_segments, const int* seg_sizes, const int* stages,
+                         const int* devices, const long long* macs, int strategy,
+                         adx_partition** out);
+void adx_partition_destroy(adx_partition* p);
+int adx_partition_num_segments(const adx_partition* p);
+int adx_partition_strategy(const adx_partition* p);
+int adx_partition_segment(const adx_partition* p, int seg, int* stages, int cap, int* n_stages,
+                          long long* macs, int* device);
+int adx_partition_contiguous(const adx_partition* p);                       /* partition.hpp:29 */
+int adx_partition_segment_of_stage(const adx_partition* p, int stage, int* seg); /* :27 */
+int adx_partition_validate(const adx_partition* p, const adx_model* m);     /* :33 */
+/* crossing_links: partition.hpp:43-44, partition.cpp:200-208 */
+int adx_crossing_links(const adx_model* m, const adx_partition* p, int* out_pairs, int cap,
+                       int* n_links);
+
+/* ------------------------------------------------------------------- plan
+ * ExecutionPlan: proj/include/asyncdiff/plan.hpp:12-53.
+ * Flat layout (ints), shared with the oracle:
+ *   [T, w, N, S, D, time_shift, n_rounds, warmup[w]...,
+ *    per round: index, broadcast, n_sampler, sampler[n_sampler]..., n_evals,
+ *               per eval: segment, device, embed_t, input_kind (0 latent, 1 cached),
+ *                         producer_segment, producer_round, emits_eps_for (-1 none)] */
+typedef struct adx_plan adx_plan;
+/* plan_async: plan.hpp:53, plan.cpp:17-97 */
+int adx_plan_async(int T, int w, int N, int S, int time_shift, adx_plan** out);
+int adx_plan_from_flat(const int* flat, int len, adx_plan** out);
+int adx_plan_to_flat(const adx_plan* p, int* out, int cap, int* len);
+void adx_plan_destroy(adx_plan* p);
+/* validate_plan: plan.hpp:56, plan.cpp:99-200.  Violations joined by '\n'. */
+int adx_plan_validate(const adx_plan* p, char* buf, int cap, int* n_violations);
+
+/* PlanCounts: plan.hpp:58-66; plan_counts: plan.cpp:202-232 */
+typedef struct {
+    int broadcasts_paper_convention;
+    int broadcasts_strictly_needed;
+    int device_count;
+    long long max_device_macs;
+    long long sequential_total_macs;
+} adx_plan_counts_t;
+int adx_plan_counts(const adx_plan* p, const adx_partition* part, adx_plan_counts_t* out,
+                    long long* evals_per_segment /* N or NULL */,
+                    long long* per_device_macs /* D or NULL */);
+/* shift_embeddings: plan.hpp:69, plan.cpp:234-244 */
+int adx_shift_embeddings(const int* timesteps, int n, int w, int* out);
+/* render_plan: plan.hpp:72, plan.cpp:246-286 */
+int adx_render_plan(const adx_plan* p, char* buf, int cap, int* len);
+
+/* ----------------------------------------------------------------- engine
+ * Device-resident denoiser: weights uploaded once per CUDA device, lazily,
+ * in the engine's precision.  `ordinals` lists the CUDA devices virtual
+ * device v maps to (v % n_ordinals): several virtual devices may share one
+ * GPU (they then run on separate streams of that GPU). */
+typedef struct adx_engine adx_engine;
+int adx_engine_create(const adx_model* m, int precision, const int* ordinals, int n_ordinals,
+                      adx_engine** out);
+void adx_engine_destroy(adx_engine* e);
+/* bytes of weights resident per ordinal (for the roofline) */
+int adx_engine_weight_bytes(const adx_engine* e, int ordinal_index, long long* bytes);
+
+/* Mean device time of one full-model pass (the 2L stage GEMV launches, one CUDA
+ * graph, CUDA events on its stream) over `iters` back-to-back passes, plus the
+ * algorithmic weight bytes one pass streams: the HBM roofline of the GEMV. */
+int adx_engine_time_eval(adx_engine* e, int t_embed, int iters, double* ms_per_pass,
+                         long long* bytes_per_pass, int* launches_per_pass);
+
+/* eval_full: denoiser.hpp:79, denoiser.cpp:222-233 (on ordinals[0]) */
+int adx_eval_full(adx_engine* e, const double* x, int t_embed, double* eps_out);
+
+/* eval_segment: denoiser.hpp:91-95, denoiser.cpp:235-267.
+ * input_is_latent=1: `input` is the latent x (d values), produced_by ignored.
+ * input_is_latent=0: `input` is a HiddenBundle boundary from segment produced_by.
+ * skips_in: n_skips links (pairs) with their features concatenated in
+ * skip_vals (each feature has width widths[producer]).
+ * Output: if seg == N, eps in out (d values), *out_is_eps=1.  Otherwise the
+ * bundle boundary in out and the crossing links produced by the segment in
+ * out_links/out_vals (caller capacity cap_links / cap_vals). */
+int adx_eval_segment(adx_engine* e, const adx_partition* p, int seg, const double* input,
+                     int input_len, int input_is_latent, int produced_by, const int* skip_links,
+                     const double* skip_vals, int n_skips, int t_embed, double* out, int out_cap,
+                     int* out_len, int* out_is_eps, int* out_links, double* out_vals,
+                     int cap_links, int cap_vals, int* n_out_links);
+
+/* RunOptions: executor.hpp:44-49 (+ InstrumentedDenoiser delays, executor.hpp:53-59) */
+typedef struct {
+    double round_timeout_s;        /* default 30 */
+    uint64_t jitter_seed;          /* accepted for API parity; GPU start order is event-driven */
+    double max_jitter_s;
+    const double* segment_delay_s; /* NULL or n_delays (must equal N) per-segment GPU sleeps */
+    int n_delays;
+    int use_graph;                 /* 1: capture the whole run in one CUDA graph (default) */
+    int instrument;                /* 1: per-round / per-eval CUDA-event timing into RunStats */
+} adx_run_options;
+void adx_run_options_default(adx_run_options* o);
+
+/* RunStats: executor.hpp:30-42.  Arrays are caller-provided (may be NULL):
+ * round_wall_s/round_comm_s/store_entries_per_round: n_rounds entries;
+ * device_busy_s/device_evals: D entries. */
+typedef struct {
+    int broadcast_count;
+    int n_rounds;
+    double warmup_wall_s;
+    double total_wall_s;
+    double* round_wall_s;
+    double* round_comm_s;
+    double* device_busy_s;
+    long long* device_evals;
+    int* store_entries_per_round;
+} adx_run_stats;
+
+/* A session is one compiled run: (plan, partition, placement) with its
+ * device buffers, streams and (optionally) one CUDA graph spanning every
+ * device.  mode: 0 = run_serial (all evals on virtual device 0, plan order),
+ * 1 = run_parallel (virtual device v = plan device v), 2 = sequential_denoise
+ * (T full-model evals, plan/partition ignored except for T).  workers must
+ * equal plan.D in mode 1 (executor.cpp:509-511). */
+enum { ADX_MODE_SERIAL = 0, ADX_MODE_PARALLEL = 1, ADX_MODE_SEQUENTIAL = 2 };
+typedef struct adx_session adx_session;
+int adx_session_create(adx_engine* e, const adx_plan* plan, const adx_partition* part,
+                       const double* alpha_bars, int T, int mode, int workers,
+                       const adx_run_options* opts, adx_session** out);
+void adx_session_destroy(adx_session* s);
+/* Host in / host out, blocking: x_T (d) -> latents ((T+1)*d), eps (T*d).
+ * Either output may be NULL. */
+int adx_session_run(adx_session* s, const double* x_T, double* traj_latents, double* traj_eps,
+                    adx_run_stats* stats);
+/* Device-resident timing path: x_T already uploaded by adx_session_upload;
+ * runs `iters` times back to back and returns the mean device time per run
+ * (CUDA events on the session's launch stream). */
+int adx_session_upload(adx_session* s, const double* x_T);
+int adx_session_time(adx_session* s, int iters, double* ms_per_run);
+/* kernels launched per run (the graph's kernel nodes) */
+int adx_session_kernel_count(const adx_session* s, int* n);
+/* algorithmic weight bytes streamed per run (every eval streams its segment's
+ * W1/W2 once) -- the numerator of the HBM roofline */
+int adx_session_weight_bytes(const adx_session* s, long long* bytes);
+/* trajectory of the last run (device -> host, fp64) */
+int adx_session_download(adx_session* s, double* traj_latents, double* traj_eps);
+
+/* One-shot wrappers mirroring the reference signatures (session create/run/destroy). */
+/* run_serial: executor.hpp:63-75, executor.cpp:248-331 */
+int adx_run_serial(adx_engine* e, const adx_plan* plan, const adx_partition* part,
+                   const double* x_T, const double* alpha_bars, int T,
+                   const adx_run_options* opts, double* traj_latents, double* traj_eps,
+                   adx_run_stats* stats);
+/* run_parallel: executor.hpp:79-93, executor.cpp:501-601 */
+int adx_run_parallel(adx_engine* e, const adx_plan* plan, const adx_partition* part,
+                     const double* x_T, const double* alpha_bars, int T, int workers,
+                     const adx_run_options* opts, double* traj_latents, double* traj_eps,
+                     adx_run_stats* stats);
+/* sequential_denoise(eval_full): diffusion.hpp:66-67, diffusion.cpp:118-142 */
+int adx_sequential_denoise(adx_engine* e, const double* x_T, const double* alpha_bars, int T,
+                           double* traj_latents, double* traj_eps);
+
+/* compare_trajectories: metrics.hpp, metrics.cpp:9-30 (host arithmetic) */
+int adx_compare_trajectories(const double* a, const double* b, int n_latents, int d,
+                             double* per_step_mse, double* final_mse, double* final_max_abs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASYNCDIFF_B200_H */

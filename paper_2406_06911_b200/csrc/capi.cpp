@@ -1,0 +1,779 @@
+// capi.cpp -- extern "C" boundary of libasyncdiff_b200.so (include/asyncdiff_b200.h).
+// Exceptions are mapped onto status codes per the reference's exception
+// classes; the message text is kept for adx_last_error().
+#include "../../include/asyncdiff_b200.h"
+
+#include "engine.hpp"
+#include "host.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+
+struct adx_model {
+    adx::Model m;
+};
+struct adx_partition {
+    adx::Partition p;
+};
+struct adx_plan {
+    adx::Plan p;
+};
+struct adx_engine {
+    std::unique_ptr<adx::Engine> e;
+};
+struct adx_session {
+    std::unique_ptr<adx::Session> s;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return ADX_OK;
+    } catch (const adx::cuda_error& e) {
+        g_err = e.what();
+        return ADX_ERR_CUDA;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return ADX_ERR_INVALID_ARGUMENT;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return ADX_ERR_OUT_OF_RANGE;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return ADX_ERR_DOMAIN;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return ADX_ERR_LOGIC;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return ADX_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return ADX_ERR_RUNTIME;
+    } catch (...) {
+        g_err = "unknown error";
+        return ADX_ERR_RUNTIME;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) throw std::invalid_argument(std::string(what) + ": null pointer");
+}
+
+#define CKC(x)                                                                                         \
+    do {                                                                                               \
+        cudaError_t e_ = (x);                                                                          \
+        if (e_ != cudaSuccess)                                                                         \
+            throw adx::cuda_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x); \
+    } while (0)
+
+// device scratch freed on scope exit
+struct DevBuf {
+    void* p = nullptr;
+    DevBuf() = default;
+    explicit DevBuf(size_t bytes) { CKC(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
+};
+
+void to_act(int prec, const double* src, size_t n, std::vector<unsigned char>& out) {
+    const int ab = adx::act_bytes(prec);
+    out.resize(n * ab);
+    for (size_t i = 0; i < n; ++i) {
+        if (ab == 8) {
+            std::memcpy(&out[i * 8], &src[i], 8);
+        } else {
+            const float f = static_cast<float>(src[i]);
+            std::memcpy(&out[i * 4], &f, 4);
+        }
+    }
+}
+
+void from_act(int prec, const unsigned char* src, size_t n, double* dst) {
+    if (adx::act_bytes(prec) == 8) {
+        std::memcpy(dst, src, n * 8);
+    } else {
+        for (size_t i = 0; i < n; ++i) {
+            float f;
+            std::memcpy(&f, src + i * 4, 4);
+            dst[i] = f;
+        }
+    }
+}
+
+// Device run of stages [first, last] (run_stage_range, denoiser.cpp:150-192)
+// on the engine's first ordinal.  `skips` holds features by link; produced
+// features are written back into it.  Returns the last stage's output.
+std::vector<double> run_range_device(adx::Engine& E, int first, int last, const std::vector<double>& cur,
+                                     std::map<std::pair<int, int>, std::vector<double>>& skips, int t_embed,
+                                     bool stage1_latent) {
+    const adx::Model& m = E.model();
+    const int prec = E.prec();
+    const int ab = adx::act_bytes(prec);
+    CKC(cudaSetDevice(E.ordinal(0)));
+    for (int i = first; i <= last; ++i) E.stage_on(0, i);
+    E.ensure_tables(0, std::max(t_embed, 1));
+    if (t_embed < 0) throw std::out_of_range("eval: embedding timestep " + std::to_string(t_embed) + " < 0");
+    cudaStream_t st;
+    CKC(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    } sg{st};
+    std::vector<unsigned char> tmp;
+    auto upload = [&](const std::vector<double>& v) {
+        DevBuf b(v.size() * ab);
+        to_act(prec, v.data(), v.size(), tmp);
+        CKC(cudaMemcpy(b.p, tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
+        return b;
+    };
+    DevBuf bad(2 * sizeof(int));
+    CKC(cudaMemset(bad.p, 0x7f, 2 * sizeof(int)));
+    DevBuf cur_d = upload(cur);
+    std::map<int, DevBuf> y;      // stage outputs
+    std::map<std::pair<int, int>, DevBuf> skip_d;
+    std::vector<DevBuf> hs;
+    int cur_n = static_cast<int>(cur.size());
+    const void* cur_p = cur_d.p;
+    for (int i = first; i <= last; ++i) {
+        std::vector<adx::Seg> in;
+        if (i == first && stage1_latent) {
+            // stage 1 consumes concat(x, e_t): the e_t part comes from the device table
+            in.push_back({cur_p, m.data_dim()});
+            in.push_back({E.etab_row(0, t_embed), m.E});
+            if (cur_n != m.data_dim() + m.E)
+                throw std::runtime_error("eval: stage 1 input width " + std::to_string(cur_n) + " != expected " +
+                                         std::to_string(m.stages[0].in));
+        } else {
+            in.push_back({cur_p, cur_n});
+        }
+        for (auto& l : m.links_into(i)) {
+            if (l.first >= first && y.count(l.first)) {
+                in.push_back({y.at(l.first).p, m.widths[l.first]});
+                continue;
+            }
+            auto it = skips.find(l);
+            if (it == skips.end())
+                throw std::runtime_error("eval: missing skip feature for link (" + std::to_string(l.first) + " -> " +
+                                         std::to_string(l.second) + ")");
+            if (!skip_d.count(l)) skip_d.emplace(l, upload(it->second));
+            in.push_back({skip_d.at(l).p, static_cast<int>(it->second.size())});
+        }
+        DevBuf h(static_cast<size_t>(m.stages[i - 1].hidden) * ab);
+        DevBuf yo(static_cast<size_t>(m.stages[i - 1].out) * ab);
+        E.enqueue_stage(0, i, in, t_embed, h.p, yo.p, static_cast<int*>(bad.p), i, st, true);
+        cur_p = yo.p;
+        cur_n = m.stages[i - 1].out;
+        hs.push_back(std::move(h));
+        y.emplace(i, std::move(yo));
+    }
+    CKC(cudaStreamSynchronize(st));
+    int flags[2];
+    CKC(cudaMemcpy(flags, bad.p, sizeof flags, cudaMemcpyDeviceToHost));
+    if (flags[0] != 0x7f7f7f7f) throw std::domain_error("eval: non-finite activation at stage " + std::to_string(flags[0]));
+    auto down = [&](int stage) {
+        const int n = m.widths[stage];
+        std::vector<unsigned char> h(static_cast<size_t>(n) * ab);
+        CKC(cudaMemcpy(h.data(), y.at(stage).p, h.size(), cudaMemcpyDeviceToHost));
+        std::vector<double> out(n);
+        from_act(prec, h.data(), n, out.data());
+        return out;
+    };
+    for (int i = first; i <= last; ++i)
+        for (auto& l : m.links_out_of(i)) skips[l] = down(i);
+    return down(last);
+}
+
+void fill_stats(const adx::RunStatsOut& s, adx_run_stats* o) {
+    if (!o) return;
+    o->broadcast_count = s.broadcast_count;
+    o->n_rounds = static_cast<int>(s.round_wall_s.size());
+    o->warmup_wall_s = s.warmup_wall_s;
+    o->total_wall_s = s.total_wall_s;
+    for (size_t i = 0; i < s.round_wall_s.size(); ++i) {
+        if (o->round_wall_s) o->round_wall_s[i] = s.round_wall_s[i];
+        if (o->round_comm_s) o->round_comm_s[i] = s.round_comm_s[i];
+    }
+    for (size_t i = 0; i < s.store_entries.size(); ++i)
+        if (o->store_entries_per_round) o->store_entries_per_round[i] = s.store_entries[i];
+    for (size_t i = 0; i < s.device_busy_s.size(); ++i) {
+        if (o->device_busy_s) o->device_busy_s[i] = s.device_busy_s[i];
+        if (o->device_evals) o->device_evals[i] = s.device_evals[i];
+    }
+}
+
+adx::RunOptions to_opts(const adx_run_options* o) {
+    adx::RunOptions r;
+    if (!o) return r;
+    r.round_timeout_s = o->round_timeout_s;
+    if (o->segment_delay_s && o->n_delays > 0) {
+        r.segment_delay_s.assign(o->segment_delay_s, o->segment_delay_s + o->n_delays);
+        for (double d : r.segment_delay_s)
+            if (d < 0.0) throw std::invalid_argument("inject_delay: delays must be >= 0");
+    }
+    r.use_graph = o->use_graph != 0;
+    r.instrument = o->instrument != 0;
+    return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* adx_last_error(void) { return g_err.c_str(); }
+int adx_version(void) { return 100; }
+int adx_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int adx_build_schedule(int T, double beta_start, double beta_end, int kind, double* betas, double* alphas,
+                       double* alpha_bars) {
+    return guard([&] {
+        std::vector<double> b, a, ab;
+        adx::build_schedule(T, beta_start, beta_end, kind, b, a, ab);
+        if (betas) std::memcpy(betas, b.data(), b.size() * 8);
+        if (alphas) std::memcpy(alphas, a.data(), a.size() * 8);
+        if (alpha_bars) std::memcpy(alpha_bars, ab.data(), ab.size() * 8);
+    });
+}
+
+int adx_ddim_step(int ordinal, int precision, const double* x, const double* eps, int d, int t,
+                  const double* alpha_bars, int T, double* out) {
+    return guard([&] {
+        need(x, "ddim_step");
+        need(eps, "ddim_step");
+        need(alpha_bars, "ddim_step");
+        need(out, "ddim_step");
+        if (t < 1 || t > T)
+            throw std::out_of_range("predict_x0: t=" + std::to_string(t) + " outside [1, " + std::to_string(T) + "]");
+        if (precision < 0 || precision > 2) throw std::invalid_argument("ddim_step: bad precision");
+        CKC(cudaSetDevice(ordinal));
+        const int ab = adx::act_bytes(precision);
+        DevBuf xd(static_cast<size_t>(d) * ab), ed(static_cast<size_t>(d) * ab), od(static_cast<size_t>(d) * ab),
+            bad(2 * sizeof(int));
+        std::vector<unsigned char> tmp;
+        to_act(precision, x, d, tmp);
+        CKC(cudaMemcpy(xd.p, tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
+        to_act(precision, eps, d, tmp);
+        CKC(cudaMemcpy(ed.p, tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
+        CKC(cudaMemset(bad.p, 0x7f, 2 * sizeof(int)));
+        adx::DdimArgs a = {};
+        a.x = xd.p;
+        a.eps = ed.p;
+        a.out = od.p;
+        a.d = d;
+        a.s1 = std::sqrt(1.0 - alpha_bars[t]);
+        a.s2 = std::sqrt(alpha_bars[t]);
+        a.s3 = std::sqrt(alpha_bars[t - 1]);
+        a.s4 = std::sqrt(1.0 - alpha_bars[t - 1]);
+        a.bad = static_cast<int*>(bad.p);
+        a.bad_key = 0;
+        adx::launch_ddim(precision, a, 0);
+        CKC(cudaDeviceSynchronize());
+        int flags[2];
+        CKC(cudaMemcpy(flags, bad.p, sizeof flags, cudaMemcpyDeviceToHost));
+        if (flags[1] != 0x7f7f7f7f) throw std::domain_error("predict_x0: non-finite eps at t=" + std::to_string(t));
+        tmp.resize(static_cast<size_t>(d) * ab);
+        CKC(cudaMemcpy(tmp.data(), od.p, tmp.size(), cudaMemcpyDeviceToHost));
+        from_act(precision, tmp.data(), d, out);
+    });
+}
+
+// ---------------------------------------------------------------- model
+int adx_model_build_toy(int L, const int* widths, int n_widths, int skip_spec, uint64_t seed, int E,
+                        adx_model** out) {
+    return guard([&] {
+        need(widths, "build_toy_denoiser");
+        need(out, "build_toy_denoiser");
+        std::vector<int> w(widths, widths + n_widths);
+        auto* h = new adx_model{adx::build_toy_denoiser(L, w, skip_spec, seed, E)};
+        *out = h;
+    });
+}
+
+int adx_model_shell(int L, const int* widths, int n_widths, const int* link_pairs, int n_links, int E,
+                    adx_model** out) {
+    return guard([&] {
+        need(widths, "make_denoiser_shell");
+        need(out, "make_denoiser_shell");
+        std::vector<int> w(widths, widths + n_widths);
+        std::vector<std::pair<int, int>> links;
+        for (int k = 0; k < n_links; ++k) links.emplace_back(link_pairs[2 * k], link_pairs[2 * k + 1]);
+        *out = new adx_model{adx::make_denoiser_shell(L, w, links, E)};
+    });
+}
+
+void adx_model_destroy(adx_model* m) { delete m; }
+
+int adx_model_info(const adx_model* m, int* L, int* E, int* n_links) {
+    return guard([&] {
+        need(m, "model_info");
+        if (L) *L = m->m.L;
+        if (E) *E = m->m.E;
+        if (n_links) *n_links = static_cast<int>(m->m.links.size());
+    });
+}
+
+int adx_model_widths(const adx_model* m, int* out) {
+    return guard([&] {
+        need(m, "model_widths");
+        std::memcpy(out, m->m.widths.data(), m->m.widths.size() * sizeof(int));
+    });
+}
+
+int adx_model_links(const adx_model* m, int* out) {
+    return guard([&] {
+        need(m, "model_links");
+        for (size_t k = 0; k < m->m.links.size(); ++k) {
+            out[2 * k] = m->m.links[k].first;
+            out[2 * k + 1] = m->m.links[k].second;
+        }
+    });
+}
+
+int adx_model_stage_shape(const adx_model* m, int stage, int* in, int* hidden, int* out, long long* macs) {
+    return guard([&] {
+        need(m, "stage_shape");
+        if (stage < 1 || stage > m->m.L) throw std::out_of_range("stage " + std::to_string(stage) + " out of range");
+        const adx::Stage& s = m->m.stages[stage - 1];
+        if (in) *in = s.in;
+        if (hidden) *hidden = s.hidden;
+        if (out) *out = s.out;
+        if (macs) *macs = s.cost_macs;
+    });
+}
+
+int adx_model_set_stage_macs(adx_model* m, int stage, long long macs) {
+    return guard([&] {
+        need(m, "set_stage_macs");
+        if (stage < 1 || stage > m->m.L) throw std::out_of_range("stage " + std::to_string(stage) + " out of range");
+        m->m.stages[stage - 1].cost_macs = macs;
+    });
+}
+
+int adx_model_tensor(adx_model* m, int stage, int which, double** data, int* rows, int* cols) {
+    return guard([&] {
+        need(m, "model_tensor");
+        adx::Model& M = m->m;
+        M.version++;
+        if (which == ADX_T_PROJ) {
+            *data = M.proj.data();
+            *rows = M.E;
+            *cols = M.E;
+            return;
+        }
+        if (stage < 1 || stage > M.L) throw std::out_of_range("stage " + std::to_string(stage) + " out of range");
+        adx::Stage& s = M.stages[stage - 1];
+        switch (which) {
+            case ADX_T_W1: *data = s.w1.data(); *rows = s.hidden; *cols = s.in; break;
+            case ADX_T_B1: *data = s.b1.data(); *rows = s.hidden; *cols = 1; break;
+            case ADX_T_TIN: *data = s.tin.data(); *rows = s.hidden; *cols = M.E; break;
+            case ADX_T_W2: *data = s.w2.data(); *rows = s.out; *cols = s.hidden; break;
+            case ADX_T_B2: *data = s.b2.data(); *rows = s.out; *cols = 1; break;
+            default: throw std::invalid_argument("model_tensor: unknown tensor id");
+        }
+    });
+}
+
+int adx_sinusoid(int t, int dim, double* out) {
+    return guard([&] {
+        auto s = adx::sinusoid(t, dim);
+        std::memcpy(out, s.data(), s.size() * 8);
+    });
+}
+
+// ------------------------------------------------------------ partition
+int adx_partition_balanced(const adx_model* m, int N, int strategy, adx_partition** out) {
+    return guard([&] {
+        need(m, "partition_balanced");
+        *out = new adx_partition{adx::partition_balanced(m->m, N, strategy)};
+    });
+}
+
+int adx_partition_create(int n_segments, const int* seg_sizes, const int* stages, const int* devices,
+                         const long long* macs, int strategy, adx_partition** out) {
+    return guard([&] {
+        adx::Partition p;
+        p.strategy = strategy;
+        int pos = 0;
+        for (int n = 0; n < n_segments; ++n) {
+            std::vector<int> st(stages + pos, stages + pos + seg_sizes[n]);
+            pos += seg_sizes[n];
+            p.segments.push_back(st);
+            p.device_of_segment.push_back(devices ? devices[n] : n);
+            p.segment_macs.push_back(macs ? macs[n] : 0);
+        }
+        *out = new adx_partition{p};
+    });
+}
+
+void adx_partition_destroy(adx_partition* p) { delete p; }
+int adx_partition_num_segments(const adx_partition* p) { return p ? p->p.num_segments() : 0; }
+int adx_partition_strategy(const adx_partition* p) { return p ? p->p.strategy : 0; }
+
+int adx_partition_segment(const adx_partition* p, int seg, int* stages, int cap, int* n_stages, long long* macs,
+                          int* device) {
+    return guard([&] {
+        need(p, "partition_segment");
+        if (seg < 1 || seg > p->p.num_segments())
+            throw std::out_of_range("partition_segment: segment " + std::to_string(seg) + " out of range");
+        const auto& s = p->p.segments[seg - 1];
+        if (n_stages) *n_stages = static_cast<int>(s.size());
+        for (size_t i = 0; i < s.size() && static_cast<int>(i) < cap; ++i) stages[i] = s[i];
+        if (macs) *macs = p->p.segment_macs[seg - 1];
+        if (device) *device = p->p.device_of_segment[seg - 1];
+    });
+}
+
+int adx_partition_contiguous(const adx_partition* p) { return p && p->p.contiguous() ? 1 : 0; }
+
+int adx_partition_segment_of_stage(const adx_partition* p, int stage, int* seg) {
+    return guard([&] {
+        need(p, "segment_of_stage");
+        *seg = p->p.segment_of_stage(stage);
+    });
+}
+
+int adx_partition_validate(const adx_partition* p, const adx_model* m) {
+    return guard([&] {
+        need(p, "partition_validate");
+        need(m, "partition_validate");
+        p->p.validate(m->m);
+    });
+}
+
+int adx_crossing_links(const adx_model* m, const adx_partition* p, int* out_pairs, int cap, int* n_links) {
+    return guard([&] {
+        need(m, "crossing_links");
+        need(p, "crossing_links");
+        auto c = adx::crossing_links(m->m, p->p);
+        *n_links = static_cast<int>(c.size());
+        for (size_t k = 0; k < c.size() && static_cast<int>(k) < cap; ++k) {
+            out_pairs[2 * k] = c[k].first;
+            out_pairs[2 * k + 1] = c[k].second;
+        }
+    });
+}
+
+// ----------------------------------------------------------------- plan
+int adx_plan_async(int T, int w, int N, int S, int time_shift, adx_plan** out) {
+    return guard([&] { *out = new adx_plan{adx::plan_async(T, w, N, S, time_shift != 0)}; });
+}
+
+int adx_plan_from_flat(const int* flat, int len, adx_plan** out) {
+    return guard([&] { *out = new adx_plan{adx::plan_from_flat(flat, len)}; });
+}
+
+int adx_plan_to_flat(const adx_plan* p, int* out, int cap, int* len) {
+    return guard([&] {
+        need(p, "plan_to_flat");
+        auto f = adx::plan_to_flat(p->p);
+        *len = static_cast<int>(f.size());
+        if (static_cast<int>(f.size()) > cap) throw std::invalid_argument("plan_to_flat: buffer too small");
+        std::memcpy(out, f.data(), f.size() * sizeof(int));
+    });
+}
+
+void adx_plan_destroy(adx_plan* p) { delete p; }
+
+int adx_plan_validate(const adx_plan* p, char* buf, int cap, int* n_violations) {
+    return guard([&] {
+        need(p, "validate_plan");
+        auto v = adx::validate_plan(p->p);
+        std::string joined;
+        for (size_t i = 0; i < v.size(); ++i) joined += (i ? "\n" : "") + v[i];
+        if (n_violations) *n_violations = static_cast<int>(v.size());
+        if (buf && cap > 0) {
+            std::strncpy(buf, joined.c_str(), cap - 1);
+            buf[cap - 1] = 0;
+        }
+    });
+}
+
+int adx_plan_counts(const adx_plan* p, const adx_partition* part, adx_plan_counts_t* out,
+                    long long* evals_per_segment, long long* per_device_macs) {
+    return guard([&] {
+        need(p, "plan_counts");
+        need(part, "plan_counts");
+        auto c = adx::plan_counts(p->p, part->p);
+        if (out) {
+            out->broadcasts_paper_convention = c.broadcasts_paper_convention;
+            out->broadcasts_strictly_needed = c.broadcasts_strictly_needed;
+            out->device_count = c.device_count;
+            out->max_device_macs = c.max_device_macs;
+            out->sequential_total_macs = c.sequential_total_macs;
+        }
+        if (evals_per_segment)
+            std::memcpy(evals_per_segment, c.evals_per_segment.data(), c.evals_per_segment.size() * 8);
+        if (per_device_macs) std::memcpy(per_device_macs, c.per_device_macs.data(), c.per_device_macs.size() * 8);
+    });
+}
+
+int adx_shift_embeddings(const int* ts, int n, int w, int* out) {
+    return guard([&] {
+        auto r = adx::shift_embeddings(std::vector<int>(ts, ts + n), w);
+        std::memcpy(out, r.data(), r.size() * sizeof(int));
+    });
+}
+
+int adx_render_plan(const adx_plan* p, char* buf, int cap, int* len) {
+    return guard([&] {
+        need(p, "render_plan");
+        auto s = adx::render_plan(p->p);
+        if (len) *len = static_cast<int>(s.size());
+        if (buf && cap > 0) {
+            std::strncpy(buf, s.c_str(), cap - 1);
+            buf[cap - 1] = 0;
+        }
+    });
+}
+
+// ----------------------------------------------------------------- engine
+int adx_engine_create(const adx_model* m, int precision, const int* ordinals, int n_ordinals, adx_engine** out) {
+    return guard([&] {
+        need(m, "engine_create");
+        std::vector<int> o;
+        if (ordinals && n_ordinals > 0)
+            o.assign(ordinals, ordinals + n_ordinals);
+        else
+            o.push_back(0);
+        *out = new adx_engine{std::make_unique<adx::Engine>(m->m, precision, o)};
+    });
+}
+
+void adx_engine_destroy(adx_engine* e) { delete e; }
+
+int adx_engine_weight_bytes(const adx_engine* e, int idx, long long* bytes) {
+    return guard([&] {
+        need(e, "engine_weight_bytes");
+        *bytes = e->e->weight_bytes_resident(idx);
+    });
+}
+
+int adx_engine_time_eval(adx_engine* e, int t_embed, int iters, double* ms_per_pass, long long* bytes_per_pass,
+                         int* launches_per_pass) {
+    return guard([&] {
+        need(e, "engine_time_eval");
+        const adx::Model& m = e->e->model();
+        long long b = 0;
+        for (int i = 1; i <= m.L; ++i) b += static_cast<long long>(e->e->stage_weight_bytes(i));
+        if (bytes_per_pass) *bytes_per_pass = b;
+        *ms_per_pass = e->e->time_eval_ms(0, t_embed, iters, launches_per_pass);
+    });
+}
+
+int adx_eval_full(adx_engine* e, const double* x, int t_embed, double* eps_out) {
+    return guard([&] {
+        need(e, "eval_full");
+        const adx::Model& m = e->e->model();
+        std::vector<double> cur(x, x + m.data_dim());
+        cur.resize(m.data_dim() + m.E, 0.0);
+        std::map<std::pair<int, int>, std::vector<double>> skips;
+        auto y = run_range_device(*e->e, 1, m.L, cur, skips, t_embed, true);
+        std::memcpy(eps_out, y.data(), y.size() * 8);
+    });
+}
+
+int adx_eval_segment(adx_engine* e, const adx_partition* p, int seg, const double* input, int input_len,
+                     int input_is_latent, int produced_by, const int* skip_links, const double* skip_vals,
+                     int n_skips, int t_embed, double* out, int out_cap, int* out_len, int* out_is_eps,
+                     int* out_links, double* out_vals, int cap_links, int cap_vals, int* n_out_links) {
+    return guard([&] {
+        need(e, "eval_segment");
+        need(p, "eval_segment");
+        const adx::Model& m = e->e->model();
+        const adx::Partition& P = p->p;
+        // require_sequential_segment (denoiser.cpp:194-202)
+        if (seg < 1 || seg > P.num_segments())
+            throw std::invalid_argument("eval_segment: segment " + std::to_string(seg) + " outside [1, " +
+                                        std::to_string(P.num_segments()) + "]");
+        if (!P.contiguous())
+            throw std::invalid_argument(
+                "eval_segment: partition is not a contiguous cascade (first-last-grouped partitions are "
+                "placement/costing only)");
+        if (input_is_latent && seg != 1)
+            throw std::invalid_argument("eval_segment: segment " + std::to_string(seg) +
+                                        " requires a HiddenBundle input, not a Latent");
+        if (!input_is_latent && seg == 1)
+            throw std::invalid_argument("eval_segment: segment 1 requires a Latent input");
+        if (!input_is_latent && produced_by != seg - 1)
+            throw std::invalid_argument("eval_segment: segment " + std::to_string(seg) + " needs a bundle from segment " +
+                                        std::to_string(seg - 1) + ", got one from segment " +
+                                        std::to_string(produced_by));
+        std::map<std::pair<int, int>, std::vector<double>> skips;
+        int pos = 0;
+        for (int k = 0; k < n_skips; ++k) {
+            const std::pair<int, int> l(skip_links[2 * k], skip_links[2 * k + 1]);
+            if (l.first < 1 || l.first > m.L) throw std::invalid_argument("eval_segment: bad skip link");
+            const int w = m.widths[l.first];
+            skips[l] = std::vector<double>(skip_vals + pos, skip_vals + pos + w);
+            pos += w;
+        }
+        std::vector<double> cur(input, input + input_len);
+        if (input_is_latent) cur.resize(input_len + m.E, 0.0);
+        const auto& range = P.segments[seg - 1];
+        auto y = run_range_device(*e->e, range.front(), range.back(), cur, skips, t_embed, input_is_latent != 0);
+        if (static_cast<int>(y.size()) > out_cap) throw std::invalid_argument("eval_segment: output buffer too small");
+        std::memcpy(out, y.data(), y.size() * 8);
+        *out_len = static_cast<int>(y.size());
+        *out_is_eps = seg == P.num_segments() ? 1 : 0;
+        // finish_segment (denoiser.cpp:204-218): crossing links produced in-segment
+        int nl = 0, vp = 0;
+        if (!*out_is_eps) {
+            for (auto& [l, f] : skips)
+                if (l.first >= range.front() && l.first <= range.back() && l.second > range.back()) {
+                    if (nl >= cap_links || vp + static_cast<int>(f.size()) > cap_vals)
+                        throw std::invalid_argument("eval_segment: skip output buffer too small");
+                    out_links[2 * nl] = l.first;
+                    out_links[2 * nl + 1] = l.second;
+                    std::memcpy(out_vals + vp, f.data(), f.size() * 8);
+                    vp += static_cast<int>(f.size());
+                    ++nl;
+                }
+        }
+        *n_out_links = nl;
+    });
+}
+
+void adx_run_options_default(adx_run_options* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->round_timeout_s = 30.0;
+    o->use_graph = 1;
+}
+
+int adx_session_create(adx_engine* e, const adx_plan* plan, const adx_partition* part, const double* alpha_bars,
+                       int T, int mode, int workers, const adx_run_options* opts, adx_session** out) {
+    return guard([&] {
+        need(e, "session_create");
+        need(alpha_bars, "session_create");
+        std::vector<double> ab(alpha_bars, alpha_bars + T + 1);
+        adx::Plan pl = plan ? plan->p : adx::Plan();
+        adx::Partition pa = part ? part->p : adx::Partition();
+        if (mode != ADX_MODE_SEQUENTIAL) {
+            need(plan, "session_create(plan)");
+            need(part, "session_create(partition)");
+        }
+        *out = new adx_session{std::make_unique<adx::Session>(e->e.get(), pl, pa, ab, mode, workers, to_opts(opts))};
+    });
+}
+
+void adx_session_destroy(adx_session* s) { delete s; }
+
+int adx_session_run(adx_session* s, const double* x_T, double* lat, double* eps, adx_run_stats* stats) {
+    return guard([&] {
+        need(s, "session_run");
+        need(x_T, "session_run");
+        adx::RunStatsOut st;
+        s->s->run(x_T, lat, eps, &st);
+        fill_stats(st, stats);
+    });
+}
+
+int adx_session_upload(adx_session* s, const double* x_T) {
+    return guard([&] {
+        need(s, "session_upload");
+        s->s->upload(x_T);
+    });
+}
+
+int adx_session_time(adx_session* s, int iters, double* ms) {
+    return guard([&] {
+        need(s, "session_time");
+        *ms = s->s->time_runs(iters);
+    });
+}
+
+int adx_session_kernel_count(const adx_session* s, int* n) {
+    return guard([&] {
+        need(s, "session_kernel_count");
+        *n = s->s->kernel_count();
+    });
+}
+
+int adx_session_weight_bytes(const adx_session* s, long long* bytes) {
+    return guard([&] {
+        need(s, "session_weight_bytes");
+        *bytes = s->s->weight_bytes_per_run();
+    });
+}
+
+int adx_session_download(adx_session* s, double* lat, double* eps) {
+    return guard([&] {
+        need(s, "session_download");
+        s->s->download(lat, eps);
+    });
+}
+
+static int run_mode(adx_engine* e, const adx_plan* plan, const adx_partition* part, const double* x_T,
+                    const double* ab, int T, int mode, int workers, const adx_run_options* opts, double* lat,
+                    double* eps, adx_run_stats* stats) {
+    adx_session* s = nullptr;
+    int rc = adx_session_create(e, plan, part, ab, T, mode, workers, opts, &s);
+    if (rc) return rc;
+    rc = adx_session_run(s, x_T, lat, eps, stats);
+    adx_session_destroy(s);
+    return rc;
+}
+
+int adx_run_serial(adx_engine* e, const adx_plan* plan, const adx_partition* part, const double* x_T,
+                   const double* alpha_bars, int T, const adx_run_options* opts, double* lat, double* eps,
+                   adx_run_stats* stats) {
+    return run_mode(e, plan, part, x_T, alpha_bars, T, ADX_MODE_SERIAL, 1, opts, lat, eps, stats);
+}
+
+int adx_run_parallel(adx_engine* e, const adx_plan* plan, const adx_partition* part, const double* x_T,
+                     const double* alpha_bars, int T, int workers, const adx_run_options* opts, double* lat,
+                     double* eps, adx_run_stats* stats) {
+    return run_mode(e, plan, part, x_T, alpha_bars, T, ADX_MODE_PARALLEL, workers, opts, lat, eps, stats);
+}
+
+int adx_sequential_denoise(adx_engine* e, const double* x_T, const double* alpha_bars, int T, double* lat,
+                           double* eps) {
+    return run_mode(e, nullptr, nullptr, x_T, alpha_bars, T, ADX_MODE_SEQUENTIAL, 1, nullptr, lat, eps, nullptr);
+}
+
+int adx_compare_trajectories(const double* a, const double* b, int n, int d, double* per, double* final_mse,
+                             double* final_max_abs) {
+    return guard([&] {
+        double last = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (int k = 0; k < d; ++k) {
+                const double df = a[static_cast<size_t>(i) * d + k] - b[static_cast<size_t>(i) * d + k];
+                s += df * df;
+            }
+            last = s / d;
+            if (per) per[i] = last;
+        }
+        if (final_mse) *final_mse = last;
+        double mx = 0.0;
+        for (int k = 0; k < d; ++k)
+            mx = std::max(mx, std::fabs(a[static_cast<size_t>(n - 1) * d + k] - b[static_cast<size_t>(n - 1) * d + k]));
+        if (final_max_abs) *final_max_abs = mx;
+    });
+}
+
+}  // extern "C"
