@@ -30,7 +30,7 @@ __all__ = [
     "Round", "ExecutionPlan", "plan_async", "validate_plan", "PlanCounts", "plan_counts", "shift_embeddings",
     "render_plan", "RunOptions", "RunStats", "InstrumentedDenoiser", "inject_delay", "run_serial",
     "run_parallel", "DivergenceReport", "compare_trajectories", "kWarmupRound", "set_default_precision",
-    "PRECISIONS",
+    "PRECISIONS", "Session", "time_model_pass",
 ]
 
 PRECISIONS = {"f64": 0, "f32": 1, "bf16": 2}
@@ -662,9 +662,9 @@ def _opts(opts: Optional[RunOptions], delays: Sequence[float]):
 
 
 def _run(mode: int, plan: ExecutionPlan, m, partition: Partition, x_T: Latent, schedule: NoiseSchedule,
-         workers: int, opts: Optional[RunOptions], precision: Optional[str]):
+         workers: int, opts: Optional[RunOptions], precision: Optional[str], devices: Optional[Sequence[int]] = None):
     model, delays = (m.model, m.segment_delay_s) if isinstance(m, InstrumentedDenoiser) else (m, [])
-    eng = model.engine(precision)
+    eng = model.engine(precision, devices)
     x = _f64(x_T.values)
     if x_T.timestep != plan.T:
         raise InvalidArgument("run: x_T.timestep != T")
@@ -698,16 +698,19 @@ def _run(mode: int, plan: ExecutionPlan, m, partition: Partition, x_T: Latent, s
 
 
 def run_serial(plan: ExecutionPlan, m, partition: Partition, x_T: Latent, schedule: NoiseSchedule,
-               opts: Optional[RunOptions] = None, precision: Optional[str] = None):
+               opts: Optional[RunOptions] = None, precision: Optional[str] = None,
+               devices: Optional[Sequence[int]] = None):
     """executor.hpp:63-75 -- all evals on one GPU stream in plan order, snapshot semantics."""
-    return _run(0, plan, m, partition, x_T, schedule, 1, opts, precision)
+    return _run(0, plan, m, partition, x_T, schedule, 1, opts, precision, devices)
 
 
 def run_parallel(plan: ExecutionPlan, m, partition: Partition, x_T: Latent, schedule: NoiseSchedule, workers: int,
-                 opts: Optional[RunOptions] = None, precision: Optional[str] = None):
+                 opts: Optional[RunOptions] = None, precision: Optional[str] = None,
+                 devices: Optional[Sequence[int]] = None):
     """executor.hpp:79-93 -- one CUDA stream pair per (virtual) device, event-ordered
-    exchange; bit-identical to run_serial."""
-    return _run(1, plan, m, partition, x_T, schedule, workers, opts, precision)
+    exchange; bit-identical to run_serial.  `devices` lists the CUDA ordinals
+    virtual device v maps to (v % len(devices))."""
+    return _run(1, plan, m, partition, x_T, schedule, workers, opts, precision, devices)
 
 
 def sequential_denoise(eps_fn: Union[LayeredDenoiser, Callable[[Latent, int], np.ndarray]], x_T: Latent,
@@ -736,6 +739,82 @@ def sequential_denoise(eps_fn: Union[LayeredDenoiser, Callable[[Latent, int], np
         traj.eps_used.append(e)
         traj.latents.append(x)
     return traj
+
+
+class Session:
+    """One compiled run (plan, partition, placement) kept resident on the GPU:
+    device buffers, streams and one CUDA graph spanning every device.  The
+    repeated-run API used by bench.py (adx_session_* in the C ABI)."""
+
+    MODES = {"serial": 0, "parallel": 1, "sequential": 2}
+
+    def __init__(self, model: LayeredDenoiser, schedule: NoiseSchedule, mode: str = "parallel",
+                 plan: Optional[ExecutionPlan] = None, partition: Optional[Partition] = None,
+                 workers: Optional[int] = None, precision: Optional[str] = None,
+                 devices: Optional[Sequence[int]] = None, opts: Optional[RunOptions] = None):
+        self.model, self.schedule, self.mode = model, schedule, mode
+        eng = model.engine(precision, devices)
+        self._eng = eng
+        ab = _f64(schedule.alpha_bars)
+        self._ab = ab
+        ph = plan._handle() if plan is not None else None
+        self._ph = ph
+        o, self._keep = _opts(opts, [])
+        h = C.c_void_p()
+        check(lib().adx_session_create(eng._h, ph._h if ph else None, partition._h if partition else None, _dp(ab),
+                                       schedule.T, self.MODES[mode], workers if workers is not None else
+                                       (plan.D if plan is not None else 1), C.byref(o), C.byref(h)))
+        self._h = h
+        self._finalizer = weakref.finalize(self, lib().adx_session_destroy, h)
+        self.d = model.data_dim()
+
+    def run(self, x_T: Latent) -> Trajectory:
+        """host x_T -> host trajectory (H2D + graph + D2H, blocking)."""
+        T = self.schedule.T
+        x = _f64(x_T.values)
+        lat = np.zeros((T + 1, self.d))
+        eps = np.zeros((T, self.d))
+        check(lib().adx_session_run(self._h, _dp(x), _dp(lat), _dp(eps), None))
+        return _traj_from(lat, eps, T)
+
+    def run_into(self, x: np.ndarray, lat: np.ndarray, eps: np.ndarray) -> None:
+        check(lib().adx_session_run(self._h, _dp(x), _dp(lat), _dp(eps), None))
+
+    def upload(self, x_T: Latent) -> None:
+        self._x = _f64(x_T.values)
+        check(lib().adx_session_upload(self._h, _dp(self._x)))
+
+    def time(self, iters: int) -> float:
+        """device-resident back-to-back runs; mean ms per run (CUDA events)."""
+        ms = C.c_double()
+        check(lib().adx_session_time(self._h, iters, C.byref(ms)))
+        return ms.value
+
+    def kernel_count(self) -> int:
+        n = C.c_int()
+        check(lib().adx_session_kernel_count(self._h, C.byref(n)))
+        return n.value
+
+    def weight_bytes(self) -> int:
+        b = C.c_longlong()
+        check(lib().adx_session_weight_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def download(self) -> Trajectory:
+        T = self.schedule.T
+        lat = np.zeros((T + 1, self.d))
+        eps = np.zeros((T, self.d))
+        check(lib().adx_session_download(self._h, _dp(lat), _dp(eps)))
+        return _traj_from(lat, eps, T)
+
+
+def time_model_pass(m: LayeredDenoiser, t_embed: int, iters: int, precision: Optional[str] = None,
+                    devices: Optional[Sequence[int]] = None):
+    """(ms per full-model pass, weight bytes per pass, GEMV launches per pass)."""
+    ms, b, n = C.c_double(), C.c_longlong(), C.c_int()
+    check(lib().adx_engine_time_eval(m.engine(precision, devices)._h, t_embed, iters, C.byref(ms), C.byref(b),
+                                     C.byref(n)))
+    return ms.value, b.value, n.value
 
 
 @dataclass

@@ -17,6 +17,7 @@
 
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -172,6 +173,134 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-streamed GEMV (the production kernel).
+//
+// One persistent CTA per SM, kTWarps warps.  Every warp owns a ring of kSlots
+// shared-memory chunk buffers (kChunk bytes) with one mbarrier each; its lane 0
+// streams the warp's rows through the ring with cp.async.bulk (1-D TMA,
+// complete_tx on the slot's mbarrier), so the bytes in flight per SM are fixed
+// by the ring (kTWarps*kSlots*kChunk = 128 KB) instead of by the compiler's load
+// scheduling.  The first kSlots chunks are issued before griddepcontrol.wait,
+// overlapping the previous kernel of the dependent GEMV chain.  Rows are dealt
+// to warps round-robin across SMs (warp g = local*grid + cta) so the last,
+// partial pass is spread over the whole chip.  Each row is reduced by one warp
+// in a fixed order (per-lane chunk/vector order, then a butterfly), so the
+// result is independent of grid size and placement.
+constexpr int kTWarps = 8;
+constexpr int kSlots = 4;
+constexpr int kChunk = 4096;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_row_chunk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+template <typename WT, typename AT>
+__global__ void __launch_bounds__(kTWarps * 32, 1) gemv_tma_kernel(const GemvArgs a) {
+    using AccT = typename Acc<WT>::T;
+    constexpr int VEC = 16 / sizeof(WT);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t x_bytes = (static_cast<size_t>(a.pitch) * sizeof(AT) + 127) & ~size_t(127);
+    AT* sx = reinterpret_cast<AT*>(smem_raw);
+    unsigned char* ring = smem_raw + x_bytes + static_cast<size_t>(warp) * kSlots * kChunk;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + x_bytes + static_cast<size_t>(kTWarps) * kSlots * kChunk) +
+                     warp * kSlots;
+
+    const int G = gridDim.x * kTWarps;
+    const int g = warp * gridDim.x + blockIdx.x;
+    const int my_rows = g < a.rows ? (a.rows - 1 - g) / G + 1 : 0;
+    const uint32_t row_bytes = static_cast<uint32_t>(a.pitch) * sizeof(WT);
+    const int cpr = static_cast<int>((row_bytes + kChunk - 1) / kChunk);  // chunks per row
+    const int nchunks = my_rows * cpr;
+    const char* Wb = static_cast<const char*>(a.W);
+
+    auto chunk_src = [&](int i, uint32_t& bytes) {
+        const int rk = i / cpr, j = i - rk * cpr;
+        const size_t row = static_cast<size_t>(g) + static_cast<size_t>(rk) * G;
+        const uint32_t off = static_cast<uint32_t>(j) * kChunk;
+        bytes = min(static_cast<uint32_t>(kChunk), row_bytes - off);
+        return Wb + row * row_bytes + off;
+    };
+
+    // ---- prologue: barriers + first kSlots chunks (weights only; independent of
+    // the producer kernel, so it runs before griddepcontrol.wait)
+    if (lane == 0) {
+        for (int s = 0; s < kSlots; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < kSlots && i < nchunks; ++i) {
+            uint32_t bytes;
+            const char* src = chunk_src(i, bytes);
+            tma_row_chunk(smem_u32(ring + i * kChunk), src, bytes, smem_u32(&bars[i]));
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    // ---- gather the concatenated input into shared memory (zero padded)
+    int off = 0;
+    for (int s = 0; s < a.nseg; ++s) {
+        const AT* src = static_cast<const AT*>(a.seg[s]);
+        for (int i = threadIdx.x; i < a.seg_len[s]; i += blockDim.x) sx[off + i] = src[i];
+        off += a.seg_len[s];
+    }
+    for (int i = off + threadIdx.x; i < a.pitch; i += blockDim.x) sx[i] = AT(0);
+    __syncthreads();
+
+    AccT acc = AccT(0);
+    for (int i = 0; i < nchunks; ++i) {
+        const int slot = i % kSlots;
+        mbar_wait(smem_u32(&bars[slot]), static_cast<uint32_t>((i / kSlots) & 1));
+        const int rk = i / cpr, j = i - rk * cpr;
+        const uint32_t cbytes = min(static_cast<uint32_t>(kChunk), row_bytes - static_cast<uint32_t>(j) * kChunk);
+        const int nv = static_cast<int>(cbytes / 16);
+        const uint4* wv = reinterpret_cast<const uint4*>(ring + slot * kChunk);
+        const AT* xs = sx + static_cast<size_t>(j) * (kChunk / sizeof(WT));
+#pragma unroll 4
+        for (int v = lane; v < nv; v += 32) acc = dot_vec<WT, AT>(wv[v], xs + static_cast<size_t>(v) * VEC, acc);
+        if (j == cpr - 1) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) {
+                const int row = g + rk * G;
+                AccT val = acc;
+                if (a.bias) val += static_cast<AccT>(static_cast<const AT*>(a.bias)[row]);
+                if (a.act) val = val > AccT(0) ? val : AccT(0.1) * val;
+                static_cast<AT*>(a.out)[row] = static_cast<AT>(val);
+                if (a.bad && !isfinite(val)) atomicMin(a.bad, a.bad_key);
+            }
+            acc = AccT(0);
+        }
+        // release the slot to the async proxy, then refill it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && i + kSlots < nchunks) {
+            uint32_t bytes;
+            const char* src = chunk_src(i + kSlots, bytes);
+            tma_row_chunk(smem_u32(ring + slot * kChunk), src, bytes, smem_u32(&bars[slot]));
+        }
+    }
+}
+
 // DDIM: x0 = (x - s1*eps)/s2 ; out = s3*x0 + s4*eps, every op rounded exactly
 // as the reference's fp64 expression (no FMA contraction).
 template <typename AT>
@@ -211,27 +340,48 @@ int num_sms() {
     return g_num_sms[dev];
 }
 
+bool use_ldg_gemv() {
+    static const bool v = [] {
+        const char* e = getenv("ADX_GEMV");
+        return e && std::string(e) == "ldg";
+    }();
+    return v;
+}
+
 template <typename WT, typename AT>
 void launch_gemv_t(int prec, const GemvArgs& a, cudaStream_t stream, bool pdl) {
     int dev = 0;
     ADX_CUDA(cudaGetDevice(&dev));
     if (!g_attr_done[dev][prec]) {
         ADX_CUDA(cudaFuncSetAttribute(gemv_kernel<WT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        ADX_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<WT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      227 * 1024));
         g_attr_done[dev][prec] = true;
     }
-    const size_t smem = static_cast<size_t>(a.pitch) * sizeof(AT);
-    if (smem > 200 * 1024) throw std::invalid_argument("gemv: input width too large for shared memory");
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((a.rows + kWarps - 1) / kWarps);
-    cfg.blockDim = dim3(kWarps * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    ADX_CUDA(cudaLaunchKernelEx(&cfg, gemv_kernel<WT, AT>, a));
+    cfg.stream = stream;
+    const size_t x_bytes = (static_cast<size_t>(a.pitch) * sizeof(AT) + 127) & ~size_t(127);
+    if (use_ldg_gemv()) {
+        const size_t smem = static_cast<size_t>(a.pitch) * sizeof(AT);
+        if (smem > 200 * 1024) throw std::invalid_argument("gemv: input width too large for shared memory");
+        cfg.gridDim = dim3((a.rows + kWarps - 1) / kWarps);
+        cfg.blockDim = dim3(kWarps * 32);
+        cfg.dynamicSmemBytes = smem;
+        ADX_CUDA(cudaLaunchKernelEx(&cfg, gemv_kernel<WT, AT>, a));
+        return;
+    }
+    const size_t smem = x_bytes + static_cast<size_t>(kTWarps) * kSlots * (kChunk + 8);
+    if (smem > 227 * 1024) throw std::invalid_argument("gemv: input width too large for shared memory");
+    const int want = (a.rows + kTWarps - 1) / kTWarps;
+    cfg.gridDim = dim3(std::max(1, std::min(want, num_sms())));
+    cfg.blockDim = dim3(kTWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    ADX_CUDA(cudaLaunchKernelEx(&cfg, gemv_tma_kernel<WT, AT>, a));
 }
 
 }  // namespace

@@ -1,0 +1,52 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol that
+include/*.h declares (no compute calls)."""
+import glob
+import os
+import re
+import subprocess
+
+import paper_2406_06911_b200 as adx
+from paper_2406_06911_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"\b(adx_[a-z0-9_]+)\s*\(", src):
+            names.add(m.group(1))
+    return names
+
+
+def test_header_declares_entry_points():
+    names = declared_symbols()
+    assert len(names) >= 40
+    assert {"adx_run_serial", "adx_run_parallel", "adx_plan_async", "adx_partition_balanced"} <= names
+
+
+def test_library_exports_every_declared_symbol():
+    L = adx.lib()
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.SO_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (adx_[a-z0-9_]+)", out))
+    missing = declared_symbols() - exported
+    assert not missing, f"declared but not exported: {sorted(missing)}"
+    for n in declared_symbols():
+        assert hasattr(L, n)
+    assert set(_lib.EXPORTS) == declared_symbols()
+
+
+def test_loads_without_gpu_and_reports_devices():
+    n = adx.lib().adx_device_count()
+    assert n >= 0
+    assert adx.lib().adx_version() == 100
+
+
+def test_status_codes_map_to_reference_exception_classes():
+    import pytest
+    with pytest.raises(adx.InvalidArgument):
+        adx.plan_async(50, 0, 2, 1)
+    with pytest.raises(ValueError):  # std::invalid_argument is a ValueError here
+        adx.build_schedule(0, 0.1, 0.2)
