@@ -162,6 +162,12 @@ int adx_engine_weight_bytes(const adx_engine* e, int ordinal_index, long long* b
 int adx_engine_time_eval(adx_engine* e, int t_embed, int iters, double* ms_per_pass,
                          long long* bytes_per_pass, int* launches_per_pass);
 
+/* Microbenchmark of the stage GEMV kernel: a dependent chain of `chain` square
+ * n x n GEMVs (distinct weights), one CUDA graph, `iters` launches; device ms
+ * per GEMV.  pdl=1 enables programmatic dependent launch between them. */
+int adx_bench_gemv(int ordinal, int precision, int n, int chain, int iters, int pdl,
+                   double* ms_per_gemv);
+
 /* eval_full: denoiser.hpp:79, denoiser.cpp:222-233 (on ordinals[0]) */
 int adx_eval_full(adx_engine* e, const double* x, int t_embed, double* eps_out);
 

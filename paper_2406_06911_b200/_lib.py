@@ -90,7 +90,7 @@ EXPORTS = [
     "adx_partition_segment_of_stage", "adx_partition_validate", "adx_crossing_links",
     "adx_plan_async", "adx_plan_from_flat", "adx_plan_to_flat", "adx_plan_destroy", "adx_plan_validate",
     "adx_plan_counts", "adx_shift_embeddings", "adx_render_plan",
-    "adx_engine_create", "adx_engine_destroy", "adx_engine_weight_bytes", "adx_engine_time_eval", "adx_eval_full", "adx_eval_segment",
+    "adx_engine_create", "adx_engine_destroy", "adx_engine_weight_bytes", "adx_engine_time_eval", "adx_bench_gemv", "adx_eval_full", "adx_eval_segment",
     "adx_run_options_default", "adx_session_create", "adx_session_destroy", "adx_session_run",
     "adx_session_upload", "adx_session_time", "adx_session_kernel_count", "adx_session_weight_bytes",
     "adx_session_download", "adx_run_serial", "adx_run_parallel", "adx_sequential_denoise",
@@ -150,6 +150,7 @@ def lib():
         "adx_engine_destroy": (None, [vp]),
         "adx_engine_weight_bytes": (i, [vp, i, P(ll)]),
         "adx_engine_time_eval": (i, [vp, i, i, P(d), P(ll), P(i)]),
+        "adx_bench_gemv": (i, [i, i, i, i, i, i, P(d)]),
         "adx_eval_full": (i, [vp, P(d), i, P(d)]),
         "adx_eval_segment": (i, [vp, vp, i, P(d), i, i, i, P(i), P(d), i, i, P(d), i, P(i), P(i), P(i),
                                  P(d), i, i, P(i)]),

@@ -294,7 +294,7 @@ int adx_ddim_step(int ordinal, int precision, const double* x, const double* eps
         CKC(cudaDeviceSynchronize());
         int flags[2];
         CKC(cudaMemcpy(flags, bad.p, sizeof flags, cudaMemcpyDeviceToHost));
-        if (flags[1] != 0x7f7f7f7f) throw std::domain_error("predict_x0: non-finite eps at t=" + std::to_string(t));
+        if (flags[0] != 0x7f7f7f7f) throw std::domain_error("predict_x0: non-finite eps at t=" + std::to_string(t));
         tmp.resize(static_cast<size_t>(d) * ab);
         CKC(cudaMemcpy(tmp.data(), od.p, tmp.size(), cudaMemcpyDeviceToHost));
         from_act(precision, tmp.data(), d, out);
@@ -569,6 +569,13 @@ int adx_engine_weight_bytes(const adx_engine* e, int idx, long long* bytes) {
     return guard([&] {
         need(e, "engine_weight_bytes");
         *bytes = e->e->weight_bytes_resident(idx);
+    });
+}
+
+int adx_bench_gemv(int ordinal, int precision, int n, int chain, int iters, int pdl, double* ms_per_gemv) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        *ms_per_gemv = adx::bench_gemv_chain(precision, n, chain, iters, pdl != 0);
     });
 }
 

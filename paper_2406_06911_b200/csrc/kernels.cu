@@ -187,9 +187,6 @@ __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
 // partial pass is spread over the whole chip.  Each row is reduced by one warp
 // in a fixed order (per-lane chunk/vector order, then a butterfly), so the
 // result is independent of grid size and placement.
-constexpr int kTWarps = 8;
-constexpr int kSlots = 4;
-constexpr int kChunk = 4096;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -213,7 +210,7 @@ __device__ __forceinline__ void tma_row_chunk(uint32_t dst, const void* src, uin
         : "memory");
 }
 
-template <typename WT, typename AT>
+template <typename WT, typename AT, int kTWarps, int kSlots, int kChunk>
 __global__ void __launch_bounds__(kTWarps * 32, 1) gemv_tma_kernel(const GemvArgs a) {
     using AccT = typename Acc<WT>::T;
     constexpr int VEC = 16 / sizeof(WT);
@@ -348,14 +345,51 @@ bool use_ldg_gemv() {
     return v;
 }
 
+// (warps per CTA, ring slots per warp, chunk bytes, CTAs per SM) of the TMA GEMV;
+// ADX_GEMV_CFG=<index> selects one for tuning runs.
+struct TmaCfg {
+    int warps, slots, chunk, ctas_per_sm;
+};
+constexpr TmaCfg kTmaCfgs[] = {{8, 4, 4096, 1}, {8, 2, 8192, 1}, {4, 4, 4096, 2}, {8, 8, 2048, 1},
+                               {16, 2, 4096, 1}, {4, 2, 8192, 2}};
+constexpr int kNumTmaCfgs = sizeof(kTmaCfgs) / sizeof(kTmaCfgs[0]);
+
+int tma_cfg_index() {
+    static int forced = -2;
+    if (forced == -2) {
+        const char* e = getenv("ADX_GEMV_CFG");
+        forced = e ? std::max(0, std::min(kNumTmaCfgs - 1, atoi(e))) : -1;
+    }
+    return forced < 0 ? 4 : forced;  // 16 warps x 2 slots x 4 KB: best of the B200 sweep
+}
+
+template <typename WT, typename AT, int W, int S, int CH>
+void launch_tma(const GemvArgs& a, cudaLaunchConfig_t& cfg, int ctas_per_sm) {
+    static bool attr_done[64] = {};
+    int dev = 0;
+    ADX_CUDA(cudaGetDevice(&dev));
+    if (!attr_done[dev]) {
+        ADX_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<WT, AT, W, S, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      227 * 1024));
+        attr_done[dev] = true;
+    }
+    const size_t x_bytes = (static_cast<size_t>(a.pitch) * sizeof(AT) + 127) & ~size_t(127);
+    const size_t smem = x_bytes + static_cast<size_t>(W) * S * (CH + 8);
+    if (smem * ctas_per_sm > 227 * 1024) ctas_per_sm = 1;
+    if (smem > 227 * 1024) throw std::invalid_argument("gemv: input width too large for shared memory");
+    const int want = (a.rows + W - 1) / W;
+    cfg.gridDim = dim3(std::max(1, std::min(want, num_sms() * ctas_per_sm)));
+    cfg.blockDim = dim3(W * 32);
+    cfg.dynamicSmemBytes = smem;
+    ADX_CUDA(cudaLaunchKernelEx(&cfg, gemv_tma_kernel<WT, AT, W, S, CH>, a));
+}
+
 template <typename WT, typename AT>
 void launch_gemv_t(int prec, const GemvArgs& a, cudaStream_t stream, bool pdl) {
     int dev = 0;
     ADX_CUDA(cudaGetDevice(&dev));
     if (!g_attr_done[dev][prec]) {
         ADX_CUDA(cudaFuncSetAttribute(gemv_kernel<WT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        ADX_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<WT, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      227 * 1024));
         g_attr_done[dev][prec] = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -365,7 +399,6 @@ void launch_gemv_t(int prec, const GemvArgs& a, cudaStream_t stream, bool pdl) {
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     cfg.stream = stream;
-    const size_t x_bytes = (static_cast<size_t>(a.pitch) * sizeof(AT) + 127) & ~size_t(127);
     if (use_ldg_gemv()) {
         const size_t smem = static_cast<size_t>(a.pitch) * sizeof(AT);
         if (smem > 200 * 1024) throw std::invalid_argument("gemv: input width too large for shared memory");
@@ -375,13 +408,15 @@ void launch_gemv_t(int prec, const GemvArgs& a, cudaStream_t stream, bool pdl) {
         ADX_CUDA(cudaLaunchKernelEx(&cfg, gemv_kernel<WT, AT>, a));
         return;
     }
-    const size_t smem = x_bytes + static_cast<size_t>(kTWarps) * kSlots * (kChunk + 8);
-    if (smem > 227 * 1024) throw std::invalid_argument("gemv: input width too large for shared memory");
-    const int want = (a.rows + kTWarps - 1) / kTWarps;
-    cfg.gridDim = dim3(std::max(1, std::min(want, num_sms())));
-    cfg.blockDim = dim3(kTWarps * 32);
-    cfg.dynamicSmemBytes = smem;
-    ADX_CUDA(cudaLaunchKernelEx(&cfg, gemv_tma_kernel<WT, AT>, a));
+    const TmaCfg& c = kTmaCfgs[tma_cfg_index()];
+    switch (tma_cfg_index()) {
+        case 0: launch_tma<WT, AT, 8, 4, 4096>(a, cfg, c.ctas_per_sm); break;
+        case 1: launch_tma<WT, AT, 8, 2, 8192>(a, cfg, c.ctas_per_sm); break;
+        case 2: launch_tma<WT, AT, 4, 4, 4096>(a, cfg, c.ctas_per_sm); break;
+        case 3: launch_tma<WT, AT, 8, 8, 2048>(a, cfg, c.ctas_per_sm); break;
+        case 4: launch_tma<WT, AT, 16, 2, 4096>(a, cfg, c.ctas_per_sm); break;
+        default: launch_tma<WT, AT, 4, 2, 8192>(a, cfg, c.ctas_per_sm); break;
+    }
 }
 
 }  // namespace
@@ -402,6 +437,64 @@ void launch_gemv(int prec, const GemvArgs& a, cudaStream_t stream, bool pdl) {
         case kBF16: launch_gemv_t<__nv_bfloat16, float>(prec, a, stream, pdl); break;
         default: throw std::invalid_argument("gemv: bad precision");
     }
+}
+
+// Microbenchmark: a dependent chain of `chain` square GEMVs (n x n, distinct
+// weight buffers so the chain streams chain*n*n*wb bytes from HBM), captured in
+// one CUDA graph and launched `iters` times; returns device ms per GEMV.
+double bench_gemv_chain(int prec, int n, int chain, int iters, bool pdl) {
+    const int pitch = (n + 7) & ~7;
+    const size_t wbytes = static_cast<size_t>(n) * pitch * weight_bytes(prec);
+    std::vector<void*> W(chain), v(chain + 1);
+    void* bad = nullptr;
+    for (int i = 0; i < chain; ++i) {
+        ADX_CUDA(cudaMalloc(&W[i], wbytes));
+        ADX_CUDA(cudaMemset(W[i], 0x11, wbytes));  // small finite values in every dtype
+    }
+    for (int i = 0; i <= chain; ++i) {
+        ADX_CUDA(cudaMalloc(&v[i], static_cast<size_t>(pitch) * act_bytes(prec)));
+        ADX_CUDA(cudaMemset(v[i], 0, static_cast<size_t>(pitch) * act_bytes(prec)));
+    }
+    ADX_CUDA(cudaMalloc(&bad, 8));
+    cudaStream_t st;
+    ADX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    ADX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    for (int i = 0; i < chain; ++i) {
+        GemvArgs a = {};
+        a.W = W[i];
+        a.rows = n;
+        a.pitch = pitch;
+        a.K = n;
+        a.nseg = 1;
+        a.seg[0] = v[i];
+        a.seg_len[0] = n;
+        a.out = v[i + 1];
+        a.act = 1;
+        launch_gemv(prec, a, st, pdl);
+    }
+    ADX_CUDA(cudaStreamEndCapture(st, &g));
+    ADX_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    cudaEvent_t e0, e1;
+    ADX_CUDA(cudaEventCreate(&e0));
+    ADX_CUDA(cudaEventCreate(&e1));
+    for (int i = 0; i < 3; ++i) ADX_CUDA(cudaGraphLaunch(ge, st));
+    ADX_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) ADX_CUDA(cudaGraphLaunch(ge, st));
+    ADX_CUDA(cudaEventRecord(e1, st));
+    ADX_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    ADX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(st);
+    for (void* p : W) cudaFree(p);
+    for (void* p : v) cudaFree(p);
+    cudaFree(bad);
+    return ms / (static_cast<double>(iters) * chain);
 }
 
 void launch_ddim(int prec, const DdimArgs& a, cudaStream_t stream) {

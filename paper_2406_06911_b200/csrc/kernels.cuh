@@ -12,6 +12,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <vector>
 
 namespace adx {
 
@@ -56,6 +57,9 @@ void launch_ddim(int prec, const DdimArgs& a, cudaStream_t stream);
 void launch_delay(double seconds, cudaStream_t stream);
 // fp64 -> activation dtype (fp64 copy or fp32 round)
 void launch_from_f64(int prec, const double* src, void* dst, int n, cudaStream_t stream);
+
+// dependent chain of square GEMVs in one CUDA graph: device ms per GEMV
+double bench_gemv_chain(int prec, int n, int chain, int iters, bool pdl);
 
 int act_bytes(int prec);     // activation element size
 int weight_bytes(int prec);  // weight element size
