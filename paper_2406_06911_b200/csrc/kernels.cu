@@ -238,11 +238,16 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) gemv_tma_kernel(const GemvArg
         return Wb + row * row_bytes + off;
     };
 
+    // x-gather barrier lives after the ring barriers
+    uint64_t* xbar = reinterpret_cast<uint64_t*>(smem_raw + x_bytes + static_cast<size_t>(kTWarps) * kSlots * kChunk) +
+                     kTWarps * kSlots;
+
     // ---- prologue: barriers + first kSlots chunks (weights only; independent of
     // the producer kernel, so it runs before griddepcontrol.wait)
     if (lane == 0) {
         for (int s = 0; s < kSlots; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])) : "memory");
+        if (warp == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(xbar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int i = 0; i < kSlots && i < nchunks; ++i) {
             uint32_t bytes;
@@ -253,15 +258,42 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) gemv_tma_kernel(const GemvArg
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
-    // ---- gather the concatenated input into shared memory (zero padded)
+    // ---- gather the concatenated input into shared memory (zero padded):
+    // 16-byte-aligned segments by one bulk TMA copy each (a single L2 round
+    // trip), the rest element-wise.
     int off = 0;
+    uint32_t tx = 0;
     for (int s = 0; s < a.nseg; ++s) {
-        const AT* src = static_cast<const AT*>(a.seg[s]);
-        for (int i = threadIdx.x; i < a.seg_len[s]; i += blockDim.x) sx[off + i] = src[i];
+        const uint32_t nb = static_cast<uint32_t>(a.seg_len[s]) * sizeof(AT);
+        const bool bulk = ((reinterpret_cast<uintptr_t>(a.seg[s]) | nb | (off * sizeof(AT))) & 15u) == 0 && nb > 0;
+        if (bulk) {
+            tx += nb;
+        } else {
+            const AT* src = static_cast<const AT*>(a.seg[s]);
+            for (int i = threadIdx.x; i < a.seg_len[s]; i += blockDim.x) sx[off + i] = src[i];
+        }
         off += a.seg_len[s];
     }
     for (int i = off + threadIdx.x; i < a.pitch; i += blockDim.x) sx[i] = AT(0);
+    if (threadIdx.x == 0) {
+        __syncwarp(1u);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(xbar)), "r"(tx)
+                     : "memory");
+        int o = 0;
+        for (int s = 0; s < a.nseg; ++s) {
+            const uint32_t nb = static_cast<uint32_t>(a.seg_len[s]) * sizeof(AT);
+            const bool bulk = ((reinterpret_cast<uintptr_t>(a.seg[s]) | nb | (o * sizeof(AT))) & 15u) == 0 && nb > 0;
+            if (bulk)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(sx + o)),
+                    "l"(a.seg[s]), "r"(nb), "r"(smem_u32(xbar))
+                    : "memory");
+            o += a.seg_len[s];
+        }
+    }
     __syncthreads();
+    mbar_wait(smem_u32(xbar), 0u);
 
     AccT acc = AccT(0);
     for (int i = 0; i < nchunks; ++i) {
@@ -374,7 +406,7 @@ void launch_tma(const GemvArgs& a, cudaLaunchConfig_t& cfg, int ctas_per_sm) {
         attr_done[dev] = true;
     }
     const size_t x_bytes = (static_cast<size_t>(a.pitch) * sizeof(AT) + 127) & ~size_t(127);
-    const size_t smem = x_bytes + static_cast<size_t>(W) * S * (CH + 8);
+    const size_t smem = x_bytes + static_cast<size_t>(W) * S * (CH + 8) + 16;
     if (smem * ctas_per_sm > 227 * 1024) ctas_per_sm = 1;
     if (smem > 227 * 1024) throw std::invalid_argument("gemv: input width too large for shared memory");
     const int want = (a.rows + W - 1) / W;
