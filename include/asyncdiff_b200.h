@@ -256,6 +256,29 @@ int adx_run_parallel(adx_engine* e, const adx_plan* plan, const adx_partition* p
 int adx_sequential_denoise(adx_engine* e, const double* x_T, const double* alpha_bars, int T,
                            double* traj_latents, double* traj_eps);
 
+/* ------------------------------------------------- one process per GPU
+ * The same async loop with rank v of a torchrun job evaluating the plan's
+ * device-v evals on its own GPU (run_parallel's worker d, executor.cpp:444-496)
+ * and exchanging stage outputs / eps over NCCL p2p, one NCCL group per
+ * exchange point.  adx_rank_program exports the rank's op list (12 ints per
+ * op: kind, seg, t, wslot, rslot, step, eps_step, point, peer, stage, slot,
+ * elems; kinds 0 eval, 1 group, 2 send, 3 recv, 4 end, 5 ddim) -- the CPU
+ * gloo test replays it with the oracle to check the exchange schedule. */
+typedef struct adx_rank_session adx_rank_session;
+int adx_rank_program(const adx_plan* plan, const adx_partition* part, const adx_model* m, int rank,
+                     int* out, int cap, int* n_ops);
+int adx_nccl_unique_id(char* out128);
+/* collective over ranks 0..plan.D-1 (same nccl_id); engine = this rank's GPU */
+int adx_rank_session_create(adx_engine* e, const adx_plan* plan, const adx_partition* part,
+                            const double* alpha_bars, int T, int rank, const char* nccl_id,
+                            const adx_run_options* opts, adx_rank_session** out);
+void adx_rank_session_destroy(adx_rank_session* s);
+/* collective; x_T / outputs are used on rank 0 only */
+int adx_rank_session_run(adx_rank_session* s, const double* x_T, double* traj_latents,
+                         double* traj_eps);
+int adx_rank_session_time(adx_rank_session* s, int iters, double* ms_per_run);
+int adx_rank_session_kernel_count(const adx_rank_session* s, int* n);
+
 /* compare_trajectories: metrics.hpp, metrics.cpp:9-30 (host arithmetic) */
 int adx_compare_trajectories(const double* a, const double* b, int n_latents, int d,
                              double* per_step_mse, double* final_mse, double* final_max_abs);

@@ -472,6 +472,30 @@ static int run_stage_range(const or_model* m, int first, int last, double* cur, 
     return OR_OK;
 }
 
+/* one stage of run_stage_range (denoiser.cpp:182-187) on an explicit concat
+ * input u (length in); the multi-rank gloo test drives segments with it. */
+int or_stage_forward(const or_model* m, int stage, const double* u, int un, int t_embed, double* y_out) {
+    const or_stage* s = &m->st[stage - 1];
+    if (un != s->in) return fail(OR_RUNTIME, "eval: stage %d input width %d != expected %d", stage, un, s->in);
+    double e[512];
+    embed(m, t_embed, e);
+    double* z = (double*)malloc(sizeof(double) * (size_t)s->h);
+    double* te = (double*)malloc(sizeof(double) * (size_t)s->h);
+    gemv(s->w1, s->h, s->in, u, z);
+    gemv(s->tin, s->h, m->E, e, te);
+    for (int j = 0; j < s->h; ++j) {
+        double v = (z[j] + s->b1[j]) + te[j];
+        z[j] = v > 0.0 ? v : 0.1 * v;
+    }
+    gemv(s->w2, s->out, s->h, z, y_out);
+    for (int j = 0; j < s->out; ++j) y_out[j] += s->b2[j];
+    free(z);
+    free(te);
+    return OR_OK;
+}
+
+void or_embed(const or_model* m, int t, double* out) { embed(m, t, out); }
+
 /* denoiser.cpp:222-233 */
 int or_eval_full(const or_model* m, const double* x, int t_embed, double* eps_out) {
     double e[512];

@@ -89,6 +89,8 @@ double* or_model_tensor(or_model* m, int stage, int which, int* rows, int* cols)
 
 int or_sinusoid(int t, int dim, double* out);
 int or_eval_full(const or_model* m, const double* x, int t_embed, double* eps_out);
+int or_stage_forward(const or_model* m, int stage, const double* u, int un, int t_embed, double* y_out);
+void or_embed(const or_model* m, int t, double* out);
 
 /* ---- partition: proj/src/partition.cpp:95-208 ---- */
 enum { OR_SEQUENTIAL_BALANCED = 0, OR_FIRST_LAST_GROUPED = 1 };

@@ -74,6 +74,8 @@ def lib():
         L.or_model_tensor.argtypes = [C.c_void_p, i, i, P(i), P(i)]
         L.or_sinusoid.argtypes = [i, i, P(d)]
         L.or_eval_full.argtypes = [C.c_void_p, P(d), i, P(d)]
+        L.or_stage_forward.argtypes = [C.c_void_p, i, P(d), i, i, P(d)]
+        L.or_embed.argtypes = [C.c_void_p, i, P(d)]
         L.or_partition_balanced.argtypes = [P(ll), i, i, i, P(i), P(ll)]
         L.or_plan_async_flat.argtypes = [i, i, i, i, i, P(i), i, P(i)]
         L.or_run_serial.argtypes = [C.c_void_p, P(i), i, P(i), P(d), i, P(d), P(d), P(d), P(i), P(i)]
@@ -228,6 +230,17 @@ class Model:
         n = r.value * c.value
         arr = np.ctypeslib.as_array(p, shape=(n,))
         return arr.reshape((r.value, c.value), order="F")
+
+    def stage_forward(self, stage: int, u, t: int) -> np.ndarray:
+        u = np.ascontiguousarray(u, np.float64)
+        out = np.empty(self.widths[stage])
+        _chk(lib().or_stage_forward(self._h, stage, _dp(u), u.size, t, _dp(out)))
+        return out
+
+    def embed(self, t: int) -> np.ndarray:
+        out = np.empty(self.E)
+        lib().or_embed(self._h, t, _dp(out))
+        return out
 
     def eval_full(self, x, t: int) -> np.ndarray:
         x = np.ascontiguousarray(x, np.float64)

@@ -94,7 +94,8 @@ EXPORTS = [
     "adx_run_options_default", "adx_session_create", "adx_session_destroy", "adx_session_run",
     "adx_session_upload", "adx_session_time", "adx_session_kernel_count", "adx_session_weight_bytes",
     "adx_session_download", "adx_run_serial", "adx_run_parallel", "adx_sequential_denoise",
-    "adx_compare_trajectories",
+    "adx_compare_trajectories", "adx_rank_program", "adx_nccl_unique_id", "adx_rank_session_create",
+    "adx_rank_session_destroy", "adx_rank_session_run", "adx_rank_session_time", "adx_rank_session_kernel_count",
 ]
 
 _lib = None
@@ -168,6 +169,13 @@ def lib():
                                  P(adx_run_stats)]),
         "adx_sequential_denoise": (i, [vp, P(d), P(d), i, P(d), P(d)]),
         "adx_compare_trajectories": (i, [P(d), P(d), i, i, P(d), P(d), P(d)]),
+        "adx_rank_program": (i, [vp, vp, vp, i, P(i), i, P(i)]),
+        "adx_nccl_unique_id": (i, [C.c_char_p]),
+        "adx_rank_session_create": (i, [vp, vp, vp, P(d), i, i, C.c_char_p, P(adx_run_options), P(vp)]),
+        "adx_rank_session_destroy": (None, [vp]),
+        "adx_rank_session_run": (i, [vp, P(d), P(d), P(d)]),
+        "adx_rank_session_time": (i, [vp, i, P(d)]),
+        "adx_rank_session_kernel_count": (i, [vp, P(i)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

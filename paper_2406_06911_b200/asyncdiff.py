@@ -30,7 +30,7 @@ __all__ = [
     "Round", "ExecutionPlan", "plan_async", "validate_plan", "PlanCounts", "plan_counts", "shift_embeddings",
     "render_plan", "RunOptions", "RunStats", "InstrumentedDenoiser", "inject_delay", "run_serial",
     "run_parallel", "DivergenceReport", "compare_trajectories", "kWarmupRound", "set_default_precision",
-    "PRECISIONS", "Session", "time_model_pass",
+    "PRECISIONS", "Session", "time_model_pass", "RankSession", "nccl_unique_id",
 ]
 
 PRECISIONS = {"f64": 0, "f32": 1, "bf16": 2}
@@ -806,6 +806,46 @@ class Session:
         eps = np.zeros((T, self.d))
         check(lib().adx_session_download(self._h, _dp(lat), _dp(eps)))
         return _traj_from(lat, eps, T)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().adx_nccl_unique_id(buf))
+    return buf.raw
+
+
+class RankSession:
+    """One process per GPU (torchrun): this rank's part of the async loop,
+    exchanging with its peers over NCCL p2p (rank.cu).  Collective: every rank
+    0..plan.D-1 constructs it with the same nccl id and calls run()/time()."""
+
+    def __init__(self, model: LayeredDenoiser, schedule: NoiseSchedule, plan: ExecutionPlan, partition: Partition,
+                 rank: int, nccl_id: bytes, device: int, precision: Optional[str] = None):
+        self.model, self.schedule, self.rank = model, schedule, rank
+        eng = model.engine(precision, [device])
+        self._eng = eng
+        self._ab = _f64(schedule.alpha_bars)
+        self._ph = plan._handle()
+        o, _ = _opts(None, [])
+        h = C.c_void_p()
+        check(lib().adx_rank_session_create(eng._h, self._ph._h, partition._h, _dp(self._ab), schedule.T, rank,
+                                            C.c_char_p(nccl_id), C.byref(o), C.byref(h)))
+        self._h = h
+        self._finalizer = weakref.finalize(self, lib().adx_rank_session_destroy, h)
+        self.d = model.data_dim()
+
+    def run_into(self, x: np.ndarray, lat: np.ndarray, eps: np.ndarray) -> None:
+        check(lib().adx_rank_session_run(self._h, _dp(x), _dp(lat), _dp(eps)))
+
+    def time(self, iters: int) -> float:
+        ms = C.c_double()
+        check(lib().adx_rank_session_time(self._h, iters, C.byref(ms)))
+        return ms.value
+
+    def kernel_count(self) -> int:
+        n = C.c_int()
+        check(lib().adx_rank_session_kernel_count(self._h, C.byref(n)))
+        return n.value
 
 
 def time_model_pass(m: LayeredDenoiser, t_embed: int, iters: int, precision: Optional[str] = None,

@@ -5,6 +5,7 @@
 
 #include "engine.hpp"
 #include "host.hpp"
+#include "schedule.hpp"
 
 #include <cuda_runtime.h>
 
@@ -780,6 +781,71 @@ int adx_compare_trajectories(const double* a, const double* b, int n, int d, dou
         for (int k = 0; k < d; ++k)
             mx = std::max(mx, std::fabs(a[static_cast<size_t>(n - 1) * d + k] - b[static_cast<size_t>(n - 1) * d + k]));
         if (final_max_abs) *final_max_abs = mx;
+    });
+}
+
+// ----------------------------------------------------- one process per GPU
+int adx_rank_program(const adx_plan* plan, const adx_partition* part, const adx_model* m, int rank, int* out,
+                     int cap, int* n_ops) {
+    return guard([&] {
+        need(plan, "rank_program");
+        need(part, "rank_program");
+        need(m, "rank_program");
+        auto ops = adx::rank_program(plan->p, part->p, m->m, rank);
+        *n_ops = static_cast<int>(ops.size());
+        if (static_cast<int>(ops.size()) * 12 > cap) throw std::invalid_argument("rank_program: buffer too small");
+        for (size_t i = 0; i < ops.size(); ++i) {
+            const adx::RankOp& o = ops[i];
+            const int f[12] = {o.kind, o.seg,   o.t,    o.wslot, o.rslot, o.step,
+                               o.eps_step, o.point, o.peer, o.stage, o.slot, static_cast<int>(o.elems)};
+            std::memcpy(out + 12 * i, f, sizeof f);
+        }
+    });
+}
+
+int adx_nccl_unique_id(char* out128) {
+    return guard([&] {
+        need(out128, "nccl_unique_id");
+        adx::nccl_unique_id(out128);
+    });
+}
+
+int adx_rank_session_create(adx_engine* e, const adx_plan* plan, const adx_partition* part,
+                            const double* alpha_bars, int T, int rank, const char* nccl_id,
+                            const adx_run_options* opts, adx_rank_session** out) {
+    return guard([&] {
+        need(e, "rank_session_create");
+        need(plan, "rank_session_create");
+        need(part, "rank_session_create");
+        need(nccl_id, "rank_session_create");
+        std::vector<double> ab(alpha_bars, alpha_bars + T + 1);
+        *out = reinterpret_cast<adx_rank_session*>(
+            adx::rank_session_create(e->e.get(), plan->p, part->p, ab, rank, nccl_id, to_opts(opts)));
+    });
+}
+
+void adx_rank_session_destroy(adx_rank_session* s) {
+    if (s) adx::rank_session_destroy(s);
+}
+
+int adx_rank_session_run(adx_rank_session* s, const double* x_T, double* lat, double* eps) {
+    return guard([&] {
+        need(s, "rank_session_run");
+        adx::rank_session_run(s, x_T, lat, eps);
+    });
+}
+
+int adx_rank_session_time(adx_rank_session* s, int iters, double* ms) {
+    return guard([&] {
+        need(s, "rank_session_time");
+        *ms = adx::rank_session_time(s, iters);
+    });
+}
+
+int adx_rank_session_kernel_count(const adx_rank_session* s, int* n) {
+    return guard([&] {
+        need(s, "rank_session_kernel_count");
+        *n = adx::rank_session_kernels(const_cast<adx_rank_session*>(s));
     });
 }
 

@@ -182,4 +182,13 @@ private:
     int enq_kernels_ = 0;
 };
 
+// one process per GPU (rank.cu): opaque session driven over NCCL
+void nccl_unique_id(char* out128);
+void* rank_session_create(Engine* e, const Plan& plan, const Partition& part, const std::vector<double>& ab,
+                          int rank, const char* id, const RunOptions& opts);
+void rank_session_destroy(void* s);
+void rank_session_run(void* s, const double* x, double* lat, double* eps);
+double rank_session_time(void* s, int iters);
+int rank_session_kernels(void* s);
+
 }  // namespace adx

@@ -1,0 +1,49 @@
+// schedule.hpp -- per-rank program of the multi-process async loop.
+//
+// One process per GPU: rank v runs exactly the evals the plan assigns to device
+// v (plan.cpp:53, 67-73, 82) and exchanges stage outputs point-to-point.  The
+// program is a flat, totally ordered list of ops that every rank derives from
+// the same (plan, partition, model) -- so the sends and receives of a pair of
+// ranks appear in the same order on both sides, and each exchange point is one
+// NCCL group (send/recv order inside a group does not matter).  The same list
+// drives the NCCL transport (rank.cu) and the CPU gloo test
+// (tests/test_multirank_gloo.py), which is how the multi-rank path is checked
+// without several GPUs.
+//
+// Slots: stage outputs live in two parity slots per stage (engine.hpp); round
+// r writes slot s(r) = (r+2)%2 and reads cross-segment inputs from s(r-1);
+// the warm-up cascade uses slot 1 (= s(-1)).
+#pragma once
+
+#include "host.hpp"
+
+#include <vector>
+
+namespace adx {
+
+enum OpKind {
+    kOpEval = 0,   // evaluate `seg` at embed `t`; wslot/rslot; latent row `step`; eps row `eps_step` (-1 none)
+    kOpGroup = 1,  // begin an exchange point (NCCL group); `point` = global exchange index
+    kOpSend = 2,   // send stage `stage` output (slot) or eps (stage = -1, local eps buffer slot) to `peer`
+    kOpRecv = 3,   // receive stage `stage` output into slot, or eps (stage = -1) into trajectory row `step`
+    kOpEnd = 4,    // end the exchange point
+    kOpDdim = 5,   // sampler step on rank 0: latent row `step` -> `step+1` with eps row `step`, timestep t
+};
+
+struct RankOp {
+    int kind = 0;
+    int seg = 0, t = 0, wslot = 0, rslot = 0, step = -1, eps_step = -1;
+    int point = -1, peer = -1, stage = 0, slot = 0;
+    long long elems = 0;  // element count of a send/recv
+};
+
+// The program of `rank` (virtual device).  Warm-up: one exchange point per
+// (step, segment); rounds: one exchange point per round.  Ranks with no part
+// in a point skip it.
+std::vector<RankOp> rank_program(const Plan& plan, const Partition& part, const Model& m, int rank);
+
+// Which ranks consume the outputs of segment `seg` (evaluate seg+1.. with a
+// link from seg) -- the union over the plan's evals and the warm-up placement.
+std::vector<int> ranks_evaluating(const Plan& plan, const Partition& part, int seg);
+
+}  // namespace adx

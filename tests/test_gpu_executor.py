@@ -156,3 +156,16 @@ def test_sequential_error_wraps_timestep():
     s = adx.build_schedule(5, 0.01, 0.1)
     with pytest.raises(adx.AdxRuntimeError, match=r"t=5: eval: non-finite activation at stage 3"):
         adx.sequential_denoise(m, adx.Latent(np.ones(2), 5), s)
+
+
+def test_rank_session_single_rank_matches_sequential():
+    """NCCL rank path (rank.cu) with one rank: N=1 plan == sequential_denoise bit-exactly."""
+    f = Fixture()
+    plan = adx.plan_async(20, 1, 1, 1)
+    part = adx.partition_balanced(f.model, 1)
+    sess = adx.RankSession(f.model, f.schedule, plan, part, 0, adx.nccl_unique_id(), 0, "f64")
+    lat, eps = np.zeros((21, 2)), np.zeros((20, 2))
+    sess.run_into(np.ascontiguousarray(f.x_T.values), lat, eps)
+    seq = adx.sequential_denoise(f.model, f.x_T, f.schedule, precision="f64")
+    assert np.array_equal(lat, seq.latent_matrix())
+    assert sess.time(2) > 0
