@@ -279,6 +279,40 @@ int adx_rank_session_run(adx_rank_session* s, const double* x_T, double* traj_la
 int adx_rank_session_time(adx_rank_session* s, int iters, double* ms_per_run);
 int adx_rank_session_kernel_count(const adx_rank_session* s, int* n);
 
+/* ------------------------------------------------------ §8(f) next rows */
+/* save_checkpoint / load_checkpoint: proj/include/asyncdiff/serialize.hpp:35-36,
+ * serialize.cpp:226-308 (<base>.json metadata + <base>.bin row-major LE fp64) */
+int adx_model_save_checkpoint(const adx_model* m, const char* base);
+int adx_model_load_checkpoint(const char* base, adx_model** out);
+/* plan_to_json / plan_from_json: serialize.hpp:29-30, serialize.cpp:109-159 */
+int adx_plan_to_json(const adx_plan* p, char* buf, int cap, int* len);
+int adx_plan_from_json(const char* text, adx_plan** out);
+
+/* LatencyReport / CostComparison: costsim.hpp:13-50 */
+typedef struct {
+    double sequential_total_s, async_total_s, warmup_s, comm_total_s, speedup, comm_ratio,
+        approx_step_s, approx_total_s;
+} adx_latency_report;
+typedef struct {
+    double predicted_total_s, measured_total_s, rel_error_total, predicted_comm_ratio,
+        measured_comm_ratio, rel_error_comm_ratio, calibrated_comm_cost_s;
+} adx_cost_comparison;
+/* predict_async: costsim.cpp:18-50.  round_bytes == NULL: flat comm_cost_s per
+ * broadcasting round (reference); else bytes-aware comm = comm_latency_s +
+ * round_bytes[r] / (link_gbs GB/s) (the NVLink cost model). */
+int adx_predict_async(const adx_plan* p, const double* seg_cost, int n_seg, double comm_cost_s,
+                      double sampler_cost_s, double comm_latency_s, double link_gbs,
+                      const long long* round_bytes, adx_latency_report* out,
+                      double* round_compute_s, double* round_comm_s);
+/* calibrate_and_compare: costsim.cpp:52-79 */
+int adx_calibrate_and_compare(const adx_plan* p, const double* delays, int n,
+                              const double* measured_round_comm_s, int n_rounds,
+                              int broadcast_count, double measured_total_s,
+                              adx_cost_comparison* out);
+/* bytes crossing devices per round in the one-process-per-GPU program */
+int adx_round_exchange_bytes(const adx_plan* p, const adx_partition* part, const adx_model* m,
+                             int precision, long long* out /* n_rounds */);
+
 /* compare_trajectories: metrics.hpp, metrics.cpp:9-30 (host arithmetic) */
 int adx_compare_trajectories(const double* a, const double* b, int n_latents, int d,
                              double* per_step_mse, double* final_mse, double* final_max_abs);

@@ -96,7 +96,20 @@ EXPORTS = [
     "adx_session_download", "adx_run_serial", "adx_run_parallel", "adx_sequential_denoise",
     "adx_compare_trajectories", "adx_rank_program", "adx_nccl_unique_id", "adx_rank_session_create",
     "adx_rank_session_destroy", "adx_rank_session_run", "adx_rank_session_time", "adx_rank_session_kernel_count",
+    "adx_model_save_checkpoint", "adx_model_load_checkpoint", "adx_plan_to_json", "adx_plan_from_json",
+    "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes",
 ]
+
+
+class adx_latency_report(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("sequential_total_s", "async_total_s", "warmup_s", "comm_total_s",
+                                           "speedup", "comm_ratio", "approx_step_s", "approx_total_s")]
+
+
+class adx_cost_comparison(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("predicted_total_s", "measured_total_s", "rel_error_total",
+                                           "predicted_comm_ratio", "measured_comm_ratio", "rel_error_comm_ratio",
+                                           "calibrated_comm_cost_s")]
 
 _lib = None
 
@@ -176,6 +189,13 @@ def lib():
         "adx_rank_session_run": (i, [vp, P(d), P(d), P(d)]),
         "adx_rank_session_time": (i, [vp, i, P(d)]),
         "adx_rank_session_kernel_count": (i, [vp, P(i)]),
+        "adx_model_save_checkpoint": (i, [vp, C.c_char_p]),
+        "adx_model_load_checkpoint": (i, [C.c_char_p, P(vp)]),
+        "adx_plan_to_json": (i, [vp, C.c_char_p, i, P(i)]),
+        "adx_plan_from_json": (i, [C.c_char_p, P(vp)]),
+        "adx_predict_async": (i, [vp, P(d), i, d, d, d, d, P(ll), P(adx_latency_report), P(d), P(d)]),
+        "adx_calibrate_and_compare": (i, [vp, P(d), i, P(d), i, i, d, P(adx_cost_comparison)]),
+        "adx_round_exchange_bytes": (i, [vp, vp, vp, i, P(ll)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -30,7 +30,10 @@ __all__ = [
     "Round", "ExecutionPlan", "plan_async", "validate_plan", "PlanCounts", "plan_counts", "shift_embeddings",
     "render_plan", "RunOptions", "RunStats", "InstrumentedDenoiser", "inject_delay", "run_serial",
     "run_parallel", "DivergenceReport", "compare_trajectories", "kWarmupRound", "set_default_precision",
-    "PRECISIONS", "Session", "time_model_pass", "RankSession", "nccl_unique_id",
+    "PRECISIONS", "Session", "time_model_pass", "RankSession", "nccl_unique_id", "save_checkpoint",
+    "load_checkpoint", "plan_to_json", "plan_from_json", "CostModel", "LatencyReport", "predict_sequential",
+    "predict_async", "CostComparison", "calibrate_and_compare", "round_exchange_bytes", "SimilarityProfile",
+    "similarity_profile",
 ]
 
 PRECISIONS = {"f64": 0, "f32": 1, "bf16": 2}
@@ -739,6 +742,183 @@ def sequential_denoise(eps_fn: Union[LayeredDenoiser, Callable[[Latent, int], np
         traj.eps_used.append(e)
         traj.latents.append(x)
     return traj
+
+
+# ------------------------------------------------------ §8(f): I/O, cost model, quality
+def save_checkpoint(base: str, m: LayeredDenoiser) -> None:
+    """serialize.hpp:35 -- <base>.json + <base>.bin (row-major LE fp64)."""
+    check(lib().adx_model_save_checkpoint(m._h, base.encode()))
+
+
+def load_checkpoint(base: str) -> LayeredDenoiser:
+    """serialize.hpp:36 -- loads a reference-format checkpoint (e.g. cmd_train output)."""
+    h = C.c_void_p()
+    check(lib().adx_model_load_checkpoint(base.encode(), C.byref(h)))
+    return LayeredDenoiser(h.value)
+
+
+def plan_to_json(plan: ExecutionPlan) -> str:
+    """serialize.cpp:109-133"""
+    ph = plan._handle()
+    n = C.c_int()
+    check(lib().adx_plan_to_json(ph._h, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib().adx_plan_to_json(ph._h, buf, len(buf), C.byref(n)))
+    return buf.value.decode()
+
+
+def plan_from_json(text: str) -> ExecutionPlan:
+    """serialize.cpp:135-159"""
+    h = C.c_void_p()
+    check(lib().adx_plan_from_json(text.encode(), C.byref(h)))
+    try:
+        buf = np.zeros(1 << 20, np.int32)
+        n = C.c_int()
+        check(lib().adx_plan_to_flat(h, _ip(buf), buf.size, C.byref(n)))
+    finally:
+        lib().adx_plan_destroy(h)
+    return ExecutionPlan.from_flat(buf[: n.value])
+
+
+@dataclass
+class CostModel:
+    """costsim.hpp:13-19 (+ bytes-aware comm: comm_latency_s + bytes / link_gbs)"""
+    segment_cost_s: List[float]
+    comm_cost_s: float = 0.0
+    sampler_cost_s: float = 0.0
+    comm_latency_s: float = 0.0
+    link_gbs: float = 0.0
+
+    def total_segment_cost_s(self) -> float:
+        return float(sum(self.segment_cost_s))
+
+
+@dataclass
+class LatencyReport:
+    """costsim.hpp:21-34"""
+    sequential_total_s: float
+    async_total_s: float
+    warmup_s: float
+    round_compute_s: List[float]
+    round_comm_s: List[float]
+    comm_total_s: float
+    speedup: float
+    comm_ratio: float
+    approx_step_s: float
+    approx_total_s: float
+
+
+def predict_sequential(T: int, cm: CostModel) -> float:
+    """costsim.cpp:14-16"""
+    return T * (cm.total_segment_cost_s() + cm.sampler_cost_s)
+
+
+def predict_async(plan: ExecutionPlan, cm: CostModel, round_bytes: Optional[Sequence[int]] = None) -> LatencyReport:
+    """costsim.cpp:18-50; with round_bytes the comm term is bytes-aware."""
+    from ._lib import adx_latency_report
+    ph = plan._handle()
+    seg = _f64(cm.segment_cost_s if cm.segment_cost_s else [0.0])
+    nr = max(len(plan.rounds), 1)
+    rc, rm = np.zeros(nr), np.zeros(nr)
+    rb = None if round_bytes is None else np.ascontiguousarray(round_bytes, np.int64)
+    out = adx_latency_report()
+    check(lib().adx_predict_async(ph._h, _dp(seg), len(cm.segment_cost_s), cm.comm_cost_s, cm.sampler_cost_s,
+                                  cm.comm_latency_s, cm.link_gbs,
+                                  None if rb is None else rb.ctypes.data_as(C.POINTER(C.c_longlong)),
+                                  C.byref(out), _dp(rc), _dp(rm)))
+    n = len(plan.rounds)
+    return LatencyReport(out.sequential_total_s, out.async_total_s, out.warmup_s, rc[:n].tolist(), rm[:n].tolist(),
+                         out.comm_total_s, out.speedup, out.comm_ratio, out.approx_step_s, out.approx_total_s)
+
+
+@dataclass
+class CostComparison:
+    """costsim.hpp:36-44"""
+    predicted_total_s: float
+    measured_total_s: float
+    rel_error_total: float
+    predicted_comm_ratio: float
+    measured_comm_ratio: float
+    rel_error_comm_ratio: float
+    calibrated_comm_cost_s: float
+
+
+def calibrate_and_compare(plan: ExecutionPlan, delays_s: Sequence[float], measured: "RunStats") -> CostComparison:
+    """costsim.cpp:52-79"""
+    from ._lib import adx_cost_comparison
+    ph = plan._handle()
+    d = _f64(list(delays_s) or [0.0])
+    rc = _f64(list(measured.round_comm_s) or [0.0])
+    out = adx_cost_comparison()
+    check(lib().adx_calibrate_and_compare(ph._h, _dp(d), len(delays_s), _dp(rc), len(measured.round_comm_s),
+                                          measured.broadcast_count, measured.total_wall_s, C.byref(out)))
+    return CostComparison(out.predicted_total_s, out.measured_total_s, out.rel_error_total, out.predicted_comm_ratio,
+                          out.measured_comm_ratio, out.rel_error_comm_ratio, out.calibrated_comm_cost_s)
+
+
+def round_exchange_bytes(plan: ExecutionPlan, partition: Partition, m: LayeredDenoiser,
+                         precision: Optional[str] = None) -> List[int]:
+    """Bytes crossing devices in each round (boundary + crossing skips + eps)."""
+    ph = plan._handle()
+    out = np.zeros(max(len(plan.rounds), 1), np.int64)
+    check(lib().adx_round_exchange_bytes(ph._h, partition._h, m._h, PRECISIONS[precision or _default_precision],
+                                         out.ctypes.data_as(C.POINTER(C.c_longlong))))
+    return out[: len(plan.rounds)].tolist()
+
+
+@dataclass
+class SimilarityProfile:
+    """metrics.hpp:23-29"""
+    pair_t: List[int]
+    cosine: List[List[float]]
+    rel_l2: List[List[float]]
+
+    def median_cosine(self) -> float:
+        allv = sorted(v for row in self.cosine for v in row)
+        if not allv:
+            return 1.0
+        n = len(allv)
+        return allv[n // 2] if n % 2 else 0.5 * (allv[n // 2 - 1] + allv[n // 2])
+
+
+def similarity_profile(m: LayeredDenoiser, p: Partition, trajectory: Trajectory, schedule: NoiseSchedule,
+                       precision: Optional[str] = None) -> SimilarityProfile:
+    """metrics.cpp:73-101: boundary activations of segments 1..N-1 at every
+    latent of a trajectory (fresh chaining on the GPU), cosine / rel-L2 between
+    adjacent steps -- the hidden-state similarity AsyncDiff relies on."""
+    N = p.num_segments()
+    prof = SimilarityProfile([], [[] for _ in range(max(0, N - 1))], [[] for _ in range(max(0, N - 1))])
+    if len(trajectory.latents) < 3 or N < 2:
+        return prof
+    per_step, ts = [], []
+    for x in trajectory.latents:
+        if x.timestep < 1:
+            break
+        skips, out = {}, []
+        so = eval_segment(m, p, 1, x, skips, x.timestep, precision)
+        for seg in range(2, N + 1):
+            out.append(so.boundary)
+            skips.update(so.skips)
+            so = eval_segment(m, p, seg, so, skips, x.timestep, precision)
+        per_step.append(out)
+        ts.append(x.timestep)
+
+    def cosine(a, b):
+        na, nb = np.linalg.norm(a), np.linalg.norm(b)
+        if na == 0.0 or nb == 0.0:
+            return 1.0 if np.linalg.norm(a - b) == 0.0 else 0.0
+        return float(np.dot(a, b) / (na * nb))
+
+    def rel_l2(a, b):
+        den = max(np.linalg.norm(a), np.linalg.norm(b))
+        return 0.0 if den == 0.0 else float(np.linalg.norm(a - b) / den)
+
+    for i in range(len(per_step) - 1):
+        prof.pair_t.append(ts[i])
+        for b in range(N - 1):
+            prof.cosine[b].append(cosine(per_step[i][b], per_step[i + 1][b]))
+            prof.rel_l2[b].append(rel_l2(per_step[i][b], per_step[i + 1][b]))
+    return prof
 
 
 class Session:

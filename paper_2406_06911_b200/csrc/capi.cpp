@@ -4,6 +4,7 @@
 #include "../../include/asyncdiff_b200.h"
 
 #include "engine.hpp"
+#include "extras.hpp"
 #include "host.hpp"
 #include "schedule.hpp"
 
@@ -846,6 +847,103 @@ int adx_rank_session_kernel_count(const adx_rank_session* s, int* n) {
     return guard([&] {
         need(s, "rank_session_kernel_count");
         *n = adx::rank_session_kernels(const_cast<adx_rank_session*>(s));
+    });
+}
+
+// ------------------------------------------------------ §8(f) next rows
+int adx_model_save_checkpoint(const adx_model* m, const char* base) {
+    return guard([&] {
+        need(m, "save_checkpoint");
+        need(base, "save_checkpoint");
+        adx::save_checkpoint(base, m->m);
+    });
+}
+
+int adx_model_load_checkpoint(const char* base, adx_model** out) {
+    return guard([&] {
+        need(base, "load_checkpoint");
+        *out = new adx_model{adx::load_checkpoint(base)};
+    });
+}
+
+int adx_plan_to_json(const adx_plan* p, char* buf, int cap, int* len) {
+    return guard([&] {
+        need(p, "plan_to_json");
+        const std::string s = adx::plan_to_json(p->p);
+        if (len) *len = static_cast<int>(s.size());
+        if (buf && cap > 0) {
+            std::strncpy(buf, s.c_str(), cap - 1);
+            buf[cap - 1] = 0;
+        }
+    });
+}
+
+int adx_plan_from_json(const char* text, adx_plan** out) {
+    return guard([&] {
+        need(text, "plan_from_json");
+        *out = new adx_plan{adx::plan_from_json(text)};
+    });
+}
+
+int adx_predict_async(const adx_plan* p, const double* seg_cost, int n_seg, double comm_cost_s,
+                      double sampler_cost_s, double comm_latency_s, double link_gbs,
+                      const long long* round_bytes, adx_latency_report* out, double* round_compute_s,
+                      double* round_comm_s) {
+    return guard([&] {
+        need(p, "predict_async");
+        need(out, "predict_async");
+        adx::CostModel cm;
+        cm.segment_cost_s.assign(seg_cost, seg_cost + n_seg);
+        cm.comm_cost_s = comm_cost_s;
+        cm.sampler_cost_s = sampler_cost_s;
+        cm.comm_latency_s = comm_latency_s;
+        cm.link_gbs = link_gbs;
+        std::vector<long long> rb;
+        if (round_bytes) rb.assign(round_bytes, round_bytes + p->p.rounds.size());
+        const adx::LatencyReport r = adx::predict_async(p->p, cm, round_bytes ? &rb : nullptr);
+        out->sequential_total_s = r.sequential_total_s;
+        out->async_total_s = r.async_total_s;
+        out->warmup_s = r.warmup_s;
+        out->comm_total_s = r.comm_total_s;
+        out->speedup = r.speedup;
+        out->comm_ratio = r.comm_ratio;
+        out->approx_step_s = r.approx_step_s;
+        out->approx_total_s = r.approx_total_s;
+        for (size_t i = 0; i < r.round_compute_s.size(); ++i) {
+            if (round_compute_s) round_compute_s[i] = r.round_compute_s[i];
+            if (round_comm_s) round_comm_s[i] = r.round_comm_s[i];
+        }
+    });
+}
+
+int adx_calibrate_and_compare(const adx_plan* p, const double* delays, int n, const double* measured_round_comm_s,
+                              int n_rounds, int broadcast_count, double measured_total_s,
+                              adx_cost_comparison* out) {
+    return guard([&] {
+        need(p, "calibrate_and_compare");
+        need(out, "calibrate_and_compare");
+        const auto c = adx::calibrate_and_compare(p->p, std::vector<double>(delays, delays + n),
+                                                  std::vector<double>(measured_round_comm_s,
+                                                                      measured_round_comm_s + n_rounds),
+                                                  broadcast_count, measured_total_s);
+        out->predicted_total_s = c.predicted_total_s;
+        out->measured_total_s = c.measured_total_s;
+        out->rel_error_total = c.rel_error_total;
+        out->predicted_comm_ratio = c.predicted_comm_ratio;
+        out->measured_comm_ratio = c.measured_comm_ratio;
+        out->rel_error_comm_ratio = c.rel_error_comm_ratio;
+        out->calibrated_comm_cost_s = c.calibrated_comm_cost_s;
+    });
+}
+
+int adx_round_exchange_bytes(const adx_plan* p, const adx_partition* part, const adx_model* m, int precision,
+                             long long* out) {
+    return guard([&] {
+        need(p, "round_exchange_bytes");
+        need(part, "round_exchange_bytes");
+        need(m, "round_exchange_bytes");
+        const auto b = adx::round_exchange_bytes(p->p, part->p, m->m, adx::act_bytes(precision));
+        std::memcpy(out, b.data(), b.size() * sizeof(long long));
     });
 }
 

@@ -1,0 +1,158 @@
+"""§8(f) next rows: checkpoint and plan JSON formats (serialize.cpp), cost model
+(costsim.cpp, proj/tests/test_costsim.cpp), exchange bytes.  CPU only except
+the last two GPU tests."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2406_06911_b200 as adx
+from oracle import oracle as O
+
+
+def reference_checkpoint_json(m):
+    """serialize.cpp:226-250 restated: nlohmann dump(2) == sorted keys, indent 2."""
+    L = m.num_stages()
+    tensors, off = [], 0
+    shapes = [("time_embed.proj", m.time_embed_dim, m.time_embed_dim)]
+    for i, st in enumerate(m.stages, 1):
+        h, inn, out, E = st.hidden_width(), st.in_width(), st.out_width(), m.time_embed_dim
+        shapes += [(f"stage{i}.w1", h, inn), (f"stage{i}.b1", h, 1), (f"stage{i}.time_in", h, E),
+                   (f"stage{i}.w2", out, h), (f"stage{i}.b2", out, 1)]
+    for name, r, c in shapes:
+        tensors.append({"name": name, "rows": r, "cols": c, "offset_doubles": off})
+        off += r * c
+    meta = {"format": "asyncdiff-checkpoint-v1", "L": L, "widths": m.widths, "time_embed_dim": m.time_embed_dim,
+            "skip_links": [list(l) for l in m.skip_links], "tensors": tensors, "total_doubles": off,
+            "endianness": "little"}
+    return json.dumps(meta, indent=2, sort_keys=True) + "\n"
+
+
+def reference_blob(m):
+    parts = [m.proj]
+    for st in m.stages:
+        parts += [st.w1, st.b1, st.time_in, st.w2, st.b2]
+    return b"".join(np.ascontiguousarray(p, "<f8").tobytes() for p in parts)
+
+
+def test_checkpoint_bytes_match_reference_format(tmp_path):
+    m = adx.build_toy_denoiser(6, [2, 8, 6, 10, 6, 8, 2], "unet-mirror", 17)
+    base = str(tmp_path / "model")
+    adx.save_checkpoint(base, m)
+    assert open(base + ".json").read() == reference_checkpoint_json(m)
+    assert open(base + ".bin", "rb").read() == reference_blob(m)
+
+
+def test_checkpoint_roundtrip_and_foreign_writer(tmp_path):
+    m = adx.build_toy_denoiser(5, [4, 8, 8, 8, 8, 4], "unet-mirror", 3)
+    m.stages[1].b1[:] = np.linspace(-1, 1, 8)  # non-zero biases survive the trip
+    base = str(tmp_path / "a")
+    adx.save_checkpoint(base, m)
+    m2 = adx.load_checkpoint(base)
+    assert m2.widths == m.widths and m2.skip_links == m.skip_links
+    for a, b in zip(m.stages, m2.stages):
+        for name in ("w1", "b1", "time_in", "w2", "b2"):
+            assert np.array_equal(getattr(a, name), getattr(b, name))
+    # a checkpoint written by an independent restatement of the writer loads too
+    base2 = str(tmp_path / "b")
+    open(base2 + ".json", "w").write(reference_checkpoint_json(m))
+    open(base2 + ".bin", "wb").write(reference_blob(m))
+    m3 = adx.load_checkpoint(base2)
+    assert np.array_equal(m3.stages[1].b1, m.stages[1].b1)
+    open(base2 + ".bin", "wb").write(reference_blob(m)[:-8])
+    with pytest.raises(adx.AdxRuntimeError, match="truncated"):
+        adx.load_checkpoint(base2)
+    with pytest.raises(adx.AdxRuntimeError, match="cannot read"):
+        adx.load_checkpoint(str(tmp_path / "missing"))
+
+
+def reference_plan_json(plan):
+    """serialize.cpp:109-133 restated."""
+    rounds = []
+    for r in plan.rounds:
+        evals = []
+        for e in r.evals:
+            inp = ({"kind": "current-latent"} if e.input.kind == "latent" else
+                   {"kind": "cached", "segment": e.input.producer_segment, "round": e.input.producer_round})
+            je = {"segment": e.segment, "device": e.device, "embed_t": e.embed_t, "input": inp}
+            if e.emits_eps_for is not None:
+                je["emits_eps_for"] = e.emits_eps_for
+            evals.append(je)
+        rounds.append({"index": r.index, "evals": evals, "sampler_steps": r.sampler_steps, "broadcast": r.broadcast})
+    return json.dumps({"T": plan.T, "w": plan.w, "N": plan.N, "S": plan.S, "D": plan.D,
+                       "time_shift": plan.time_shift, "warmup_steps": plan.warmup_steps, "rounds": rounds},
+                      indent=2, sort_keys=True)
+
+
+@pytest.mark.parametrize("args", [(20, 1, 2, 1, False), (10, 2, 3, 2, True), (5, 5, 1, 1, False)])
+def test_plan_json_matches_reference_and_roundtrips(args):
+    plan = adx.plan_async(*args)
+    text = adx.plan_to_json(plan)
+    assert text == reference_plan_json(plan)
+    assert adx.plan_from_json(text) == plan
+
+
+def test_cost_model_worked_example():  # test_costsim.cpp:29-42 (G8)
+    plan = adx.plan_async(50, 1, 4, 1)
+    rep = adx.predict_async(plan, adx.CostModel([0.010] * 4, 0.001, 0.0))
+    assert rep.sequential_total_s == pytest.approx(2.0, rel=1e-12)
+    assert rep.async_total_s == pytest.approx(0.040 + 0.49 + 0.048, rel=1e-12)
+    assert rep.speedup == pytest.approx(2.0 / 0.578, rel=1e-9)
+    assert rep.approx_total_s == pytest.approx(0.040 + 49 * 0.011, rel=1e-12)
+
+
+def test_cost_model_properties():  # test_costsim.cpp:14-27, 44-70
+    for N in (2, 3, 4):
+        rep = adx.predict_async(adx.plan_async(1000, 1, N, 1), adx.CostModel([0.01] * N))
+        assert rep.speedup == pytest.approx(N, rel=0.01)
+    cm = adx.CostModel([0.010] * 3, 0.002)
+    r1 = adx.predict_async(adx.plan_async(50, 1, 3, 1), cm)
+    r2 = adx.predict_async(adx.plan_async(50, 1, 3, 2), cm)
+    assert r2.comm_total_s < 0.55 * r1.comm_total_s + 0.002 and r2.async_total_s < r1.async_total_s
+    for w in (1, 5, 20):
+        rep = adx.predict_async(adx.plan_async(20, w, 1, 1), adx.CostModel([0.013]))
+        assert rep.async_total_s == pytest.approx(adx.predict_sequential(20, adx.CostModel([0.013])), rel=1e-12)
+    with pytest.raises(adx.InvalidArgument):
+        adx.predict_async(adx.plan_async(20, 1, 3, 1), adx.CostModel([0.01] * 2))
+
+
+def test_calibrate_and_compare():  # costsim.cpp:52-79
+    plan = adx.plan_async(20, 1, 2, 1)
+    stats = adx.RunStats(round_comm_s=[0.001] * 19, broadcast_count=19, total_wall_s=0.01 * 2 + 19 * 0.011)
+    c = adx.calibrate_and_compare(plan, [0.01, 0.01], stats)
+    assert c.calibrated_comm_cost_s == pytest.approx(0.001)
+    assert c.predicted_total_s == pytest.approx(0.02 + 19 * 0.01 + 18 * 0.001)
+    assert c.rel_error_total < 0.01
+
+
+def test_round_exchange_bytes_and_bytes_aware_model():
+    m = adx.build_toy_denoiser(6, [2, 8, 8, 8, 8, 8, 2], "unet-mirror", 11)
+    plan, part = adx.plan_async(20, 1, 2, 1), adx.partition_balanced(m, 2)
+    b = adx.round_exchange_bytes(plan, part, m, "f64")
+    # stages 1, 2, 3 (skips (1,6), (2,5) and the boundary; (3,4) is the boundary itself) + eps
+    assert b[:-1] == [(3 * 8 + 2) * 8] * 18 and b[-1] == 2 * 8
+    cm = adx.CostModel([1e-4, 1e-4], comm_latency_s=5e-6, link_gbs=770.0)
+    rep = adx.predict_async(plan, cm, b)
+    assert rep.round_comm_s[0] == pytest.approx(5e-6 + 208 / 770e9)
+
+
+@pytest.mark.gpu
+def test_similarity_profile_on_gpu():  # metrics.cpp:73-101
+    m = adx.build_toy_denoiser(6, [2, 8, 8, 8, 8, 8, 2], "unet-mirror", 11)
+    s = adx.build_schedule(20, 0.01, 0.15)
+    seq = adx.sequential_denoise(m, adx.Latent(O.random_normals(12, 2), 20), s, precision="f64")
+    prof = adx.similarity_profile(m, adx.partition_balanced(m, 3), seq, s, precision="f64")
+    assert len(prof.cosine) == 2 and len(prof.pair_t) == 19
+    assert prof.median_cosine() > 0.9
+
+
+@pytest.mark.gpu
+def test_cmd_bench_style_calibration_on_gpu():  # experiment.cpp:391-455 with GPU sleeps
+    m = adx.build_toy_denoiser(6, [2, 8, 8, 8, 8, 8, 2], "unet-mirror", 11)
+    s = adx.build_schedule(12, 0.01, 0.15)
+    plan, part = adx.plan_async(12, 1, 2, 1), adx.partition_balanced(m, 2)
+    delays = [0.004, 0.004]
+    _, stats = adx.run_parallel(plan, adx.inject_delay(m, delays), part, adx.Latent(O.random_normals(12, 2), 12), s, 2)
+    c = adx.calibrate_and_compare(plan, delays, stats)
+    assert c.rel_error_total < 0.25
