@@ -279,6 +279,17 @@ int adx_rank_session_run(adx_rank_session* s, const double* x_T, double* traj_la
 int adx_rank_session_time(adx_rank_session* s, int iters, double* ms_per_run);
 int adx_rank_session_kernel_count(const adx_rank_session* s, int* n);
 
+/* --------------------------------- tcgen05 kernels of the UNet-shaped family
+ * (no reference function: builder-written oracle, SURVEY §8a extension list).
+ * A/B/X/Wt are bf16 bit patterns (uint16), outputs fp32.  iters > 0 also times
+ * `iters` back-to-back launches (CUDA events). */
+/* C[M x N] = act(A[M x K] . B[N x K]^T + bias); K % 64 == 0; bn in {0,32,64,128,256} */
+int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B,
+                const float* bias, int act, float* C, int bn, int iters, double* ms_per_iter);
+/* conv3x3 / stride 1 / pad 1, NHWC: X [batch][H][W][Cin], Wt [Cout][9*Cin] ((r*3+s)*Cin+ci) */
+int adx_tc_conv3x3(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X,
+                   const uint16_t* Wt, const float* bias, float* out, int iters, double* ms_per_iter);
+
 /* ------------------------------------------------------ §8(f) next rows */
 /* save_checkpoint / load_checkpoint: proj/include/asyncdiff/serialize.hpp:35-36,
  * serialize.cpp:226-308 (<base>.json metadata + <base>.bin row-major LE fp64) */

@@ -97,7 +97,7 @@ EXPORTS = [
     "adx_compare_trajectories", "adx_rank_program", "adx_nccl_unique_id", "adx_rank_session_create",
     "adx_rank_session_destroy", "adx_rank_session_run", "adx_rank_session_time", "adx_rank_session_kernel_count",
     "adx_model_save_checkpoint", "adx_model_load_checkpoint", "adx_plan_to_json", "adx_plan_from_json",
-    "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes",
+    "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes", "adx_tc_gemm", "adx_tc_conv3x3",
 ]
 
 
@@ -196,6 +196,9 @@ def lib():
         "adx_predict_async": (i, [vp, P(d), i, d, d, d, d, P(ll), P(adx_latency_report), P(d), P(d)]),
         "adx_calibrate_and_compare": (i, [vp, P(d), i, P(d), i, i, d, P(adx_cost_comparison)]),
         "adx_round_exchange_bytes": (i, [vp, vp, vp, i, P(ll)]),
+        "adx_tc_gemm": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), i, P(C.c_float), i, i, P(d)]),
+        "adx_tc_conv3x3": (i, [i, i, i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_float), i,
+                               P(d)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

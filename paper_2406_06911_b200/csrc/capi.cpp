@@ -7,6 +7,7 @@
 #include "extras.hpp"
 #include "host.hpp"
 #include "schedule.hpp"
+#include "tc_gemm.cuh"
 
 #include <cuda_runtime.h>
 
@@ -847,6 +848,75 @@ int adx_rank_session_kernel_count(const adx_rank_session* s, int* n) {
     return guard([&] {
         need(s, "rank_session_kernel_count");
         *n = adx::rank_session_kernels(const_cast<adx_rank_session*>(s));
+    });
+}
+
+// ------------------------------------------- tcgen05 GEMM / conv (UNet family)
+int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B, const float* bias, int act,
+                float* C, int bn, int iters, double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        DevBuf a(static_cast<size_t>(M) * K * 2), b(static_cast<size_t>(N) * K * 2), c(static_cast<size_t>(M) * N * 4),
+            bi(static_cast<size_t>(N) * 4);
+        CKC(cudaMemcpy(a.p, A, static_cast<size_t>(M) * K * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(b.p, B, static_cast<size_t>(N) * K * 2, cudaMemcpyHostToDevice));
+        if (bias) CKC(cudaMemcpy(bi.p, bias, static_cast<size_t>(N) * 4, cudaMemcpyHostToDevice));
+        adx::TcArgs p;
+        p.bias = bias ? static_cast<const float*>(bi.p) : nullptr;
+        p.act = act;
+        p.out_f32 = static_cast<float*>(c.p);
+        p.ldo = N;
+        adx::tc_gemm(a.p, b.p, M, N, K, p, 0, bn);
+        CKC(cudaDeviceSynchronize());
+        if (iters > 0 && ms_per_iter) {
+            cudaEvent_t e0, e1;
+            CKC(cudaEventCreate(&e0));
+            CKC(cudaEventCreate(&e1));
+            CKC(cudaEventRecord(e0));
+            for (int i = 0; i < iters; ++i) adx::tc_gemm(a.p, b.p, M, N, K, p, 0, bn);
+            CKC(cudaEventRecord(e1));
+            CKC(cudaEventSynchronize(e1));
+            float ms = 0;
+            CKC(cudaEventElapsedTime(&ms, e0, e1));
+            *ms_per_iter = ms / iters;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        if (C) CKC(cudaMemcpy(C, c.p, static_cast<size_t>(M) * N * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int adx_tc_conv3x3(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X, const uint16_t* Wt,
+                   const float* bias, float* out, int iters, double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        const size_t nx = static_cast<size_t>(batch) * H * W * Cin, nw = static_cast<size_t>(Cout) * 9 * Cin,
+                     no = static_cast<size_t>(batch) * H * W * Cout;
+        DevBuf x(nx * 2), w(nw * 2), o(no * 4), bi(static_cast<size_t>(Cout) * 4);
+        CKC(cudaMemcpy(x.p, X, nx * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(w.p, Wt, nw * 2, cudaMemcpyHostToDevice));
+        if (bias) CKC(cudaMemcpy(bi.p, bias, static_cast<size_t>(Cout) * 4, cudaMemcpyHostToDevice));
+        adx::TcArgs p;
+        p.bias = bias ? static_cast<const float*>(bi.p) : nullptr;
+        p.out_f32 = static_cast<float*>(o.p);
+        p.ldo = Cout;
+        adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, 0);
+        CKC(cudaDeviceSynchronize());
+        if (iters > 0 && ms_per_iter) {
+            cudaEvent_t e0, e1;
+            CKC(cudaEventCreate(&e0));
+            CKC(cudaEventCreate(&e1));
+            CKC(cudaEventRecord(e0));
+            for (int i = 0; i < iters; ++i) adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, 0);
+            CKC(cudaEventRecord(e1));
+            CKC(cudaEventSynchronize(e1));
+            float ms = 0;
+            CKC(cudaEventElapsedTime(&ms, e0, e1));
+            *ms_per_iter = ms / iters;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        if (out) CKC(cudaMemcpy(out, o.p, no * 4, cudaMemcpyDeviceToHost));
     });
 }
 

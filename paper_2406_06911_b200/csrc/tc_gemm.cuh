@@ -1,0 +1,34 @@
+// tc_gemm.cuh -- tcgen05 GEMM / implicit-GEMM conv3x3 (see tc_gemm.cu).
+#pragma once
+
+#include "host.hpp"
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace adx {
+
+// fused epilogue: out = scale * (act(acc + bias[n] + chan_add[img][n]) + residual[m][n])
+struct TcArgs {
+    // filled by the launcher
+    int M = 0, N = 0, k_blocks = 0;
+    int H = 0, W = 0, box_w = 0, box_h = 0, cin = 0;
+    // epilogue
+    const float* bias = nullptr;          // [N]
+    const float* chan_add = nullptr;      // [images][N] (e.g. time-embedding projection)
+    const __nv_bfloat16* residual = nullptr;
+    long long ldr = 0;
+    int act = 0;                          // 0 none, 1 SiLU (applied before the residual)
+    float out_scale = 1.0f;
+    __nv_bfloat16* out_bf16 = nullptr;    // exactly one of out_bf16 / out_f32
+    float* out_f32 = nullptr;
+    long long ldo = 0;
+};
+
+// D[M x N] = A[M x K] . B[N x K]^T (bf16 in, fp32 accumulate in TMEM); bn = 0 picks the tile width
+void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn = 0);
+// conv3x3 / stride 1 / pad 1 over NHWC bf16 X [batch][H][W][Cin], weights Wt [Cout][3*3*Cin]
+void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin, int Cout, TcArgs p,
+                cudaStream_t st, int bn = 0);
+
+}  // namespace adx

@@ -1,0 +1,80 @@
+"""tcgen05 GEMM and implicit-GEMM conv3x3 (UNet-family kernels) vs a plain
+fp32 PyTorch reference on the same bf16-representable inputs.  The kernel
+accumulates in fp32 (TMEM), so only summation order differs: tolerance 2e-3
+relative to the output scale."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2406_06911_b200 as adx
+from paper_2406_06911_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def bits_f32(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << 16).view(np.float32)
+
+
+P16 = C.POINTER(C.c_uint16)
+PF = C.POINTER(C.c_float)
+
+
+def run_gemm(A, B, bias=None, act=0, bn=0):
+    M, K = A.shape
+    N = B.shape[0]
+    out = np.zeros((M, N), np.float32)
+    ab, bb = bf16_bits(A), bf16_bits(B)
+    bias_p = None if bias is None else np.ascontiguousarray(bias, np.float32).ctypes.data_as(PF)
+    _lib.check(adx.lib().adx_tc_gemm(0, M, N, K, ab.ctypes.data_as(P16), bb.ctypes.data_as(P16), bias_p, act,
+                                     out.ctypes.data_as(PF), bn, 0, None))
+    ref = torch.from_numpy(bits_f32(ab)) @ torch.from_numpy(bits_f32(bb)).T
+    if bias is not None:
+        ref = ref + torch.from_numpy(np.asarray(bias, np.float32))
+    if act == 1:
+        ref = torch.nn.functional.silu(ref)
+    return out, ref.numpy()
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 128, 64, 0), (256, 320, 640, 0), (1000, 200, 128, 0),
+                                      (384, 512, 1024, 256), (130, 64, 192, 64), (128, 40, 64, 32)])
+def test_tc_gemm_matches_fp32_reference(M, N, K, bn):
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32) / np.sqrt(K)
+    out, ref = run_gemm(A, B, bn=bn)
+    err = np.abs(out - ref).max() / (np.abs(ref).max() + 1e-6)
+    assert err < 2e-3, err
+
+
+def test_tc_gemm_bias_silu_epilogue():
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((256, 128)).astype(np.float32)
+    B = rng.standard_normal((192, 128)).astype(np.float32) / 12.0
+    bias = rng.standard_normal(192).astype(np.float32)
+    out, ref = run_gemm(A, B, bias=bias, act=1)
+    assert np.abs(out - ref).max() / np.abs(ref).max() < 2e-3
+
+
+@pytest.mark.parametrize("batch,H,W,Cin,Cout", [(1, 16, 16, 64, 64), (2, 24, 24, 128, 192), (1, 12, 48, 64, 320)])
+def test_tc_conv3x3_matches_fp32_reference(batch, H, W, Cin, Cout):
+    rng = np.random.default_rng(batch * H + Cin)
+    X = rng.standard_normal((batch, H, W, Cin)).astype(np.float32)
+    Wt = (rng.standard_normal((Cout, 3, 3, Cin)) / np.sqrt(9 * Cin)).astype(np.float32)
+    bias = rng.standard_normal(Cout).astype(np.float32)
+    xb, wb = bf16_bits(X), bf16_bits(Wt)
+    out = np.zeros((batch, H, W, Cout), np.float32)
+    _lib.check(adx.lib().adx_tc_conv3x3(0, batch, H, W, Cin, Cout, xb.ctypes.data_as(P16), wb.ctypes.data_as(P16),
+                                        bias.ctypes.data_as(PF), out.ctypes.data_as(PF), 0, None))
+    xt = torch.from_numpy(bits_f32(xb)).permute(0, 3, 1, 2)  # NCHW
+    wt = torch.from_numpy(bits_f32(wb)).permute(0, 3, 1, 2)  # Cout, Cin, 3, 3
+    ref = torch.nn.functional.conv2d(xt, wt, torch.from_numpy(bias), padding=1).permute(0, 2, 3, 1).numpy()
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    assert err < 2e-3, err
