@@ -279,6 +279,28 @@ int adx_rank_session_run(adx_rank_session* s, const double* x_T, double* traj_la
 int adx_rank_session_time(adx_rank_session* s, int iters, double* ms_per_run);
 int adx_rank_session_kernel_count(const adx_rank_session* s, int* n);
 
+/* ------------------------------------------------------ UNet-shaped family
+ * A LayeredDenoiser whose stages are UNet blocks (conv_in, resnet[+spatial
+ * transformer], stride-2 down, nearest-2x up, mid, out) with the reference's
+ * mirror skip links as channel-concat skips.  The returned
+ * adx_model works with every partition / plan / engine / run entry point above
+ * (engine precision ADX_F32: bf16 tensor-core stages, fp32 latent and eps). */
+typedef struct {
+    int H, W, c_lat;
+    int n_levels;
+    int ch[8];
+    int attn[8];
+    int n_res, head_dim, ctx_len, ctx_dim, temb_dim, groups, mid_attn;
+    uint64_t seed;
+} adx_unet_spec;
+int adx_model_build_unet(const adx_unet_spec* spec, adx_model** out);
+/* kind (0 conv_in, 1 res, 2 down, 3 up, 4 out, 5 mid res), cin, cskip, cout, H, W, attn */
+int adx_unet_stage_info(const adx_model* m, int stage, int* info7);
+/* stage parameters (stage 0 = shared time-embedding MLP) for the builder-written oracle */
+int adx_unet_stage_params(const adx_model* m, int stage, char* names, int names_cap, int* shapes,
+                          int* n_params, float* data, long long data_cap, long long* n_data);
+int adx_unet_context(const adx_model* m, float* out /* ctx_len * ctx_dim */);
+
 /* --------------------------------- tcgen05 kernels of the UNet-shaped family
  * (no reference function: builder-written oracle, SURVEY §8a extension list).
  * A/B/X/Wt are bf16 bit patterns (uint16), outputs fp32.  iters > 0 also times

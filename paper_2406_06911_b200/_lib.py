@@ -98,7 +98,15 @@ EXPORTS = [
     "adx_rank_session_destroy", "adx_rank_session_run", "adx_rank_session_time", "adx_rank_session_kernel_count",
     "adx_model_save_checkpoint", "adx_model_load_checkpoint", "adx_plan_to_json", "adx_plan_from_json",
     "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes", "adx_tc_gemm", "adx_tc_conv3x3",
+    "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context",
 ]
+
+
+class adx_unet_spec(C.Structure):
+    _fields_ = [("H", C.c_int), ("W", C.c_int), ("c_lat", C.c_int), ("n_levels", C.c_int), ("ch", C.c_int * 8),
+                ("attn", C.c_int * 8), ("n_res", C.c_int), ("head_dim", C.c_int), ("ctx_len", C.c_int),
+                ("ctx_dim", C.c_int), ("temb_dim", C.c_int), ("groups", C.c_int), ("mid_attn", C.c_int),
+                ("seed", C.c_uint64)]
 
 
 class adx_latency_report(C.Structure):
@@ -196,6 +204,10 @@ def lib():
         "adx_predict_async": (i, [vp, P(d), i, d, d, d, d, P(ll), P(adx_latency_report), P(d), P(d)]),
         "adx_calibrate_and_compare": (i, [vp, P(d), i, P(d), i, i, d, P(adx_cost_comparison)]),
         "adx_round_exchange_bytes": (i, [vp, vp, vp, i, P(ll)]),
+        "adx_model_build_unet": (i, [P(adx_unet_spec), P(vp)]),
+        "adx_unet_stage_info": (i, [vp, i, P(i)]),
+        "adx_unet_stage_params": (i, [vp, i, C.c_char_p, i, P(i), P(i), P(C.c_float), ll, P(ll)]),
+        "adx_unet_context": (i, [vp, P(C.c_float)]),
         "adx_tc_gemm": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), i, P(C.c_float), i, i, P(d)]),
         "adx_tc_conv3x3": (i, [i, i, i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_float), i,
                                P(d)]),

@@ -33,7 +33,7 @@ __all__ = [
     "PRECISIONS", "Session", "time_model_pass", "RankSession", "nccl_unique_id", "save_checkpoint",
     "load_checkpoint", "plan_to_json", "plan_from_json", "CostModel", "LatencyReport", "predict_sequential",
     "predict_async", "CostComparison", "calibrate_and_compare", "round_exchange_bytes", "SimilarityProfile",
-    "similarity_profile",
+    "similarity_profile", "build_unet_denoiser", "unet_stage_info", "unet_stage_params", "unet_context",
 ]
 
 PRECISIONS = {"f64": 0, "f32": 1, "bf16": 2}
@@ -280,6 +280,64 @@ def make_denoiser_shell(L: int, widths: Sequence[int], skip_links: Sequence[Tupl
     h = C.c_void_p()
     check(lib().adx_model_shell(L, _ip(w), w.size, _ip(lk), len(skip_links), time_embed_dim, C.byref(h)))
     return LayeredDenoiser(h.value)
+
+
+UNET_KINDS = {0: "conv_in", 1: "res", 2: "down", 3: "up", 4: "out", 5: "mid_res"}
+
+
+def build_unet_denoiser(H: int = 96, W: int = 96, c_lat: int = 4, ch: Sequence[int] = (320, 640, 1280, 1280),
+                        attn: Sequence[int] = (1, 1, 1, 0), n_res: int = 2, head_dim: int = 64, ctx_len: int = 77,
+                        ctx_dim: int = 1024, temb_dim: int = 1280, groups: int = 32, mid_attn: int = 1,
+                        seed: int = 0) -> LayeredDenoiser:
+    """UNet-shaped denoiser behind the reference's stage contract (defaults: the
+    SD-2.1 UNet topology at a 96x96x4 latent, random init).  Works with every
+    partition / plan / run entry point; engine precision must be "f32"."""
+    from ._lib import adx_unet_spec
+    s = adx_unet_spec()
+    s.H, s.W, s.c_lat, s.n_levels = H, W, c_lat, len(ch)
+    for i, (c, a) in enumerate(zip(ch, attn)):
+        s.ch[i], s.attn[i] = c, int(a)
+    s.n_res, s.head_dim, s.ctx_len, s.ctx_dim = n_res, head_dim, ctx_len, ctx_dim
+    s.temb_dim, s.groups, s.mid_attn, s.seed = temb_dim, groups, int(mid_attn), seed
+    h = C.c_void_p()
+    check(lib().adx_model_build_unet(C.byref(s), C.byref(h)))
+    m = LayeredDenoiser(h.value)
+    m.unet_spec = dict(H=H, W=W, c_lat=c_lat, ch=list(ch), attn=list(attn), n_res=n_res, head_dim=head_dim,
+                       ctx_len=ctx_len, ctx_dim=ctx_dim, temb_dim=temb_dim, groups=groups, mid_attn=mid_attn,
+                       seed=seed)
+    return m
+
+
+def unet_stage_info(m: LayeredDenoiser, stage: int) -> dict:
+    buf = np.zeros(7, np.int32)
+    check(lib().adx_unet_stage_info(m._h, stage, _ip(buf)))
+    k, cin, cskip, cout, H, W, at = buf.tolist()
+    return dict(kind=UNET_KINDS[k], cin=cin, cskip=cskip, cout=cout, H=H, W=W, attn=at)
+
+
+def unet_stage_params(m: LayeredDenoiser, stage: int) -> Dict[str, np.ndarray]:
+    """fp32 parameters of one UNet stage (0 = shared time-embedding MLP)."""
+    n, nd = C.c_int(), C.c_longlong()
+    check(lib().adx_unet_stage_params(m._h, stage, None, 0, None, C.byref(n), None, 0, C.byref(nd)))
+    names = C.create_string_buffer(64 * n.value + 64)
+    shapes = np.zeros(2 * n.value + 2, np.int32)
+    data = np.zeros(max(nd.value, 1), np.float32)
+    check(lib().adx_unet_stage_params(m._h, stage, names, len(names), _ip(shapes), C.byref(n),
+                                      data.ctypes.data_as(C.POINTER(C.c_float)), data.size, C.byref(nd)))
+    out, pos = {}, 0
+    for i, name in enumerate(names.value.decode().split("\n")):
+        r, c = int(shapes[2 * i]), int(shapes[2 * i + 1])
+        cnt = r * (c if c else 1)
+        out[name] = data[pos:pos + cnt].reshape((r, c) if c else (r,)).copy()
+        pos += cnt
+    return out
+
+
+def unet_context(m: LayeredDenoiser) -> np.ndarray:
+    sp = m.unet_spec
+    out = np.zeros(sp["ctx_len"] * sp["ctx_dim"], np.float32)
+    check(lib().adx_unet_context(m._h, out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out.reshape(sp["ctx_len"], sp["ctx_dim"])
 
 
 def sinusoid(t: int, dim: int) -> np.ndarray:

@@ -8,6 +8,7 @@
 #include "host.hpp"
 #include "schedule.hpp"
 #include "tc_gemm.cuh"
+#include "unet.hpp"
 
 #include <cuda_runtime.h>
 
@@ -848,6 +849,76 @@ int adx_rank_session_kernel_count(const adx_rank_session* s, int* n) {
     return guard([&] {
         need(s, "rank_session_kernel_count");
         *n = adx::rank_session_kernels(const_cast<adx_rank_session*>(s));
+    });
+}
+
+// ------------------------------------------------------ UNet-shaped family
+int adx_model_build_unet(const adx_unet_spec* s, adx_model** out) {
+    return guard([&] {
+        need(s, "build_unet");
+        if (s->n_levels < 1 || s->n_levels > 8) throw std::invalid_argument("build_unet: 1..8 levels");
+        adx::UNetSpec sp;
+        sp.H = s->H;
+        sp.W = s->W;
+        sp.c_lat = s->c_lat;
+        sp.ch.assign(s->ch, s->ch + s->n_levels);
+        sp.attn.assign(s->attn, s->attn + s->n_levels);
+        sp.n_res = s->n_res;
+        sp.head_dim = s->head_dim;
+        sp.ctx_len = s->ctx_len;
+        sp.ctx_dim = s->ctx_dim;
+        sp.temb_dim = s->temb_dim;
+        sp.groups = s->groups;
+        sp.mid_attn = s->mid_attn;
+        sp.seed = s->seed;
+        *out = new adx_model{adx::build_unet_model(sp)};
+    });
+}
+
+int adx_unet_stage_info(const adx_model* m, int stage, int* info /* kind, cin, cskip, cout, H, W, attn */) {
+    return guard([&] {
+        need(m, "unet_stage_info");
+        if (m->m.kind != 1) throw std::invalid_argument("unet_stage_info: not a UNet model");
+        const adx::UStage& s = m->m.unet->st.at(stage - 1);
+        const int v[7] = {s.kind, s.cin, s.cskip, s.cout, s.H, s.W, s.attn};
+        std::memcpy(info, v, sizeof v);
+    });
+}
+
+// parameters of a stage (0 = shared time-embedding MLP): names '\n'-joined,
+// shapes as (rows, cols) pairs (cols = 0 for vectors), data concatenated fp32
+int adx_unet_stage_params(const adx_model* m, int stage, char* names, int names_cap, int* shapes, int* n_params,
+                          float* data, long long data_cap, long long* n_data) {
+    return guard([&] {
+        need(m, "unet_stage_params");
+        if (m->m.kind != 1) throw std::invalid_argument("unet_stage_params: not a UNet model");
+        const auto ps = adx::unet_stage_params(*m->m.unet, stage);
+        std::string joined;
+        long long total = 0;
+        for (size_t i = 0; i < ps.size(); ++i) {
+            joined += (i ? "\n" : "") + ps[i].name;
+            if (shapes) {
+                shapes[2 * i] = ps[i].shape[0];
+                shapes[2 * i + 1] = ps[i].shape.size() > 1 ? ps[i].shape[1] : 0;
+            }
+            if (data && total + static_cast<long long>(ps[i].data.size()) <= data_cap)
+                std::memcpy(data + total, ps[i].data.data(), ps[i].data.size() * sizeof(float));
+            total += static_cast<long long>(ps[i].data.size());
+        }
+        if (names && names_cap > 0) {
+            std::strncpy(names, joined.c_str(), names_cap - 1);
+            names[names_cap - 1] = 0;
+        }
+        *n_params = static_cast<int>(ps.size());
+        *n_data = total;
+    });
+}
+
+int adx_unet_context(const adx_model* m, float* out) {
+    return guard([&] {
+        need(m, "unet_context");
+        if (m->m.kind != 1) throw std::invalid_argument("unet_context: not a UNet model");
+        std::memcpy(out, m->m.unet->ctx.data(), m->m.unet->ctx.size() * sizeof(float));
     });
 }
 

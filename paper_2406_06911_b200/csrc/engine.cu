@@ -1,6 +1,8 @@
 // engine.cu -- device-resident AsyncDiff executor (see engine.hpp).
 #include "engine.hpp"
 
+#include "unet_dev.hpp"
+
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -99,9 +101,26 @@ Engine::Engine(const Model& m, int prec, std::vector<int> ordinals)
         dev_[i].ordinal = ordinals_[i];
         dev_[i].stages.resize(model_.L);
     }
+    if (model_.kind == 1 && prec_ != kF32)
+        throw std::invalid_argument("engine: the UNet family runs bf16 tensor-core stages with an f32 trajectory "
+                                    "(precision f32)");
+    unet_.resize(ordinals_.size());
+}
+
+UNetDevice& Engine::unet(int idx) {
+    auto& u = unet_[idx % unet_.size()];
+    if (!u) {
+        CK(cudaSetDevice(ordinal(idx)));
+        u = std::make_shared<UNetDevice>(model_, ordinal(idx));
+    }
+    return *u;
 }
 
 Engine::~Engine() {
+    for (size_t i = 0; i < unet_.size(); ++i) {
+        cudaSetDevice(ordinals_[i]);
+        unet_[i].reset();
+    }
     for (auto& d : dev_) {
         cudaSetDevice(d.ordinal);
         for (auto& s : d.stages) {
@@ -123,6 +142,10 @@ size_t Engine::stage_weight_bytes(int stage) const {
 const DevStage& Engine::stage_on(int idx, int stage) {
     DevShared& d = dev_[idx % dev_.size()];
     DevStage& ds = d.stages[stage - 1];
+    if (model_.kind == 1) {
+        unet(idx).ensure_stage(stage);
+        return ds;
+    }
     if (ds.w1) return ds;
     CK(cudaSetDevice(d.ordinal));
     const Stage& st = model_.stages[stage - 1];
@@ -137,6 +160,7 @@ const DevStage& Engine::stage_on(int idx, int stage) {
 // e_t table and per-stage bias tables c_t = b1 + Tin . e_t for t in [0, T]
 // (the time term of denoiser.cpp:182, hoisted out of the hot loop).
 void Engine::ensure_tables(int idx, int T) {
+    if (model_.kind == 1) unet(idx).ensure_tables(T);
     DevShared& d = dev_[idx % dev_.size()];
     CK(cudaSetDevice(d.ordinal));
     const int E = model_.E;
@@ -183,12 +207,18 @@ int Engine::enqueue_stage(int idx, int stage, const std::vector<Seg>& inputs, in
                           int* bad, int key, cudaStream_t stream, bool pdl) {
     const Stage& st = model_.stages[stage - 1];
     const DevStage& ds = dev_[idx % dev_.size()].stages[stage - 1];
-    if (!ds.w1 || ds.ctab_T < embed_t) throw std::logic_error("engine: stage weights/tables not resident");
     int K = 0;
     for (auto& s : inputs) K += s.n;
     if (K != st.in)
         throw std::runtime_error("eval: stage " + std::to_string(stage) + " input width " + std::to_string(K) +
                                  " != expected " + std::to_string(st.in));
+    if (model_.kind == 1) {  // UNet-shaped family: tcgen05 conv / GEMM stage program
+        std::vector<Seg> in = inputs;
+        if (stage == 1) in.resize(1);  // latent only (the shared e_t segment is not used)
+        unet(idx).enqueue(stage, in, embed_t, y, prec_ == kF64, stream);
+        return 1;
+    }
+    if (!ds.w1 || ds.ctab_T < embed_t) throw std::logic_error("engine: stage weights/tables not resident");
     if (static_cast<int>(inputs.size()) > kMaxSegs)
         throw std::invalid_argument("eval: stage " + std::to_string(stage) + " has too many concat inputs");
     GemvArgs a1 = {};
@@ -467,7 +497,7 @@ void Session::alloc_buffers() {
                 E_->stage_on(v.idx, i);
                 if (i < L) need.insert(i);
                 void* h = nullptr;
-                CK(cudaMalloc(&h, static_cast<size_t>(m.widths[i]) * ab_bytes_));
+                CK(cudaMalloc(&h, static_cast<size_t>(std::max(m.widths[i], 1)) * E_->stage_bytes()));
                 v.H[i] = h;
                 for (auto& l : m.links_into(i))
                     if (stage_seg_[l.first] != seg) need.insert(l.first);
@@ -478,8 +508,8 @@ void Session::alloc_buffers() {
         for (int p : need) {
             std::array<void*, 2> y{};
             for (int s = 0; s < 2; ++s) {
-                CK(cudaMalloc(&y[s], static_cast<size_t>(m.widths[p]) * ab_bytes_));
-                CK(cudaMemset(y[s], 0, static_cast<size_t>(m.widths[p]) * ab_bytes_));
+                CK(cudaMalloc(&y[s], static_cast<size_t>(m.widths[p]) * E_->stage_bytes()));
+                CK(cudaMemset(y[s], 0, static_cast<size_t>(m.widths[p]) * E_->stage_bytes()));
             }
             v.Y[p] = y;
         }
@@ -582,7 +612,7 @@ void Session::enqueue_transfers(VDev& v, int seg, int slot, int eps_step) {
     for (auto& [p, c] : xfers) {
         VDev& cv = vd_[c];
         if (cv.read_rec[slot] && waited.insert(c).second) CK(cudaStreamWaitEvent(v.comm, cv.read_done[slot], 0));
-        const size_t bytes = static_cast<size_t>(m.widths[p]) * ab_bytes_;
+        const size_t bytes = static_cast<size_t>(m.widths[p]) * E_->stage_bytes();
         if (cv.ordinal == v.ordinal)
             CK(cudaMemcpyAsync(cv.Y.at(p)[slot], v.Y.at(p)[slot], bytes, cudaMemcpyDeviceToDevice, v.comm));
         else

@@ -80,12 +80,16 @@ public:
     // the launching stream), mean over `iters` back-to-back passes.  Used for the
     // HBM roofline of the stage GEMV kernel.
     double time_eval_ms(int idx, int t_embed, int iters, int* launches);
+    // element size of stage outputs (bf16 for the UNet family, the activation dtype otherwise)
+    int stage_bytes() const { return model_.kind == 1 ? 2 : act_bytes(prec_); }
 
 private:
+    class UNetDevice& unet(int idx);
     Model model_;
     int prec_;
     std::vector<int> ordinals_;
     std::vector<DevShared> dev_;
+    std::vector<std::shared_ptr<class UNetDevice>> unet_;
 };
 
 struct RunOptions {

@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <optional>
 #include <random>
 #include <stdexcept>
@@ -54,7 +55,11 @@ struct Stage {
     long long cost_macs = 0;
 };
 
+struct UNetDesc;  // unet.hpp
+
 struct Model {
+    int kind = 0;                          // 0: reference MLP stages, 1: UNet-shaped family
+    std::shared_ptr<const UNetDesc> unet;  // kind 1 only
     int L = 0;
     int E = 0;
     std::vector<int> widths;                      // L+1

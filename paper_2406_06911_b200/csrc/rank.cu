@@ -201,7 +201,7 @@ private:
                 E_->stage_on(0, i);
                 if (i < m.L) need.insert(i);
                 void* h = nullptr;
-                CKR(cudaMalloc(&h, static_cast<size_t>(m.widths[i]) * ab_bytes_));
+                CKR(cudaMalloc(&h, static_cast<size_t>(std::max(m.widths[i], 1)) * E_->stage_bytes()));
                 H_[i] = h;
                 for (auto& l : m.links_into(i))
                     if (stage_seg_[l.first] != seg) need.insert(l.first);
@@ -212,8 +212,8 @@ private:
         for (int p : need) {
             std::array<void*, 2> y{};
             for (int s = 0; s < 2; ++s) {
-                CKR(cudaMalloc(&y[s], static_cast<size_t>(m.widths[p]) * ab_bytes_));
-                CKR(cudaMemset(y[s], 0, static_cast<size_t>(m.widths[p]) * ab_bytes_));
+                CKR(cudaMalloc(&y[s], static_cast<size_t>(m.widths[p]) * E_->stage_bytes()));
+                CKR(cudaMemset(y[s], 0, static_cast<size_t>(m.widths[p]) * E_->stage_bytes()));
             }
             Y_[p] = y;
         }
@@ -285,12 +285,16 @@ private:
                     break;
                 case kOpSend: {
                     const void* src = op.stage < 0 ? EPS_[op.slot] : Y_.at(op.stage)[op.slot];
-                    CKN(nccl().Send(src, op.elems * ab_bytes_, ncclInt8, op.peer, comm_, cstr_), "ncclSend");
+                    CKN(nccl().Send(src, op.elems * (op.stage < 0 ? ab_bytes_ : E_->stage_bytes()), ncclInt8,
+                                    op.peer, comm_, cstr_),
+                        "ncclSend");
                     break;
                 }
                 case kOpRecv: {
                     void* dst = op.stage < 0 ? off_m(traj_eps_, op.step * row) : Y_.at(op.stage)[op.slot];
-                    CKN(nccl().Recv(dst, op.elems * ab_bytes_, ncclInt8, op.peer, comm_, cstr_), "ncclRecv");
+                    CKN(nccl().Recv(dst, op.elems * (op.stage < 0 ? ab_bytes_ : E_->stage_bytes()), ncclInt8,
+                                    op.peer, comm_, cstr_),
+                        "ncclRecv");
                     break;
                 }
                 case kOpEnd:

@@ -219,6 +219,10 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
             const int hh = h0 + row / p.box_w, ww = w0 + row % p.box_w;
             valid = hh < p.H && ww < p.W;
             m = (static_cast<long long>(img) * p.H + hh) * p.W + ww;
+            if (p.sub2) {  // stride-2 conv: keep even pixels, write the half-resolution grid
+                valid = valid && !(hh & 1) && !(ww & 1);
+                m = (static_cast<long long>(img) * (p.H / 2) + hh / 2) * (p.W / 2) + ww / 2;
+            }
         } else {
             m = static_cast<long long>(tile_m) * BM + row;
             valid = m < p.M;
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const int n = n0 + c + j;
-                if (n >= p.N) continue;
+                if (n >= (p.n_store ? p.n_store : p.N)) continue;
                 float x = v[j];
                 if (p.bias) x += p.bias[n];
                 if (p.chan_add) x += p.chan_add[static_cast<long long>(img) * p.N + n];
@@ -313,14 +317,21 @@ int pick_bn(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; 
 
 // D = A[M x K] . B[N x K]^T ; A, B bf16 row-major (K contiguous), K % 64 == 0
 void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn) {
+    tc_gemm_strided(A, K, B, K, M, N, K, p, st, bn);
+}
+
+void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,
+                     cudaStream_t st, int bn) {
     if (K % BK) throw std::invalid_argument("tc_gemm: K must be a multiple of 64");
+    if ((lda | ldb) % 8) throw std::invalid_argument("tc_gemm: row strides must be multiples of 8 elements");
     if (bn == 0) bn = pick_bn(N);
     const cuuint64_t da[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
-    const cuuint64_t sa_[1] = {static_cast<cuuint64_t>(K) * 2};
+    const cuuint64_t sa_[1] = {static_cast<cuuint64_t>(lda) * 2};
+    const cuuint64_t sb_[1] = {static_cast<cuuint64_t>(ldb) * 2};
     const cuuint32_t ba[2] = {BK, BM};
     const cuuint64_t db[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N)};
     const cuuint32_t bb[2] = {BK, static_cast<cuuint32_t>(bn)};
-    const CUtensorMap ma = make_map(A, 2, da, sa_, ba), mb = make_map(B, 2, db, sa_, bb);
+    const CUtensorMap ma = make_map(A, 2, da, sa_, ba), mb = make_map(B, 2, db, sb_, bb);
     p.M = M;
     p.N = N;
     p.k_blocks = K / BK;
@@ -336,7 +347,7 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
                 cudaStream_t st, int bn) {
     if (Cin % BK) throw std::invalid_argument("tc_conv3x3: Cin must be a multiple of 64");
     int bw = 0;
-    for (int c : {128, 64, 32, 16, 8})
+    for (int c : {128, 64, 32, 16, 8, 4})
         if (W % c == 0 && c <= W && BM % c == 0) {
             bw = c;
             break;

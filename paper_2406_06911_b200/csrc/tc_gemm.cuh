@@ -23,10 +23,15 @@ struct TcArgs {
     __nv_bfloat16* out_bf16 = nullptr;    // exactly one of out_bf16 / out_f32
     float* out_f32 = nullptr;
     long long ldo = 0;
+    int sub2 = 0;                         // conv: write only even (h, w) at (h/2, w/2) -> stride-2 conv
+    int n_store = 0;                      // store only the first n_store columns (0: all N)
 };
 
 // D[M x N] = A[M x K] . B[N x K]^T (bf16 in, fp32 accumulate in TMEM); bn = 0 picks the tile width
 void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn = 0);
+// same with explicit row strides (elements; multiples of 8) -- e.g. one head's slice of a packed QKV
+void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,
+                     cudaStream_t st, int bn = 0);
 // conv3x3 / stride 1 / pad 1 over NHWC bf16 X [batch][H][W][Cin], weights Wt [Cout][3*3*Cin]
 void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin, int Cout, TcArgs p,
                 cudaStream_t st, int bn = 0);

@@ -1,0 +1,364 @@
+// unet_dev.cu -- device side of the UNet-shaped family: per-GPU parameters,
+// per-t channel-add tables, cross-attention K/V precomputed from the fixed
+// context, scratch per stream, and the per-stage enqueue (resnet / spatial
+// transformer / down / up / in / out) on the tcgen05 GEMM + conv kernels.
+#include "unet_dev.hpp"
+
+#include "tc_gemm.cuh"
+#include "unet_kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace adx {
+
+#define CKD(x)                                                                                   \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess)                                                                   \
+            throw cuda_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x); \
+    } while (0)
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+uint16_t to_bf16_bits(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return static_cast<uint16_t>(u >> 16);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+void* upload_bf16(const std::vector<float>& v) {
+    std::vector<uint16_t> h(v.size());
+    for (size_t i = 0; i < v.size(); ++i) h[i] = to_bf16_bits(v[i]);
+    void* d = nullptr;
+    CKD(cudaMalloc(&d, std::max<size_t>(h.size(), 8) * 2));
+    CKD(cudaMemcpy(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+    return d;
+}
+
+void* upload_f32(const std::vector<float>& v) {
+    void* d = nullptr;
+    CKD(cudaMalloc(&d, std::max<size_t>(v.size(), 8) * 4));
+    CKD(cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+    return d;
+}
+
+int pad64(int n) { return (n + 63) / 64 * 64; }
+
+}  // namespace
+
+UNetDevice::UNetDevice(const Model& m, int ordinal) : m_(m), d_(*m.unet), ordinal_(ordinal) {
+    st_.resize(m.L + 1);
+}
+
+UNetDevice::~UNetDevice() {
+    cudaSetDevice(ordinal_);
+    for (auto& s : st_) {
+        for (auto& kv : s.p) cudaFree(kv.second);
+        cudaFree(s.chan_add);
+        cudaFree(s.k2);
+        cudaFree(s.vt2);
+    }
+    for (auto& kv : scratch_) {
+        UScratch& s = kv.second;
+        for (void* p : {static_cast<void*>(s.a), static_cast<void*>(s.b), static_cast<void*>(s.c),
+                        static_cast<void*>(s.r), static_cast<void*>(s.qkv), static_cast<void*>(s.att),
+                        static_cast<void*>(s.ff), static_cast<void*>(s.ff2), static_cast<void*>(s.P),
+                        static_cast<void*>(s.VT), static_cast<void*>(s.S), static_cast<void*>(s.gn)})
+            cudaFree(p);
+    }
+}
+
+long long UNetDevice::param_bytes(int stage) const {
+    long long b = 0;
+    for (auto& kv : st_[stage].bytes) b += kv.second;
+    return b;
+}
+
+void UNetDevice::ensure_stage(int stage) {
+    UDevStage& ds = st_[stage];
+    if (ds.ready) return;
+    CKD(cudaSetDevice(ordinal_));
+    const UNetSpec& sp = d_.spec;
+    auto ps = unet_stage_params(d_, stage);
+    for (auto& p : ps) {
+        const bool matrix = p.shape.size() == 2;
+        if (p.name == "tf.k2.w" || p.name == "tf.v2.w" || p.name == "temb.w" || p.name == "temb.b") continue;
+        ds.p[p.name] = matrix ? upload_bf16(p.data) : upload_f32(p.data);
+        ds.bytes[p.name] = static_cast<long long>(p.data.size()) * (matrix ? 2 : 4);
+    }
+    const UStage& s = d_.st[stage - 1];
+    if (s.attn) {
+        // cross-attention K2 = ctx . Wk2^T, V2 = ctx . Wv2^T are constant per run:
+        // precompute once (fp32), pad the context length to a multiple of 64
+        const int C = s.cout, Lc = sp.ctx_len, Lp = pad64(Lc), Dc = sp.ctx_dim;
+        const std::vector<float>* wk = nullptr;
+        const std::vector<float>* wv = nullptr;
+        for (auto& p : ps) {
+            if (p.name == "tf.k2.w") wk = &p.data;
+            if (p.name == "tf.v2.w") wv = &p.data;
+        }
+        std::vector<float> k2(static_cast<size_t>(Lp) * C, 0.f), vt2(static_cast<size_t>(C) * Lp, 0.f);
+        for (int l = 0; l < Lc; ++l)
+            for (int c = 0; c < C; ++c) {
+                float ak = 0.f, av = 0.f;
+                for (int k = 0; k < Dc; ++k) {
+                    const float x = d_.ctx[static_cast<size_t>(l) * Dc + k];
+                    ak += (*wk)[static_cast<size_t>(c) * Dc + k] * x;
+                    av += (*wv)[static_cast<size_t>(c) * Dc + k] * x;
+                }
+                k2[static_cast<size_t>(l) * C + c] = ak;
+                vt2[static_cast<size_t>(c) * Lp + l] = av;
+            }
+        ds.k2 = static_cast<bf16*>(upload_bf16(k2));
+        ds.vt2 = static_cast<bf16*>(upload_bf16(vt2));
+    }
+    ds.ready = true;
+}
+
+void UNetDevice::ensure_tables(int T) {
+    CKD(cudaSetDevice(ordinal_));
+    std::vector<std::vector<float>> temb;
+    for (int stage = 1; stage <= m_.L; ++stage) {
+        UDevStage& ds = st_[stage];
+        const UStage& s = d_.st[stage - 1];
+        if (!ds.ready || ds.chan_T >= T || (s.kind != kRes && s.kind != kMidRes)) continue;
+        if (temb.empty())
+            for (int t = 0; t <= T; ++t) temb.push_back(unet_temb(d_, t));
+        const auto ps = unet_stage_params(d_, stage);
+        std::vector<float> flat;
+        for (int t = 0; t <= T; ++t) {
+            const auto ca = unet_chan_add(ps, temb[t]);
+            flat.insert(flat.end(), ca.begin(), ca.end());
+        }
+        cudaFree(ds.chan_add);
+        ds.chan_add = static_cast<float*>(upload_f32(flat));
+        ds.chan_T = T;
+    }
+}
+
+UScratch& UNetDevice::scratch(cudaStream_t st) {
+    auto it = scratch_.find(st);
+    if (it != scratch_.end()) return it->second;
+    CKD(cudaSetDevice(ordinal_));
+    const UNetSpec& sp = d_.spec;
+    size_t act = 0, qkv = 0, ff = 0, S = 0, vt = 0, gn = 0;
+    for (const UStage& s : d_.st) {
+        const size_t hw = static_cast<size_t>(s.H) * s.W;
+        act = std::max({act, hw * (s.cin + s.cskip), static_cast<size_t>(s.Ho()) * s.Wo() * s.cout, hw * 64,
+                        4 * hw * s.cin});
+        gn = std::max({gn, group_norm_scratch_bytes(1, static_cast<int>(4 * hw), sp.groups)});
+        if (s.attn) {
+            const size_t L = hw, Lp = pad64(static_cast<int>(L));
+            qkv = std::max(qkv, L * 3 * s.cout);
+            ff = std::max(ff, L * 8 * s.cout);
+            S = std::max(S, L * std::max(Lp, static_cast<size_t>(pad64(sp.ctx_len))));
+            vt = std::max(vt, 64 * Lp);
+        }
+    }
+    UScratch s;
+    auto al = [](size_t bytes) {
+        void* p = nullptr;
+        CKD(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+        return p;
+    };
+    s.a = static_cast<bf16*>(al(act * 2));
+    s.b = static_cast<bf16*>(al(act * 2));
+    s.c = static_cast<bf16*>(al(act * 2));
+    s.r = static_cast<bf16*>(al(act * 2));
+    s.qkv = static_cast<bf16*>(al(qkv * 2));
+    s.att = static_cast<bf16*>(al(act * 2));
+    s.ff = static_cast<bf16*>(al(ff * 2));
+    s.ff2 = static_cast<bf16*>(al(ff * 2));
+    s.P = static_cast<bf16*>(al(S * 2));
+    s.S = static_cast<float*>(al(S * 4));
+    s.VT = static_cast<bf16*>(al(vt * 2));
+    s.gn = static_cast<float2*>(al(gn));
+    return scratch_.emplace(st, s).first->second;
+}
+
+const void* UNetDevice::P(int stage, const char* name) const {
+    auto it = st_[stage].p.find(name);
+    if (it == st_[stage].p.end()) throw std::logic_error(std::string("unet: missing parameter ") + name);
+    return it->second;
+}
+const float* UNetDevice::F(int stage, const char* name) const { return static_cast<const float*>(P(stage, name)); }
+
+// multi-head attention out[L x C] = softmax(q k^T / 8) v, one head (64) at a time;
+// v_t != nullptr: pre-transposed values [C x Lkp] (cross attention)
+void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16* k, long long ldk, const bf16* v,
+                           long long ldv, const bf16* v_t, int L, int Lk, int C, bf16* out, cudaStream_t st) {
+    const int Lkp = pad64(Lk);
+    for (int h = 0; h < C / 64; ++h) {
+        TcArgs a;
+        a.out_f32 = s.S;
+        a.ldo = Lkp;
+        a.out_scale = 0.125f;  // 1/sqrt(64)
+        tc_gemm_strided(q + h * 64, ldq, k + h * 64, ldk, L, Lk, 64, a, st);
+        softmax_rows(s.S, Lkp, L, Lk, s.P, Lkp, Lkp, st);
+        const bf16* vt = v_t ? v_t + static_cast<long long>(h) * 64 * Lkp : s.VT;
+        if (!v_t) transpose_head(v + h * 64, ldv, Lk, Lkp, 64, s.VT, st);
+        TcArgs o;
+        o.out_bf16 = out + h * 64;
+        o.ldo = C;
+        tc_gemm(s.P, vt, L, 64, Lkp, o, st);
+    }
+}
+
+// SpatialTransformer: GN -> proj_in -> [LN self-attn] -> [LN cross-attn] -> [LN GEGLU FF] -> proj_out + x
+void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16* y, cudaStream_t st) {
+    UScratch& s = scratch(st);
+    const UNetSpec& sp = d_.spec;
+    const int L = H * W;
+    Cat2 xc{x, C, nullptr, 0};
+    group_norm(xc, 1, L, sp.groups, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"), 1e-6f, 0, s.a, s.gn, st);
+    TcArgs pi;
+    pi.bias = F(stage, "tf.proj_in.b");
+    pi.out_bf16 = s.b;
+    pi.ldo = C;
+    tc_gemm(s.a, P(stage, "tf.proj_in.w"), L, C, C, pi, st);  // h = s.b
+    // self attention
+    layer_norm(s.b, L, C, F(stage, "tf.ln1.gamma"), F(stage, "tf.ln1.beta"), 1e-5f, s.a, st);
+    TcArgs qk;
+    qk.out_bf16 = s.qkv;
+    qk.ldo = 3 * C;
+    tc_gemm(s.a, P(stage, "tf.qkv.w"), L, 3 * C, C, qk, st);
+    attention(s, s.qkv, 3 * C, s.qkv + C, 3 * C, s.qkv + 2 * C, 3 * C, nullptr, L, L, C, s.att, st);
+    TcArgs o1;
+    o1.bias = F(stage, "tf.o1.b");
+    o1.residual = s.b;
+    o1.ldr = C;
+    o1.out_bf16 = s.b;  // in place: each element is read and written by one epilogue thread
+    o1.ldo = C;
+    tc_gemm(s.att, P(stage, "tf.o1.w"), L, C, C, o1, st);
+    // cross attention against the fixed context
+    layer_norm(s.b, L, C, F(stage, "tf.ln2.gamma"), F(stage, "tf.ln2.beta"), 1e-5f, s.a, st);
+    TcArgs q2;
+    q2.out_bf16 = s.qkv;
+    q2.ldo = C;
+    tc_gemm(s.a, P(stage, "tf.q2.w"), L, C, C, q2, st);
+    attention(s, s.qkv, C, st_[stage].k2, C, nullptr, 0, st_[stage].vt2, L, sp.ctx_len, C, s.att, st);
+    TcArgs o2;
+    o2.bias = F(stage, "tf.o2.b");
+    o2.residual = s.b;
+    o2.ldr = C;
+    o2.out_bf16 = s.b;
+    o2.ldo = C;
+    tc_gemm(s.att, P(stage, "tf.o2.w"), L, C, C, o2, st);
+    // GEGLU feed-forward
+    layer_norm(s.b, L, C, F(stage, "tf.ln3.gamma"), F(stage, "tf.ln3.beta"), 1e-5f, s.a, st);
+    TcArgs f1;
+    f1.bias = F(stage, "tf.ff1.b");
+    f1.out_bf16 = s.ff;
+    f1.ldo = 8 * C;
+    tc_gemm(s.a, P(stage, "tf.ff1.w"), L, 8 * C, C, f1, st);
+    geglu(s.ff, L, 4 * C, s.ff2, st);
+    TcArgs f2;
+    f2.bias = F(stage, "tf.ff2.b");
+    f2.residual = s.b;
+    f2.ldr = C;
+    f2.out_bf16 = s.b;
+    f2.ldo = C;
+    tc_gemm(s.ff2, P(stage, "tf.ff2.w"), L, C, 4 * C, f2, st);
+    TcArgs po;
+    po.bias = F(stage, "tf.proj_out.b");
+    po.residual = x;
+    po.ldr = C;
+    po.out_bf16 = y;
+    po.ldo = C;
+    tc_gemm(s.b, P(stage, "tf.proj_out.w"), L, C, C, po, st);
+}
+
+void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, bool latent_f64, cudaStream_t st) {
+    ensure_stage(stage);
+    const UNetSpec& sp = d_.spec;
+    const UStage& s = d_.st[stage - 1];
+    UScratch& sc = scratch(st);
+    const int HW = s.H * s.W;
+    switch (s.kind) {
+        case kConvIn: {
+            pack_latent(in[0].p, latent_f64, HW, sp.c_lat, 64, sc.a, st);
+            TcArgs a;
+            a.bias = F(stage, "conv.b");
+            a.out_bf16 = static_cast<bf16*>(y);
+            a.ldo = s.cout;
+            tc_conv3x3(sc.a, P(stage, "conv.w"), 1, s.H, s.W, 64, s.cout, a, st);
+            break;
+        }
+        case kDown: {
+            TcArgs a;
+            a.bias = F(stage, "conv.b");
+            a.out_bf16 = static_cast<bf16*>(y);
+            a.ldo = s.cout;
+            a.sub2 = 1;
+            tc_conv3x3(in[0].p, P(stage, "conv.w"), 1, s.H, s.W, s.cin, s.cout, a, st);
+            break;
+        }
+        case kUp: {
+            upsample2x(static_cast<const bf16*>(in[0].p), 1, s.H, s.W, s.cin, sc.a, st);
+            TcArgs a;
+            a.bias = F(stage, "conv.b");
+            a.out_bf16 = static_cast<bf16*>(y);
+            a.ldo = s.cout;
+            tc_conv3x3(sc.a, P(stage, "conv.w"), 1, 2 * s.H, 2 * s.W, s.cin, s.cout, a, st);
+            break;
+        }
+        case kOut: {
+            Cat2 x{static_cast<const bf16*>(in[0].p), s.cin, nullptr, 0};
+            group_norm(x, 1, HW, sp.groups, F(stage, "gn.gamma"), F(stage, "gn.beta"), 1e-5f, 1, sc.a, sc.gn, st);
+            TcArgs a;
+            a.bias = F(stage, "conv.b");
+            a.out_f32 = static_cast<float*>(y);
+            a.ldo = sp.c_lat;
+            a.n_store = sp.c_lat;
+            if (latent_f64) throw std::invalid_argument("unet: the UNet family runs in f32 trajectory precision");
+            tc_conv3x3(sc.a, P(stage, "conv.w"), 1, s.H, s.W, s.cin, 32, a, st);
+            break;
+        }
+        default: {  // resnet (+ transformer)
+            const int C = s.cout, cin = s.cin + s.cskip;
+            const bf16* x0 = static_cast<const bf16*>(in[0].p);
+            const bf16* x1 = s.cskip ? static_cast<const bf16*>(in[1].p) : nullptr;
+            Cat2 xc{x0, s.cin, x1, s.cskip};
+            group_norm(xc, 1, HW, sp.groups, F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.a, sc.gn, st);
+            TcArgs c1;
+            c1.bias = F(stage, "conv1.b");
+            c1.chan_add = st_[stage].chan_add + static_cast<long long>(t) * C;
+            c1.out_bf16 = sc.b;
+            c1.ldo = C;
+            tc_conv3x3(sc.a, P(stage, "conv1.w"), 1, s.H, s.W, cin, C, c1, st);
+            Cat2 hc{sc.b, C, nullptr, 0};
+            group_norm(hc, 1, HW, sp.groups, F(stage, "gn2.gamma"), F(stage, "gn2.beta"), 1e-5f, 1, sc.a, sc.gn, st);
+            const bf16* res = x0;
+            if (cin != C) {
+                const bf16* xin = x0;
+                if (s.cskip) {
+                    concat_channels(xc, HW, sc.c, st);
+                    xin = sc.c;
+                }
+                TcArgs sh;
+                sh.bias = F(stage, "short.b");
+                sh.out_bf16 = sc.r;
+                sh.ldo = C;
+                tc_gemm(xin, P(stage, "short.w"), HW, C, cin, sh, st);
+                res = sc.r;
+            }
+            TcArgs c2;
+            c2.bias = F(stage, "conv2.b");
+            c2.residual = res;
+            c2.ldr = C;
+            bf16* out = s.attn ? sc.c : static_cast<bf16*>(y);
+            c2.out_bf16 = out;
+            c2.ldo = C;
+            tc_conv3x3(sc.a, P(stage, "conv2.w"), 1, s.H, s.W, C, C, c2, st);
+            if (s.attn) transformer(stage, sc.c, s.H, s.W, C, static_cast<bf16*>(y), st);
+        }
+    }
+}
+
+}  // namespace adx

@@ -1,0 +1,69 @@
+"""UNet-shaped family on the sm_100a path (tcgen05 conv/GEMM stages, bf16
+activations, fp32 latent): numerics vs the builder-written numpy oracle
+(oracle/unet_oracle.py -- parity unpinned by reference vectors),
+and the reference's executor invariants, which are model-agnostic and exact."""
+import numpy as np
+import pytest
+
+import paper_2406_06911_b200 as adx
+from oracle import oracle as O
+from oracle.unet_oracle import UNetOracle
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(H=16, W=16, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64, temb_dim=128, seed=5)
+TOL = 3e-2  # bf16 activations: relative L2 of eps / latents vs the fp32-math oracle
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-12))
+
+
+@pytest.fixture(scope="module")
+def small():
+    m = adx.build_unet_denoiser(**SMALL)
+    s = adx.build_schedule(4, 0.01, 0.15)
+    x = adx.Latent(O.random_normals(12, m.data_dim()).astype(np.float64), 4)
+    return m, s, x
+
+
+def test_unet_sequential_matches_oracle(small):
+    m, s, x = small
+    traj = adx.sequential_denoise(m, x, s, precision="f32")
+    orc = UNetOracle(adx, m)
+    xv = x.values.astype(np.float32)
+    lat = [xv]
+    for k, t in enumerate(range(4, 0, -1)):
+        eps = orc.eval_full(lat[-1], t)
+        assert rel(traj.eps_used[k], eps) < TOL, (t, rel(traj.eps_used[k], eps))
+        # continue the oracle from the GPU latent so errors do not compound across steps
+        lat.append(O.ddim_step(traj.latents[k].values, eps, t, s.alpha_bars).astype(np.float32))
+        assert rel(traj.latents[k + 1].values, lat[-1]) < TOL
+    assert np.all(np.isfinite(traj.latent_matrix()))
+
+
+def test_unet_async_invariants_bit_exact(small):
+    m, s, x = small
+    seq = adx.sequential_denoise(m, x, s, precision="f32")
+    for N in (2, 3):
+        part = adx.partition_balanced(m, N)
+        full, _ = adx.run_serial(adx.plan_async(4, 4, N, 1), m, part, x, s, precision="f32")
+        assert np.array_equal(full.latent_matrix(), seq.latent_matrix())  # w = T == sequential
+        plan = adx.plan_async(4, 1, N, 1)
+        ser, _ = adx.run_serial(plan, m, part, x, s, precision="f32")
+        par, _ = adx.run_parallel(plan, m, part, x, s, plan.D, precision="f32")
+        assert np.array_equal(ser.latent_matrix(), par.latent_matrix())  # parallel == serial
+    one = adx.partition_balanced(m, 1)
+    for w in (1, 3):
+        t1, _ = adx.run_serial(adx.plan_async(4, w, 1, 1), m, one, x, s, precision="f32")
+        assert np.array_equal(t1.latent_matrix(), seq.latent_matrix())  # N = 1 == sequential
+
+
+def test_unet_stride_async_runs(small):
+    m, s, x = small
+    part = adx.partition_balanced(m, 2)
+    plan = adx.plan_async(4, 1, 2, 2)
+    ser, _ = adx.run_serial(plan, m, part, x, s, precision="f32")
+    par, _ = adx.run_parallel(plan, m, part, x, s, plan.D, precision="f32")
+    assert np.array_equal(ser.latent_matrix(), par.latent_matrix())
+    assert np.all(np.isfinite(ser.latent_matrix()))
