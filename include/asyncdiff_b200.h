@@ -308,6 +308,10 @@ int adx_unet_context(const adx_model* m, float* out /* ctx_len * ctx_dim */);
 /* C[M x N] = act(A[M x K] . B[N x K]^T + bias); K % 64 == 0; bn in {0,32,64,128,256} */
 int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B,
                 const float* bias, int act, float* C, int bn, int iters, double* ms_per_iter);
+/* fused multi-head attention (64-wide heads, scale 1/8): out[L x C] bf16 from Q [L x C],
+ * K [Lk x C] and V transposed VT [C x ldvt] (ldvt >= Lk, multiple of 8) */
+int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K,
+                     const uint16_t* VT, int ldvt, uint16_t* out, int iters, double* ms_per_iter);
 /* conv3x3 / stride 1 / pad 1, NHWC: X [batch][H][W][Cin], Wt [Cout][9*Cin] ((r*3+s)*Cin+ci) */
 int adx_tc_conv3x3(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X,
                    const uint16_t* Wt, const float* bias, float* out, int iters, double* ms_per_iter);

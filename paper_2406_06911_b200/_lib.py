@@ -98,7 +98,7 @@ EXPORTS = [
     "adx_rank_session_destroy", "adx_rank_session_run", "adx_rank_session_time", "adx_rank_session_kernel_count",
     "adx_model_save_checkpoint", "adx_model_load_checkpoint", "adx_plan_to_json", "adx_plan_from_json",
     "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes", "adx_tc_gemm", "adx_tc_conv3x3",
-    "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context",
+    "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context", "adx_tc_attention",
 ]
 
 
@@ -209,6 +209,8 @@ def lib():
         "adx_unet_stage_params": (i, [vp, i, C.c_char_p, i, P(i), P(i), P(C.c_float), ll, P(ll)]),
         "adx_unet_context": (i, [vp, P(C.c_float)]),
         "adx_tc_gemm": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), i, P(C.c_float), i, i, P(d)]),
+        "adx_tc_attention": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_uint16), i, P(C.c_uint16), i,
+                                 P(d)]),
         "adx_tc_conv3x3": (i, [i, i, i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_float), i,
                                P(d)]),
     }

@@ -7,6 +7,7 @@
 #include "extras.hpp"
 #include "host.hpp"
 #include "schedule.hpp"
+#include "tc_attn.cuh"
 #include "tc_gemm.cuh"
 #include "unet.hpp"
 
@@ -954,6 +955,38 @@ int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint1
             cudaEventDestroy(e1);
         }
         if (C) CKC(cudaMemcpy(C, c.p, static_cast<size_t>(M) * N * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K, const uint16_t* VT,
+                     int ldvt, uint16_t* out, int iters, double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        DevBuf q(static_cast<size_t>(L) * C * 2), k(static_cast<size_t>(Lk) * C * 2),
+            v(static_cast<size_t>(C) * ldvt * 2), o(static_cast<size_t>(L) * C * 2);
+        CKC(cudaMemcpy(q.p, Q, static_cast<size_t>(L) * C * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(k.p, K, static_cast<size_t>(Lk) * C * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(v.p, VT, static_cast<size_t>(C) * ldvt * 2, cudaMemcpyHostToDevice));
+        auto run = [&] {
+            adx::tc_attention(q.p, C, k.p, C, v.p, ldvt, L, Lk, C, static_cast<__nv_bfloat16*>(o.p), C, 0);
+        };
+        run();
+        CKC(cudaDeviceSynchronize());
+        if (iters > 0 && ms_per_iter) {
+            cudaEvent_t e0, e1;
+            CKC(cudaEventCreate(&e0));
+            CKC(cudaEventCreate(&e1));
+            CKC(cudaEventRecord(e0));
+            for (int i = 0; i < iters; ++i) run();
+            CKC(cudaEventRecord(e1));
+            CKC(cudaEventSynchronize(e1));
+            float ms = 0;
+            CKC(cudaEventElapsedTime(&ms, e0, e1));
+            *ms_per_iter = ms / iters;
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        if (out) CKC(cudaMemcpy(out, o.p, static_cast<size_t>(L) * C * 2, cudaMemcpyDeviceToHost));
     });
 }
 

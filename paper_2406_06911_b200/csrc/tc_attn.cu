@@ -1,0 +1,346 @@
+// tc_attn.cu -- fused multi-head attention on tcgen05 (flash style) for the
+// UNet-shaped family: out = softmax(Q K^T / sqrt(64)) V per 64-wide head.
+//
+// One CTA per (128-query tile, head), 6 warps:
+//   warp 0    TMA: Q tile once; K tile [128 keys x 64] and V^T tile
+//             [64 dims x 128 keys] per KV block into a 2-stage ring (SW128);
+//   warp 1    TMEM alloc + single-thread MMA issue: S = Q K^T (M128 N128 K64)
+//             into TMEM cols [0,128), then O_blk = P V (M128 N64 K128) into
+//             cols [128,192);
+//   warps 2-5 softmax / epilogue, thread = query row: tcgen05.ld its S row,
+//             online softmax (running max / sum in registers, exp2), P (bf16)
+//             written straight into the 128B-swizzled SMEM layout the PV MMA
+//             reads as its A operand, O accumulated in registers with the
+//             softmax rescale, normalised and stored as bf16 at the end.
+// S never touches HBM (the unfused path wrote an L x L fp32 matrix per head).
+#include "tc_attn.cuh"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+namespace adx {
+
+#define CKA(x)                                                                                   \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess)                                                                   \
+            throw cuda_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x); \
+    } while (0)
+
+namespace {
+
+constexpr int QT = 128, KT = 128, HD = 64, STG = 2;
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\nW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}\n" ::"r"(sa(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, int c1, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            sa(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(sa(b))
+        : "memory");
+}
+__device__ __forceinline__ uint64_t sdesc(const void* p) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((sa(p) >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+__device__ __forceinline__ void mma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(b))
+                 : "memory");
+}
+__device__ __forceinline__ void tld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+constexpr uint32_t idesc(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+struct AttnArgs {
+    int L, Lk, C;  // query tokens, key tokens, model width (heads * 64)
+    __nv_bfloat16* out;
+    long long ldo;
+};
+
+__global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                                      const __grid_constant__ CUtensorMap tmK,
+                                                      const __grid_constant__ CUtensorMap tmVT, const AttnArgs p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2, P_B = QT * KT * 2;
+    uint8_t* sQ = smem;
+    uint8_t* sK = sQ + Q_B;                 // STG x K_B
+    uint8_t* sV = sK + STG * K_B;           // STG x (2 halves of [64 x 64])
+    uint8_t* sP = sV + STG * V_B;           // 2 halves of [128 x 64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_B);
+    uint64_t* q_full = bars;
+    uint64_t* kv_full = bars + 1;           // [STG]
+    uint64_t* kv_empty = bars + 1 + STG;    // [STG]
+    uint64_t* s_full = bars + 1 + 2 * STG;
+    uint64_t* s_free = s_full + 1;
+    uint64_t* p_full = s_full + 2;
+    uint64_t* o_full = s_full + 3;
+    uint64_t* o_free = s_full + 4;
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(s_full + 5);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qt = blockIdx.x, head = blockIdx.y;
+    const int nkv = (p.Lk + KT - 1) / KT;
+
+    if (warp == 0 && lane == 0) {
+        bar_init(q_full, 1);
+        for (int s = 0; s < STG; ++s) {
+            bar_init(&kv_full[s], 1);
+            bar_init(&kv_empty[s], 1);
+        }
+        bar_init(s_full, 1);
+        bar_init(s_free, 4);
+        bar_init(p_full, 4);
+        bar_init(o_full, 1);
+        bar_init(o_free, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(sa(tptr)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tptr;
+    const uint32_t tS = tmem, tO = tmem + 128;
+
+    if (warp == 0 && lane == 0) {
+        // ------------------------------------------------------------ TMA
+        bar_expect(q_full, Q_B);
+        tma2d(sQ, &tmQ, head * HD, qt * QT, q_full);
+        for (int j = 0; j < nkv; ++j) {
+            const int s = j % STG;
+            bar_wait(&kv_empty[s], ((j / STG) & 1) ^ 1);
+            bar_expect(&kv_full[s], K_B + V_B);
+            tma2d(sK + s * K_B, &tmK, head * HD, j * KT, &kv_full[s]);
+            // V^T rows = this head's 64 dims, two 64-key halves (128-byte rows each)
+            tma2d(sV + s * V_B, &tmVT, j * KT, head * HD, &kv_full[s]);
+            tma2d(sV + s * V_B + V_B / 2, &tmVT, j * KT + 64, head * HD, &kv_full[s]);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ------------------------------------------------------------ MMA
+        bar_wait(q_full, 0);
+        for (int j = 0; j < nkv; ++j) {
+            const int s = j % STG;
+            bar_wait(&kv_full[s], (j / STG) & 1);
+            bar_wait(s_free, (j & 1) ^ 1);  // softmax warps finished reading S_{j-1}
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < HD / 16; ++k)
+                mma(tS, sdesc(sQ + k * 32), sdesc(sK + s * K_B + k * 32), idesc(QT, KT), k > 0);
+            commit(s_full);
+            bar_wait(p_full, j & 1);        // P_j written to SMEM
+            bar_wait(o_free, (j & 1) ^ 1);  // O_{j-1} read out of TMEM
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < KT / 16; ++k) {
+                const int half = k / 4, kk = k % 4;
+                mma(tO, sdesc(sP + half * (P_B / 2) + kk * 32), sdesc(sV + s * V_B + half * (V_B / 2) + kk * 32),
+                    idesc(QT, HD), k > 0);
+            }
+            commit(o_full);
+            commit(&kv_empty[s]);
+        }
+    } else if (warp >= 2) {
+        // --------------------------------------------------- softmax + epilogue
+        const int q = warp & 3;
+        const int r = q * 32 + lane;  // query row within the tile
+        const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
+        const float sl2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
+        float m = -INFINITY, l = 0.f;
+        float o[HD];
+#pragma unroll
+        for (int i = 0; i < HD; ++i) o[i] = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+            bar_wait(s_full, j & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int valid = min(KT, p.Lk - j * KT);
+            // pass 1 over the S row in TMEM: running max
+            float mx = m;
+#pragma unroll
+            for (int c = 0; c < KT; c += 16) {
+                float v[16];
+                tld16(tS + lrow + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (c + i < valid) mx = fmaxf(mx, v[i]);
+            }
+            const float alpha = exp2f((m - mx) * sl2);
+            // pass 2: P = exp2((s - max) * scale*log2e) -> SW128 K-major A tile in SMEM
+            // (half h = keys [64h, 64h+64), 16-byte chunk k of row r at k ^ (r & 7))
+            float sum = 0.f;
+#pragma unroll
+            for (int c = 0; c < KT; c += 16) {
+                float v[16];
+                tld16(tS + lrow + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    v[i] = c + i < valid ? exp2f((v[i] - mx) * sl2) : 0.f;
+                    sum += v[i];
+                }
+                uint8_t* row = sP + (c / 64) * (P_B / 2) + r * 128;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int k = ((c % 64) / 8) + hh;
+                    uint4 u;
+                    __nv_bfloat162 b0 = __floats2bfloat162_rn(v[hh * 8 + 0], v[hh * 8 + 1]);
+                    __nv_bfloat162 b1 = __floats2bfloat162_rn(v[hh * 8 + 2], v[hh * 8 + 3]);
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(v[hh * 8 + 4], v[hh * 8 + 5]);
+                    __nv_bfloat162 b3 = __floats2bfloat162_rn(v[hh * 8 + 6], v[hh * 8 + 7]);
+                    u.x = *reinterpret_cast<uint32_t*>(&b0);
+                    u.y = *reinterpret_cast<uint32_t*>(&b1);
+                    u.z = *reinterpret_cast<uint32_t*>(&b2);
+                    u.w = *reinterpret_cast<uint32_t*>(&b3);
+                    *reinterpret_cast<uint4*>(row + ((k ^ (r & 7)) * 16)) = u;
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                bar_arrive(s_free);
+                bar_arrive(p_full);
+            }
+            l = l * alpha + sum;
+            m = mx;
+            bar_wait(o_full, j & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < HD; c += 16) {
+                float v[16];
+                tld16(tO + lrow + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * alpha + v[i];
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) bar_arrive(o_free);
+        }
+        const long long row = static_cast<long long>(qt) * QT + r;
+        if (row < p.L) {
+            const float inv = 1.0f / l;
+            __nv_bfloat16* dst = p.out + row * p.ldo + head * HD;
+#pragma unroll
+            for (int c = 0; c < HD; c += 8) {
+                uint4 v;
+                __nv_bfloat162 b0 = __floats2bfloat162_rn(o[c] * inv, o[c + 1] * inv);
+                __nv_bfloat162 b1 = __floats2bfloat162_rn(o[c + 2] * inv, o[c + 3] * inv);
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(o[c + 4] * inv, o[c + 5] * inv);
+                __nv_bfloat162 b3 = __floats2bfloat162_rn(o[c + 6] * inv, o[c + 7] * inv);
+                v.x = *reinterpret_cast<uint32_t*>(&b0);
+                v.y = *reinterpret_cast<uint32_t*>(&b1);
+                v.z = *reinterpret_cast<uint32_t*>(&b2);
+                v.w = *reinterpret_cast<uint32_t*>(&b3);
+                *reinterpret_cast<uint4*>(dst + c) = v;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    });
+    if (!fn) throw cuda_error("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2-D bf16 map: rows x cols (cols contiguous, row stride ld elements), box (64 cols, box_rows)
+CUtensorMap map2d(const void* base, long long rows, long long cols, long long ld, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r =
+        encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw cuda_error("attention: cuTensorMapEncodeTiled failed " + std::to_string(r));
+    return m;
+}
+
+}  // namespace
+
+void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, const void* VT, long long ldvt, int L,
+                  int Lk, int C, __nv_bfloat16* out, long long ldo, cudaStream_t st) {
+    if (C % HD) throw std::invalid_argument("attention: C must be a multiple of 64");
+    if ((ldq | ldk | ldvt | ldo) % 8) throw std::invalid_argument("attention: strides must be multiples of 8");
+    const CUtensorMap mq = map2d(Q, L, C, ldq, QT);
+    const CUtensorMap mk = map2d(K, Lk, C, ldk, KT);
+    const CUtensorMap mv = map2d(VT, C, Lk, ldvt, HD);  // rows = dims, cols = keys
+    AttnArgs a{L, Lk, C, out, ldo};
+    constexpr size_t smem = 1024 + QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + QT * KT * 2 + 256;
+    static bool attr[64] = {};
+    int dev = 0;
+    CKA(cudaGetDevice(&dev));
+    if (!attr[dev]) {
+        CKA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr[dev] = true;
+    }
+    dim3 grid((L + QT - 1) / QT, C / HD);
+    attn_kernel<<<grid, 192, smem, st>>>(mq, mk, mv, a);
+    CKA(cudaGetLastError());
+}
+
+}  // namespace adx

@@ -1,0 +1,16 @@
+// tc_attn.cuh -- fused tcgen05 multi-head attention (see tc_attn.cu).
+#pragma once
+
+#include "host.hpp"
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace adx {
+
+// out[L x C] (row stride ldo) = per 64-wide head softmax(Q K^T / 8) V, with
+// Q [L x C] (ldq), K [Lk x C] (ldk) and V given transposed: VT [C x >=Lk] (ldvt)
+void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, const void* VT, long long ldvt, int L,
+                  int Lk, int C, __nv_bfloat16* out, long long ldo, cudaStream_t st);
+
+}  // namespace adx

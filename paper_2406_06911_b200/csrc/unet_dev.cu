@@ -4,11 +4,13 @@
 // transformer / down / up / in / out) on the tcgen05 GEMM + conv kernels.
 #include "unet_dev.hpp"
 
+#include "tc_attn.cuh"
 #include "tc_gemm.cuh"
 #include "unet_kernels.cuh"
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace adx {
@@ -158,7 +160,7 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
             qkv = std::max(qkv, L * 3 * s.cout);
             ff = std::max(ff, L * 8 * s.cout);
             S = std::max(S, L * std::max(Lp, static_cast<size_t>(pad64(sp.ctx_len))));
-            vt = std::max(vt, 64 * Lp);
+            vt = std::max(vt, static_cast<size_t>(s.cout) * Lp);
         }
     }
     UScratch s;
@@ -194,6 +196,19 @@ const float* UNetDevice::F(int stage, const char* name) const { return static_ca
 void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16* k, long long ldk, const bf16* v,
                            long long ldv, const bf16* v_t, int L, int Lk, int C, bf16* out, cudaStream_t st) {
     const int Lkp = pad64(Lk);
+    static const bool unfused = [] {
+        const char* e = getenv("ADX_ATTN");
+        return e && std::string(e) == "unfused";
+    }();
+    if (!unfused) {  // fused tcgen05 flash attention (tc_attn.cu): S stays in TMEM
+        const bf16* vt = v_t;
+        if (!vt) {
+            transpose_head(v, ldv, Lk, Lkp, C, s.VT, st);
+            vt = s.VT;
+        }
+        tc_attention(q, ldq, k, ldk, vt, Lkp, L, Lk, C, out, C, st);
+        return;
+    }
     for (int h = 0; h < C / 64; ++h) {
         TcArgs a;
         a.out_f32 = s.S;

@@ -78,3 +78,27 @@ def test_tc_conv3x3_matches_fp32_reference(batch, H, W, Cin, Cout):
     ref = torch.nn.functional.conv2d(xt, wt, torch.from_numpy(bias), padding=1).permute(0, 2, 3, 1).numpy()
     err = np.abs(out - ref).max() / np.abs(ref).max()
     assert err < 2e-3, err
+
+
+@pytest.mark.parametrize("L,Lk,C", [(256, 256, 64), (9216 // 16, 576, 128), (144, 144, 320), (300, 77, 128),
+                                     (1024, 1024, 640)])
+def test_tc_attention_matches_fp32_reference(L, Lk, C):
+    rng = np.random.default_rng(L + Lk + C)
+    Q = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
+    K = bf16_bits(rng.standard_normal((Lk, C)).astype(np.float32))
+    V = rng.standard_normal((Lk, C)).astype(np.float32)
+    ldvt = (Lk + 63) // 64 * 64
+    VT = np.zeros((C, ldvt), np.float32)
+    VT[:, :Lk] = V.T
+    VTb = bf16_bits(VT)
+    out = np.zeros((L, C), np.uint16)
+    _lib.check(adx.lib().adx_tc_attention(0, L, Lk, C, Q.ctypes.data_as(P16), K.ctypes.data_as(P16),
+                                          VTb.ctypes.data_as(P16), ldvt, out.ctypes.data_as(P16), 0, None))
+    q = torch.from_numpy(bits_f32(Q)).view(L, C // 64, 64).transpose(0, 1)
+    k = torch.from_numpy(bits_f32(K)).view(Lk, C // 64, 64).transpose(0, 1)
+    v = torch.from_numpy(bits_f32(VTb)[:, :Lk].T.copy()).view(Lk, C // 64, 64).transpose(0, 1)
+    ref = torch.softmax(q @ k.transpose(1, 2) / 8.0, dim=-1) @ v
+    ref = ref.transpose(0, 1).reshape(L, C).numpy()
+    got = bits_f32(out)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 2e-2, err
