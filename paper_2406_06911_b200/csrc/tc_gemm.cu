@@ -227,10 +227,66 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
             m = static_cast<long long>(tile_m) * BM + row;
             valid = m < p.M;
         }
+        const int nlim = p.n_store ? p.n_store : p.N;
+        const bool vec_ok = ((p.ldo | p.ldr) & 7) == 0;
         for (int c = 0; c < BN; c += 16) {
             float v[16];
             tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
             if (!valid) continue;
+            const int nb = n0 + c;
+            if (vec_ok && nb + 16 <= nlim) {
+                // vectorised epilogue: 16 consecutive columns of this row, 16-byte loads / stores
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    if (p.bias) {
+                        const float4 b = *reinterpret_cast<const float4*>(p.bias + nb + j);
+                        v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
+                    }
+                    if (p.chan_add) {
+                        const float4 b =
+                            *reinterpret_cast<const float4*>(p.chan_add + static_cast<long long>(img) * p.N + nb + j);
+                        v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
+                    }
+                }
+                if (p.act == 1) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = silu(v[j]);
+                }
+                if (p.residual) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + nb);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint4 u = rp[h];
+                        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[k]));
+                            v[h * 8 + 2 * k] += f.x;
+                            v[h * 8 + 2 * k + 1] += f.y;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] *= p.out_scale;
+                if (p.out_f32) {
+                    float4* op = reinterpret_cast<float4*>(p.out_f32 + m * p.ldo + nb);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) op[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                } else {
+                    uint4* op = reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + nb);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t w4[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[h * 8 + 2 * k], v[h * 8 + 2 * k + 1]);
+                            w4[k] = *reinterpret_cast<const uint32_t*>(&b2);
+                        }
+                        op[h] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    }
+                }
+                continue;
+            }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const int n = n0 + c + j;
@@ -306,12 +362,28 @@ void dispatch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 
         case 32: launch_t<32, CONV>(a, b, p, grid, st); break;
         case 64: launch_t<64, CONV>(a, b, p, grid, st); break;
         case 128: launch_t<128, CONV>(a, b, p, grid, st); break;
+        case 160: launch_t<160, CONV>(a, b, p, grid, st); break;
+        case 192: launch_t<192, CONV>(a, b, p, grid, st); break;
         case 256: launch_t<256, CONV>(a, b, p, grid, st); break;
-        default: throw std::invalid_argument("tc_gemm: BN must be 32/64/128/256");
+        default: throw std::invalid_argument("tc_gemm: BN must be 32/64/128/160/192/256");
     }
 }
 
-int pick_bn(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
+// N tile: least padded columns, ties to the wider tile (fewer CTAs re-reading A)
+int pick_bn(int N) {
+    if (N <= 32) return 32;
+    if (N <= 64) return 64;
+    int best = 256;
+    long long waste = (N + 255) / 256 * 256LL - N;
+    for (int bn : {192, 160, 128}) {
+        const long long w = (N + bn - 1) / bn * static_cast<long long>(bn) - N;
+        if (w < waste) {
+            waste = w;
+            best = bn;
+        }
+    }
+    return best;
+}
 
 }  // namespace
 
