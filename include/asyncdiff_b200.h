@@ -168,6 +168,10 @@ int adx_engine_time_eval(adx_engine* e, int t_embed, int iters, double* ms_per_p
 int adx_bench_gemv(int ordinal, int precision, int n, int chain, int iters, int pdl,
                    double* ms_per_gemv);
 
+/* One eager full-model pass with CUDA events around every tensor-core launch:
+ * out9 = {launches, ms, algorithmic FLOPs} for conv3x3, GEMM, attention. */
+int adx_engine_profile_pass(adx_engine* e, int t_embed, double* out9);
+
 /* eval_full: denoiser.hpp:79, denoiser.cpp:222-233 (on ordinals[0]) */
 int adx_eval_full(adx_engine* e, const double* x, int t_embed, double* eps_out);
 

@@ -99,6 +99,7 @@ EXPORTS = [
     "adx_model_save_checkpoint", "adx_model_load_checkpoint", "adx_plan_to_json", "adx_plan_from_json",
     "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes", "adx_tc_gemm", "adx_tc_conv3x3",
     "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context", "adx_tc_attention",
+    "adx_engine_profile_pass",
 ]
 
 
@@ -173,6 +174,7 @@ def lib():
         "adx_engine_weight_bytes": (i, [vp, i, P(ll)]),
         "adx_engine_time_eval": (i, [vp, i, i, P(d), P(ll), P(i)]),
         "adx_bench_gemv": (i, [i, i, i, i, i, i, P(d)]),
+        "adx_engine_profile_pass": (i, [vp, i, P(d)]),
         "adx_eval_full": (i, [vp, P(d), i, P(d)]),
         "adx_eval_segment": (i, [vp, vp, i, P(d), i, i, i, P(i), P(d), i, i, P(d), i, P(i), P(i), P(i),
                                  P(d), i, i, P(i)]),

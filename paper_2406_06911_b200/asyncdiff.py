@@ -1086,6 +1086,16 @@ class RankSession:
         return n.value
 
 
+def profile_model_pass(m: LayeredDenoiser, t_embed: int, precision: Optional[str] = None,
+                       devices: Optional[Sequence[int]] = None) -> Dict[str, dict]:
+    """Per tensor-core kernel family, one eager pass: launches, device ms (CUDA
+    events per launch) and algorithmic FLOPs."""
+    out = np.zeros(9)
+    check(lib().adx_engine_profile_pass(m.engine(precision, devices)._h, t_embed, _dp(out)))
+    return {k: dict(launches=int(out[3 * i]), ms=float(out[3 * i + 1]), flops=float(out[3 * i + 2]))
+            for i, k in enumerate(("conv3x3", "gemm", "attention"))}
+
+
 def time_model_pass(m: LayeredDenoiser, t_embed: int, iters: int, precision: Optional[str] = None,
                     devices: Optional[Sequence[int]] = None):
     """(ms per full-model pass, weight bytes per pass, GEMV launches per pass)."""

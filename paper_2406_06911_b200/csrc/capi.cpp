@@ -596,6 +596,16 @@ int adx_engine_time_eval(adx_engine* e, int t_embed, int iters, double* ms_per_p
     });
 }
 
+int adx_engine_profile_pass(adx_engine* e, int t_embed, double* out9) {
+    return guard([&] {
+        need(e, "engine_profile_pass");
+        double prof[3][3];
+        e->e->time_eval_ms(0, t_embed, 1, nullptr, prof);
+        for (int k = 0; k < 3; ++k)
+            for (int j = 0; j < 3; ++j) out9[3 * k + j] = prof[k][j];
+    });
+}
+
 int adx_eval_full(adx_engine* e, const double* x, int t_embed, double* eps_out) {
     return guard([&] {
         need(e, "eval_full");

@@ -1,6 +1,7 @@
 // engine.cu -- device-resident AsyncDiff executor (see engine.hpp).
 #include "engine.hpp"
 
+#include "tc_gemm.cuh"
 #include "unet_dev.hpp"
 
 #include <cuda_bf16.h>
@@ -252,7 +253,7 @@ int Engine::enqueue_stage(int idx, int stage, const std::vector<Seg>& inputs, in
     return 2;
 }
 
-double Engine::time_eval_ms(int idx, int t_embed, int iters, int* launches) {
+double Engine::time_eval_ms(int idx, int t_embed, int iters, int* launches, double (*profile)[3]) {
     const int ord = ordinal(idx);
     CK(cudaSetDevice(ord));
     const Model& m = model_;
@@ -277,20 +278,33 @@ double Engine::time_eval_ms(int idx, int t_embed, int iters, int* launches) {
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     int n = 0;
+    auto pass = [&]() {
+        n = 0;
+        for (int i = 1; i <= m.L; ++i) {
+            std::vector<Seg> in;
+            if (i == 1) {
+                in.push_back({x, m.data_dim()});
+                in.push_back({etab_row(idx, t_embed), m.E});
+            } else {
+                in.push_back({y[i - 1], m.widths[i - 1]});
+            }
+            for (auto& l : m.links_into(i)) in.push_back({y[l.first], m.widths[l.first]});
+            n += enqueue_stage(idx, i, in, t_embed, h[i], y[i], bad, i, st, true);
+        }
+    };
+    if (profile) {  // eager pass with per-launch CUDA events around every tensor-core kernel
+        pass();
+        CK(cudaStreamSynchronize(st));
+        tc_profile_enable(true);
+        pass();
+        tc_profile_enable(false);
+        CK(cudaStreamSynchronize(st));
+        tc_profile_collect(profile);
+    }
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
-    for (int i = 1; i <= m.L; ++i) {
-        std::vector<Seg> in;
-        if (i == 1) {
-            in.push_back({x, m.data_dim()});
-            in.push_back({etab_row(idx, t_embed), m.E});
-        } else {
-            in.push_back({y[i - 1], m.widths[i - 1]});
-        }
-        for (auto& l : m.links_into(i)) in.push_back({y[l.first], m.widths[l.first]});
-        n += enqueue_stage(idx, i, in, t_embed, h[i], y[i], bad, i, st, true);
-    }
+    pass();
     CK(cudaStreamEndCapture(st, &g));
     CK(cudaGraphInstantiate(&ge, g, 0));
     cudaEvent_t a, b;

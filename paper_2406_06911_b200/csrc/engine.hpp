@@ -79,7 +79,9 @@ public:
     // Device time of one full-model pass (2L stage GEMVs, CUDA graph, events on
     // the launching stream), mean over `iters` back-to-back passes.  Used for the
     // HBM roofline of the stage GEMV kernel.
-    double time_eval_ms(int idx, int t_embed, int iters, int* launches);
+    // profile != nullptr: also run one eager pass with per-launch events around every
+    // tensor-core kernel; per kind (conv, GEMM, attention): {launches, ms, flops}
+    double time_eval_ms(int idx, int t_embed, int iters, int* launches, double (*profile)[3] = nullptr);
     // element size of stage outputs (bf16 for the UNet family, the activation dtype otherwise)
     int stage_bytes() const { return model_.kind == 1 ? 2 : act_bytes(prec_); }
 

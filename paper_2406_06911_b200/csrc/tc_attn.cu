@@ -15,6 +15,8 @@
 // S never touches HBM (the unfused path wrote an L x L fp32 matrix per head).
 #include "tc_attn.cuh"
 
+#include "tc_gemm.cuh"
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -339,7 +341,9 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
         attr[dev] = true;
     }
     dim3 grid((L + QT - 1) / QT, C / HD);
+    tc_profile_record_begin(st);
     attn_kernel<<<grid, 192, smem, st>>>(mq, mk, mv, a);
+    tc_profile_record_end(st, 2, 4.0 * L * Lk * C);
     CKA(cudaGetLastError());
 }
 

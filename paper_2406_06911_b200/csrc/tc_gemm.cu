@@ -385,7 +385,50 @@ int pick_bn(int N) {
     return best;
 }
 
+struct ProfRec {
+    int kind;
+    double flops;
+    cudaEvent_t a, b;
+};
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_prof_open;
+
 }  // namespace
+
+void tc_profile_enable(bool on) { g_prof_on = on; }
+
+void tc_profile_record_begin(cudaStream_t st) {
+    if (!g_prof_on) return;
+    cudaEvent_t e;
+    CKT(cudaEventCreate(&e));
+    CKT(cudaEventRecord(e, st));
+    g_prof_open.push_back(e);
+}
+
+void tc_profile_record_end(cudaStream_t st, int kind, double flops) {
+    if (!g_prof_on || g_prof_open.empty()) return;
+    cudaEvent_t e;
+    CKT(cudaEventCreate(&e));
+    CKT(cudaEventRecord(e, st));
+    g_prof.push_back({kind, flops, g_prof_open.back(), e});
+    g_prof_open.pop_back();
+}
+
+void tc_profile_collect(double out[3][3]) {
+    for (int k = 0; k < 3; ++k) out[k][0] = out[k][1] = out[k][2] = 0.0;
+    for (auto& r : g_prof) {
+        CKT(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        CKT(cudaEventElapsedTime(&ms, r.a, r.b));
+        out[r.kind][0] += 1;
+        out[r.kind][1] += ms;
+        out[r.kind][2] += r.flops;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+}
 
 // D = A[M x K] . B[N x K]^T ; A, B bf16 row-major (K contiguous), K % 64 == 0
 void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn) {
@@ -408,7 +451,9 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     p.N = N;
     p.k_blocks = K / BK;
     dim3 grid((M + BM - 1) / BM, (N + bn - 1) / bn, 1);
+    tc_profile_record_begin(st);
     dispatch<false>(ma, mb, p, grid, bn, st);
+    tc_profile_record_end(st, 1, 2.0 * M * N * K);
 }
 
 // 3x3 conv, stride 1, pad 1, as an implicit GEMM over NHWC bf16:
@@ -446,7 +491,10 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     p.box_h = bh;
     p.cin = Cin;
     dim3 grid(((H + bh - 1) / bh) * (W / bw), (Cout + bn - 1) / bn, batch);
+    tc_profile_record_begin(st);
     dispatch<true>(ma, mb, p, grid, bn, st);
+    // algorithmic FLOPs (a stride-2 conv does a quarter of the work it launches)
+    tc_profile_record_end(st, 0, 2.0 * batch * H * W * Cout * 9.0 * Cin / (p.sub2 ? 4.0 : 1.0));
 }
 
 }  // namespace adx

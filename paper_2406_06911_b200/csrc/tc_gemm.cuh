@@ -27,6 +27,15 @@ struct TcArgs {
     int n_store = 0;                      // store only the first n_store columns (0: all N)
 };
 
+// In-run kernel profiling (eager passes only): when enabled, every tensor-core
+// launch is bracketed by CUDA events on its stream and recorded with its
+// algorithmic FLOPs; kind 0 conv3x3, 1 GEMM, 2 attention.
+void tc_profile_enable(bool on);
+void tc_profile_record_begin(cudaStream_t st);
+void tc_profile_record_end(cudaStream_t st, int kind, double flops);
+// per kind: {launches, total ms, total flops}; clears the records
+void tc_profile_collect(double out[3][3]);
+
 // D[M x N] = A[M x K] . B[N x K]^T (bf16 in, fp32 accumulate in TMEM); bn = 0 picks the tile width
 void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn = 0);
 // same with explicit row strides (elements; multiples of 8) -- e.g. one head's slice of a packed QKV
