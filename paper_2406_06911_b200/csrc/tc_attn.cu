@@ -35,7 +35,7 @@ namespace adx {
 
 namespace {
 
-constexpr int QT = 128, KT = 128, HD = 64, STG = 2;
+constexpr int QT = 128, KT = 128, HD = 64, STG = 3;
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
@@ -93,6 +93,31 @@ __device__ __forceinline__ void tld16(uint32_t taddr, float* v) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+// 64 consecutive TMEM columns of this thread's lane; no wait (caller batches tcgen05.wait::ld)
+#define TLD64_REGS(P)                                                                                          \
+    "=r"(P[0]), "=r"(P[1]), "=r"(P[2]), "=r"(P[3]), "=r"(P[4]), "=r"(P[5]), "=r"(P[6]), "=r"(P[7]), "=r"(P[8]), \
+        "=r"(P[9]), "=r"(P[10]), "=r"(P[11]), "=r"(P[12]), "=r"(P[13]), "=r"(P[14]), "=r"(P[15]), "=r"(P[16]),  \
+        "=r"(P[17]), "=r"(P[18]), "=r"(P[19]), "=r"(P[20]), "=r"(P[21]), "=r"(P[22]), "=r"(P[23]), "=r"(P[24]), \
+        "=r"(P[25]), "=r"(P[26]), "=r"(P[27]), "=r"(P[28]), "=r"(P[29]), "=r"(P[30]), "=r"(P[31]), "=r"(P[32]), \
+        "=r"(P[33]), "=r"(P[34]), "=r"(P[35]), "=r"(P[36]), "=r"(P[37]), "=r"(P[38]), "=r"(P[39]), "=r"(P[40]), \
+        "=r"(P[41]), "=r"(P[42]), "=r"(P[43]), "=r"(P[44]), "=r"(P[45]), "=r"(P[46]), "=r"(P[47]), "=r"(P[48]), \
+        "=r"(P[49]), "=r"(P[50]), "=r"(P[51]), "=r"(P[52]), "=r"(P[53]), "=r"(P[54]), "=r"(P[55]), "=r"(P[56]), \
+        "=r"(P[57]), "=r"(P[58]), "=r"(P[59]), "=r"(P[60]), "=r"(P[61]), "=r"(P[62]), "=r"(P[63])
+__device__ __forceinline__ void tld64_nowait(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,"
+        "%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : TLD64_REGS(r)
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 constexpr uint32_t idesc(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
            (static_cast<uint32_t>(M >> 4) << 24);
@@ -111,19 +136,19 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2, P_B = QT * KT * 2;
     uint8_t* sQ = smem;
-    uint8_t* sK = sQ + Q_B;                 // STG x K_B
-    uint8_t* sV = sK + STG * K_B;           // STG x (2 halves of [64 x 64])
-    uint8_t* sP = sV + STG * V_B;           // 2 halves of [128 x 64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_B);
+    uint8_t* sK = sQ + Q_B;        // STG x K_B
+    uint8_t* sV = sK + STG * K_B;  // STG x (2 halves of [64 dims x 64 keys])
+    uint8_t* sP = sV + STG * V_B;  // 2 buffers x (2 halves of [128 rows x 64 keys])
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_B);
     uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;           // [STG]
-    uint64_t* kv_empty = bars + 1 + STG;    // [STG]
-    uint64_t* s_full = bars + 1 + 2 * STG;
-    uint64_t* s_free = s_full + 1;
-    uint64_t* p_full = s_full + 2;
-    uint64_t* o_full = s_full + 3;
-    uint64_t* o_free = s_full + 4;
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(s_full + 5);
+    uint64_t* kv_full = bars + 1;         // [STG]
+    uint64_t* kv_empty = kv_full + STG;   // [STG]
+    uint64_t* s_full = kv_empty + STG;    // [2] MMA -> softmax
+    uint64_t* s_free = s_full + 2;        // [2] softmax -> MMA (S buffer read)
+    uint64_t* p_full = s_free + 2;        // [2] softmax -> MMA (P buffer written)
+    uint64_t* o_full = p_full + 2;        // [2] MMA -> softmax
+    uint64_t* o_free = o_full + 2;        // [2] softmax -> MMA (O buffer merged)
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(o_free + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qt = blockIdx.x, head = blockIdx.y;
@@ -135,22 +160,24 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
             bar_init(&kv_full[s], 1);
             bar_init(&kv_empty[s], 1);
         }
-        bar_init(s_full, 1);
-        bar_init(s_free, 4);
-        bar_init(p_full, 4);
-        bar_init(o_full, 1);
-        bar_init(o_free, 4);
+        for (int b = 0; b < 2; ++b) {
+            bar_init(&s_full[b], 1);
+            bar_init(&s_free[b], 4);
+            bar_init(&p_full[b], 4);
+            bar_init(&o_full[b], 1);
+            bar_init(&o_free[b], 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(sa(tptr)) : "memory");
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sa(tptr)) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tptr;
-    const uint32_t tS = tmem, tO = tmem + 128;
+    // TMEM columns: S buffers [0,128) and [128,256); O buffers [256,320) and [320,384)
 
     if (warp == 0 && lane == 0) {
         // ------------------------------------------------------------ TMA
@@ -167,27 +194,36 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
         }
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------------------ MMA
-        bar_wait(q_full, 0);
-        for (int j = 0; j < nkv; ++j) {
-            const int s = j % STG;
+        // iteration j issues S_j (overlapping the softmax of S_{j-1}) and PV_{j-1}
+        auto issue_s = [&](int j) {
+            const int s = j % STG, b = j & 1;
             bar_wait(&kv_full[s], (j / STG) & 1);
-            bar_wait(s_free, (j & 1) ^ 1);  // softmax warps finished reading S_{j-1}
+            bar_wait(&s_free[b], ((j >> 1) & 1) ^ 1);  // softmax read S_{j-2}
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < HD / 16; ++k)
-                mma(tS, sdesc(sQ + k * 32), sdesc(sK + s * K_B + k * 32), idesc(QT, KT), k > 0);
-            commit(s_full);
-            bar_wait(p_full, j & 1);        // P_j written to SMEM
-            bar_wait(o_free, (j & 1) ^ 1);  // O_{j-1} read out of TMEM
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                mma(tmem + b * 128, sdesc(sQ + k * 32), sdesc(sK + s * K_B + k * 32), idesc(QT, KT), k > 0);
+            commit(&s_full[b]);
+        };
+        bar_wait(q_full, 0);
+        issue_s(0);
+        // S_{j+1} is issued before waiting for P_j, so it runs under the softmax of tile j
+        for (int j = 1; j <= nkv; ++j) {
+            if (j < nkv) issue_s(j);
+            {
+                const int jj = j - 1, s = jj % STG, b = jj & 1;
+                bar_wait(&p_full[b], (jj >> 1) & 1);         // P_jj in SMEM
+                bar_wait(&o_free[b], ((jj >> 1) & 1) ^ 1);   // O_{jj-2} merged
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-            for (int k = 0; k < KT / 16; ++k) {
-                const int half = k / 4, kk = k % 4;
-                mma(tO, sdesc(sP + half * (P_B / 2) + kk * 32), sdesc(sV + s * V_B + half * (V_B / 2) + kk * 32),
-                    idesc(QT, HD), k > 0);
+                for (int k = 0; k < KT / 16; ++k) {
+                    const int half = k / 4, kk = k % 4;
+                    mma(tmem + 256 + b * 64, sdesc(sP + b * P_B + half * (P_B / 2) + kk * 32),
+                        sdesc(sV + s * V_B + half * (V_B / 2) + kk * 32), idesc(QT, HD), k > 0);
+                }
+                commit(&o_full[b]);
+                commit(&kv_empty[s]);
             }
-            commit(o_full);
-            commit(&kv_empty[s]);
         }
     } else if (warp >= 2) {
         // --------------------------------------------------- softmax + epilogue
@@ -195,38 +231,64 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
         const int r = q * 32 + lane;  // query row within the tile
         const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
         const float sl2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
-        float m = -INFINITY, l = 0.f;
+        float m = -INFINITY, l = 0.f, alpha_pend = 0.f;
         float o[HD];
 #pragma unroll
         for (int i = 0; i < HD; ++i) o[i] = 0.f;
+        // O_jj merge (deferred by one tile): o = o * alpha_jj + O_jj
+        auto merge = [&](int jj, float alpha) {
+            const int b = jj & 1;
+            bar_wait(&o_full[b], (jj >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t ov[HD];
+            tld64_nowait(tmem + 256 + b * 64 + lrow, ov);
+            tld_wait();
+#pragma unroll
+            for (int i = 0; i < HD; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(ov[i]));
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) bar_arrive(&o_free[b]);
+        };
         for (int j = 0; j < nkv; ++j) {
-            bar_wait(s_full, j & 1);
+            const int b = j & 1;
+            const uint32_t tS = tmem + b * 128 + lrow;
+            bar_wait(&s_full[b], (j >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int valid = min(KT, p.Lk - j * KT);
-            // pass 1 over the S row in TMEM: running max
-            float mx = m;
+            // the whole S row (128 fp32) in two batched 64-column TMEM loads, one wait
+            uint32_t sr[KT];
+            tld64_nowait(tS, sr);
+            tld64_nowait(tS + 64, sr + 64);
+            tld_wait();
+            // row max with 8 independent chains (a single 128-long FMNMX chain is latency bound)
+            // ragged last tile: mask the dead keys to -inf once so the hot loops carry no predicates
+            if (valid < KT) {
 #pragma unroll
-            for (int c = 0; c < KT; c += 16) {
-                float v[16];
-                tld16(tS + lrow + c, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (c + i < valid) mx = fmaxf(mx, v[i]);
+                for (int i = 0; i < KT; ++i)
+                    if (i >= valid) sr[i] = 0xff800000u;
             }
-            const float alpha = exp2f((m - mx) * sl2);
-            // pass 2: P = exp2((s - max) * scale*log2e) -> SW128 K-major A tile in SMEM
+            float mp[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) mp[a] = m;
+#pragma unroll
+            for (int i = 0; i < KT; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(sr[i]));
+            const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                                   fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+            const float alpha = ex2((m - mx) * sl2);
+            const float off = -mx * sl2;
+            // P = exp2(s*scale*log2e - max*scale*log2e) -> SW128 K-major A tile in SMEM
             // (half h = keys [64h, 64h+64), 16-byte chunk k of row r at k ^ (r & 7))
-            float sum = 0.f;
+            float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent sum chains
+            uint8_t* pbuf = sP + b * P_B;
 #pragma unroll
             for (int c = 0; c < KT; c += 16) {
                 float v[16];
-                tld16(tS + lrow + c, v);
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    v[i] = c + i < valid ? exp2f((v[i] - mx) * sl2) : 0.f;
-                    sum += v[i];
+                    v[i] = ex2(fmaf(__uint_as_float(sr[c + i]), sl2, off));
+                    sp[i & 7] += v[i];
                 }
-                uint8_t* row = sP + (c / 64) * (P_B / 2) + r * 128;
+                uint8_t* row = pbuf + (c / 64) * (P_B / 2) + r * 128;
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     const int k = ((c % 64) / 8) + hh;
@@ -246,24 +308,16 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-                bar_arrive(s_free);
-                bar_arrive(p_full);
+                bar_arrive(&s_free[b]);
+                bar_arrive(&p_full[b]);
             }
+            const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
             l = l * alpha + sum;
             m = mx;
-            bar_wait(o_full, j & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-            for (int c = 0; c < HD; c += 16) {
-                float v[16];
-                tld16(tO + lrow + c, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * alpha + v[i];
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) bar_arrive(o_free);
+            if (j >= 1) merge(j - 1, alpha_pend);
+            alpha_pend = alpha;
         }
+        merge(nkv - 1, alpha_pend);
         const long long row = static_cast<long long>(qt) * QT + r;
         if (row < p.L) {
             const float inv = 1.0f / l;
@@ -286,7 +340,7 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -332,7 +386,7 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
     const CUtensorMap mk = map2d(K, Lk, C, ldk, KT);
     const CUtensorMap mv = map2d(VT, C, Lk, ldvt, HD);  // rows = dims, cols = keys
     AttnArgs a{L, Lk, C, out, ldo};
-    constexpr size_t smem = 1024 + QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + QT * KT * 2 + 256;
+    constexpr size_t smem = 1024 + QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + 2 * QT * KT * 2 + 256;
     static bool attr[64] = {};
     int dev = 0;
     CKA(cudaGetDevice(&dev));
