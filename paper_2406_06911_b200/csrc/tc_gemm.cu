@@ -120,6 +120,7 @@ constexpr uint32_t tmem_cols() {
 }
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 // ------------------------------------------------------------------ kernel
 template <int BN, bool CONV>
@@ -229,6 +230,36 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
         }
         const int nlim = p.n_store ? p.n_store : p.N;
         const bool vec_ok = ((p.ldo | p.ldr) & 7) == 0;
+        if (p.act == 2) {
+            // GEGLU: the host interleaved the weight rows per tile, so columns [0, BN/2)
+            // of this tile are hidden units n0/2 + c and [BN/2, BN) their gates;
+            // out[m][n0/2 + c] = (h + bh) * gelu(g + bg)  (the 2x-wide product never reaches HBM)
+            for (int c = 0; c < BN / 2; c += 16) {
+                float v[16], g[16];
+                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + BN / 2 + c, g);
+                if (!valid) continue;
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    const float4 bh = *reinterpret_cast<const float4*>(p.bias + n0 + c + j);
+                    const float4 bg = *reinterpret_cast<const float4*>(p.bias + n0 + BN / 2 + c + j);
+                    v[j] += bh.x, v[j + 1] += bh.y, v[j + 2] += bh.z, v[j + 3] += bh.w;
+                    g[j] += bg.x, g[j + 1] += bg.y, g[j + 2] += bg.z, g[j + 3] += bg.w;
+                }
+                uint4* op = reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + n0 / 2 + c);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t w4[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int j = h * 8 + 2 * k;
+                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[j] * gelu(g[j]), v[j + 1] * gelu(g[j + 1]));
+                        w4[k] = *reinterpret_cast<const uint32_t*>(&b2);
+                    }
+                    op[h] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                }
+            }
+        } else
         for (int c = 0; c < BN; c += 16) {
             float v[16];
             tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
@@ -439,6 +470,12 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
                      cudaStream_t st, int bn) {
     if (K % BK) throw std::invalid_argument("tc_gemm: K must be a multiple of 64");
     if ((lda | ldb) % 8) throw std::invalid_argument("tc_gemm: row strides must be multiples of 8 elements");
+    if (p.act == 2) {  // fused GEGLU (see the epilogue): fixed 256-wide tiles of [128 hidden | 128 gate]
+        if (bn && bn != 256) throw std::invalid_argument("tc_gemm: GEGLU epilogue needs 256-wide N tiles");
+        if (N % 256 || !p.out_bf16 || !p.bias || p.residual || p.chan_add || (p.ldo % 8))
+            throw std::invalid_argument("tc_gemm: GEGLU epilogue needs N % 256 == 0, bias, bf16 output, ldo % 8 == 0");
+        bn = 256;
+    }
     if (bn == 0) bn = pick_bn(N);
     const cuuint64_t da[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
     const cuuint64_t sa_[1] = {static_cast<cuuint64_t>(lda) * 2};

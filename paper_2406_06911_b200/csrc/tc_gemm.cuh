@@ -18,7 +18,9 @@ struct TcArgs {
     const float* chan_add = nullptr;      // [images][N] (e.g. time-embedding projection)
     const __nv_bfloat16* residual = nullptr;
     long long ldr = 0;
-    int act = 0;                          // 0 none, 1 SiLU (applied before the residual)
+    int act = 0;                          // 0 none, 1 SiLU (applied before the residual),
+                                          // 2 GEGLU over tile-interleaved [hidden | gate] columns
+                                          //   (GEMM only; output width N/2; see geglu_interleave_rows)
     float out_scale = 1.0f;
     __nv_bfloat16* out_bf16 = nullptr;    // exactly one of out_bf16 / out_f32
     float* out_f32 = nullptr;

@@ -90,6 +90,22 @@ void UNetDevice::ensure_stage(int stage) {
     auto ps = unet_stage_params(d_, stage);
     for (auto& p : ps) {
         const bool matrix = p.shape.size() == 2;
+        if (p.name == "tf.ff1.w" || p.name == "tf.ff1.b") {
+            // GEGLU fused into the ff1 GEMM epilogue: rows [hidden | gate] interleaved per
+            // 256-wide N tile: tile t = hidden rows [128t, 128t+128) then gate rows 4C + same
+            const int rows = p.shape[0], cols = matrix ? p.shape[1] : 1, H = rows / 2;
+            if (H % 128) throw std::invalid_argument("unet: GEGLU width must be a multiple of 128");
+            std::vector<float> perm(p.data.size());
+            for (int t = 0; t < H / 128; ++t)
+                for (int i = 0; i < 256; ++i) {
+                    const int src = i < 128 ? 128 * t + i : H + 128 * t + (i - 128);
+                    std::copy_n(p.data.begin() + static_cast<size_t>(src) * cols, cols,
+                                perm.begin() + static_cast<size_t>(256 * t + i) * cols);
+                }
+            ds.p[p.name] = matrix ? upload_bf16(perm) : upload_f32(perm);
+            ds.bytes[p.name] = static_cast<long long>(p.data.size()) * (matrix ? 2 : 4);
+            continue;
+        }
         if (p.name == "tf.k2.w" || p.name == "tf.v2.w" || p.name == "temb.w" || p.name == "temb.b") continue;
         ds.p[p.name] = matrix ? upload_bf16(p.data) : upload_f32(p.data);
         ds.bytes[p.name] = static_cast<long long>(p.data.size()) * (matrix ? 2 : 4);
@@ -154,7 +170,7 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
         const size_t hw = static_cast<size_t>(s.H) * s.W;
         act = std::max({act, hw * (s.cin + s.cskip), static_cast<size_t>(s.Ho()) * s.Wo() * s.cout, hw * 64,
                         4 * hw * s.cin});
-        gn = std::max({gn, group_norm_scratch_bytes(1, static_cast<int>(4 * hw), sp.groups)});
+        gn = std::max({gn, group_norm_scratch_bytes(1, static_cast<int>(4 * hw), sp.groups, s.cin + s.cskip + s.cout)});
         if (s.attn) {
             const size_t L = hw, Lp = pad64(static_cast<int>(L));
             qkv = std::max(qkv, L * 3 * s.cout);
@@ -181,6 +197,8 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
     s.S = static_cast<float*>(al(S * 4));
     s.VT = static_cast<bf16*>(al(vt * 2));
     s.gn = static_cast<float2*>(al(gn));
+    CKD(cudaMemsetAsync(s.gn, 0, gn, st));  // group_norm's ticket counter starts at zero (stream-ordered:
+                                             // also valid when first reached inside a graph capture)
     return scratch_.emplace(st, s).first->second;
 }
 
@@ -269,10 +287,10 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
     layer_norm(s.b, L, C, F(stage, "tf.ln3.gamma"), F(stage, "tf.ln3.beta"), 1e-5f, s.a, st);
     TcArgs f1;
     f1.bias = F(stage, "tf.ff1.b");
-    f1.out_bf16 = s.ff;
-    f1.ldo = 8 * C;
+    f1.act = 2;  // GEGLU in the epilogue: s.ff2 = hidden * gelu(gate), 4C wide
+    f1.out_bf16 = s.ff2;
+    f1.ldo = 4 * C;
     tc_gemm(s.a, P(stage, "tf.ff1.w"), L, 8 * C, C, f1, st);
-    geglu(s.ff, L, 4 * C, s.ff2, st);
     TcArgs f2;
     f2.bias = F(stage, "tf.ff2.b");
     f2.residual = s.b;

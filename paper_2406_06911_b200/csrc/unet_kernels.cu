@@ -33,94 +33,215 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// channel c of pixel p of image n from a two-segment channel concat
-__device__ __forceinline__ float cat_at(const Cat2& x, long long pix, int c) {
-    return c < x.c0 ? b2f(x.p0[pix * x.c0 + c]) : b2f(x.p1[pix * x.c1 + (c - x.c0)]);
+// 8 consecutive channels (one 16-byte vector) of pixel `pix` from a two-segment
+// channel concat; both segments are multiples of 8 channels (checked on the host)
+__device__ __forceinline__ uint4 cat_vec(const Cat2& x, long long pix, int v) {
+    const int c = v * 8;
+    return c < x.c0 ? __ldg(reinterpret_cast<const uint4*>(x.p0 + pix * x.c0 + c))
+                    : __ldg(reinterpret_cast<const uint4*>(x.p1 + pix * x.c1 + (c - x.c0)));
+}
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 t = __bfloat1622float2(h[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 b = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+        w[i] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    return u;
 }
 
-// GroupNorm pass 1: partial (sum, sumsq) per (image, chunk, group), fp32 over <= kChunkPix pixels
-constexpr int kChunkPix = 256;
-__global__ void gn_partials(Cat2 x, int HW, int groups, int chunks, float2* part) {
-    const int n = blockIdx.z, ch = blockIdx.y, g = blockIdx.x;
-    const int C = x.c0 + x.c1, cpg = C / groups;
-    const int p0 = ch * kChunkPix, p1 = min(HW, p0 + kChunkPix);
-    float s = 0.f, ss = 0.f;
-    const int elems = (p1 - p0) * cpg;
-    for (int e = threadIdx.x; e < elems; e += blockDim.x) {
-        const int pp = p0 + e / cpg, c = g * cpg + e % cpg;
-        const float v = cat_at(x, static_cast<long long>(n) * HW + pp, c);
-        s += v;
-        ss += v * v;
-    }
-    __shared__ float sh[2][32];
-    s = warp_sum(s);
-    ss = warp_sum(ss);
-    if ((threadIdx.x & 31) == 0) {
-        sh[0][threadIdx.x >> 5] = s;
-        sh[1][threadIdx.x >> 5] = ss;
+// GroupNorm scratch: [ticket counter (64 B)][per-channel (scale, shift) float2, batch*C][partials]
+constexpr int kGnMaxChunks = 148;  // one statistics CTA per SM
+struct GnLayout {
+    unsigned* counter;
+    float2* ab;
+    float2* part;
+};
+__host__ __device__ inline GnLayout gn_layout(float2* scratch, int batch, int C) {
+    GnLayout l;
+    l.counter = reinterpret_cast<unsigned*>(scratch);
+    l.ab = scratch + 8;
+    l.part = l.ab + static_cast<long long>(batch) * C;
+    return l;
+}
+
+// GroupNorm pass 1, one CTA per (pixel chunk, image).  Thread (r, v) owns the 8
+// channels of vector v and pixels p0 + r, p0 + r + rpb, ...; per-channel partial
+// (sum, sumsq) are reduced to per-group partials in a fixed order.  The last CTA
+// (ticket) merges all chunks in fp64 (fixed order) and folds mean / rstd / gamma /
+// beta into per-channel (a, b) with y = x * a + b.  Deterministic and independent of
+// which CTA happens to finish last.
+__global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, const float* gamma,
+                         const float* beta, float eps, float2* scratch) {
+    extern __shared__ float sm[];  // [2][rpb][C]
+    const int n = blockIdx.y, ch = blockIdx.x, batch = gridDim.y;
+    const int C = x.c0 + x.c1, nv = C / 8, cpg = C / groups;
+    const int rpb = blockDim.x / nv, r = threadIdx.x / nv, v = threadIdx.x % nv;
+    const GnLayout L = gn_layout(scratch, batch, C);
+    const int p0 = ch * chunk_pix, p1 = min(HW, p0 + chunk_pix);
+    if (r < rpb) {
+        float s[8], ss[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] = ss[i] = 0.f;
+        for (int p = p0 + r; p < p1; p += rpb) {
+            float f[8];
+            unpack8(cat_vec(x, static_cast<long long>(n) * HW + p, v), f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                s[i] += f[i];
+                ss[i] = fmaf(f[i], f[i], ss[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            sm[r * C + v * 8 + i] = s[i];
+            sm[(rpb + r) * C + v * 8 + i] = ss[i];
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        float a = 0.f, b = 0.f;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-            a += sh[0][w];
-            b += sh[1][w];
-        }
-        part[(static_cast<long long>(n) * chunks + ch) * groups + g] = make_float2(a, b);
-    }
-}
-
-// GroupNorm pass 2: every block merges the partials of its image in fp64
-// (fixed order), then normalises its pixels: y = (x-mu)*rstd*gamma + beta (+SiLU)
-__global__ void gn_apply(Cat2 x, int HW, int groups, int chunks, const float2* part, const float* gamma,
-                         const float* beta, float eps, int act, bf16* out, int pix_per_block) {
-    extern __shared__ float st[];  // [2*groups]: mean, rstd
-    const int n = blockIdx.y;
-    const int C = x.c0 + x.c1, cpg = C / groups;
     for (int g = threadIdx.x; g < groups; g += blockDim.x) {
-        double s = 0.0, ss = 0.0;
-        for (int ch = 0; ch < chunks; ++ch) {
-            const float2 v = part[(static_cast<long long>(n) * chunks + ch) * groups + g];
-            s += v.x;
-            ss += v.y;
+        float a = 0.f, b = 0.f;
+        for (int rr = 0; rr < rpb; ++rr)
+            for (int c = g * cpg; c < (g + 1) * cpg; ++c) {
+                a += sm[rr * C + c];
+                b += sm[(rpb + rr) * C + c];
+            }
+        L.part[(static_cast<long long>(n) * chunks + ch) * groups + g] = make_float2(a, b);
+    }
+    // ticket: the last CTA of the grid finalises every image
+    __shared__ unsigned last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(L.counter, 1u) == static_cast<unsigned>(chunks * batch - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // fp64 merge of the chunk partials: nsub threads per (image, group), each over a fixed
+    // strided subset with 4 loads in flight, then combined in sub order (fixed = deterministic)
+    const int ngs = batch * groups, nsub = max(1, static_cast<int>(blockDim.x) / ngs);
+    double* red = reinterpret_cast<double*>(sm);  // [nsub][ngs][2], then [ngs][2] mean / rstd
+    if (threadIdx.x < nsub * ngs) {
+        const int ng = threadIdx.x % ngs, sub = threadIdx.x / ngs, nn = ng / groups, g = ng % groups;
+        const float2* pp = L.part + static_cast<long long>(nn) * chunks * groups + g;
+        double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+        int k = sub;
+        for (; k + 3 * nsub < chunks; k += 4 * nsub) {
+            float2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcg(pp + static_cast<long long>(k + u * nsub) * groups);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] += v[u].x, b[u] += v[u].y;
         }
-        const double cnt = static_cast<double>(HW) * cpg;
-        const double mu = s / cnt;
-        const double var = fmax(ss / cnt - mu * mu, 0.0);
-        st[g] = static_cast<float>(mu);
-        st[groups + g] = static_cast<float>(rsqrt(var + eps));
+        for (; k < chunks; k += nsub) {
+            const float2 v = __ldcg(pp + static_cast<long long>(k) * groups);
+            a[0] += v.x, b[0] += v.y;
+        }
+        red[2 * (sub * ngs + ng)] = (a[0] + a[1]) + (a[2] + a[3]);
+        red[2 * (sub * ngs + ng) + 1] = (b[0] + b[1]) + (b[2] + b[3]);
     }
     __syncthreads();
-    const long long base = static_cast<long long>(blockIdx.x) * pix_per_block;
-    const long long end = min(static_cast<long long>(HW), base + pix_per_block);
-    for (long long e = threadIdx.x; e < (end - base) * C; e += blockDim.x) {
-        const long long pp = base + e / C;
-        const int c = static_cast<int>(e % C);
-        const long long pix = static_cast<long long>(n) * HW + pp;
-        const int g = c / cpg;
-        float v = (cat_at(x, pix, c) - st[g]) * st[groups + g] * gamma[c] + beta[c];
-        if (act) v = silu(v);
-        out[pix * C + c] = __float2bfloat16(v);
+    double mv[2] = {0.0, 0.0};
+    const int ng = threadIdx.x;
+    if (ng < ngs) {
+        double a = 0.0, b = 0.0;
+        for (int sub = 0; sub < nsub; ++sub) a += red[2 * (sub * ngs + ng)], b += red[2 * (sub * ngs + ng) + 1];
+        const double cnt = static_cast<double>(HW) * cpg;
+        const double mu = a / cnt;
+        const double var = fmax(b / cnt - mu * mu, 0.0);
+        mv[0] = mu;
+        mv[1] = 1.0 / sqrt(var + static_cast<double>(eps));
+    }
+    __syncthreads();
+    double* st = red;
+    if (ng < ngs) st[2 * ng] = mv[0], st[2 * ng + 1] = mv[1];
+    __syncthreads();
+    for (int nc = threadIdx.x; nc < batch * C; nc += blockDim.x) {
+        const int nn = nc / C, c = nc % C, g = c / cpg;
+        const double mu = st[2 * (nn * groups + g)], rs = st[2 * (nn * groups + g) + 1];
+        const float a = static_cast<float>(rs * gamma[c]);
+        L.ab[nc] = make_float2(a, static_cast<float>(beta[c] - mu * rs * gamma[c]));
+    }
+    if (threadIdx.x == 0) *L.counter = 0u;  // re-arm for the next launch on this scratch
+}
+
+// GroupNorm pass 2: y = x * a[c] + b[c] (+SiLU), 8 channels per thread
+__global__ void gn_apply(Cat2 x, long long pixels, int HW, const float2* __restrict__ ab, int act, bf16* out) {
+    const int C = x.c0 + x.c1, nv = C / 8;
+    const long long n = pixels * nv;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long pix = i / nv;
+        const int v = static_cast<int>(i - pix * nv);
+        const float2* abv = ab + (pix / HW) * C + v * 8;
+        float f[8];
+        unpack8(cat_vec(x, pix, v), f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float2 q = __ldg(abv + k);
+            f[k] = fmaf(f[k], q.x, q.y);
+            if (act) f[k] = silu(f[k]);
+        }
+        reinterpret_cast<uint4*>(out)[i] = pack8(f);
     }
 }
 
-// LayerNorm over C per token, one warp per token
+// LayerNorm over C per token, one warp per token, row held in registers (C <= 2048)
+constexpr int kLnMaxVec = 8;
 __global__ void layernorm_k(const bf16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
                             bf16* out) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= tokens) return;
-    const bf16* r = x + static_cast<long long>(warp) * C;
+    const int nv = C / 8;
+    const uint4* r = reinterpret_cast<const uint4*>(x + static_cast<long long>(warp) * C);
+    float f[kLnMaxVec][8];
     float s = 0.f;
-    for (int c = lane; c < C; c += 32) s += b2f(r[c]);
+#pragma unroll
+    for (int j = 0; j < kLnMaxVec; ++j) {
+        const int v = lane + 32 * j;
+        if (v < nv) {
+            unpack8(__ldg(r + v), f[j]);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += f[j][k];
+        }
+    }
     const float mu = warp_sum(s) / C;
     float ss = 0.f;
-    for (int c = lane; c < C; c += 32) {
-        const float d = b2f(r[c]) - mu;
-        ss += d * d;
-    }
+#pragma unroll
+    for (int j = 0; j < kLnMaxVec; ++j)
+        if (lane + 32 * j < nv) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float d = f[j][k] - mu;
+                ss = fmaf(d, d, ss);
+            }
+        }
     const float rstd = rsqrtf(warp_sum(ss) / C + eps);
-    bf16* o = out + static_cast<long long>(warp) * C;
-    for (int c = lane; c < C; c += 32) o[c] = __float2bfloat16((b2f(r[c]) - mu) * rstd * gamma[c] + beta[c]);
+    uint4* o = reinterpret_cast<uint4*>(out + static_cast<long long>(warp) * C);
+#pragma unroll
+    for (int j = 0; j < kLnMaxVec; ++j) {
+        const int v = lane + 32 * j;
+        if (v < nv) {
+            const float4* g4 = reinterpret_cast<const float4*>(gamma + v * 8);
+            const float4* b4 = reinterpret_cast<const float4*>(beta + v * 8);
+            const float4 ga = __ldg(g4), gb = __ldg(g4 + 1), ba = __ldg(b4), bb = __ldg(b4 + 1);
+            const float gg[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+            const float be[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+            float y[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) y[k] = (f[j][k] - mu) * rstd * gg[k] + be[k];
+            o[v] = pack8(y);
+        }
+    }
 }
 
 // softmax over the first `valid` columns of each fp32 row (already scaled);
@@ -161,40 +282,48 @@ __global__ void softmax_rows(const float* S, long long lds, int valid, bf16* P, 
         p[c] = __float2bfloat16(c < valid ? __expf(r[c] - mx) * inv : 0.f);
 }
 
-// out[t][j] = F[t][j] * gelu(F[t][j + H])   (diffusers GEGLU: hidden * gelu(gate))
+// out[t][j] = F[t][j] * gelu(F[t][j + H])   (diffusers GEGLU: hidden * gelu(gate)), 8 per thread
 __global__ void geglu_k(const bf16* F, long long tokens, int H, bf16* out) {
-    const long long n = tokens * H;
+    const int hv = H / 8;
+    const long long n = tokens * hv;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long t = i / H;
-        const int j = static_cast<int>(i % H);
-        const float a = b2f(F[t * 2 * H + j]), g = b2f(F[t * 2 * H + H + j]);
-        out[i] = __float2bfloat16(a * gelu(g));
+        const long long t = i / hv;
+        const int j = static_cast<int>(i - t * hv);
+        const uint4* row = reinterpret_cast<const uint4*>(F + t * 2 * H);
+        float a[8], g[8];
+        unpack8(__ldg(row + j), a);
+        unpack8(__ldg(row + hv + j), g);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] *= gelu(g[k]);
+        reinterpret_cast<uint4*>(out)[i] = pack8(a);
     }
 }
 
+// nearest 2x upsample, NHWC, 8 channels per thread
 __global__ void upsample2x_k(const bf16* x, int batch, int H, int W, int C, bf16* out) {
-    const long long n = static_cast<long long>(batch) * 2 * H * 2 * W * C;
+    const int nv = C / 8;
+    const long long n = static_cast<long long>(batch) * 2 * H * 2 * W * nv;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % C);
-        long long p = i / C;
+        long long p = i / nv;
+        const int v = static_cast<int>(i - p * nv);
         const int w2 = static_cast<int>(p % (2 * W));
         p /= 2 * W;
         const int h2 = static_cast<int>(p % (2 * H));
         const long long b = p / (2 * H);
-        out[i] = x[((b * H + h2 / 2) * W + w2 / 2) * C + c];
+        reinterpret_cast<uint4*>(out)[i] =
+            __ldg(reinterpret_cast<const uint4*>(x + ((b * H + h2 / 2) * W + w2 / 2) * C) + v);
     }
 }
 
 __global__ void concat_k(Cat2 x, long long pixels, bf16* out) {
-    const int C = x.c0 + x.c1;
-    const long long n = pixels * C;
+    const int nv = (x.c0 + x.c1) / 8;
+    const long long n = pixels * nv;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long p = i / C;
-        const int c = static_cast<int>(i % C);
-        out[i] = c < x.c0 ? x.p0[p * x.c0 + c] : x.p1[p * x.c1 + (c - x.c0)];
+        const long long p = i / nv;
+        reinterpret_cast<uint4*>(out)[i] = cat_vec(x, p, static_cast<int>(i - p * nv));
     }
 }
 
@@ -231,25 +360,43 @@ int grid_for(long long n, int threads = 256) {
 
 }  // namespace
 
+void check_vec8(const Cat2& x, const char* who) {
+    if ((x.c0 % 8) || (x.c1 % 8))
+        throw std::invalid_argument(std::string(who) + ": channel segments must be multiples of 8");
+}
+
 void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
                 int silu_act, __nv_bfloat16* out, float2* scratch, cudaStream_t st) {
     const int C = x.c0 + x.c1;
     if (C % groups) throw std::invalid_argument("group_norm: channels not divisible by groups");
-    const int chunks = (HW + kChunkPix - 1) / kChunkPix;
-    gn_partials<<<dim3(groups, chunks, batch), 256, 0, st>>>(x, HW, groups, chunks, scratch);
+    check_vec8(x, "group_norm");
+    const int nv = C / 8;
+    if (nv > 1024) throw std::invalid_argument("group_norm: more than 8192 channels");
+    const int chunk_pix = (HW + kGnMaxChunks - 1) / kGnMaxChunks;
+    const int chunks = (HW + chunk_pix - 1) / chunk_pix;
+    const int rpb = std::max(1, 512 / nv);
+    const int threads = rpb * nv, nsub = std::max(1, threads / (batch * groups));
+    size_t smem = static_cast<size_t>(2) * rpb * C * sizeof(float);
+    smem = std::max(smem, static_cast<size_t>(nsub) * batch * groups * 2 * sizeof(double));
+    if (smem > 48 * 1024) throw std::invalid_argument("group_norm: statistics tile exceeds 48 KB shared memory");
+    gn_stats<<<dim3(chunks, batch), threads, smem, st>>>(x, HW, groups, chunk_pix, chunks, gamma, beta, eps,
+                                                        scratch);
     CKU(cudaGetLastError());
-    const int ppb = std::max(1, 8192 / C);
-    gn_apply<<<dim3((HW + ppb - 1) / ppb, batch), 256, 2 * groups * sizeof(float), st>>>(
-        x, HW, groups, chunks, scratch, gamma, beta, eps, silu_act, out, ppb);
+    const GnLayout L = gn_layout(scratch, batch, C);
+    const long long pixels = static_cast<long long>(batch) * HW;
+    gn_apply<<<grid_for(pixels * nv), 256, 0, st>>>(x, pixels, HW, L.ab, silu_act, out);
     CKU(cudaGetLastError());
 }
 
-size_t group_norm_scratch_bytes(int batch, int HW, int groups) {
-    return static_cast<size_t>(batch) * ((HW + kChunkPix - 1) / kChunkPix) * groups * sizeof(float2);
+size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C) {
+    const int chunk_pix = (std::max(HW, 1) + kGnMaxChunks - 1) / kGnMaxChunks;
+    const int chunks = (HW + chunk_pix - 1) / chunk_pix;
+    return (8 + static_cast<size_t>(batch) * C + static_cast<size_t>(batch) * chunks * groups) * sizeof(float2);
 }
 
 void layer_norm(const __nv_bfloat16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
                 __nv_bfloat16* out, cudaStream_t st) {
+    if (C % 8 || C > 256 * kLnMaxVec) throw std::invalid_argument("layer_norm: C must be a multiple of 8, <= 2048");
     layernorm_k<<<(tokens + 7) / 8, 256, 0, st>>>(x, tokens, C, gamma, beta, eps, out);
     CKU(cudaGetLastError());
 }
@@ -261,17 +408,20 @@ void softmax_rows(const float* S, long long lds, int rows, int valid, __nv_bfloa
 }
 
 void geglu(const __nv_bfloat16* F, long long tokens, int H, __nv_bfloat16* out, cudaStream_t st) {
-    geglu_k<<<grid_for(tokens * H), 256, 0, st>>>(F, tokens, H, out);
+    if (H % 8) throw std::invalid_argument("geglu: hidden width must be a multiple of 8");
+    geglu_k<<<grid_for(tokens * H / 8), 256, 0, st>>>(F, tokens, H, out);
     CKU(cudaGetLastError());
 }
 
 void upsample2x(const __nv_bfloat16* x, int batch, int H, int W, int C, __nv_bfloat16* out, cudaStream_t st) {
-    upsample2x_k<<<grid_for(4LL * batch * H * W * C), 256, 0, st>>>(x, batch, H, W, C, out);
+    if (C % 8) throw std::invalid_argument("upsample2x: C must be a multiple of 8");
+    upsample2x_k<<<grid_for(4LL * batch * H * W * C / 8), 256, 0, st>>>(x, batch, H, W, C, out);
     CKU(cudaGetLastError());
 }
 
 void concat_channels(const Cat2& x, long long pixels, __nv_bfloat16* out, cudaStream_t st) {
-    concat_k<<<grid_for(pixels * (x.c0 + x.c1)), 256, 0, st>>>(x, pixels, out);
+    check_vec8(x, "concat_channels");
+    concat_k<<<grid_for(pixels * (x.c0 + x.c1) / 8), 256, 0, st>>>(x, pixels, out);
     CKU(cudaGetLastError());
 }
 

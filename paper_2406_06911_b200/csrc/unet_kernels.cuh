@@ -18,7 +18,8 @@ struct Cat2 {
 
 void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
                 int silu_act, __nv_bfloat16* out, float2* scratch, cudaStream_t st);
-size_t group_norm_scratch_bytes(int batch, int HW, int groups);
+// scratch for group_norm; must be zeroed once at allocation (holds a self-resetting ticket counter)
+size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C);
 void layer_norm(const __nv_bfloat16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
                 __nv_bfloat16* out, cudaStream_t st);
 void softmax_rows(const float* S, long long lds, int rows, int valid, __nv_bfloat16* P, long long ldp, int padded,
