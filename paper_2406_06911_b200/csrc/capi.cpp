@@ -240,6 +240,36 @@ adx::RunOptions to_opts(const adx_run_options* o) {
 
 }  // namespace
 
+// time `iters` back-to-back launches of fn(stream) replayed from one CUDA graph
+// (no host launch overhead between kernels), after one warm replay
+template <typename Fn>
+static double time_graph_ms(Fn fn, int iters) {
+    cudaStream_t st;
+    CKC(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    CKC(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) fn(st);
+    CKC(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t ge;
+    CKC(cudaGraphInstantiate(&ge, g, 0));
+    CKC(cudaGraphLaunch(ge, st));
+    cudaEvent_t e0, e1;
+    CKC(cudaEventCreate(&e0));
+    CKC(cudaEventCreate(&e1));
+    CKC(cudaEventRecord(e0, st));
+    CKC(cudaGraphLaunch(ge, st));
+    CKC(cudaEventRecord(e1, st));
+    CKC(cudaEventSynchronize(e1));
+    float ms = 0;
+    CKC(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(st);
+    return ms / iters;
+}
+
 extern "C" {
 
 const char* adx_last_error(void) { return g_err.c_str(); }
@@ -950,20 +980,8 @@ int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint1
         p.ldo = N;
         adx::tc_gemm(a.p, b.p, M, N, K, p, 0, bn);
         CKC(cudaDeviceSynchronize());
-        if (iters > 0 && ms_per_iter) {
-            cudaEvent_t e0, e1;
-            CKC(cudaEventCreate(&e0));
-            CKC(cudaEventCreate(&e1));
-            CKC(cudaEventRecord(e0));
-            for (int i = 0; i < iters; ++i) adx::tc_gemm(a.p, b.p, M, N, K, p, 0, bn);
-            CKC(cudaEventRecord(e1));
-            CKC(cudaEventSynchronize(e1));
-            float ms = 0;
-            CKC(cudaEventElapsedTime(&ms, e0, e1));
-            *ms_per_iter = ms / iters;
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-        }
+        if (iters > 0 && ms_per_iter)
+            *ms_per_iter = time_graph_ms([&](cudaStream_t st) { adx::tc_gemm(a.p, b.p, M, N, K, p, st, bn); }, iters);
         if (C) CKC(cudaMemcpy(C, c.p, static_cast<size_t>(M) * N * 4, cudaMemcpyDeviceToHost));
     });
 }
@@ -977,25 +995,12 @@ int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const
         CKC(cudaMemcpy(q.p, Q, static_cast<size_t>(L) * C * 2, cudaMemcpyHostToDevice));
         CKC(cudaMemcpy(k.p, K, static_cast<size_t>(Lk) * C * 2, cudaMemcpyHostToDevice));
         CKC(cudaMemcpy(v.p, VT, static_cast<size_t>(C) * ldvt * 2, cudaMemcpyHostToDevice));
-        auto run = [&] {
-            adx::tc_attention(q.p, C, k.p, C, v.p, ldvt, L, Lk, C, static_cast<__nv_bfloat16*>(o.p), C, 0);
+        auto run = [&](cudaStream_t st) {
+            adx::tc_attention(q.p, C, k.p, C, v.p, ldvt, L, Lk, C, static_cast<__nv_bfloat16*>(o.p), C, st);
         };
-        run();
+        run(0);
         CKC(cudaDeviceSynchronize());
-        if (iters > 0 && ms_per_iter) {
-            cudaEvent_t e0, e1;
-            CKC(cudaEventCreate(&e0));
-            CKC(cudaEventCreate(&e1));
-            CKC(cudaEventRecord(e0));
-            for (int i = 0; i < iters; ++i) run();
-            CKC(cudaEventRecord(e1));
-            CKC(cudaEventSynchronize(e1));
-            float ms = 0;
-            CKC(cudaEventElapsedTime(&ms, e0, e1));
-            *ms_per_iter = ms / iters;
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-        }
+        if (iters > 0 && ms_per_iter) *ms_per_iter = time_graph_ms(run, iters);
         if (out) CKC(cudaMemcpy(out, o.p, static_cast<size_t>(L) * C * 2, cudaMemcpyDeviceToHost));
     });
 }
@@ -1016,20 +1021,9 @@ int adx_tc_conv3x3(int ordinal, int batch, int H, int W, int Cin, int Cout, cons
         p.ldo = Cout;
         adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, 0);
         CKC(cudaDeviceSynchronize());
-        if (iters > 0 && ms_per_iter) {
-            cudaEvent_t e0, e1;
-            CKC(cudaEventCreate(&e0));
-            CKC(cudaEventCreate(&e1));
-            CKC(cudaEventRecord(e0));
-            for (int i = 0; i < iters; ++i) adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, 0);
-            CKC(cudaEventRecord(e1));
-            CKC(cudaEventSynchronize(e1));
-            float ms = 0;
-            CKC(cudaEventElapsedTime(&ms, e0, e1));
-            *ms_per_iter = ms / iters;
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-        }
+        if (iters > 0 && ms_per_iter)
+            *ms_per_iter = time_graph_ms(
+                [&](cudaStream_t st) { adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, st); }, iters);
         if (out) CKC(cudaMemcpy(out, o.p, no * 4, cudaMemcpyDeviceToHost));
     });
 }

@@ -22,7 +22,11 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -39,6 +43,7 @@ namespace adx {
 namespace {
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int kMaxSplitsDev = 8;  // split-K cluster size bound (portable cluster size)
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -122,6 +127,156 @@ constexpr uint32_t tmem_cols() {
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
+
+// --------------------------------------------------------------- epilogue
+// output row (pixel) of tile row `row`; false when the row is padding (or an odd
+// pixel of a stride-2 conv)
+template <bool CONV>
+__device__ __forceinline__ bool row_to_m(const TcArgs& p, int tile_m, int img, int h0, int w0, int row,
+                                         long long& m) {
+    if constexpr (CONV) {
+        const int hh = h0 + row / p.box_w, ww = w0 + row % p.box_w;
+        // rows past the box (box_w * box_h < 128) hold stale SMEM: computed, never stored
+        bool valid = row < p.box_w * p.box_h && hh < p.H && ww < p.W;
+        m = (static_cast<long long>(img) * p.H + hh) * p.W + ww;
+        if (p.sub2) {  // stride-2 conv: keep even pixels, write the half-resolution grid
+            valid = valid && !(hh & 1) && !(ww & 1);
+            m = (static_cast<long long>(img) * (p.H / 2) + hh / 2) * (p.W / 2) + ww / 2;
+        }
+        return valid;
+    } else {
+        m = static_cast<long long>(tile_m) * BM + row;
+        return m < p.M;
+    }
+}
+
+__device__ __forceinline__ uint4 pack_bf16x8(const float* v) {
+    uint32_t w4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+        w4[k] = *reinterpret_cast<const uint32_t*>(&b2);
+    }
+    return make_uint4(w4[0], w4[1], w4[2], w4[3]);
+}
+
+// fused epilogue on 16 accumulator columns [nb, nb + 16) of output row m
+__device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int nb, float* v) {
+    const int nlim = p.n_store ? p.n_store : p.N;
+    if ((((p.ldo | p.ldr) & 7) == 0) && nb + 16 <= nlim) {
+        // vectorised: 16-byte loads / stores
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+            if (p.bias) {
+                const float4 b = *reinterpret_cast<const float4*>(p.bias + nb + j);
+                v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
+            }
+            if (p.chan_add) {
+                const float4 b = *reinterpret_cast<const float4*>(p.chan_add + static_cast<long long>(img) * p.N + nb + j);
+                v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
+            }
+        }
+        if (p.act == 1) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = silu(v[j]);
+        }
+        if (p.residual) {
+            const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + nb);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint4 u = rp[h];
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[k]));
+                    v[h * 8 + 2 * k] += f.x;
+                    v[h * 8 + 2 * k + 1] += f.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] *= p.out_scale;
+        if (p.out_f32) {
+            float4* op = reinterpret_cast<float4*>(p.out_f32 + m * p.ldo + nb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) op[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        } else {
+            uint4* op = reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + nb);
+            op[0] = pack_bf16x8(v);
+            op[1] = pack_bf16x8(v + 8);
+        }
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int n = nb + j;
+        if (n >= nlim) continue;
+        float x = v[j];
+        if (p.bias) x += p.bias[n];
+        if (p.chan_add) x += p.chan_add[static_cast<long long>(img) * p.N + n];
+        if (p.act == 1) x = silu(x);
+        if (p.residual) x += __bfloat162float(p.residual[m * p.ldr + n]);
+        x *= p.out_scale;
+        if (p.out_f32)
+            p.out_f32[m * p.ldo + n] = x;
+        else
+            p.out_bf16[m * p.ldo + n] = __float2bfloat16(x);
+    }
+}
+
+// GEGLU epilogue: the host interleaved the weight rows per 256-wide tile, so tile
+// columns [0, 128) are hidden units n0/2 + c and [128, 256) their gates;
+// out[m][n0/2 + c] = (h + bh) * gelu(g + bg)  (the 2x-wide product never reaches HBM)
+__device__ __forceinline__ void epi_geglu16(const TcArgs& p, long long m, int n0, int c, float* v, float* g) {
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+        const float4 bh = *reinterpret_cast<const float4*>(p.bias + n0 + c + j);
+        const float4 bg = *reinterpret_cast<const float4*>(p.bias + n0 + 128 + c + j);
+        v[j] += bh.x, v[j + 1] += bh.y, v[j + 2] += bh.z, v[j + 3] += bh.w;
+        g[j] += bg.x, g[j + 1] += bg.y, g[j + 2] += bg.z, g[j + 3] += bg.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] *= gelu(g[j]);
+    uint4* op = reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + n0 / 2 + c);
+    op[0] = pack_bf16x8(v);
+    op[1] = pack_bf16x8(v + 8);
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of `local` in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+// not volatile / no memory clobber: the staged partials are immutable between the two
+// cluster barriers, so the compiler may batch these remote loads (latency ~200 cycles)
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+    float4 v;
+    asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+// sum of float4 #j4 of the staged row chunk over all S CTAs, in split order 0..S-1:
+// all S loads are issued before the (fixed-order) additions
+__device__ __forceinline__ float4 reduce_dsmem4(const uint32_t* a, int S, int off) {
+    float4 x[kMaxSplitsDev];
+#pragma unroll
+    for (int r = 0; r < kMaxSplitsDev; ++r)
+        if (r < S) x[r] = ld_dsmem4(a[r] + off);
+    float4 acc = x[0];
+#pragma unroll
+    for (int r = 1; r < kMaxSplitsDev; ++r)
+        if (r < S) acc.x += x[r].x, acc.y += x[r].y, acc.z += x[r].z, acc.w += x[r].w;
+    return acc;
+}
+
 // ------------------------------------------------------------------ kernel
 template <int BN, bool CONV>
 __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -138,9 +293,14 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
     uint32_t* tptr = reinterpret_cast<uint32_t*>(tfull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile_m = blockIdx.x, tile_n = blockIdx.y, img = blockIdx.z;
+    // split-K: the p.splits CTAs of one output tile form a cluster along x; CTA
+    // `split` contracts k blocks [kb0, kb1) and the partials are reduced over DSMEM
+    const int S = p.splits;
+    const int tile_m = blockIdx.x / S, split = blockIdx.x - (blockIdx.x / S) * S;
+    const int tile_n = blockIdx.y, img = blockIdx.z;
     const int n0 = tile_n * BN;
-    const int nkb = p.k_blocks;
+    const int kb0 = (p.k_blocks * split) / S, kb1 = (p.k_blocks * (split + 1)) / S;
+    const int nkb = kb1 - kb0;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -173,11 +333,11 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
 
     if (warp == 0 && lane == 0) {
         // ---------------------------------------------------------- producer
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % STAGES;
-            const uint32_t ph = (kb / STAGES) & 1;
+        for (int i = 0; i < nkb; ++i) {
+            const int kb = kb0 + i, s = i % STAGES;
+            const uint32_t ph = (i / STAGES) & 1;
             bar_wait(&empty[s], ph ^ 1);
-            bar_expect(&full[s], A_BYTES + B_BYTES);
+            bar_expect(&full[s], (CONV ? p.box_w * p.box_h * BK * 2 : A_BYTES) + B_BYTES);
             if constexpr (CONV) {
                 // k block kb -> tap (r, s) and channel block; A box at the
                 // tap-shifted window (OOB rows/cols are zero-filled = padding)
@@ -194,16 +354,16 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------------- MMA issuer
         constexpr uint32_t idesc = idesc_bf16<BN>();
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % STAGES;
-            const uint32_t ph = (kb / STAGES) & 1;
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = (i / STAGES) & 1;
             bar_wait(&full[s], ph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
                 const uint64_t a = sdesc(sA + s * A_BYTES + k * 32);
                 const uint64_t b = sdesc(sB + s * B_BYTES + k * 32);
-                mma_bf16(tmem, a, b, idesc, (kb | k) != 0 ? 1u : 0u);
+                mma_bf16(tmem, a, b, idesc, (i | k) != 0 ? 1u : 0u);
             }
             mma_commit(&empty[s]);
         }
@@ -214,126 +374,77 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
         const int row = q * 32 + lane;
-        long long m;  // output row (pixel) index
-        bool valid;
-        if constexpr (CONV) {
-            const int hh = h0 + row / p.box_w, ww = w0 + row % p.box_w;
-            valid = hh < p.H && ww < p.W;
-            m = (static_cast<long long>(img) * p.H + hh) * p.W + ww;
-            if (p.sub2) {  // stride-2 conv: keep even pixels, write the half-resolution grid
-                valid = valid && !(hh & 1) && !(ww & 1);
-                m = (static_cast<long long>(img) * (p.H / 2) + hh / 2) * (p.W / 2) + ww / 2;
+        const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        if (S > 1) {
+            // stage this CTA's fp32 partial in its own SMEM (the drained pipeline
+            // buffers), rows padded by 4 floats so 8 lanes' float4 stores hit 32 banks
+            float* stg = reinterpret_cast<float*>(smem) + row * (BN + 4);
+            for (int c = 0; c < BN; c += 16) {
+                float v[16];
+                tmem_ld16(trow + c, v);
+#pragma unroll
+                for (int j = 0; j < 16; j += 4)
+                    *reinterpret_cast<float4*>(stg + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
             }
         } else {
-            m = static_cast<long long>(tile_m) * BM + row;
-            valid = m < p.M;
+            long long m;
+            const bool valid = row_to_m<CONV>(p, tile_m, img, h0, w0, row, m);
+            if (p.act == 2) {
+                for (int c = 0; c < BN / 2; c += 16) {
+                    float v[16], g[16];
+                    tmem_ld16(trow + c, v);
+                    tmem_ld16(trow + BN / 2 + c, g);
+                    if (valid) epi_geglu16(p, m, n0, c, v, g);
+                }
+            } else {
+                for (int c = 0; c < BN; c += 16) {
+                    float v[16];
+                    tmem_ld16(trow + c, v);
+                    if (valid) epi16(p, m, img, n0 + c, v);
+                }
+            }
         }
-        const int nlim = p.n_store ? p.n_store : p.N;
-        const bool vec_ok = ((p.ldo | p.ldr) & 7) == 0;
-        if (p.act == 2) {
-            // GEGLU: the host interleaved the weight rows per tile, so columns [0, BN/2)
-            // of this tile are hidden units n0/2 + c and [BN/2, BN) their gates;
-            // out[m][n0/2 + c] = (h + bh) * gelu(g + bg)  (the 2x-wide product never reaches HBM)
-            for (int c = 0; c < BN / 2; c += 16) {
-                float v[16], g[16];
-                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + BN / 2 + c, g);
+    }
+    if (S > 1) {
+        // split-K reduction: CTA `split` owns tile rows [r0, r1) and sums the S staged
+        // partials in split order 0..S-1 over DSMEM (fixed order: deterministic)
+        __syncwarp();
+        cluster_sync_all();
+        if (warp >= 2) {
+            const int r0 = (BM * split) / S, r1 = (BM * (split + 1)) / S;
+            const uint32_t base = sa(smem);
+            const int et = threadIdx.x - 64;  // 0..127
+            const int cols = p.act == 2 ? BN / 2 : BN, chunks = cols / 16;
+            for (int it = et; it < (r1 - r0) * chunks; it += 128) {
+                const int row = r0 + it / chunks, c = (it % chunks) * 16;
+                long long m;
+                const bool valid = row_to_m<CONV>(p, tile_m, img, h0, w0, row, m);
                 if (!valid) continue;
+                float v[16], g[16];
+                uint32_t a[kMaxSplitsDev];
+#pragma unroll
+                for (int r = 0; r < kMaxSplitsDev; ++r)
+                    a[r] = mapa(base + static_cast<uint32_t>((row * (BN + 4) + c) * 4), r < S ? r : 0);
 #pragma unroll
                 for (int j = 0; j < 16; j += 4) {
-                    const float4 bh = *reinterpret_cast<const float4*>(p.bias + n0 + c + j);
-                    const float4 bg = *reinterpret_cast<const float4*>(p.bias + n0 + BN / 2 + c + j);
-                    v[j] += bh.x, v[j + 1] += bh.y, v[j + 2] += bh.z, v[j + 3] += bh.w;
-                    g[j] += bg.x, g[j + 1] += bg.y, g[j + 2] += bg.z, g[j + 3] += bg.w;
+                    const float4 x = reduce_dsmem4(a, S, j * 4);
+                    v[j] = x.x, v[j + 1] = x.y, v[j + 2] = x.z, v[j + 3] = x.w;
                 }
-                uint4* op = reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + n0 / 2 + c);
+                if (p.act == 2) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t w4[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int j = h * 8 + 2 * k;
-                        const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[j] * gelu(g[j]), v[j + 1] * gelu(g[j + 1]));
-                        w4[k] = *reinterpret_cast<const uint32_t*>(&b2);
-                    }
-                    op[h] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-                }
-            }
-        } else
-        for (int c = 0; c < BN; c += 16) {
-            float v[16];
-            tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-            if (!valid) continue;
-            const int nb = n0 + c;
-            if (vec_ok && nb + 16 <= nlim) {
-                // vectorised epilogue: 16 consecutive columns of this row, 16-byte loads / stores
-#pragma unroll
-                for (int j = 0; j < 16; j += 4) {
-                    if (p.bias) {
-                        const float4 b = *reinterpret_cast<const float4*>(p.bias + nb + j);
-                        v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
-                    }
-                    if (p.chan_add) {
-                        const float4 b =
-                            *reinterpret_cast<const float4*>(p.chan_add + static_cast<long long>(img) * p.N + nb + j);
-                        v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
+                    for (int j = 0; j < 16; j += 4) {
+                        const float4 x = reduce_dsmem4(a, S, (BN / 2 + j) * 4);
+                        g[j] = x.x, g[j + 1] = x.y, g[j + 2] = x.z, g[j + 3] = x.w;
                     }
                 }
-                if (p.act == 1) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = silu(v[j]);
-                }
-                if (p.residual) {
-                    const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + nb);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const uint4 u = rp[h];
-                        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[k]));
-                            v[h * 8 + 2 * k] += f.x;
-                            v[h * 8 + 2 * k + 1] += f.y;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] *= p.out_scale;
-                if (p.out_f32) {
-                    float4* op = reinterpret_cast<float4*>(p.out_f32 + m * p.ldo + nb);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) op[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                } else {
-                    uint4* op = reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + nb);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t w4[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[h * 8 + 2 * k], v[h * 8 + 2 * k + 1]);
-                            w4[k] = *reinterpret_cast<const uint32_t*>(&b2);
-                        }
-                        op[h] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-                    }
-                }
-                continue;
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int n = n0 + c + j;
-                if (n >= (p.n_store ? p.n_store : p.N)) continue;
-                float x = v[j];
-                if (p.bias) x += p.bias[n];
-                if (p.chan_add) x += p.chan_add[static_cast<long long>(img) * p.N + n];
-                if (p.act == 1) x = silu(x);
-                if (p.residual) x += __bfloat162float(p.residual[m * p.ldr + n]);
-                x *= p.out_scale;
-                if (p.out_f32)
-                    p.out_f32[m * p.ldo + n] = x;
+                if (p.act == 2)
+                    epi_geglu16(p, m, n0, c, v, g);
                 else
-                    p.out_bf16[m * p.ldo + n] = __float2bfloat16(x);
+                    epi16(p, m, img, n0 + c, v);
             }
         }
+        __syncwarp();
+        cluster_sync_all();  // keep every CTA's SMEM alive until all slices are reduced
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -376,6 +487,8 @@ CUtensorMap make_map(const void* base, int rank, const cuuint64_t* dims, const c
 template <int BN, bool CONV>
 void launch_t(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 grid, cudaStream_t st) {
     constexpr size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256;
+    static_assert(static_cast<size_t>(BM) * (BN + 4) * 4 <= STAGES * (BM * BK * 2 + BN * BK * 2),
+                  "split-K staging must fit in the pipeline buffers");
     static bool attr[64] = {};
     int dev = 0;
     CKT(cudaGetDevice(&dev));
@@ -383,8 +496,19 @@ void launch_t(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 
         CKT(cudaFuncSetAttribute(tc_gemm_kernel<BN, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr[dev] = true;
     }
-    tc_gemm_kernel<BN, CONV><<<grid, 192, smem, st>>>(a, b, p);
-    CKT(cudaGetLastError());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(192, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(p.splits);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = p.splits > 1 ? 1 : 0;  // plain launch when the tile is not split
+    CKT(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CONV>, a, b, p));
 }
 
 template <bool CONV>
@@ -400,20 +524,91 @@ void dispatch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 
     }
 }
 
-// N tile: least padded columns, ties to the wider tile (fewer CTAs re-reading A)
-int pick_bn(int N) {
-    if (N <= 32) return 32;
-    if (N <= 64) return 64;
-    int best = 256;
-    long long waste = (N + 255) / 256 * 256LL - N;
-    for (int bn : {192, 160, 128}) {
-        const long long w = (N + bn - 1) / bn * static_cast<long long>(bn) - N;
-        if (w < waste) {
-            waste = w;
-            best = bn;
+constexpr int kSMs = 148;
+
+// ADX_TC_TRACE=1: print every launch's tile plan to stderr
+bool tc_trace() {
+    static const bool on = [] {
+        const char* e = getenv("ADX_TC_TRACE");
+        return e && *e == '1';
+    }();
+    return on;
+}
+constexpr int kMaxSplits = kMaxSplitsDev;
+
+// How many S-CTA clusters of tc_gemm_kernel<BN, CONV> the GPU holds at once
+// (clusters must fit inside one GPC: e.g. 7-CTA clusters at 1 CTA/SM leave SMs idle)
+template <int BN, bool CONV>
+int cluster_capacity_t(int S) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> cache;
+    int dev = 0;
+    CKT(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({dev, S});
+    if (it != cache.end()) return it->second;
+    constexpr size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256;
+    CKT(cudaFuncSetAttribute(tc_gemm_kernel<BN, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(S * 64, 1, 1);
+    cfg.blockDim = dim3(192, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(S);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, tc_gemm_kernel<BN, CONV>, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = kSMs / S;  // fall back to the ideal packing
+    }
+    cache[{dev, S}] = n;
+    return n;
+}
+
+template <bool CONV>
+int cluster_capacity(int bn, int S) {
+    switch (bn) {
+        case 32: return cluster_capacity_t<32, CONV>(S);
+        case 64: return cluster_capacity_t<64, CONV>(S);
+        case 128: return cluster_capacity_t<128, CONV>(S);
+        case 160: return cluster_capacity_t<160, CONV>(S);
+        case 192: return cluster_capacity_t<192, CONV>(S);
+        default: return cluster_capacity_t<256, CONV>(S);
+    }
+}
+
+// N tile and split-K factor minimising the modelled time
+//   waves x (BN + 64) x ceil(k_blocks / S) x (1.15 if split) (+ 2 k-blocks of reduction)
+// where waves = ceil(tiles / concurrent S-clusters) (occupancy query, so GPC packing
+// is accounted for) and 64 models the per-tile A-operand cost a narrower tile
+// amortises worse.  Every split stages a 128 x BN fp32 partial that the cluster
+// reduces over DSMEM -- only worth it when the unsplit grid leaves SMs idle.
+// bn_fixed != 0 pins the tile width.
+template <bool CONV>
+void tile_plan(int m_tiles, int N, int batch, int k_blocks, int bn_fixed, int& bn_out, int& s_out) {
+    double best = 1e300;
+    for (int bn : {256, 192, 160, 128, 64, 32}) {
+        if (bn_fixed && bn != bn_fixed) continue;
+        if (!bn_fixed && bn < 128 && N > 2 * bn) continue;  // narrow tiles only for narrow outputs
+        const long long tiles = static_cast<long long>(m_tiles) * ((N + bn - 1) / bn) * batch;
+        for (int S = 1; S <= kMaxSplits; ++S) {
+            if (S > 1 && (k_blocks / S < 4 || tiles >= kSMs)) break;
+            const long long cap = std::max(1, cluster_capacity<CONV>(bn, S));
+            const long long waves = (tiles + cap - 1) / cap;
+            const double t = static_cast<double>(waves) * (bn + 64) * ((k_blocks + S - 1) / S) *
+                                 (S > 1 ? 1.15 : 1.0) +
+                             (S > 1 ? 2.0 * (bn + 64) : 0.0);
+            if (t < best - 1e-9) {
+                best = t;
+                bn_out = bn;
+                s_out = S;
+            }
         }
     }
-    return best;
 }
 
 struct ProfRec {
@@ -476,7 +671,8 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
             throw std::invalid_argument("tc_gemm: GEGLU epilogue needs N % 256 == 0, bias, bf16 output, ldo % 8 == 0");
         bn = 256;
     }
-    if (bn == 0) bn = pick_bn(N);
+    int S = 1;
+    tile_plan<false>((M + BM - 1) / BM, N, 1, K / BK, bn, bn, S);
     const cuuint64_t da[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
     const cuuint64_t sa_[1] = {static_cast<cuuint64_t>(lda) * 2};
     const cuuint64_t sb_[1] = {static_cast<cuuint64_t>(ldb) * 2};
@@ -487,7 +683,9 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     p.M = M;
     p.N = N;
     p.k_blocks = K / BK;
-    dim3 grid((M + BM - 1) / BM, (N + bn - 1) / bn, 1);
+    p.splits = S;
+    dim3 grid(((M + BM - 1) / BM) * S, (N + bn - 1) / bn, 1);
+    if (tc_trace()) fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d grid=%ux%u\n", M, N, K, bn, S, grid.x, grid.y);
     tc_profile_record_begin(st);
     dispatch<false>(ma, mb, p, grid, bn, st);
     tc_profile_record_end(st, 1, 2.0 * M * N * K);
@@ -500,15 +698,28 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
 void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin, int Cout, TcArgs p,
                 cudaStream_t st, int bn) {
     if (Cin % BK) throw std::invalid_argument("tc_conv3x3: Cin must be a multiple of 64");
-    int bw = 0;
-    for (int c : {128, 64, 32, 16, 8, 4})
-        if (W % c == 0 && c <= W && BM % c == 0) {
-            bw = c;
-            break;
+    // box = bw columns x bh rows of output pixels, bw | W, bw * bh <= 128 and a multiple
+    // of 8 (whole 1024-byte swizzle atoms); minimise the MMA rows computed per image
+    // (e.g. 24 x 24 -> 24 x 5 boxes: 640 rows, not 768 with 8 x 16)
+    int bw = 0, bh = 0;
+    long long best_rows = 0;
+    for (int c = std::min(W, BM); c >= 1; --c) {
+        if (W % c) continue;
+        for (int r = std::min(BM / c, H); r >= 1; --r) {
+            if ((c * r) % 8) continue;
+            const long long rows = static_cast<long long>((H + r - 1) / r) * (W / c) * BM;
+            if (!bw || rows < best_rows || (rows == best_rows && c * r > bw * bh)) {
+                bw = c;
+                bh = r;
+                best_rows = rows;
+            }
+            break;  // the tallest legal box for this width
         }
-    if (!bw) throw std::invalid_argument("tc_conv3x3: W must be divisible by 8, 16, 32, 64 or 128");
-    const int bh = BM / bw;
-    if (bn == 0) bn = pick_bn(Cout);
+    }
+    if (!bw) throw std::invalid_argument("tc_conv3x3: no legal TMA box for this image width");
+    const int m_tiles = ((H + bh - 1) / bh) * (W / bw);
+    int S = 1;
+    tile_plan<true>(m_tiles, Cout, batch, 9 * Cin / BK, bn, bn, S);
     const cuuint64_t dx[4] = {static_cast<cuuint64_t>(Cin), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                               static_cast<cuuint64_t>(batch)};
     const cuuint64_t sx[3] = {static_cast<cuuint64_t>(Cin) * 2, static_cast<cuuint64_t>(W) * Cin * 2,
@@ -527,7 +738,11 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     p.box_w = bw;
     p.box_h = bh;
     p.cin = Cin;
-    dim3 grid(((H + bh - 1) / bh) * (W / bw), (Cout + bn - 1) / bn, batch);
+    p.splits = S;
+    dim3 grid(m_tiles * S, (Cout + bn - 1) / bn, batch);
+    if (tc_trace())
+        fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u\n", H, W, Cin, Cout, bw, bh, bn, S,
+                grid.x, grid.y, grid.z);
     tc_profile_record_begin(st);
     dispatch<true>(ma, mb, p, grid, bn, st);
     // algorithmic FLOPs (a stride-2 conv does a quarter of the work it launches)

@@ -27,6 +27,7 @@ struct TcArgs {
     long long ldo = 0;
     int sub2 = 0;                         // conv: write only even (h, w) at (h/2, w/2) -> stride-2 conv
     int n_store = 0;                      // store only the first n_store columns (0: all N)
+    int splits = 1;                       // filled by the launcher: split-K factor (cluster size)
 };
 
 // In-run kernel profiling (eager passes only): when enabled, every tensor-core
@@ -39,6 +40,8 @@ void tc_profile_record_end(cudaStream_t st, int kind, double flops);
 void tc_profile_collect(double out[3][3]);
 
 // D[M x N] = A[M x K] . B[N x K]^T (bf16 in, fp32 accumulate in TMEM); bn = 0 picks the tile width
+// and the split-K factor jointly (tile_plan); small-M layers are split over K across a
+// thread-block cluster and reduced deterministically over DSMEM
 void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn = 0);
 // same with explicit row strides (elements; multiples of 8) -- e.g. one head's slice of a packed QKV
 void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,

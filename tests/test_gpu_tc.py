@@ -44,7 +44,10 @@ def run_gemm(A, B, bias=None, act=0, bn=0):
 
 
 @pytest.mark.parametrize("M,N,K,bn", [(128, 128, 64, 0), (256, 320, 640, 0), (1000, 200, 128, 0),
-                                      (384, 512, 1024, 256), (130, 64, 192, 64), (128, 40, 64, 32)])
+                                      (384, 512, 1024, 256), (130, 64, 192, 64), (128, 40, 64, 32),
+                                      # small M, long K: split-K over a cluster, DSMEM reduction
+                                      (256, 512, 4096, 0), (144, 1280, 11520, 0), (100, 96, 2048, 0),
+                                      (576, 640, 5760, 160)])
 def test_tc_gemm_matches_fp32_reference(M, N, K, bn):
     rng = np.random.default_rng(M + N + K)
     A = rng.standard_normal((M, K)).astype(np.float32)
@@ -52,6 +55,15 @@ def test_tc_gemm_matches_fp32_reference(M, N, K, bn):
     out, ref = run_gemm(A, B, bn=bn)
     err = np.abs(out - ref).max() / (np.abs(ref).max() + 1e-6)
     assert err < 2e-3, err
+
+
+def test_tc_gemm_split_k_is_deterministic():
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((144, 5760)).astype(np.float32)
+    B = rng.standard_normal((1280, 5760)).astype(np.float32) / 76.0
+    o1, _ = run_gemm(A, B)
+    o2, _ = run_gemm(A, B)
+    assert np.array_equal(o1, o2)
 
 
 def test_tc_gemm_bias_silu_epilogue():
@@ -63,7 +75,11 @@ def test_tc_gemm_bias_silu_epilogue():
     assert np.abs(out - ref).max() / np.abs(ref).max() < 2e-3
 
 
-@pytest.mark.parametrize("batch,H,W,Cin,Cout", [(1, 16, 16, 64, 64), (2, 24, 24, 128, 192), (1, 12, 48, 64, 320)])
+@pytest.mark.parametrize("batch,H,W,Cin,Cout", [(1, 16, 16, 64, 64), (2, 24, 24, 128, 192), (1, 12, 48, 64, 320),
+                                                 # low-resolution levels: split-K conv
+                                                 (1, 12, 12, 1280, 1280), (1, 24, 24, 640, 640),
+                                                 # widths that do not divide 128: partial (< 128-row) boxes
+                                                 (1, 7, 20, 64, 64), (2, 10, 6, 128, 96)])
 def test_tc_conv3x3_matches_fp32_reference(batch, H, W, Cin, Cout):
     rng = np.random.default_rng(batch * H + Cin)
     X = rng.standard_normal((batch, H, W, Cin)).astype(np.float32)
