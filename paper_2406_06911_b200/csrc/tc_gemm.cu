@@ -59,6 +59,9 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void bar_arrive1(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
+}
 __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes) : "memory");
 }
@@ -285,36 +288,64 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
     // 1024-byte alignment of the swizzled tiles
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
+    constexpr uint32_t ACC_COLS = tmem_cols<BN>();  // one accumulator; two are allocated
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(tfull + 1);
+    uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
+    uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // split-K: the p.splits CTAs of one output tile form a cluster along x; CTA
-    // `split` contracts k blocks [kb0, kb1) and the partials are reduced over DSMEM
+    // Work units.  S == 1: persistent -- CTA b takes output tiles b, b + G, ... (m fastest,
+    // so the CTAs in flight share the B tile) with the TMEM accumulator double-buffered:
+    // the epilogue of one tile overlaps the mainloop of the next.  S > 1 (split-K): the
+    // S CTAs of one tile form a cluster along x, one unit each; CTA `split` contracts
+    // k blocks [kb0, kb1) and the partials are reduced over DSMEM below.
     const int S = p.splits;
-    const int tile_m = blockIdx.x / S, split = blockIdx.x - (blockIdx.x / S) * S;
-    const int tile_n = blockIdx.y, img = blockIdx.z;
-    const int n0 = tile_n * BN;
+    const int split = S > 1 ? static_cast<int>(blockIdx.x % S) : 0;
+    int u0, ustride, uend;
+    if (S == 1) {
+        u0 = blockIdx.x;
+        ustride = gridDim.x;
+        uend = p.m_tiles * p.n_tiles * p.batch;
+    } else {
+        u0 = static_cast<int>(blockIdx.x / S) + p.m_tiles * (blockIdx.y + p.n_tiles * blockIdx.z);
+        ustride = 1;
+        uend = u0 + 1;
+    }
     const int kb0 = (p.k_blocks * split) / S, kb1 = (p.k_blocks * (split + 1)) / S;
     const int nkb = kb1 - kb0;
+    auto coords = [&](int u, int& tile_m, int& tile_n, int& img, int& h0, int& w0) {
+        tile_m = u % p.m_tiles;
+        const int r = u / p.m_tiles;
+        tile_n = r % p.n_tiles;
+        img = r / p.n_tiles;
+        h0 = w0 = 0;
+        if constexpr (CONV) {  // conv tile origin: box_h rows x box_w cols of one image
+            const int tiles_w = p.W / p.box_w;
+            h0 = (tile_m / tiles_w) * p.box_h;
+            w0 = (tile_m % tiles_w) * p.box_w;
+        }
+    };
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             bar_init(&full[s], 1);
             bar_init(&empty[s], 1);
         }
-        bar_init(tfull, 1);
+        for (int a = 0; a < 2; ++a) {
+            bar_init(&tfull[a], 1);
+            bar_init(&tempty[a], 4);  // one arrival per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tptr)),
-                     "n"(tmem_cols<BN>())
+                     "n"(2 * ACC_COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -323,86 +354,102 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tptr;
 
-    // conv tile origin (output pixels of one image: box_h rows x box_w cols)
-    int h0 = 0, w0 = 0;
-    if constexpr (CONV) {
-        const int tiles_w = p.W / p.box_w;
-        h0 = (tile_m / tiles_w) * p.box_h;
-        w0 = (tile_m % tiles_w) * p.box_w;
-    }
-
     if (warp == 0 && lane == 0) {
         // ---------------------------------------------------------- producer
-        for (int i = 0; i < nkb; ++i) {
-            const int kb = kb0 + i, s = i % STAGES;
-            const uint32_t ph = (i / STAGES) & 1;
-            bar_wait(&empty[s], ph ^ 1);
-            bar_expect(&full[s], (CONV ? p.box_w * p.box_h * BK * 2 : A_BYTES) + B_BYTES);
-            if constexpr (CONV) {
-                // k block kb -> tap (r, s) and channel block; A box at the
-                // tap-shifted window (OOB rows/cols are zero-filled = padding)
-                const int cpb = p.cin / BK;
-                const int tap = kb / cpb, cb = kb - tap * cpb;
-                const int dr = tap / 3 - 1, ds = tap % 3 - 1;
-                tma4d(sA + s * A_BYTES, &tmA, cb * BK, w0 + ds, h0 + dr, img, &full[s]);
-                tma2d(sB + s * B_BYTES, &tmB, kb * BK, n0, &full[s]);
-            } else {
-                tma2d(sA + s * A_BYTES, &tmA, kb * BK, tile_m * BM, &full[s]);
-                tma2d(sB + s * B_BYTES, &tmB, kb * BK, n0, &full[s]);
+        int it = 0;  // ring position, continuous across tiles
+        for (int u = u0; u < uend; u += ustride) {
+            int tile_m, tile_n, img, h0, w0;
+            coords(u, tile_m, tile_n, img, h0, w0);
+            const int n0 = tile_n * BN;
+            for (int i = 0; i < nkb; ++i, ++it) {
+                const int kb = kb0 + i, s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                bar_wait(&empty[s], ph ^ 1);
+                bar_expect(&full[s], (CONV ? p.box_w * p.box_h * BK * 2 : A_BYTES) + B_BYTES);
+                if constexpr (CONV) {
+                    // k block kb -> tap (r, s) and channel block; A box at the
+                    // tap-shifted window (OOB rows/cols are zero-filled = padding)
+                    const int cpb = p.cin / BK;
+                    const int tap = kb / cpb, cb = kb - tap * cpb;
+                    const int dr = tap / 3 - 1, ds = tap % 3 - 1;
+                    tma4d(sA + s * A_BYTES, &tmA, cb * BK, w0 + ds, h0 + dr, img, &full[s]);
+                    tma2d(sB + s * B_BYTES, &tmB, kb * BK, n0, &full[s]);
+                } else {
+                    tma2d(sA + s * A_BYTES, &tmA, kb * BK, tile_m * BM, &full[s]);
+                    tma2d(sB + s * B_BYTES, &tmB, kb * BK, n0, &full[s]);
+                }
             }
         }
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------------- MMA issuer
         constexpr uint32_t idesc = idesc_bf16<BN>();
-        for (int i = 0; i < nkb; ++i) {
-            const int s = i % STAGES;
-            const uint32_t ph = (i / STAGES) & 1;
-            bar_wait(&full[s], ph);
+        int it = 0, lu = 0;
+        for (int u = u0; u < uend; u += ustride, ++lu) {
+            const int acc = lu & 1;
+            bar_wait(&tempty[acc], ((lu >> 1) & 1) ^ 1);  // the epilogue drained this accumulator
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t tacc = tmem + acc * ACC_COLS;
+            for (int i = 0; i < nkb; ++i, ++it) {
+                const int s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                bar_wait(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-                const uint64_t a = sdesc(sA + s * A_BYTES + k * 32);
-                const uint64_t b = sdesc(sB + s * B_BYTES + k * 32);
-                mma_bf16(tmem, a, b, idesc, (i | k) != 0 ? 1u : 0u);
+                for (int k = 0; k < BK / 16; ++k) {
+                    const uint64_t a = sdesc(sA + s * A_BYTES + k * 32);
+                    const uint64_t b = sdesc(sB + s * B_BYTES + k * 32);
+                    mma_bf16(tacc, a, b, idesc, (i | k) != 0 ? 1u : 0u);
+                }
+                mma_commit(&empty[s]);
             }
-            mma_commit(&empty[s]);
+            mma_commit(&tfull[acc]);
         }
-        mma_commit(tfull);
     } else if (warp >= 2) {
         // --------------------------------------------------------- epilogue
-        bar_wait(tfull, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
         const int row = q * 32 + lane;
-        const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        if (S > 1) {
-            // stage this CTA's fp32 partial in its own SMEM (the drained pipeline
-            // buffers), rows padded by 4 floats so 8 lanes' float4 stores hit 32 banks
-            float* stg = reinterpret_cast<float*>(smem) + row * (BN + 4);
-            for (int c = 0; c < BN; c += 16) {
-                float v[16];
-                tmem_ld16(trow + c, v);
-#pragma unroll
-                for (int j = 0; j < 16; j += 4)
-                    *reinterpret_cast<float4*>(stg + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            }
-        } else {
-            long long m;
-            const bool valid = row_to_m<CONV>(p, tile_m, img, h0, w0, row, m);
-            if (p.act == 2) {
-                for (int c = 0; c < BN / 2; c += 16) {
-                    float v[16], g[16];
-                    tmem_ld16(trow + c, v);
-                    tmem_ld16(trow + BN / 2 + c, g);
-                    if (valid) epi_geglu16(p, m, n0, c, v, g);
-                }
-            } else {
+        int lu = 0;
+        for (int u = u0; u < uend; u += ustride, ++lu) {
+            int tile_m, tile_n, img, h0, w0;
+            coords(u, tile_m, tile_n, img, h0, w0);
+            const int n0 = tile_n * BN;
+            const int acc = lu & 1;
+            bar_wait(&tfull[acc], (lu >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t trow = tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16);
+            if (S > 1) {
+                // stage this CTA's fp32 partial in its own SMEM (the drained pipeline
+                // buffers), rows padded by 4 floats so 8 lanes' float4 stores hit 32 banks
+                float* stg = reinterpret_cast<float*>(smem) + row * (BN + 4);
                 for (int c = 0; c < BN; c += 16) {
                     float v[16];
                     tmem_ld16(trow + c, v);
-                    if (valid) epi16(p, m, img, n0 + c, v);
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(stg + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                }
+            } else {
+                long long m;
+                const bool valid = row_to_m<CONV>(p, tile_m, img, h0, w0, row, m);
+                if (p.act == 2) {
+                    for (int c = 0; c < BN / 2; c += 16) {
+                        float v[16], g[16];
+                        tmem_ld16(trow + c, v);
+                        tmem_ld16(trow + BN / 2 + c, g);
+                        if (valid) epi_geglu16(p, m, n0, c, v, g);
+                    }
+                } else {
+                    for (int c = 0; c < BN; c += 16) {
+                        float v[16];
+                        tmem_ld16(trow + c, v);
+                        if (valid) epi16(p, m, img, n0 + c, v);
+                    }
                 }
             }
+            // hand the accumulator back to the MMA warp
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) bar_arrive1(&tempty[acc]);
         }
     }
     if (S > 1) {
@@ -411,6 +458,9 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
         __syncwarp();
         cluster_sync_all();
         if (warp >= 2) {
+            int tile_m, tile_n, img, h0, w0;
+            coords(u0, tile_m, tile_n, img, h0, w0);
+            const int n0 = tile_n * BN;
             const int r0 = (BM * split) / S, r1 = (BM * (split + 1)) / S;
             const uint32_t base = sa(smem);
             const int et = threadIdx.x - 64;  // 0..127
@@ -450,7 +500,7 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tmem_cols<BN>())
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * ACC_COLS)
                      : "memory");
 }
 
@@ -581,6 +631,14 @@ int cluster_capacity(int bn, int S) {
     }
 }
 
+// S == 1: persistent grid of min(tiles, resident CTAs); S > 1: one CTA per (tile, split)
+template <bool CONV>
+dim3 launch_grid(const TcArgs& p, int bn) {
+    const long long tiles = static_cast<long long>(p.m_tiles) * p.n_tiles * p.batch;
+    if (p.splits > 1) return dim3(p.m_tiles * p.splits, p.n_tiles, p.batch);
+    return dim3(static_cast<unsigned>(std::min<long long>(tiles, cluster_capacity<CONV>(bn, 1))), 1, 1);
+}
+
 // N tile and split-K factor minimising the modelled time
 //   waves x (BN + 64) x ceil(k_blocks / S) x (1.15 if split) (+ 2 k-blocks of reduction)
 // where waves = ceil(tiles / concurrent S-clusters) (occupancy query, so GPC packing
@@ -684,7 +742,10 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     p.N = N;
     p.k_blocks = K / BK;
     p.splits = S;
-    dim3 grid(((M + BM - 1) / BM) * S, (N + bn - 1) / bn, 1);
+    p.m_tiles = (M + BM - 1) / BM;
+    p.n_tiles = (N + bn - 1) / bn;
+    p.batch = 1;
+    const dim3 grid = launch_grid<false>(p, bn);
     if (tc_trace()) fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d grid=%ux%u\n", M, N, K, bn, S, grid.x, grid.y);
     tc_profile_record_begin(st);
     dispatch<false>(ma, mb, p, grid, bn, st);
@@ -739,7 +800,10 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     p.box_h = bh;
     p.cin = Cin;
     p.splits = S;
-    dim3 grid(m_tiles * S, (Cout + bn - 1) / bn, batch);
+    p.m_tiles = m_tiles;
+    p.n_tiles = (Cout + bn - 1) / bn;
+    p.batch = batch;
+    const dim3 grid = launch_grid<true>(p, bn);
     if (tc_trace())
         fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u\n", H, W, Cin, Cout, bw, bh, bn, S,
                 grid.x, grid.y, grid.z);

@@ -13,6 +13,7 @@ struct TcArgs {
     // filled by the launcher
     int M = 0, N = 0, k_blocks = 0;
     int H = 0, W = 0, box_w = 0, box_h = 0, cin = 0;
+    int m_tiles = 0, n_tiles = 0, batch = 1;  // output tile grid (per image) and images
     // epilogue
     const float* bias = nullptr;          // [N]
     const float* chan_add = nullptr;      // [images][N] (e.g. time-embedding projection)
