@@ -30,7 +30,7 @@ __all__ = [
     "Round", "ExecutionPlan", "plan_async", "validate_plan", "PlanCounts", "plan_counts", "shift_embeddings",
     "render_plan", "RunOptions", "RunStats", "InstrumentedDenoiser", "inject_delay", "run_serial",
     "run_parallel", "DivergenceReport", "compare_trajectories", "kWarmupRound", "set_default_precision",
-    "PRECISIONS", "Session", "time_model_pass", "RankSession", "nccl_unique_id", "save_checkpoint",
+    "PRECISIONS", "Session", "time_model_pass", "profile_model_pass", "RankSession", "nccl_unique_id", "save_checkpoint",
     "load_checkpoint", "plan_to_json", "plan_from_json", "CostModel", "LatencyReport", "predict_sequential",
     "predict_async", "CostComparison", "calibrate_and_compare", "round_exchange_bytes", "SimilarityProfile",
     "similarity_profile", "build_unet_denoiser", "unet_stage_info", "unet_stage_params", "unet_context",

@@ -15,6 +15,8 @@
 // S never touches HBM (the unfused path wrote an L x L fp32 matrix per head).
 #include "tc_attn.cuh"
 
+#include "pdl.cuh"
+
 #include "tc_gemm.cuh"
 
 #include <cuda.h>
@@ -176,6 +178,7 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    pdl_wait();  // prologue done: wait for the producers of Q / K / V^T
     const uint32_t tmem = *tptr;
     // TMEM columns: S buffers [0,128) and [128,256); O buffers [256,320) and [320,384)
 
@@ -396,7 +399,7 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
     }
     dim3 grid((L + QT - 1) / QT, C / HD);
     tc_profile_record_begin(st);
-    attn_kernel<<<grid, 192, smem, st>>>(mq, mk, mv, a);
+    CKA(launch_pdl(attn_kernel, grid, dim3(192), smem, st, 1, mq, mk, mv, a));
     tc_profile_record_end(st, 2, 4.0 * L * Lk * C);
     CKA(cudaGetLastError());
 }

@@ -19,6 +19,8 @@
 //            stores.
 #include "tc_gemm.cuh"
 
+#include "pdl.cuh"
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tptr;
+    pdl_wait();  // prologue done: wait for the producers of A / residual
 
     if (warp == 0 && lane == 0) {
         // ---------------------------------------------------------- producer
@@ -546,19 +549,7 @@ void launch_t(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 
         CKT(cudaFuncSetAttribute(tc_gemm_kernel<BN, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr[dev] = true;
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(192, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = static_cast<unsigned>(p.splits);
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = p.splits > 1 ? 1 : 0;  // plain launch when the tile is not split
-    CKT(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, CONV>, a, b, p));
+    CKT(launch_pdl(tc_gemm_kernel<BN, CONV>, grid, dim3(192), smem, st, static_cast<unsigned>(p.splits), a, b, p));
 }
 
 template <bool CONV>

@@ -5,9 +5,12 @@
 // (deterministic, placement independent).
 #include "unet_kernels.cuh"
 
+#include "pdl.cuh"
+
 #include <cuda_bf16.h>
 
 #include <stdexcept>
+#include <utility>
 #include <string>
 
 namespace adx {
@@ -83,6 +86,7 @@ __host__ __device__ inline GnLayout gn_layout(float2* scratch, int batch, int C)
 // which CTA happens to finish last.
 __global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, const float* gamma,
                          const float* beta, float eps, float2* scratch) {
+    pdl_wait();
     extern __shared__ float sm[];  // [2][rpb][C]
     const int n = blockIdx.y, ch = blockIdx.x, batch = gridDim.y;
     const int C = x.c0 + x.c1, nv = C / 8, cpg = C / groups;
@@ -93,13 +97,22 @@ __global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, 
         float s[8], ss[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) s[i] = ss[i] = 0.f;
-        for (int p = p0 + r; p < p1; p += rpb) {
-            float f[8];
-            unpack8(cat_vec(x, static_cast<long long>(n) * HW + p, v), f);
+        // 4 rows in flight per thread (the loads do not depend on the running sums)
+        for (int p = p0 + r; p < p1; p += 4 * rpb) {
+            uint4 u[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                s[i] += f[i];
-                ss[i] = fmaf(f[i], f[i], ss[i]);
+            for (int k = 0; k < 4; ++k)
+                if (p + k * rpb < p1) u[k] = cat_vec(x, static_cast<long long>(n) * HW + p + k * rpb, v);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (p + k * rpb >= p1) break;
+                float f[8];
+                unpack8(u[k], f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    s[i] += f[i];
+                    ss[i] = fmaf(f[i], f[i], ss[i]);
+                }
             }
         }
 #pragma unroll
@@ -109,13 +122,23 @@ __global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, 
         }
     }
     __syncthreads();
+    // rows -> per channel (one thread per channel), then channels -> per group; fixed order
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        float a = 0.f, b = 0.f;
+        for (int rr = 0; rr < rpb; ++rr) {
+            a += sm[rr * C + c];
+            b += sm[(rpb + rr) * C + c];
+        }
+        sm[c] = a;
+        sm[rpb * C + c] = b;  // row 0 of each half: only this thread reads / writes column c
+    }
+    __syncthreads();
     for (int g = threadIdx.x; g < groups; g += blockDim.x) {
         float a = 0.f, b = 0.f;
-        for (int rr = 0; rr < rpb; ++rr)
-            for (int c = g * cpg; c < (g + 1) * cpg; ++c) {
-                a += sm[rr * C + c];
-                b += sm[(rpb + rr) * C + c];
-            }
+        for (int c = g * cpg; c < (g + 1) * cpg; ++c) {
+            a += sm[c];
+            b += sm[rpb * C + c];
+        }
         L.part[(static_cast<long long>(n) * chunks + ch) * groups + g] = make_float2(a, b);
     }
     // ticket: the last CTA of the grid finalises every image
@@ -176,6 +199,7 @@ __global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, 
 
 // GroupNorm pass 2: y = x * a[c] + b[c] (+SiLU), 8 channels per thread
 __global__ void gn_apply(Cat2 x, long long pixels, int HW, const float2* __restrict__ ab, int act, bf16* out) {
+    pdl_wait();
     const int C = x.c0 + x.c1, nv = C / 8;
     const long long n = pixels * nv;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -199,6 +223,7 @@ __global__ void gn_apply(Cat2 x, long long pixels, int HW, const float2* __restr
 constexpr int kLnMaxVec = 8;
 __global__ void layernorm_k(const bf16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
                             bf16* out) {
+    pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= tokens) return;
     const int nv = C / 8;
@@ -246,7 +271,8 @@ __global__ void layernorm_k(const bf16* x, int tokens, int C, const float* gamma
 
 // softmax over the first `valid` columns of each fp32 row (already scaled);
 // P bf16 with zeros in the padding columns [valid, ldp)
-__global__ void softmax_rows(const float* S, long long lds, int valid, bf16* P, long long ldp, int padded) {
+__global__ void softmax_rows_k(const float* S, long long lds, int valid, bf16* P, long long ldp, int padded) {
+    pdl_wait();
     const long long row = blockIdx.x;
     const float* r = S + row * lds;
     __shared__ float red[32];
@@ -284,6 +310,7 @@ __global__ void softmax_rows(const float* S, long long lds, int valid, bf16* P, 
 
 // out[t][j] = F[t][j] * gelu(F[t][j + H])   (diffusers GEGLU: hidden * gelu(gate)), 8 per thread
 __global__ void geglu_k(const bf16* F, long long tokens, int H, bf16* out) {
+    pdl_wait();
     const int hv = H / 8;
     const long long n = tokens * hv;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -302,6 +329,7 @@ __global__ void geglu_k(const bf16* F, long long tokens, int H, bf16* out) {
 
 // nearest 2x upsample, NHWC, 8 channels per thread
 __global__ void upsample2x_k(const bf16* x, int batch, int H, int W, int C, bf16* out) {
+    pdl_wait();
     const int nv = C / 8;
     const long long n = static_cast<long long>(batch) * 2 * H * 2 * W * nv;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -318,6 +346,7 @@ __global__ void upsample2x_k(const bf16* x, int batch, int H, int W, int C, bf16
 }
 
 __global__ void concat_k(Cat2 x, long long pixels, bf16* out) {
+    pdl_wait();
     const int nv = (x.c0 + x.c1) / 8;
     const long long n = pixels * nv;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -330,6 +359,7 @@ __global__ void concat_k(Cat2 x, long long pixels, bf16* out) {
 // latent (fp32 or fp64, H*W*c_lat, HWC order) -> bf16 NHWC with cpad channels (zeros above c_lat)
 template <typename T>
 __global__ void pack_latent_k(const T* x, long long pixels, int c_lat, int cpad, bf16* out) {
+    pdl_wait();
     const long long n = pixels * cpad;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -341,6 +371,7 @@ __global__ void pack_latent_k(const T* x, long long pixels, int c_lat, int cpad,
 
 // VT[d][k] = V[k * ldv + d] for k < L, 0 for L <= k < Lpad  (one head, head_dim rows)
 __global__ void transpose_head_k(const bf16* V, long long ldv, int L, int Lpad, int hd, bf16* VT) {
+    pdl_wait();
     __shared__ bf16 tile[32][33];
     const int k0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -379,12 +410,13 @@ void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma
     size_t smem = static_cast<size_t>(2) * rpb * C * sizeof(float);
     smem = std::max(smem, static_cast<size_t>(nsub) * batch * groups * 2 * sizeof(double));
     if (smem > 48 * 1024) throw std::invalid_argument("group_norm: statistics tile exceeds 48 KB shared memory");
-    gn_stats<<<dim3(chunks, batch), threads, smem, st>>>(x, HW, groups, chunk_pix, chunks, gamma, beta, eps,
-                                                        scratch);
+    CKU(launch_pdl(gn_stats, dim3(chunks, batch), dim3(threads), smem, st, 1, x, HW, groups, chunk_pix, chunks, gamma,
+                   beta, eps, scratch));
     CKU(cudaGetLastError());
     const GnLayout L = gn_layout(scratch, batch, C);
     const long long pixels = static_cast<long long>(batch) * HW;
-    gn_apply<<<grid_for(pixels * nv), 256, 0, st>>>(x, pixels, HW, L.ab, silu_act, out);
+    CKU(launch_pdl(gn_apply, dim3(grid_for(pixels * nv)), dim3(256), 0, st, 1, x, pixels, HW,
+                   static_cast<const float2*>(L.ab), silu_act, out));
     CKU(cudaGetLastError());
 }
 
@@ -397,31 +429,32 @@ size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C) {
 void layer_norm(const __nv_bfloat16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
                 __nv_bfloat16* out, cudaStream_t st) {
     if (C % 8 || C > 256 * kLnMaxVec) throw std::invalid_argument("layer_norm: C must be a multiple of 8, <= 2048");
-    layernorm_k<<<(tokens + 7) / 8, 256, 0, st>>>(x, tokens, C, gamma, beta, eps, out);
+    CKU(launch_pdl(layernorm_k, dim3((tokens + 7) / 8), dim3(256), 0, st, 1, x, tokens, C, gamma, beta, eps, out));
     CKU(cudaGetLastError());
 }
 
 void softmax_rows(const float* S, long long lds, int rows, int valid, __nv_bfloat16* P, long long ldp, int padded,
                   cudaStream_t st) {
-    softmax_rows<<<rows, 256, 0, st>>>(S, lds, valid, P, ldp, padded);
+    CKU(launch_pdl(softmax_rows_k, dim3(rows), dim3(256), 0, st, 1, S, lds, valid, P, ldp, padded));
     CKU(cudaGetLastError());
 }
 
 void geglu(const __nv_bfloat16* F, long long tokens, int H, __nv_bfloat16* out, cudaStream_t st) {
     if (H % 8) throw std::invalid_argument("geglu: hidden width must be a multiple of 8");
-    geglu_k<<<grid_for(tokens * H / 8), 256, 0, st>>>(F, tokens, H, out);
+    CKU(launch_pdl(geglu_k, dim3(grid_for(tokens * H / 8)), dim3(256), 0, st, 1, F, tokens, H, out));
     CKU(cudaGetLastError());
 }
 
 void upsample2x(const __nv_bfloat16* x, int batch, int H, int W, int C, __nv_bfloat16* out, cudaStream_t st) {
     if (C % 8) throw std::invalid_argument("upsample2x: C must be a multiple of 8");
-    upsample2x_k<<<grid_for(4LL * batch * H * W * C / 8), 256, 0, st>>>(x, batch, H, W, C, out);
+    CKU(launch_pdl(upsample2x_k, dim3(grid_for(4LL * batch * H * W * C / 8)), dim3(256), 0, st, 1, x, batch, H, W, C,
+                   out));
     CKU(cudaGetLastError());
 }
 
 void concat_channels(const Cat2& x, long long pixels, __nv_bfloat16* out, cudaStream_t st) {
     check_vec8(x, "concat_channels");
-    concat_k<<<grid_for(pixels * (x.c0 + x.c1) / 8), 256, 0, st>>>(x, pixels, out);
+    CKU(launch_pdl(concat_k, dim3(grid_for(pixels * (x.c0 + x.c1) / 8)), dim3(256), 0, st, 1, x, pixels, out));
     CKU(cudaGetLastError());
 }
 
@@ -438,7 +471,8 @@ void pack_latent(const void* x, bool f64, long long pixels, int c_lat, int cpad,
 
 void transpose_head(const __nv_bfloat16* V, long long ldv, int L, int Lpad, int hd, __nv_bfloat16* VT,
                     cudaStream_t st) {
-    transpose_head_k<<<dim3((Lpad + 31) / 32, (hd + 31) / 32), dim3(32, 8), 0, st>>>(V, ldv, L, Lpad, hd, VT);
+    CKU(launch_pdl(transpose_head_k, dim3((Lpad + 31) / 32, (hd + 31) / 32), dim3(32, 8), 0, st, 1, V, ldv, L, Lpad, hd,
+                   VT));
     CKU(cudaGetLastError());
 }
 
