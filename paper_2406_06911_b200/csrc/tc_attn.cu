@@ -119,6 +119,40 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ void tst16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+        "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+        "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
+}
+__device__ __forceinline__ void tst_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 2^x on the FMA / integer pipes: x = n + f, n = rint(x) via the 1.5 * 2^23 trick,
+// 2^f on [-0.5, 0.5] by a degree-3 minimax fit (max rel. error 7.5e-5 << bf16's
+// 3.9e-3), 2^n added to the exponent field; x clamped at -126 (P ~1e-38: negligible)
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -126.f);
+    const float t = x + 12582912.f;
+    const int n = __float_as_int(t) - 0x4B400000;
+    const float f = x - (t - 12582912.f);
+    const float p = fmaf(f, fmaf(f, fmaf(f, 0.05517132f, 0.24261054f), 0.69326097f), 0.99992812f);
+    return __int_as_float(__float_as_int(p) + (n << 23));
+}
+// every POLY_EVERY-th exponential goes to the FMA pipe (0: all on MUFU ex2)
+#ifndef ADX_ATTN_POLY_EVERY
+#define ADX_ATTN_POLY_EVERY 0
+#endif
+constexpr int POLY_EVERY = ADX_ATTN_POLY_EVERY;
+__device__ __forceinline__ float ex2_mix(float x, int i) {
+    if constexpr (POLY_EVERY > 0) {
+        if (i % POLY_EVERY == POLY_EVERY - 1) return ex2_poly(x);
+    }
+    return ex2(x);
+}
 
 constexpr uint32_t idesc(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
@@ -131,12 +165,13 @@ struct AttnArgs {
     long long ldo;
 };
 
-__global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CUtensorMap tmQ,
+__global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                       const __grid_constant__ CUtensorMap tmK,
                                                       const __grid_constant__ CUtensorMap tmVT, const AttnArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2, P_B = QT * KT * 2;
+    constexpr int XCH_OFF = Q_B + STG * (K_B + V_B) + 2 * P_B + 256;  // after the barriers
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + Q_B;        // STG x K_B
     uint8_t* sV = sK + STG * K_B;  // STG x (2 halves of [64 dims x 64 keys])
@@ -147,10 +182,11 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
     uint64_t* kv_empty = kv_full + STG;   // [STG]
     uint64_t* s_full = kv_empty + STG;    // [2] MMA -> softmax
     uint64_t* s_free = s_full + 2;        // [2] softmax -> MMA (S buffer read)
-    uint64_t* p_full = s_free + 2;        // [2] softmax -> MMA (P buffer written)
-    uint64_t* o_full = p_full + 2;        // [2] MMA -> softmax
-    uint64_t* o_free = o_full + 2;        // [2] softmax -> MMA (O buffer merged)
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(o_free + 2);
+    uint64_t* p_full = s_free + 2;        // [2] softmax -> MMA (P buffer written, O rescaled)
+    uint64_t* pv_done = p_full + 2;       // [2] MMA -> softmax: PV_j done (P buffer j&1 free)
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(pv_done + 2);
+    float* xmax = reinterpret_cast<float*>(smem + XCH_OFF);  // [2 tiles][2 halves][128 rows] partial row max,
+                                                             // then [2 halves][128 rows] row sums
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qt = blockIdx.x, head = blockIdx.y;
@@ -164,10 +200,9 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
         }
         for (int b = 0; b < 2; ++b) {
             bar_init(&s_full[b], 1);
-            bar_init(&s_free[b], 4);
-            bar_init(&p_full[b], 4);
-            bar_init(&o_full[b], 1);
-            bar_init(&o_free[b], 4);
+            bar_init(&s_free[b], 8);
+            bar_init(&p_full[b], 8);
+            bar_init(&pv_done[b], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -180,7 +215,7 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     pdl_wait();  // prologue done: wait for the producers of Q / K / V^T
     const uint32_t tmem = *tptr;
-    // TMEM columns: S buffers [0,128) and [128,256); O buffers [256,320) and [320,384)
+    // TMEM columns: S buffers [0,128) and [128,256); O accumulator [256,320)
 
     if (warp == 0 && lane == 0) {
         // ------------------------------------------------------------ TMA
@@ -215,86 +250,103 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
             if (j < nkv) issue_s(j);
             {
                 const int jj = j - 1, s = jj % STG, b = jj & 1;
-                bar_wait(&p_full[b], (jj >> 1) & 1);         // P_jj in SMEM
-                bar_wait(&o_free[b], ((jj >> 1) & 1) ^ 1);   // O_{jj-2} merged
+                bar_wait(&p_full[b], (jj >> 1) & 1);  // P_jj in SMEM (and O rescaled if needed)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int k = 0; k < KT / 16; ++k) {
                     const int half = k / 4, kk = k % 4;
-                    mma(tmem + 256 + b * 64, sdesc(sP + b * P_B + half * (P_B / 2) + kk * 32),
-                        sdesc(sV + s * V_B + half * (V_B / 2) + kk * 32), idesc(QT, HD), k > 0);
+                    mma(tmem + 256, sdesc(sP + b * P_B + half * (P_B / 2) + kk * 32),
+                        sdesc(sV + s * V_B + half * (V_B / 2) + kk * 32), idesc(QT, HD), (jj | k) > 0);
                 }
-                commit(&o_full[b]);
+                commit(&pv_done[b]);
                 commit(&kv_empty[s]);
             }
         }
     } else if (warp >= 2) {
         // --------------------------------------------------- softmax + epilogue
+        // 8 warps: warp pair (w, w+4) shares TMEM lane quadrant q (rows 32q..32q+31) and
+        // splits the 128 keys of a tile in two 64-key halves (two warps per SM
+        // sub-partition on one tile); the pair exchanges partial row maxima through
+        // SMEM (named barrier 1+q, 64 threads).  O accumulates in TMEM across KV tiles;
+        // m is the max the exponentials use and only moves when the row max grows by
+        // > 8 (log2 units): the O rescale is rare and P stays <= 2^8.
         const int q = warp & 3;
+        const int half = (warp - 2) >> 2;
         const int r = q * 32 + lane;  // query row within the tile
         const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
+        const uint32_t tO = tmem + 256 + lrow;
         const float sl2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
-        float m = -INFINITY, l = 0.f, alpha_pend = 0.f;
-        float o[HD];
-#pragma unroll
-        for (int i = 0; i < HD; ++i) o[i] = 0.f;
-        // O_jj merge (deferred by one tile): o = o * alpha_jj + O_jj
-        auto merge = [&](int jj, float alpha) {
-            const int b = jj & 1;
-            bar_wait(&o_full[b], (jj >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t ov[HD];
-            tld64_nowait(tmem + 256 + b * 64 + lrow, ov);
-            tld_wait();
-#pragma unroll
-            for (int i = 0; i < HD; ++i) o[i] = fmaf(o[i], alpha, __uint_as_float(ov[i]));
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) bar_arrive(&o_free[b]);
-        };
+        auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory"); };
+        float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nkv; ++j) {
             const int b = j & 1;
-            const uint32_t tS = tmem + b * 128 + lrow;
+            const uint32_t tS = tmem + b * 128 + half * 64 + lrow;
             bar_wait(&s_full[b], (j >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int valid = min(KT, p.Lk - j * KT);
-            // the whole S row (128 fp32) in two batched 64-column TMEM loads, one wait
-            uint32_t sr[KT];
+            uint32_t sr[64];
             tld64_nowait(tS, sr);
-            tld64_nowait(tS + 64, sr + 64);
             tld_wait();
-            // row max with 8 independent chains (a single 128-long FMNMX chain is latency bound)
+            // S_j is in registers: release its TMEM buffer to the MMA warp (S_{j+2}) now
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) bar_arrive(&s_free[b]);
             // ragged last tile: mask the dead keys to -inf once so the hot loops carry no predicates
-            if (valid < KT) {
+            const int valid = min(KT, p.Lk - j * KT) - half * 64;
+            if (valid < 64) {
 #pragma unroll
-                for (int i = 0; i < KT; ++i)
+                for (int i = 0; i < 64; ++i)
                     if (i >= valid) sr[i] = 0xff800000u;
             }
-            float mp[8];
+            float mp[8];  // 8 independent max chains
 #pragma unroll
-            for (int a = 0; a < 8; ++a) mp[a] = m;
+            for (int a = 0; a < 8; ++a) mp[a] = __uint_as_float(sr[a]);
 #pragma unroll
-            for (int i = 0; i < KT; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(sr[i]));
-            const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+            for (int i = 8; i < 64; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(sr[i]));
+            const float mh = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
                                    fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
-            const float alpha = ex2((m - mx) * sl2);
-            const float off = -mx * sl2;
-            // P = exp2(s*scale*log2e - max*scale*log2e) -> SW128 K-major A tile in SMEM
-            // (half h = keys [64h, 64h+64), 16-byte chunk k of row r at k ^ (r & 7))
-            float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent sum chains
-            uint8_t* pbuf = sP + b * P_B;
+            xmax[(b * 2 + half) * QT + r] = mh;
+            pair_sync();
+            const float mx = fmaxf(mh, xmax[(b * 2 + (half ^ 1)) * QT + r]);
+            // P buffer b was last read by PV_{j-2}
+            if (j >= 2) bar_wait(&pv_done[b], ((j >> 1) & 1) ^ 1);
+            if (j == 0) {
+                m = mx;
+            } else {
+                const bool need = (mx - m) * sl2 > 8.f;
+                if (__any_sync(0xffffffffu, need)) {  // rare: rescale O and l to the new max
+                    const int qb = (j - 1) & 1;        // O must be final for PV_{j-1}
+                    bar_wait(&pv_done[qb], ((j - 1) >> 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const float alpha = need ? ex2((m - mx) * sl2) : 1.f;
 #pragma unroll
-            for (int c = 0; c < KT; c += 16) {
+                    for (int c = 0; c < HD / 2; c += 16) {  // this warp's 32 of the 64 O columns
+                        float ov[16];
+                        tld16(tO + half * (HD / 2) + c, ov);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) ov[i] *= alpha;
+                        tst16(tO + half * (HD / 2) + c, ov);
+                    }
+                    tst_wait();
+                    l *= alpha;
+                    if (need) m = mx;
+                }
+            }
+            const float off = -m * sl2;
+            // P = exp2(s*scale*log2e - m*scale*log2e) -> SW128 K-major A tile in SMEM
+            // (this warp's half = keys [64h, 64h+64), 16-byte chunk k of row r at k ^ (r & 7))
+            float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent sum chains
+            uint8_t* row = sP + b * P_B + half * (P_B / 2) + r * 128;
+#pragma unroll
+            for (int c = 0; c < 64; c += 16) {
                 float v[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    v[i] = ex2(fmaf(__uint_as_float(sr[c + i]), sl2, off));
+                    v[i] = ex2_mix(fmaf(__uint_as_float(sr[c + i]), sl2, off), i);
                     sp[i & 7] += v[i];
                 }
-                uint8_t* row = pbuf + (c / 64) * (P_B / 2) + r * 128;
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
-                    const int k = ((c % 64) / 8) + hh;
+                    const int k = c / 8 + hh;
                     uint4 u;
                     __nv_bfloat162 b0 = __floats2bfloat162_rn(v[hh * 8 + 0], v[hh * 8 + 1]);
                     __nv_bfloat162 b1 = __floats2bfloat162_rn(v[hh * 8 + 2], v[hh * 8 + 3]);
@@ -310,28 +362,31 @@ __global__ void __launch_bounds__(192, 1) attn_kernel(const __grid_constant__ CU
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) {
-                bar_arrive(&s_free[b]);
-                bar_arrive(&p_full[b]);
-            }
-            const float sum = ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
-            l = l * alpha + sum;
-            m = mx;
-            if (j >= 1) merge(j - 1, alpha_pend);
-            alpha_pend = alpha;
+            if (lane == 0) bar_arrive(&p_full[b]);
+            l += ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
         }
-        merge(nkv - 1, alpha_pend);
+        // epilogue: row sum = half 0 + half 1 (fixed order); O final after the last PV,
+        // each warp of the pair normalises and stores 32 of the 64 columns
+        float* xsum = xmax + 4 * QT;  // own region: the partner may still read tile nkv-1's maxima
+        xsum[half * QT + r] = l;
+        pair_sync();
+        const float lt = xsum[r] + xsum[QT + r];
+        bar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float ov[HD / 2];
+        tld16(tO + half * (HD / 2), ov);
+        tld16(tO + half * (HD / 2) + 16, ov + 16);
         const long long row = static_cast<long long>(qt) * QT + r;
         if (row < p.L) {
-            const float inv = 1.0f / l;
-            __nv_bfloat16* dst = p.out + row * p.ldo + head * HD;
+            const float inv = 1.0f / lt;
+            __nv_bfloat16* dst = p.out + row * p.ldo + head * HD + half * (HD / 2);
 #pragma unroll
-            for (int c = 0; c < HD; c += 8) {
+            for (int c = 0; c < HD / 2; c += 8) {
                 uint4 v;
-                __nv_bfloat162 b0 = __floats2bfloat162_rn(o[c] * inv, o[c + 1] * inv);
-                __nv_bfloat162 b1 = __floats2bfloat162_rn(o[c + 2] * inv, o[c + 3] * inv);
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(o[c + 4] * inv, o[c + 5] * inv);
-                __nv_bfloat162 b3 = __floats2bfloat162_rn(o[c + 6] * inv, o[c + 7] * inv);
+                __nv_bfloat162 b0 = __floats2bfloat162_rn(ov[c] * inv, ov[c + 1] * inv);
+                __nv_bfloat162 b1 = __floats2bfloat162_rn(ov[c + 2] * inv, ov[c + 3] * inv);
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(ov[c + 4] * inv, ov[c + 5] * inv);
+                __nv_bfloat162 b3 = __floats2bfloat162_rn(ov[c + 6] * inv, ov[c + 7] * inv);
                 v.x = *reinterpret_cast<uint32_t*>(&b0);
                 v.y = *reinterpret_cast<uint32_t*>(&b1);
                 v.z = *reinterpret_cast<uint32_t*>(&b2);
@@ -389,7 +444,8 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
     const CUtensorMap mk = map2d(K, Lk, C, ldk, KT);
     const CUtensorMap mv = map2d(VT, C, Lk, ldvt, HD);  // rows = dims, cols = keys
     AttnArgs a{L, Lk, C, out, ldo};
-    constexpr size_t smem = 1024 + QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + 2 * QT * KT * 2 + 256;
+    constexpr size_t smem =
+        1024 + QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + 2 * QT * KT * 2 + 256 + 6 * QT * sizeof(float);
     static bool attr[64] = {};
     int dev = 0;
     CKA(cudaGetDevice(&dev));
@@ -399,7 +455,7 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
     }
     dim3 grid((L + QT - 1) / QT, C / HD);
     tc_profile_record_begin(st);
-    CKA(launch_pdl(attn_kernel, grid, dim3(192), smem, st, 1, mq, mk, mv, a));
+    CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, st, 1, mq, mk, mv, a));
     tc_profile_record_end(st, 2, 4.0 * L * Lk * C);
     CKA(cudaGetLastError());
 }
