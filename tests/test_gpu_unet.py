@@ -67,3 +67,20 @@ def test_unet_stride_async_runs(small):
     par, _ = adx.run_parallel(plan, m, part, x, s, plan.D, precision="f32")
     assert np.array_equal(ser.latent_matrix(), par.latent_matrix())
     assert np.all(np.isfinite(ser.latent_matrix()))
+
+
+def test_unet_rank_session_single_rank_matches_sequential(small):
+    """NCCL one-process-per-GPU path (rank.cu) on the UNet family with one rank:
+    N=1 plan == sequential_denoise bit-exactly (bf16 stage buffers through the
+    rank program, fp32 trajectory)."""
+    m, s, x = small
+    T = 4
+    plan = adx.plan_async(T, 1, 1, 1)
+    part = adx.partition_balanced(m, 1)
+    sess = adx.RankSession(m, s, plan, part, 0, adx.nccl_unique_id(), 0, "f32")
+    d = m.data_dim()
+    lat, eps = np.zeros((T + 1, d)), np.zeros((T, d))
+    sess.run_into(np.ascontiguousarray(x.values, np.float64), lat, eps)
+    seq = adx.sequential_denoise(m, x, s, precision="f32")
+    assert np.array_equal(lat, seq.latent_matrix())
+    assert sess.time(1) > 0
