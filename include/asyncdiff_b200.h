@@ -309,7 +309,7 @@ int adx_unet_context(const adx_model* m, float* out /* ctx_len * ctx_dim */);
  * (no reference function: builder-written oracle, SURVEY §8a extension list).
  * A/B/X/Wt are bf16 bit patterns (uint16), outputs fp32.  iters > 0 also times
  * `iters` back-to-back launches (CUDA events). */
-/* C[M x N] = act(A[M x K] . B[N x K]^T + bias); K % 64 == 0; bn in {0,32,64,128,256} */
+/* C[M x N] = act(A[M x K] . B[N x K]^T + bias); K % 64 == 0; bn in {0,32,64,80,96,128,160,192,256} */
 int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B,
                 const float* bias, int act, float* C, int bn, int iters, double* ms_per_iter);
 /* fused multi-head attention (64-wide heads, scale 1/8): out[L x C] bf16 from Q [L x C],
@@ -319,6 +319,10 @@ int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const
 /* conv3x3 / stride 1 / pad 1, NHWC: X [batch][H][W][Cin], Wt [Cout][9*Cin] ((r*3+s)*Cin+ci) */
 int adx_tc_conv3x3(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X,
                    const uint16_t* Wt, const float* bias, float* out, int iters, double* ms_per_iter);
+/* tile-plan override for tuning (tools_tc_tune.py): every following GEMM / conv
+ * launch in this process uses N tile `bn` and split-K factor `splits` (0, 0:
+ * back to the measured plan table, then the model) */
+int adx_tc_plan_override(int bn, int splits);
 
 /* ------------------------------------------------------ §8(f) next rows */
 /* save_checkpoint / load_checkpoint: proj/include/asyncdiff/serialize.hpp:35-36,

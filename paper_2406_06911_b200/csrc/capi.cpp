@@ -986,6 +986,10 @@ int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint1
     });
 }
 
+int adx_tc_plan_override(int bn, int splits) {
+    return guard([&] { adx::tc_plan_override(bn, splits); });
+}
+
 int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K, const uint16_t* VT,
                      int ldvt, uint16_t* out, int iters, double* ms_per_iter) {
     return guard([&] {

@@ -557,11 +557,13 @@ void dispatch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 
     switch (bn) {
         case 32: launch_t<32, CONV>(a, b, p, grid, st); break;
         case 64: launch_t<64, CONV>(a, b, p, grid, st); break;
+        case 80: launch_t<80, CONV>(a, b, p, grid, st); break;
+        case 96: launch_t<96, CONV>(a, b, p, grid, st); break;
         case 128: launch_t<128, CONV>(a, b, p, grid, st); break;
         case 160: launch_t<160, CONV>(a, b, p, grid, st); break;
         case 192: launch_t<192, CONV>(a, b, p, grid, st); break;
         case 256: launch_t<256, CONV>(a, b, p, grid, st); break;
-        default: throw std::invalid_argument("tc_gemm: BN must be 32/64/128/160/192/256");
+        default: throw std::invalid_argument("tc_gemm: BN must be 32/64/80/96/128/160/192/256");
     }
 }
 
@@ -615,6 +617,8 @@ int cluster_capacity(int bn, int S) {
     switch (bn) {
         case 32: return cluster_capacity_t<32, CONV>(S);
         case 64: return cluster_capacity_t<64, CONV>(S);
+        case 80: return cluster_capacity_t<80, CONV>(S);
+        case 96: return cluster_capacity_t<96, CONV>(S);
         case 128: return cluster_capacity_t<128, CONV>(S);
         case 160: return cluster_capacity_t<160, CONV>(S);
         case 192: return cluster_capacity_t<192, CONV>(S);
@@ -637,6 +641,27 @@ dim3 launch_grid(const TcArgs& p, int bn) {
 // amortises worse.  Every split stages a 128 x BN fp32 partial that the cluster
 // reduces over DSMEM -- only worth it when the unsplit grid leaves SMs idle.
 // bn_fixed != 0 pins the tile width.
+int g_override_bn = 0, g_override_splits = 0;
+
+// Measured plans (tools_tc_tune.py on B200: every (BN, S) timed per shape, best kept).
+// GEMM rows: {0, M, N, K, 0, bn, S}; conv rows: {1, H, W, Cin, Cout, bn, S} (batch 1).
+struct PlanRow {
+    int conv, a, b, c, d, bn, s;
+};
+constexpr PlanRow kPlanTable[] = {
+#include "tc_plan_table.inc"
+    {-1, 0, 0, 0, 0, 0, 0}};
+
+bool plan_lookup(int conv, int a, int b, int c, int d, int& bn, int& s) {
+    for (const PlanRow& r : kPlanTable)
+        if (r.conv == conv && r.a == a && r.b == b && r.c == c && r.d == d) {
+            bn = r.bn;
+            s = r.s;
+            return true;
+        }
+    return false;
+}
+
 template <bool CONV>
 void tile_plan(int m_tiles, int N, int batch, int k_blocks, int bn_fixed, int& bn_out, int& s_out) {
     double best = 1e300;
@@ -672,6 +697,14 @@ std::vector<cudaEvent_t> g_prof_open;
 }  // namespace
 
 void tc_profile_enable(bool on) { g_prof_on = on; }
+
+void tc_plan_override(int bn, int splits) {
+    if (bn && bn != 32 && bn != 64 && bn != 80 && bn != 96 && bn != 128 && bn != 160 && bn != 192 && bn != 256)
+        throw std::invalid_argument("tc_plan_override: BN must be 0/32/64/80/96/128/160/192/256");
+    if (splits < 0 || splits > kMaxSplits) throw std::invalid_argument("tc_plan_override: splits must be 0..8");
+    g_override_bn = bn;
+    g_override_splits = splits;
+}
 
 void tc_profile_record_begin(cudaStream_t st) {
     if (!g_prof_on) return;
@@ -721,7 +754,15 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
         bn = 256;
     }
     int S = 1;
-    tile_plan<false>((M + BM - 1) / BM, N, 1, K / BK, bn, bn, S);
+    const bool geglu = p.act == 2;
+    if (!geglu && bn == 0 && g_override_bn) {
+        bn = g_override_bn;
+        S = std::max(1, g_override_splits);
+    } else if (!(bn == 0 && !geglu && plan_lookup(0, M, N, K, 0, bn, S))) {
+        tile_plan<false>((M + BM - 1) / BM, N, 1, K / BK, bn, bn, S);
+    }
+    if (geglu && g_override_splits) S = g_override_splits;  // the GEGLU tile width stays 256
+    if (S > 1 && (K / BK) / S < 1) S = std::max(1, K / BK);
     const cuuint64_t da[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
     const cuuint64_t sa_[1] = {static_cast<cuuint64_t>(lda) * 2};
     const cuuint64_t sb_[1] = {static_cast<cuuint64_t>(ldb) * 2};
@@ -771,7 +812,12 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     if (!bw) throw std::invalid_argument("tc_conv3x3: no legal TMA box for this image width");
     const int m_tiles = ((H + bh - 1) / bh) * (W / bw);
     int S = 1;
-    tile_plan<true>(m_tiles, Cout, batch, 9 * Cin / BK, bn, bn, S);
+    if (bn == 0 && g_override_bn) {
+        bn = g_override_bn;
+        S = std::max(1, g_override_splits);
+    } else if (!(bn == 0 && batch == 1 && plan_lookup(1, H, W, Cin, Cout, bn, S))) {
+        tile_plan<true>(m_tiles, Cout, batch, 9 * Cin / BK, bn, bn, S);
+    }
     const cuuint64_t dx[4] = {static_cast<cuuint64_t>(Cin), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                               static_cast<cuuint64_t>(batch)};
     const cuuint64_t sx[3] = {static_cast<cuuint64_t>(Cin) * 2, static_cast<cuuint64_t>(W) * Cin * 2,

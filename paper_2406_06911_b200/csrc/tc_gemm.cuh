@@ -31,6 +31,9 @@ struct TcArgs {
     int splits = 1;                       // filled by the launcher: split-K factor (cluster size)
 };
 
+// force (bn, splits) for every following launch (tuning); (0, 0) restores the plan table / model
+void tc_plan_override(int bn, int splits);
+
 // In-run kernel profiling (eager passes only): when enabled, every tensor-core
 // launch is bracketed by CUDA events on its stream and recorded with its
 // algorithmic FLOPs; kind 0 conv3x3, 1 GEMM, 2 attention.
