@@ -9,6 +9,7 @@
 
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <utility>
 #include <string>
@@ -219,6 +220,144 @@ __global__ void gn_apply(Cat2 x, long long pixels, int HW, const float2* __restr
     }
 }
 
+// GroupNorm in one cooperative launch (batch 1): CTA c of G (<= #SMs, all co-resident)
+// owns pixels [c*chunk, (c+1)*chunk): it loads them into SMEM once while accumulating
+// per-channel (sum, sumsq), reduces rows -> channels -> groups in a fixed order and
+// publishes its group partials; after a grid barrier every CTA folds all G partials
+// in the same fixed fp64 order (identical statistics everywhere, deterministic),
+// builds per-channel (a, b) and normalises its SMEM copy: one HBM read of x.
+__global__ void gn_fused(Cat2 x, int HW, int groups, int chunk_pix, const float* gamma, const float* beta, float eps,
+                         int act, float2* scratch, bf16* out) {
+    extern __shared__ __align__(16) uint8_t gsm[];
+    pdl_wait();
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int C = x.c0 + x.c1, nv = C / 8, cpg = C / groups;
+    const int rpb = blockDim.x / nv, r = threadIdx.x / nv, v = threadIdx.x % nv;
+    const int p0 = cta * chunk_pix, p1 = min(HW, p0 + chunk_pix), np = max(0, p1 - p0);
+    uint4* tile = reinterpret_cast<uint4*>(gsm);                              // [chunk_pix][nv]
+    float* red = reinterpret_cast<float*>(gsm + static_cast<size_t>(chunk_pix) * C * 2);  // [2][rpb][C]
+    float2* ab = reinterpret_cast<float2*>(red + 2 * rpb * C);               // [C]
+    double* st = reinterpret_cast<double*>(ab + C);                          // [nsub][groups][2], then [groups][2]
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(scratch + 1);
+    float2* part = scratch + 8;
+    if (r < rpb) {
+        float s[8], ss[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] = ss[i] = 0.f;
+        for (int q = r; q < np; q += 4 * rpb) {
+            uint4 u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (q + k * rpb < np) u[k] = cat_vec(x, p0 + q + k * rpb, v);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (q + k * rpb >= np) break;
+                tile[(q + k * rpb) * nv + v] = u[k];
+                float f[8];
+                unpack8(u[k], f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    s[i] += f[i];
+                    ss[i] = fmaf(f[i], f[i], ss[i]);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            red[r * C + v * 8 + i] = s[i];
+            red[(rpb + r) * C + v * 8 + i] = ss[i];
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        float a = 0.f, b = 0.f;
+        for (int rr = 0; rr < rpb; ++rr) {
+            a += red[rr * C + c];
+            b += red[(rpb + rr) * C + c];
+        }
+        red[c] = a;
+        red[rpb * C + c] = b;
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+        float a = 0.f, b = 0.f;
+        for (int c = g * cpg; c < (g + 1) * cpg; ++c) {
+            a += red[c];
+            b += red[rpb * C + c];
+        }
+        part[static_cast<long long>(cta) * groups + g] = make_float2(a, b);
+    }
+    // grid barrier (co-residency guaranteed by the cooperative launch): arrival count +
+    // generation; the last CTA to arrive re-arms the count and bumps the generation, so
+    // consecutive launches with different grid sizes reuse the same two words
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int* count = reinterpret_cast<unsigned int*>(bar);
+        unsigned int* gen = count + 1;
+        unsigned int g0;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g0) : "l"(gen) : "memory");
+        __threadfence();
+        if (atomicAdd(count, 1u) == static_cast<unsigned int>(G - 1)) {
+            *count = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            unsigned int cur;
+            do {
+                __nanosleep(64);
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
+            } while (cur == g0);
+        }
+    }
+    __syncthreads();
+    // statistics: nsub threads per group over a fixed strided subset of the G partials
+    const int nsub = max(1, static_cast<int>(blockDim.x) / groups);
+    if (threadIdx.x < nsub * groups) {
+        const int g = threadIdx.x % groups, sub = threadIdx.x / groups;
+        double a = 0.0, b = 0.0;
+        for (int k = sub; k < G; k += nsub) {
+            const float2 pv = __ldcg(&part[static_cast<long long>(k) * groups + g]);
+            a += pv.x;
+            b += pv.y;
+        }
+        st[2 * (sub * groups + g)] = a;
+        st[2 * (sub * groups + g) + 1] = b;
+    }
+    __syncthreads();
+    double mv0 = 0.0, mv1 = 0.0;
+    if (threadIdx.x < groups) {
+        const int g = threadIdx.x;
+        double a = 0.0, b = 0.0;
+        for (int sub = 0; sub < nsub; ++sub) a += st[2 * (sub * groups + g)], b += st[2 * (sub * groups + g) + 1];
+        const double cnt = static_cast<double>(HW) * cpg;
+        mv0 = a / cnt;
+        mv1 = 1.0 / sqrt(fmax(b / cnt - mv0 * mv0, 0.0) + static_cast<double>(eps));
+    }
+    __syncthreads();
+    if (threadIdx.x < groups) st[2 * threadIdx.x] = mv0, st[2 * threadIdx.x + 1] = mv1;
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        const int g = c / cpg;
+        const double rs = st[2 * g + 1];
+        ab[c] = make_float2(static_cast<float>(rs * gamma[c]), static_cast<float>(beta[c] - st[2 * g] * rs * gamma[c]));
+    }
+    __syncthreads();
+    // normalise the SMEM copy, 16-byte coalesced stores
+    uint4* o = reinterpret_cast<uint4*>(out) + static_cast<long long>(p0) * nv;
+    for (int i = threadIdx.x; i < np * nv; i += blockDim.x) {
+        const int vv = i % nv;
+        float f[8];
+        unpack8(tile[i], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float2 q = ab[vv * 8 + k];
+            f[k] = fmaf(f[k], q.x, q.y);
+            if (act) f[k] = silu(f[k]);
+        }
+        o[i] = pack8(f);
+    }
+}
+
 // LayerNorm over C per token, one warp per token, row held in registers (C <= 2048)
 constexpr int kLnMaxVec = 8;
 __global__ void layernorm_k(const bf16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
@@ -396,6 +535,46 @@ void check_vec8(const Cat2& x, const char* who) {
         throw std::invalid_argument(std::string(who) + ": channel segments must be multiples of 8");
 }
 
+// one-launch cooperative GroupNorm when the chunk of every SM fits in SMEM (see gn_fused);
+// returns false (nothing launched) otherwise.  ADX_GN_FUSED=0 disables it.
+bool group_norm_fused(const Cat2& x, int HW, int groups, const float* gamma, const float* beta, float eps, int act,
+                      __nv_bfloat16* out, float2* scratch, cudaStream_t st) {
+    static const int mode = [] {
+        const char* e = getenv("ADX_GN_FUSED");
+        return e ? atoi(e) : 1;
+    }();
+    if (!mode) return false;
+    int dev = 0, sms = 0;
+    CKU(cudaGetDevice(&dev));
+    CKU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int C = x.c0 + x.c1, nv = C / 8;
+    if (nv > 512) return false;
+    const int chunk_pix = (HW + sms - 1) / sms;
+    const int G = (HW + chunk_pix - 1) / chunk_pix;
+    const int rpb = std::max(1, 512 / nv), threads = rpb * nv;
+    const int nsub = std::max(1, threads / groups);
+    const size_t smem = static_cast<size_t>(chunk_pix) * C * 2 + static_cast<size_t>(2) * rpb * C * 4 +
+                        static_cast<size_t>(C) * 8 + static_cast<size_t>(nsub) * groups * 16;
+    if (smem > 200 * 1024) return false;
+    static bool attr[64] = {};
+    if (!attr[dev]) {
+        CKU(cudaFuncSetAttribute(gn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CKU(cudaLaunchKernelEx(&cfg, gn_fused, x, HW, groups, chunk_pix, gamma, beta, eps, act, scratch, out));
+    return true;
+}
+
 void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
                 int silu_act, __nv_bfloat16* out, float2* scratch, cudaStream_t st) {
     const int C = x.c0 + x.c1;
@@ -403,6 +582,7 @@ void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma
     check_vec8(x, "group_norm");
     const int nv = C / 8;
     if (nv > 1024) throw std::invalid_argument("group_norm: more than 8192 channels");
+    if (batch == 1 && group_norm_fused(x, HW, groups, gamma, beta, eps, silu_act, out, scratch, st)) return;
     const int chunk_pix = (HW + kGnMaxChunks - 1) / kGnMaxChunks;
     const int chunks = (HW + chunk_pix - 1) / chunk_pix;
     const int rpb = std::max(1, 512 / nv);
