@@ -4,7 +4,7 @@
 Metric (BASELINE.json): per-image denoise latency (ms) & speedup vs the 1-GPU
 sequential run.  A "step" is one full x_T -> x_0 denoise of one image.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1b|c1a] [--precision f32]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1b|c1a] [--precision bf16|f32|f64]
   python bench.py --impl reference ...     # the reference's CPU path (oracle port)
 
 Workloads: c2 = BASELINE configs[1], the SD-2.1-shaped UNet
@@ -303,7 +303,7 @@ def run_ours(args, cfg):
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": ngpu, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": "bf16" if cfg["family"] == "unet" else prec,
+        "dtype": prec,
         "data": "synthetic (random-init weights from seeded Rng; x_T ~ N(0,1) from Rng(12))",
         "config": config_block(args, cfg, N), "seq_ms": seq_ms, "speedup_vs_seq": seq_ms / ms if ms > 0 else None,
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": d * 8, "d2h_bytes_per_step": (2 * T + 1) * d * act},
@@ -367,7 +367,7 @@ def run_ranks(args, cfg, ws, rank):
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": "bf16" if cfg["family"] == "unet" else prec, "data": "synthetic",
+        "dtype": prec, "data": "synthetic",
         "config": config_block(args, cfg, N), "seq_ms": seq_ms, "speedup_vs_seq": seq_ms / ms,
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": d * 8, "d2h_bytes_per_step": (2 * T + 1) * d * act},
         "gpu_launches": launches, "roofline": roof, "clocks": clocks, "transport": "NCCL p2p, one process per GPU",
@@ -382,13 +382,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="f32", choices=["f64", "f32", "bf16"])
+    ap.add_argument("--precision", default=None, choices=["f64", "f32", "bf16"],
+                    help="MLP configs: engine precision (default f32); UNet configs: bf16 (default, bf16 "
+                         "tensor-core stages) or f32 (fp32 activations, split-bf16 products, the 1e-3 parity mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
-    if cfg["family"] == "unet":
-        args.precision = "f32"  # bf16 tensor-core stages, f32 latent trajectory
+    if args.precision is None:
+        args.precision = "bf16" if cfg["family"] == "unet" else "f32"  # UNet: bf16 stages, f32 latent
+    if cfg["family"] == "unet" and args.precision == "f64":
+        raise SystemExit("UNet configs run precision bf16 or f32")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

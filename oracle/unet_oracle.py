@@ -8,6 +8,10 @@ contract it shares with the reference family.  It restates the stage programs
 of paper_2406_06911_b200/csrc/unet_dev.cu in fp32 numpy (float64 for norm
 statistics), rounding to bf16 exactly where the GPU stores bf16 tensors, and
 reads the same deterministic parameters through adx_unet_stage_params.
+
+exact=True is the fp64 oracle of the fp32 (ADX_F32) GPU mode ("the
+builder's CPU fp64 UNet oracle defines the rel-L2 <= 1e-3 check"): float64
+everywhere, no rounding.
 """
 from __future__ import annotations
 
@@ -41,8 +45,10 @@ def sinusoid(t, dim):
 
 
 class UNetOracle:
-    def __init__(self, adx, model):
+    def __init__(self, adx, model, exact: bool = False):
         self.adx, self.m = adx, model
+        self.exact = exact
+        self.dt = np.float64 if exact else np.float32
         self.sp = model.unet_spec
         self.L = model.num_stages()
         self.links = model.skip_links
@@ -52,14 +58,17 @@ class UNetOracle:
         self._kv = {}
 
     # ---------------------------------------------------------- primitives
-    @staticmethod
-    def conv3x3(x, w, b, stride2=False):
+    def r(self, x):
+        """the GPU's storage rounding: bf16 in the bf16 mode, none (fp64) in the exact mode"""
+        return np.asarray(x, np.float64) if self.exact else bf(x)
+
+    def conv3x3(self, x, w, b, stride2=False):
         H, W, Ci = x.shape
         Co = w.shape[0]
-        wt = bf(w).reshape(Co, 3, 3, Ci)
-        xp = np.zeros((H + 2, W + 2, Ci), np.float32)
+        wt = self.r(w).reshape(Co, 3, 3, Ci)
+        xp = np.zeros((H + 2, W + 2, Ci), self.dt)
         xp[1:-1, 1:-1] = x
-        acc = np.zeros((H, W, Co), np.float32)
+        acc = np.zeros((H, W, Co), self.dt)
         for r in range(3):
             for s in range(3):
                 acc += (xp[r:r + H, s:s + W].reshape(-1, Ci) @ wt[:, r, s, :].T).reshape(H, W, Co)
@@ -75,45 +84,42 @@ class UNetOracle:
         mu = xv.mean(axis=(0, 2))
         var = np.maximum((xv * xv).mean(axis=(0, 2)) - mu * mu, 0.0)
         rstd = 1.0 / np.sqrt(var + eps)
-        y = ((x.reshape(-1, g, C // g) - mu[None, :, None].astype(np.float32)) *
-             rstd[None, :, None].astype(np.float32)).reshape(H, W, C) * gamma + beta
-        return bf(silu(y) if act else y)
+        y = ((x.reshape(-1, g, C // g) - mu[None, :, None].astype(self.dt)) *
+             rstd[None, :, None].astype(self.dt)).reshape(H, W, C) * gamma + beta
+        return self.r(silu(y) if act else y)
 
-    @staticmethod
-    def layer_norm(x, gamma, beta, eps=1e-5):
+    def layer_norm(self, x, gamma, beta, eps=1e-5):
         mu = x.mean(axis=1, keepdims=True)
         var = ((x - mu) ** 2).mean(axis=1, keepdims=True)
-        return bf((x - mu) / np.sqrt(var + eps) * gamma + beta)
+        return self.r((x - mu) / np.sqrt(var + eps) * gamma + beta)
 
-    @staticmethod
-    def lin(x, w, b=None):
-        y = x @ bf(w).T
+    def lin(self, x, w, b=None):
+        y = x @ self.r(w).T
         return y + b if b is not None else y
 
-    @staticmethod
-    def attention(q, k, v, Lk):
-        """q [L, C], k [Lk, C], v [Lk, C] (bf16-valued) -> [L, C] bf16, per 64-wide head"""
+    def attention(self, q, k, v, Lk):
+        """q [L, C], k [Lk, C], v [Lk, C] -> [L, C], per 64-wide head"""
         L, C = q.shape
-        out = np.zeros((L, C), np.float32)
+        out = np.zeros((L, C), self.dt)
         for h in range(C // 64):
             sl = slice(64 * h, 64 * h + 64)
-            S = (q[:, sl] @ k[:Lk, sl].T) * np.float32(0.125)
+            S = (q[:, sl] @ k[:Lk, sl].T) * self.dt(0.125)
             S = S - S.max(axis=1, keepdims=True)
             P = np.exp(S)
-            P = bf(P / P.sum(axis=1, keepdims=True))
-            out[:, sl] = bf(P @ v[:Lk, sl])
+            P = self.r(P / P.sum(axis=1, keepdims=True))
+            out[:, sl] = self.r(P @ v[:Lk, sl])
         return out
 
     def temb(self, t):
         p = self.params[0]
-        h = silu(p["temb.lin1.w"] @ sinusoid(t, self.sp["ch"][0]).astype(np.float32) + p["temb.lin1.b"])
+        h = silu(p["temb.lin1.w"] @ sinusoid(t, self.sp["ch"][0]).astype(self.dt) + p["temb.lin1.b"])
         return p["temb.lin2.w"] @ h + p["temb.lin2.b"]
 
     def cross_kv(self, stage):
         if stage not in self._kv:
             p = self.params[stage]
-            k2 = bf(self.ctx @ p["tf.k2.w"].T)
-            v2 = bf(self.ctx @ p["tf.v2.w"].T)
+            k2 = self.r(self.ctx.astype(self.dt) @ p["tf.k2.w"].T)
+            v2 = self.r(self.ctx.astype(self.dt) @ p["tf.v2.w"].T)
             self._kv[stage] = (k2, v2)
         return self._kv[stage]
 
@@ -122,21 +128,21 @@ class UNetOracle:
         p = self.params[stage]
         H, W, C = x.shape
         a = self.group_norm(x, p["tf.gn.gamma"], p["tf.gn.beta"], 1e-6, False).reshape(-1, C)
-        h = bf(self.lin(a, p["tf.proj_in.w"], p["tf.proj_in.b"]))
+        h = self.r(self.lin(a, p["tf.proj_in.w"], p["tf.proj_in.b"]))
         a = self.layer_norm(h, p["tf.ln1.gamma"], p["tf.ln1.beta"])
-        qkv = bf(self.lin(a, p["tf.qkv.w"]))
+        qkv = self.r(self.lin(a, p["tf.qkv.w"]))
         att = self.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], H * W)
-        h = bf(self.lin(att, p["tf.o1.w"], p["tf.o1.b"]) + h)
+        h = self.r(self.lin(att, p["tf.o1.w"], p["tf.o1.b"]) + h)
         a = self.layer_norm(h, p["tf.ln2.gamma"], p["tf.ln2.beta"])
-        q2 = bf(self.lin(a, p["tf.q2.w"]))
+        q2 = self.r(self.lin(a, p["tf.q2.w"]))
         k2, v2 = self.cross_kv(stage)
         att = self.attention(q2, k2, v2, self.sp["ctx_len"])
-        h = bf(self.lin(att, p["tf.o2.w"], p["tf.o2.b"]) + h)
+        h = self.r(self.lin(att, p["tf.o2.w"], p["tf.o2.b"]) + h)
         a = self.layer_norm(h, p["tf.ln3.gamma"], p["tf.ln3.beta"])
-        f = bf(self.lin(a, p["tf.ff1.w"], p["tf.ff1.b"]))
-        g = bf(f[:, :4 * C] * gelu(f[:, 4 * C:]))
-        h = bf(self.lin(g, p["tf.ff2.w"], p["tf.ff2.b"]) + h)
-        y = bf(self.lin(h, p["tf.proj_out.w"], p["tf.proj_out.b"]) + x.reshape(-1, C))
+        f = self.r(self.lin(a, p["tf.ff1.w"], p["tf.ff1.b"]))
+        g = self.r(f[:, :4 * C] * gelu(f[:, 4 * C:]))
+        h = self.r(self.lin(g, p["tf.ff2.w"], p["tf.ff2.b"]) + h)
+        y = self.r(self.lin(h, p["tf.proj_out.w"], p["tf.proj_out.b"]) + x.reshape(-1, C))
         return y.reshape(H, W, C)
 
     def stage(self, stage, inputs, t):
@@ -145,14 +151,14 @@ class UNetOracle:
         kind = info["kind"]
         H, W = info["H"], info["W"]
         if kind == "conv_in":
-            x = np.zeros((H, W, 64), np.float32)
-            x[:, :, :self.sp["c_lat"]] = bf(np.asarray(inputs[0], np.float32).reshape(H, W, self.sp["c_lat"]))
-            return bf(self.conv3x3(x, p["conv.w"], p["conv.b"]))
+            x = np.zeros((H, W, 64), self.dt)
+            x[:, :, :self.sp["c_lat"]] = self.r(np.asarray(inputs[0], self.dt).reshape(H, W, self.sp["c_lat"]))
+            return self.r(self.conv3x3(x, p["conv.w"], p["conv.b"]))
         if kind == "down":
-            return bf(self.conv3x3(inputs[0], p["conv.w"], p["conv.b"], stride2=True))
+            return self.r(self.conv3x3(inputs[0], p["conv.w"], p["conv.b"], stride2=True))
         if kind == "up":
             x = inputs[0].repeat(2, axis=0).repeat(2, axis=1)
-            return bf(self.conv3x3(x, p["conv.w"], p["conv.b"]))
+            return self.r(self.conv3x3(x, p["conv.w"], p["conv.b"]))
         if kind == "out":
             a = self.group_norm(inputs[0], p["gn.gamma"], p["gn.beta"], 1e-5, True)
             return self.conv3x3(a, p["conv.w"], p["conv.b"])[:, :, :self.sp["c_lat"]].reshape(-1)
@@ -161,18 +167,18 @@ class UNetOracle:
         C = info["cout"]
         a = self.group_norm(x, p["gn1.gamma"], p["gn1.beta"], 1e-5, True)
         ca = p["temb.w"] @ silu(self.temb(t)) + p["temb.b"]
-        hb = bf(self.conv3x3(a, p["conv1.w"], p["conv1.b"]) + ca)
+        hb = self.r(self.conv3x3(a, p["conv1.w"], p["conv1.b"]) + ca)
         a = self.group_norm(hb, p["gn2.gamma"], p["gn2.beta"], 1e-5, True)
         res = x
         if x.shape[2] != C:
-            res = bf(self.lin(x.reshape(-1, x.shape[2]), p["short.w"], p["short.b"])).reshape(H, W, C)
-        out = bf(self.conv3x3(a, p["conv2.w"], p["conv2.b"]) + res)
+            res = self.r(self.lin(x.reshape(-1, x.shape[2]), p["short.w"], p["short.b"])).reshape(H, W, C)
+        out = self.r(self.conv3x3(a, p["conv2.w"], p["conv2.b"]) + res)
         if info["attn"]:
             out = self.transformer(stage, out)
         return out
 
     def eval_full(self, x, t):
-        """one denoiser evaluation: eps (fp32, H*W*c_lat)"""
+        """one denoiser evaluation: eps (H*W*c_lat; fp32, or fp64 in the exact mode)"""
         outs = {}
         cur = x
         for s in range(1, self.L + 1):

@@ -250,7 +250,8 @@ class LayeredDenoiser:
         return np.ctypeslib.as_array(p, shape=(n,)).reshape(r.value, c.value)
 
     def engine(self, precision: Optional[str] = None, devices: Sequence[int] = None) -> "_Engine":
-        key = (precision or _default_precision, tuple(devices or _default_devices))
+        key = (precision or getattr(self, "default_precision", None) or _default_precision,
+               tuple(devices or _default_devices))
         eng = self._engines.get(key)
         if eng is None or eng.version != self.version:
             eng = _Engine(self, key[0], key[1])
@@ -291,7 +292,10 @@ def build_unet_denoiser(H: int = 96, W: int = 96, c_lat: int = 4, ch: Sequence[i
                         seed: int = 0) -> LayeredDenoiser:
     """UNet-shaped denoiser behind the reference's stage contract (defaults: the
     SD-2.1 UNet topology at a 96x96x4 latent, random init).  Works with every
-    partition / plan / run entry point; engine precision must be "f32"."""
+    partition / plan / run entry point.  Engine precision "bf16" (the default for
+    this family): bf16 activations on the tcgen05 kernels, fp32 latent; "f32": fp32
+    activations with split-bf16 tensor-core products (the north_star's rel-L2 <=
+    1e-3 mode, checked against the fp64 oracle)."""
     from ._lib import adx_unet_spec
     s = adx_unet_spec()
     s.H, s.W, s.c_lat, s.n_levels = H, W, c_lat, len(ch)
@@ -302,6 +306,7 @@ def build_unet_denoiser(H: int = 96, W: int = 96, c_lat: int = 4, ch: Sequence[i
     h = C.c_void_p()
     check(lib().adx_model_build_unet(C.byref(s), C.byref(h)))
     m = LayeredDenoiser(h.value)
+    m.default_precision = "bf16"
     m.unet_spec = dict(H=H, W=W, c_lat=c_lat, ch=list(ch), attn=list(attn), n_res=n_res, head_dim=head_dim,
                        ctx_len=ctx_len, ctx_dim=ctx_dim, temb_dim=temb_dim, groups=groups, mid_attn=mid_attn,
                        seed=seed)
@@ -919,7 +924,8 @@ def round_exchange_bytes(plan: ExecutionPlan, partition: Partition, m: LayeredDe
     """Bytes crossing devices in each round (boundary + crossing skips + eps)."""
     ph = plan._handle()
     out = np.zeros(max(len(plan.rounds), 1), np.int64)
-    check(lib().adx_round_exchange_bytes(ph._h, partition._h, m._h, PRECISIONS[precision or _default_precision],
+    prec = precision or getattr(m, "default_precision", None) or _default_precision
+    check(lib().adx_round_exchange_bytes(ph._h, partition._h, m._h, PRECISIONS[prec],
                                          out.ctypes.data_as(C.POINTER(C.c_longlong))))
     return out[: len(plan.rounds)].tolist()
 

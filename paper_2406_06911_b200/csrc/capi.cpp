@@ -1124,7 +1124,7 @@ int adx_round_exchange_bytes(const adx_plan* p, const adx_partition* part, const
         need(p, "round_exchange_bytes");
         need(part, "round_exchange_bytes");
         need(m, "round_exchange_bytes");
-        const auto b = adx::round_exchange_bytes(p->p, part->p, m->m, adx::act_bytes(precision));
+        const auto b = adx::round_exchange_bytes(p->p, part->p, m->m, precision);
         std::memcpy(out, b.data(), b.size() * sizeof(long long));
     });
 }

@@ -102,9 +102,9 @@ Engine::Engine(const Model& m, int prec, std::vector<int> ordinals)
         dev_[i].ordinal = ordinals_[i];
         dev_[i].stages.resize(model_.L);
     }
-    if (model_.kind == 1 && prec_ != kF32)
-        throw std::invalid_argument("engine: the UNet family runs bf16 tensor-core stages with an f32 trajectory "
-                                    "(precision f32)");
+    if (model_.kind == 1 && prec_ == kF64)
+        throw std::invalid_argument("engine: the UNet family runs precision bf16 (bf16 tensor-core stages) or f32 "
+                                    "(fp32 activations, split-bf16 products) with an f32 trajectory");
     unet_.resize(ordinals_.size());
 }
 
@@ -112,7 +112,7 @@ UNetDevice& Engine::unet(int idx) {
     auto& u = unet_[idx % unet_.size()];
     if (!u) {
         CK(cudaSetDevice(ordinal(idx)));
-        u = std::make_shared<UNetDevice>(model_, ordinal(idx));
+        u = std::make_shared<UNetDevice>(model_, ordinal(idx), prec_ == kF32);
     }
     return *u;
 }

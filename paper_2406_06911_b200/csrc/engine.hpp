@@ -83,7 +83,8 @@ public:
     // tensor-core kernel; per kind (conv, GEMM, attention): {launches, ms, flops}
     double time_eval_ms(int idx, int t_embed, int iters, int* launches, double (*profile)[3] = nullptr);
     // element size of stage outputs (bf16 for the UNet family, the activation dtype otherwise)
-    int stage_bytes() const { return model_.kind == 1 ? 2 : act_bytes(prec_); }
+    // bytes per stage-output element: UNet bf16 mode 2, UNet f32 mode 4, MLP the engine precision
+    int stage_bytes() const { return model_.kind == 1 ? (prec_ == kF32 ? 4 : 2) : act_bytes(prec_); }
 
 private:
     class UNetDevice& unet(int idx);

@@ -453,7 +453,9 @@ CostComparison calibrate_and_compare(const Plan& plan, const std::vector<double>
 
 // bytes that cross devices in each round of the one-process-per-GPU program
 // (every send of every rank at the round's exchange point)
-std::vector<long long> round_exchange_bytes(const Plan& plan, const Partition& part, const Model& m, int act_bytes);
+// precision: engine precision (kF64 / kF32 / kBF16); stage outputs travel at the stage element size
+// (UNet: bf16 in the bf16 mode, fp32 in the f32 mode), eps at the trajectory element size
+std::vector<long long> round_exchange_bytes(const Plan& plan, const Partition& part, const Model& m, int precision);
 
 }  // namespace adx
 
@@ -461,12 +463,14 @@ std::vector<long long> round_exchange_bytes(const Plan& plan, const Partition& p
 
 namespace adx {
 
-std::vector<long long> round_exchange_bytes(const Plan& plan, const Partition& part, const Model& m, int act_bytes) {
+std::vector<long long> round_exchange_bytes(const Plan& plan, const Partition& part, const Model& m, int precision) {
     std::vector<long long> out(plan.rounds.size(), 0);
+    const int traj = precision == 0 ? 8 : 4;                           // kF64 : kF32 / kBF16 trajectory
+    const int stage = m.kind == 1 ? (precision == 1 ? 4 : 2) : traj;  // UNet f32 : bf16 stage outputs
     const int base = plan.w * plan.N;  // warm-up exchange points come first
     for (int r = 0; r < plan.D; ++r)
         for (const RankOp& op : rank_program(plan, part, m, r))
-            if (op.kind == kOpSend && op.point >= base) out[op.point - base] += op.elems * act_bytes;
+            if (op.kind == kOpSend && op.point >= base) out[op.point - base] += op.elems * (op.stage < 0 ? traj : stage);
     return out;
 }
 

@@ -36,6 +36,8 @@ LatencyReport predict_async(const Plan& plan, const CostModel& cm, const std::ve
 CostComparison calibrate_and_compare(const Plan& plan, const std::vector<double>& delays,
                                      const std::vector<double>& measured_round_comm_s, int broadcast_count,
                                      double measured_total_s);
-std::vector<long long> round_exchange_bytes(const Plan& plan, const Partition& part, const Model& m, int act_bytes);
+// precision: engine precision (kF64 / kF32 / kBF16); stage outputs travel at the stage element size
+// (UNet: bf16 in the bf16 mode, fp32 in the f32 mode), eps at the trajectory element size
+std::vector<long long> round_exchange_bytes(const Plan& plan, const Partition& part, const Model& m, int precision);
 
 }  // namespace adx

@@ -168,7 +168,7 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float* v) {
 // fused epilogue on 16 accumulator columns [nb, nb + 16) of output row m
 __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int nb, float* v) {
     const int nlim = p.n_store ? p.n_store : p.N;
-    if ((((p.ldo | p.ldr) & 7) == 0) && nb + 16 <= nlim) {
+    if ((((p.ldo | p.ldr) & 7) == 0) && nb + 16 <= nlim && !p.residual_f32) {
         // vectorised: 16-byte loads / stores
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
@@ -221,6 +221,7 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int
         if (p.chan_add) x += p.chan_add[static_cast<long long>(img) * p.N + n];
         if (p.act == 1) x = silu(x);
         if (p.residual) x += __bfloat162float(p.residual[m * p.ldr + n]);
+        if (p.residual_f32) x += p.residual_f32[m * p.ldr + n];
         x *= p.out_scale;
         if (p.out_f32)
             p.out_f32[m * p.ldo + n] = x;
@@ -242,6 +243,12 @@ __device__ __forceinline__ void epi_geglu16(const TcArgs& p, long long m, int n0
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] *= gelu(g[j]);
+    if (p.out_f32) {
+        float4* op = reinterpret_cast<float4*>(p.out_f32 + m * p.ldo + n0 / 2 + c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) op[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        return;
+    }
     uint4* op = reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + n0 / 2 + c);
     op[0] = pack_bf16x8(v);
     op[1] = pack_bf16x8(v + 8);
@@ -749,8 +756,9 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     if ((lda | ldb) % 8) throw std::invalid_argument("tc_gemm: row strides must be multiples of 8 elements");
     if (p.act == 2) {  // fused GEGLU (see the epilogue): fixed 256-wide tiles of [128 hidden | 128 gate]
         if (bn && bn != 256) throw std::invalid_argument("tc_gemm: GEGLU epilogue needs 256-wide N tiles");
-        if (N % 256 || !p.out_bf16 || !p.bias || p.residual || p.chan_add || (p.ldo % 8))
-            throw std::invalid_argument("tc_gemm: GEGLU epilogue needs N % 256 == 0, bias, bf16 output, ldo % 8 == 0");
+        if (N % 256 || !(p.out_bf16 || p.out_f32) || !p.bias || p.residual || p.residual_f32 || p.chan_add ||
+            (p.ldo % 8))
+            throw std::invalid_argument("tc_gemm: GEGLU epilogue needs N % 256 == 0, bias, no residual, ldo % 8 == 0");
         bn = 256;
     }
     int S = 1;

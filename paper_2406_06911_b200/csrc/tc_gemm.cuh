@@ -18,6 +18,7 @@ struct TcArgs {
     const float* bias = nullptr;          // [N]
     const float* chan_add = nullptr;      // [images][N] (e.g. time-embedding projection)
     const __nv_bfloat16* residual = nullptr;
+    const float* residual_f32 = nullptr;  // fp32 residual (ADX_F32 mode); at most one of the two
     long long ldr = 0;
     int act = 0;                          // 0 none, 1 SiLU (applied before the residual),
                                           // 2 GEGLU over tile-interleaved [hidden | gate] columns

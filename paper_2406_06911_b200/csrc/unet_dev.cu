@@ -52,9 +52,38 @@ void* upload_f32(const std::vector<float>& v) {
 
 int pad64(int n) { return (n + 63) / 64 * 64; }
 
+// host split of an fp32 matrix [rows][K] into the ADX_F32 mode's B operand: every group of
+// g columns -> [hi | lo | hi] (bf16 bits), hi = bf16(w), lo = bf16(w - hi)
+std::vector<uint16_t> split_b(const std::vector<float>& w, long long rows, int K, int g) {
+    std::vector<uint16_t> out(static_cast<size_t>(rows) * 3 * K);
+    for (long long r = 0; r < rows; ++r)
+        for (int c = 0; c < K; ++c) {
+            const float x = w[static_cast<size_t>(r) * K + c];
+            const uint16_t hb = to_bf16_bits(x);
+            float hf;
+            const uint32_t hu = static_cast<uint32_t>(hb) << 16;
+            std::memcpy(&hf, &hu, 4);
+            const uint16_t lb = to_bf16_bits(x - hf);
+            const int grp = c / g, cg = c % g;
+            uint16_t* o = out.data() + static_cast<size_t>(r) * 3 * K + 3LL * grp * g + cg;
+            o[0] = hb;
+            o[g] = lb;
+            o[2 * g] = hb;
+        }
+    return out;
+}
+
+void* upload_u16(const std::vector<uint16_t>& h) {
+    void* d = nullptr;
+    CKD(cudaMalloc(&d, std::max<size_t>(h.size(), 8) * 2));
+    CKD(cudaMemcpy(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+    return d;
+}
+
 }  // namespace
 
-UNetDevice::UNetDevice(const Model& m, int ordinal) : m_(m), d_(*m.unet), ordinal_(ordinal) {
+UNetDevice::UNetDevice(const Model& m, int ordinal, bool exact)
+    : m_(m), d_(*m.unet), ordinal_(ordinal), exact_(exact) {
     st_.resize(m.L + 1);
 }
 
@@ -71,7 +100,11 @@ UNetDevice::~UNetDevice() {
         for (void* p : {static_cast<void*>(s.a), static_cast<void*>(s.b), static_cast<void*>(s.c),
                         static_cast<void*>(s.r), static_cast<void*>(s.qkv), static_cast<void*>(s.att),
                         static_cast<void*>(s.ff), static_cast<void*>(s.ff2), static_cast<void*>(s.P),
-                        static_cast<void*>(s.VT), static_cast<void*>(s.S), static_cast<void*>(s.gn)})
+                        static_cast<void*>(s.VT), static_cast<void*>(s.S), static_cast<void*>(s.gn),
+                        static_cast<void*>(s.fa), static_cast<void*>(s.fb), static_cast<void*>(s.fc),
+                        static_cast<void*>(s.fr), static_cast<void*>(s.fqkv), static_cast<void*>(s.fatt),
+                        static_cast<void*>(s.fff), static_cast<void*>(s.fvt), static_cast<void*>(s.sa),
+                        static_cast<void*>(s.sq), static_cast<void*>(s.sk), static_cast<void*>(s.sv)})
             cudaFree(p);
     }
 }
@@ -90,6 +123,26 @@ void UNetDevice::ensure_stage(int stage) {
     auto ps = unet_stage_params(d_, stage);
     for (auto& p : ps) {
         const bool matrix = p.shape.size() == 2;
+        if (exact_ && matrix && p.name != "tf.k2.w" && p.name != "tf.v2.w" && p.name != "temb.w") {
+            // ADX_F32: split-bf16 weights, [hi | lo | hi] per conv tap (g = Cin) or per row (g = K);
+            // the GEGLU ff1 rows are tile-interleaved first, exactly as in the bf16 mode
+            const int rows = p.shape[0], K = p.shape[1];
+            std::vector<float> w = p.data;
+            if (p.name == "tf.ff1.w") {
+                const int H = rows / 2;
+                if (H % 128) throw std::invalid_argument("unet: GEGLU width must be a multiple of 128");
+                for (int t = 0; t < H / 128; ++t)
+                    for (int i = 0; i < 256; ++i) {
+                        const int src = i < 128 ? 128 * t + i : H + 128 * t + (i - 128);
+                        std::copy_n(p.data.begin() + static_cast<size_t>(src) * K, K,
+                                    w.begin() + static_cast<size_t>(256 * t + i) * K);
+                    }
+            }
+            const bool conv = p.name.rfind("conv", 0) == 0;
+            ds.p[p.name] = upload_u16(split_b(w, rows, K, conv ? K / 9 : K));
+            ds.bytes[p.name] = static_cast<long long>(w.size()) * 6;
+            continue;
+        }
         if (p.name == "tf.ff1.w" || p.name == "tf.ff1.b") {
             // GEGLU fused into the ff1 GEMM epilogue: rows [hidden | gate] interleaved per
             // 256-wide N tile: tile t = hidden rows [128t, 128t+128) then gate rows 4C + same
@@ -133,8 +186,13 @@ void UNetDevice::ensure_stage(int stage) {
                 k2[static_cast<size_t>(l) * C + c] = ak;
                 vt2[static_cast<size_t>(c) * Lp + l] = av;
             }
-        ds.k2 = static_cast<bf16*>(upload_bf16(k2));
-        ds.vt2 = static_cast<bf16*>(upload_bf16(vt2));
+        if (exact_) {  // split operands: K2' per 64-wide head, V2'^T along the (padded) context keys
+            ds.k2 = static_cast<bf16*>(upload_u16(split_b(k2, Lp, C, 64)));
+            ds.vt2 = static_cast<bf16*>(upload_u16(split_b(vt2, C, Lp, Lp)));
+        } else {
+            ds.k2 = static_cast<bf16*>(upload_bf16(k2));
+            ds.vt2 = static_cast<bf16*>(upload_bf16(vt2));
+        }
     }
     ds.ready = true;
 }
@@ -197,6 +255,31 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
     s.S = static_cast<float*>(al(S * 4));
     s.VT = static_cast<bf16*>(al(vt * 2));
     s.gn = static_cast<float2*>(al(gn));
+    if (exact_) {
+        size_t spl = 0, ffx = 0, vtx = 0;
+        for (const UStage& st : d_.st) {
+            const size_t hw = static_cast<size_t>(st.H) * st.W;
+            spl = std::max({spl, 3 * 4 * hw * st.cin, 3 * hw * (st.cin + st.cskip), 3 * hw * st.cout});
+            if (st.attn) {
+                const size_t L = hw, Lp = pad64(static_cast<int>(L));
+                spl = std::max({spl, 3 * L * 4 * st.cout, 3 * L * Lp});
+                ffx = std::max(ffx, L * 4 * st.cout);
+                vtx = std::max(vtx, 64 * Lp);
+            }
+        }
+        s.fa = static_cast<float*>(al(act * 4));
+        s.fb = static_cast<float*>(al(act * 4));
+        s.fc = static_cast<float*>(al(act * 4));
+        s.fr = static_cast<float*>(al(act * 4));
+        s.fatt = static_cast<float*>(al(act * 4));
+        s.fqkv = static_cast<float*>(al(qkv * 4));
+        s.fff = static_cast<float*>(al(ffx * 4));
+        s.fvt = static_cast<float*>(al(vtx * 4));
+        s.sa = static_cast<bf16*>(al(spl * 2));
+        s.sq = static_cast<bf16*>(al(3 * act * 2));
+        s.sk = static_cast<bf16*>(al(3 * act * 2));
+        s.sv = static_cast<bf16*>(al(3 * vtx * 2));
+    }
     CKD(cudaMemsetAsync(s.gn, 0, gn, st));  // group_norm's ticket counter starts at zero (stream-ordered:
                                              // also valid when first reached inside a graph capture)
     return scratch_.emplace(st, s).first->second;
@@ -309,6 +392,7 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
 
 void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, bool latent_f64, cudaStream_t st) {
     ensure_stage(stage);
+    if (exact_) return enqueue_exact(stage, in, t, y, latent_f64, st);
     const UNetSpec& sp = d_.spec;
     const UStage& s = d_.st[stage - 1];
     UScratch& sc = scratch(st);
@@ -390,6 +474,202 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
             c2.ldo = C;
             tc_conv3x3(sc.a, P(stage, "conv2.w"), 1, s.H, s.W, C, C, c2, st);
             if (s.attn) transformer(stage, sc.c, s.H, s.W, C, static_cast<bf16*>(y), st);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ ADX_F32 mode
+// Every contraction runs on the bf16 tcgen05 kernels as A'.W'^T with A' = [hi|hi|lo] and
+// W' = [hi|lo|hi] concatenated along K (= hi.hi + hi.lo + lo.hi, fp32 accumulation in
+// TMEM); activations, norms, softmax and residuals stay fp32.
+
+void UNetDevice::gemm_x(UScratch& s, const float* x, int M, int K, const char* wname, int stage, int N, TcArgs a,
+                        cudaStream_t st) {
+    split3(x, M, K, K, K, 0, s.sa, st);
+    tc_gemm(s.sa, P(stage, wname), M, N, 3 * K, a, st);
+}
+
+void UNetDevice::conv_x(UScratch& s, const float* x, int H, int W, int Cin, const char* wname, int stage, int Cout,
+                        TcArgs a, cudaStream_t st) {
+    split3(x, static_cast<long long>(H) * W, Cin, Cin, Cin, 0, s.sa, st);
+    tc_conv3x3(s.sa, P(stage, wname), 1, H, W, 3 * Cin, Cout, a, st);
+}
+
+// unfused attention, one 64-wide head at a time: S = Q'_h K'_h^T (K = 192), fp32 softmax in
+// place, P' = split(P) along keys, O_h = P' V'_h^T (K = 3 * Lkp); ks = K' [Lk][3C] split per
+// head (B pattern); V from fp32 v (transposed + split here) or pre-split vts [C][3 * Lkp]
+void UNetDevice::attention_exact(UScratch& s, const float* q, long long ldq, const bf16* ks, const float* v,
+                                 long long ldv, const bf16* vts, int L, int Lk, int C, float* out, cudaStream_t st) {
+    const int Lkp = pad64(Lk);
+    split3(q, L, C, ldq, 64, 0, s.sq, st);
+    for (int h = 0; h < C / 64; ++h) {
+        TcArgs a;
+        a.out_f32 = s.S;
+        a.ldo = Lkp;
+        a.out_scale = 0.125f;
+        tc_gemm_strided(s.sq + h * 192, 3LL * C, ks + h * 192, 3LL * C, L, Lk, 192, a, st);
+        softmax_rows_f32(s.S, Lkp, L, Lk, Lkp, st);
+        split3(s.S, L, Lkp, Lkp, Lkp, 0, s.sa, st);
+        const bf16* vt = vts ? vts + static_cast<long long>(h) * 64 * 3 * Lkp : s.sv;
+        if (!vts) {
+            transpose_f32(v + h * 64, ldv, Lk, Lkp, 64, s.fvt, st);
+            split3(s.fvt, 64, Lkp, Lkp, Lkp, 1, s.sv, st);
+        }
+        TcArgs o;
+        o.out_f32 = out + h * 64;
+        o.ldo = C;
+        tc_gemm(s.sa, vt, L, 64, 3 * Lkp, o, st);
+    }
+}
+
+void UNetDevice::transformer_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st) {
+    UScratch& s = scratch(st);
+    const UNetSpec& sp = d_.spec;
+    const int L = H * W;
+    group_norm(Cat2F{x, C, nullptr, 0}, 1, L, sp.groups, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"), 1e-6f, 0,
+               s.fa, s.gn, st);
+    TcArgs pi;
+    pi.bias = F(stage, "tf.proj_in.b");
+    pi.out_f32 = s.fb;
+    pi.ldo = C;
+    gemm_x(s, s.fa, L, C, "tf.proj_in.w", stage, C, pi, st);  // h = fb
+    layer_norm(s.fb, L, C, F(stage, "tf.ln1.gamma"), F(stage, "tf.ln1.beta"), 1e-5f, s.fa, st);
+    TcArgs qk;
+    qk.out_f32 = s.fqkv;
+    qk.ldo = 3 * C;
+    gemm_x(s, s.fa, L, C, "tf.qkv.w", stage, 3 * C, qk, st);
+    split3(s.fqkv + C, L, C, 3LL * C, 64, 1, s.sk, st);
+    attention_exact(s, s.fqkv, 3LL * C, s.sk, s.fqkv + 2 * C, 3LL * C, nullptr, L, L, C, s.fatt, st);
+    TcArgs o1;
+    o1.bias = F(stage, "tf.o1.b");
+    o1.residual_f32 = s.fb;
+    o1.ldr = C;
+    o1.out_f32 = s.fb;
+    o1.ldo = C;
+    gemm_x(s, s.fatt, L, C, "tf.o1.w", stage, C, o1, st);
+    layer_norm(s.fb, L, C, F(stage, "tf.ln2.gamma"), F(stage, "tf.ln2.beta"), 1e-5f, s.fa, st);
+    TcArgs q2;
+    q2.out_f32 = s.fqkv;
+    q2.ldo = C;
+    gemm_x(s, s.fa, L, C, "tf.q2.w", stage, C, q2, st);
+    attention_exact(s, s.fqkv, C, st_[stage].k2, nullptr, 0, st_[stage].vt2, L, sp.ctx_len, C, s.fatt, st);
+    TcArgs o2;
+    o2.bias = F(stage, "tf.o2.b");
+    o2.residual_f32 = s.fb;
+    o2.ldr = C;
+    o2.out_f32 = s.fb;
+    o2.ldo = C;
+    gemm_x(s, s.fatt, L, C, "tf.o2.w", stage, C, o2, st);
+    layer_norm(s.fb, L, C, F(stage, "tf.ln3.gamma"), F(stage, "tf.ln3.beta"), 1e-5f, s.fa, st);
+    TcArgs f1;
+    f1.bias = F(stage, "tf.ff1.b");
+    f1.act = 2;  // GEGLU in the epilogue, fp32 out, 4C wide
+    f1.out_f32 = s.fff;
+    f1.ldo = 4 * C;
+    gemm_x(s, s.fa, L, C, "tf.ff1.w", stage, 8 * C, f1, st);
+    TcArgs f2;
+    f2.bias = F(stage, "tf.ff2.b");
+    f2.residual_f32 = s.fb;
+    f2.ldr = C;
+    f2.out_f32 = s.fb;
+    f2.ldo = C;
+    gemm_x(s, s.fff, L, 4 * C, "tf.ff2.w", stage, C, f2, st);
+    TcArgs po;
+    po.bias = F(stage, "tf.proj_out.b");
+    po.residual_f32 = x;
+    po.ldr = C;
+    po.out_f32 = y;
+    po.ldo = C;
+    gemm_x(s, s.fb, L, C, "tf.proj_out.w", stage, C, po, st);
+}
+
+void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, void* y, bool latent_f64,
+                               cudaStream_t st) {
+    const UNetSpec& sp = d_.spec;
+    const UStage& s = d_.st[stage - 1];
+    UScratch& sc = scratch(st);
+    const int HW = s.H * s.W;
+    float* yf = static_cast<float*>(y);
+    switch (s.kind) {
+        case kConvIn: {
+            pack_latent_f32(in[0].p, latent_f64, HW, sp.c_lat, 64, sc.fa, st);
+            TcArgs a;
+            a.bias = F(stage, "conv.b");
+            a.out_f32 = yf;
+            a.ldo = s.cout;
+            conv_x(sc, sc.fa, s.H, s.W, 64, "conv.w", stage, s.cout, a, st);
+            break;
+        }
+        case kDown: {
+            TcArgs a;
+            a.bias = F(stage, "conv.b");
+            a.out_f32 = yf;
+            a.ldo = s.cout;
+            a.sub2 = 1;
+            conv_x(sc, static_cast<const float*>(in[0].p), s.H, s.W, s.cin, "conv.w", stage, s.cout, a, st);
+            break;
+        }
+        case kUp: {
+            // nearest 2x of fp32 = the bf16 copy kernel over twice the channel count
+            upsample2x(static_cast<const bf16*>(in[0].p), 1, s.H, s.W, 2 * s.cin, reinterpret_cast<bf16*>(sc.fa), st);
+            TcArgs a;
+            a.bias = F(stage, "conv.b");
+            a.out_f32 = yf;
+            a.ldo = s.cout;
+            conv_x(sc, sc.fa, 2 * s.H, 2 * s.W, s.cin, "conv.w", stage, s.cout, a, st);
+            break;
+        }
+        case kOut: {
+            if (latent_f64) throw std::invalid_argument("unet: the UNet family runs in f32 trajectory precision");
+            Cat2F x{static_cast<const float*>(in[0].p), s.cin, nullptr, 0};
+            group_norm(x, 1, HW, sp.groups, F(stage, "gn.gamma"), F(stage, "gn.beta"), 1e-5f, 1, sc.fa, sc.gn, st);
+            TcArgs a;
+            a.bias = F(stage, "conv.b");
+            a.out_f32 = yf;
+            a.ldo = sp.c_lat;
+            a.n_store = sp.c_lat;
+            conv_x(sc, sc.fa, s.H, s.W, s.cin, "conv.w", stage, 32, a, st);
+            break;
+        }
+        default: {  // resnet (+ transformer)
+            const int C = s.cout, cin = s.cin + s.cskip;
+            const float* x0 = static_cast<const float*>(in[0].p);
+            const float* x1 = s.cskip ? static_cast<const float*>(in[1].p) : nullptr;
+            Cat2F xc{x0, s.cin, x1, s.cskip};
+            group_norm(xc, 1, HW, sp.groups, F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.fa, sc.gn, st);
+            TcArgs c1;
+            c1.bias = F(stage, "conv1.b");
+            c1.chan_add = st_[stage].chan_add + static_cast<long long>(t) * C;
+            c1.out_f32 = sc.fb;
+            c1.ldo = C;
+            conv_x(sc, sc.fa, s.H, s.W, cin, "conv1.w", stage, C, c1, st);
+            group_norm(Cat2F{sc.fb, C, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn2.gamma"), F(stage, "gn2.beta"),
+                       1e-5f, 1, sc.fa, sc.gn, st);
+            const float* res = x0;
+            if (cin != C) {
+                const float* xin = x0;
+                if (s.cskip) {  // fp32 channel concat = the bf16 copy kernel over twice the channels
+                    concat_channels(Cat2{reinterpret_cast<const bf16*>(x0), 2 * s.cin, reinterpret_cast<const bf16*>(x1),
+                                         2 * s.cskip},
+                                    HW, reinterpret_cast<bf16*>(sc.fc), st);
+                    xin = sc.fc;
+                }
+                TcArgs sh;
+                sh.bias = F(stage, "short.b");
+                sh.out_f32 = sc.fr;
+                sh.ldo = C;
+                gemm_x(sc, xin, HW, cin, "short.w", stage, C, sh, st);
+                res = sc.fr;
+            }
+            TcArgs c2;
+            c2.bias = F(stage, "conv2.b");
+            c2.residual_f32 = res;
+            c2.ldr = C;
+            float* out = s.attn ? sc.fc : yf;
+            c2.out_f32 = out;
+            c2.ldo = C;
+            conv_x(sc, sc.fa, s.H, s.W, C, "conv2.w", stage, C, c2, st);
+            if (s.attn) transformer_exact(stage, sc.fc, s.H, s.W, C, yf, st);
         }
     }
 }

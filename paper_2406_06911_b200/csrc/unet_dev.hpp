@@ -2,6 +2,7 @@
 #pragma once
 
 #include "engine.hpp"
+#include "tc_gemm.cuh"
 #include "unet.hpp"
 
 #include <cuda_bf16.h>
@@ -27,11 +28,17 @@ struct UScratch {
                   *ff = nullptr, *ff2 = nullptr, *P = nullptr, *VT = nullptr;
     float* S = nullptr;
     float2* gn = nullptr;
+    // ADX_F32 mode: fp32 activations and split-bf16 operands (3 columns per column)
+    float *fa = nullptr, *fb = nullptr, *fc = nullptr, *fr = nullptr, *fqkv = nullptr, *fatt = nullptr, *fff = nullptr,
+          *fvt = nullptr;
+    __nv_bfloat16 *sa = nullptr, *sq = nullptr, *sk = nullptr, *sv = nullptr;
 };
 
 class UNetDevice {
 public:
-    UNetDevice(const Model& m, int ordinal);
+    // exact = ADX_F32 mode: fp32 activations, split-bf16 tensor-core products (rel-L2 <= 1e-3
+    // vs the fp64 oracle); otherwise ADX_BF16: bf16 activations
+    UNetDevice(const Model& m, int ordinal, bool exact);
     ~UNetDevice();
     void ensure_stage(int stage);
     void ensure_tables(int T);
@@ -48,6 +55,17 @@ private:
                    const __nv_bfloat16* v, long long ldv, const __nv_bfloat16* v_t, int L, int Lk, int C,
                    __nv_bfloat16* out, cudaStream_t st);
     void transformer(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
+    // ADX_F32 mode
+    void enqueue_exact(int stage, const std::vector<Seg>& in, int t, void* y, bool latent_f64, cudaStream_t st);
+    void transformer_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st);
+    void attention_exact(UScratch& s, const float* q, long long ldq, const __nv_bfloat16* ks, const float* v,
+                         long long ldv, const __nv_bfloat16* vts, int L, int Lk, int C, float* out, cudaStream_t st);
+    // split-bf16 GEMM / conv: out = act(split(x) . W'^T + ...) with W' stored split on the device
+    void gemm_x(UScratch& s, const float* x, int M, int K, const char* wname, int stage, int N, TcArgs a,
+                cudaStream_t st);
+    void conv_x(UScratch& s, const float* x, int H, int W, int Cin, const char* wname, int stage, int Cout, TcArgs a,
+                cudaStream_t st);
+    bool exact_ = false;
 
     const Model& m_;
     const UNetDesc& d_;

@@ -37,13 +37,6 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// 8 consecutive channels (one 16-byte vector) of pixel `pix` from a two-segment
-// channel concat; both segments are multiples of 8 channels (checked on the host)
-__device__ __forceinline__ uint4 cat_vec(const Cat2& x, long long pix, int v) {
-    const int c = v * 8;
-    return c < x.c0 ? __ldg(reinterpret_cast<const uint4*>(x.p0 + pix * x.c0 + c))
-                    : __ldg(reinterpret_cast<const uint4*>(x.p1 + pix * x.c1 + (c - x.c0)));
-}
 __device__ __forceinline__ void unpack8(const uint4& u, float* f) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
@@ -62,6 +55,46 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
         w[i] = *reinterpret_cast<uint32_t*>(&b);
     }
     return u;
+}
+
+// 8 consecutive elements of an activation tensor: one 16-byte vector (bf16) or two (fp32)
+template <typename T>
+struct Vec8;
+template <>
+struct Vec8<bf16> {
+    using raw = uint4;
+    __device__ static raw load(const bf16* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+    __device__ static void unpack(const raw& u, float* f) { unpack8(u, f); }
+    __device__ static raw pack(const float* f) { return pack8(f); }
+    __device__ static void store(bf16* p, const raw& u) { *reinterpret_cast<uint4*>(p) = u; }
+};
+struct F8 {
+    float4 a, b;
+};
+template <>
+struct Vec8<float> {
+    using raw = F8;
+    __device__ static raw load(const float* p) {
+        return {__ldg(reinterpret_cast<const float4*>(p)), __ldg(reinterpret_cast<const float4*>(p) + 1)};
+    }
+    __device__ static void unpack(const raw& u, float* f) {
+        f[0] = u.a.x, f[1] = u.a.y, f[2] = u.a.z, f[3] = u.a.w, f[4] = u.b.x, f[5] = u.b.y, f[6] = u.b.z, f[7] = u.b.w;
+    }
+    __device__ static raw pack(const float* f) {
+        return {make_float4(f[0], f[1], f[2], f[3]), make_float4(f[4], f[5], f[6], f[7])};
+    }
+    __device__ static void store(float* p, const raw& u) {
+        reinterpret_cast<float4*>(p)[0] = u.a;
+        reinterpret_cast<float4*>(p)[1] = u.b;
+    }
+};
+
+// 8 consecutive channels (one vector) of pixel `pix` from a two-segment channel
+// concat; both segments are multiples of 8 channels (checked on the host)
+template <typename T>
+__device__ __forceinline__ typename Vec8<T>::raw cat_vec(const Cat2T<T>& x, long long pix, int v) {
+    const int c = v * 8;
+    return c < x.c0 ? Vec8<T>::load(x.p0 + pix * x.c0 + c) : Vec8<T>::load(x.p1 + pix * x.c1 + (c - x.c0));
 }
 
 // GroupNorm scratch: [ticket counter (64 B)][per-channel (scale, shift) float2, batch*C][partials]
@@ -85,7 +118,8 @@ __host__ __device__ inline GnLayout gn_layout(float2* scratch, int batch, int C)
 // (ticket) merges all chunks in fp64 (fixed order) and folds mean / rstd / gamma /
 // beta into per-channel (a, b) with y = x * a + b.  Deterministic and independent of
 // which CTA happens to finish last.
-__global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, const float* gamma,
+template <typename T>
+__global__ void gn_stats(Cat2T<T> x, int HW, int groups, int chunk_pix, int chunks, const float* gamma,
                          const float* beta, float eps, float2* scratch) {
     pdl_wait();
     extern __shared__ float sm[];  // [2][rpb][C]
@@ -100,7 +134,7 @@ __global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, 
         for (int i = 0; i < 8; ++i) s[i] = ss[i] = 0.f;
         // 4 rows in flight per thread (the loads do not depend on the running sums)
         for (int p = p0 + r; p < p1; p += 4 * rpb) {
-            uint4 u[4];
+            typename Vec8<T>::raw u[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (p + k * rpb < p1) u[k] = cat_vec(x, static_cast<long long>(n) * HW + p + k * rpb, v);
@@ -108,7 +142,7 @@ __global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, 
             for (int k = 0; k < 4; ++k) {
                 if (p + k * rpb >= p1) break;
                 float f[8];
-                unpack8(u[k], f);
+                Vec8<T>::unpack(u[k], f);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     s[i] += f[i];
@@ -199,7 +233,8 @@ __global__ void gn_stats(Cat2 x, int HW, int groups, int chunk_pix, int chunks, 
 }
 
 // GroupNorm pass 2: y = x * a[c] + b[c] (+SiLU), 8 channels per thread
-__global__ void gn_apply(Cat2 x, long long pixels, int HW, const float2* __restrict__ ab, int act, bf16* out) {
+template <typename T>
+__global__ void gn_apply(Cat2T<T> x, long long pixels, int HW, const float2* __restrict__ ab, int act, T* out) {
     pdl_wait();
     const int C = x.c0 + x.c1, nv = C / 8;
     const long long n = pixels * nv;
@@ -209,14 +244,14 @@ __global__ void gn_apply(Cat2 x, long long pixels, int HW, const float2* __restr
         const int v = static_cast<int>(i - pix * nv);
         const float2* abv = ab + (pix / HW) * C + v * 8;
         float f[8];
-        unpack8(cat_vec(x, pix, v), f);
+        Vec8<T>::unpack(cat_vec(x, pix, v), f);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const float2 q = __ldg(abv + k);
             f[k] = fmaf(f[k], q.x, q.y);
             if (act) f[k] = silu(f[k]);
         }
-        reinterpret_cast<uint4*>(out)[i] = pack8(f);
+        Vec8<T>::store(out + i * 8, Vec8<T>::pack(f));
     }
 }
 
@@ -226,16 +261,18 @@ __global__ void gn_apply(Cat2 x, long long pixels, int HW, const float2* __restr
 // publishes its group partials; after a grid barrier every CTA folds all G partials
 // in the same fixed fp64 order (identical statistics everywhere, deterministic),
 // builds per-channel (a, b) and normalises its SMEM copy: one HBM read of x.
-__global__ void gn_fused(Cat2 x, int HW, int groups, int chunk_pix, const float* gamma, const float* beta, float eps,
-                         int act, float2* scratch, bf16* out) {
+template <typename T>
+__global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const float* gamma, const float* beta,
+                         float eps, int act, float2* scratch, T* out) {
     extern __shared__ __align__(16) uint8_t gsm[];
     pdl_wait();
     const int G = gridDim.x, cta = blockIdx.x;
     const int C = x.c0 + x.c1, nv = C / 8, cpg = C / groups;
     const int rpb = blockDim.x / nv, r = threadIdx.x / nv, v = threadIdx.x % nv;
     const int p0 = cta * chunk_pix, p1 = min(HW, p0 + chunk_pix), np = max(0, p1 - p0);
-    uint4* tile = reinterpret_cast<uint4*>(gsm);                              // [chunk_pix][nv]
-    float* red = reinterpret_cast<float*>(gsm + static_cast<size_t>(chunk_pix) * C * 2);  // [2][rpb][C]
+    using Raw = typename Vec8<T>::raw;
+    Raw* tile = reinterpret_cast<Raw*>(gsm);                                  // [chunk_pix][nv]
+    float* red = reinterpret_cast<float*>(gsm + static_cast<size_t>(chunk_pix) * nv * sizeof(Raw));  // [2][rpb][C]
     float2* ab = reinterpret_cast<float2*>(red + 2 * rpb * C);               // [C]
     double* st = reinterpret_cast<double*>(ab + C);                          // [nsub][groups][2], then [groups][2]
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(scratch + 1);
@@ -245,7 +282,7 @@ __global__ void gn_fused(Cat2 x, int HW, int groups, int chunk_pix, const float*
 #pragma unroll
         for (int i = 0; i < 8; ++i) s[i] = ss[i] = 0.f;
         for (int q = r; q < np; q += 4 * rpb) {
-            uint4 u[4];
+            Raw u[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (q + k * rpb < np) u[k] = cat_vec(x, p0 + q + k * rpb, v);
@@ -254,7 +291,7 @@ __global__ void gn_fused(Cat2 x, int HW, int groups, int chunk_pix, const float*
                 if (q + k * rpb >= np) break;
                 tile[(q + k * rpb) * nv + v] = u[k];
                 float f[8];
-                unpack8(u[k], f);
+                Vec8<T>::unpack(u[k], f);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     s[i] += f[i];
@@ -343,37 +380,38 @@ __global__ void gn_fused(Cat2 x, int HW, int groups, int chunk_pix, const float*
     }
     __syncthreads();
     // normalise the SMEM copy, 16-byte coalesced stores
-    uint4* o = reinterpret_cast<uint4*>(out) + static_cast<long long>(p0) * nv;
+    T* o = out + static_cast<long long>(p0) * C;
     for (int i = threadIdx.x; i < np * nv; i += blockDim.x) {
         const int vv = i % nv;
         float f[8];
-        unpack8(tile[i], f);
+        Vec8<T>::unpack(tile[i], f);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const float2 q = ab[vv * 8 + k];
             f[k] = fmaf(f[k], q.x, q.y);
             if (act) f[k] = silu(f[k]);
         }
-        o[i] = pack8(f);
+        Vec8<T>::store(o + static_cast<long long>(i) * 8, Vec8<T>::pack(f));
     }
 }
 
 // LayerNorm over C per token, one warp per token, row held in registers (C <= 2048)
 constexpr int kLnMaxVec = 8;
-__global__ void layernorm_k(const bf16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
-                            bf16* out) {
+template <typename T>
+__global__ void layernorm_k(const T* x, int tokens, int C, const float* gamma, const float* beta, float eps,
+                            T* out) {
     pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= tokens) return;
     const int nv = C / 8;
-    const uint4* r = reinterpret_cast<const uint4*>(x + static_cast<long long>(warp) * C);
+    const T* r = x + static_cast<long long>(warp) * C;
     float f[kLnMaxVec][8];
     float s = 0.f;
 #pragma unroll
     for (int j = 0; j < kLnMaxVec; ++j) {
         const int v = lane + 32 * j;
         if (v < nv) {
-            unpack8(__ldg(r + v), f[j]);
+            Vec8<T>::unpack(Vec8<T>::load(r + v * 8), f[j]);
 #pragma unroll
             for (int k = 0; k < 8; ++k) s += f[j][k];
         }
@@ -390,7 +428,7 @@ __global__ void layernorm_k(const bf16* x, int tokens, int C, const float* gamma
             }
         }
     const float rstd = rsqrtf(warp_sum(ss) / C + eps);
-    uint4* o = reinterpret_cast<uint4*>(out + static_cast<long long>(warp) * C);
+    T* o = out + static_cast<long long>(warp) * C;
 #pragma unroll
     for (int j = 0; j < kLnMaxVec; ++j) {
         const int v = lane + 32 * j;
@@ -403,7 +441,7 @@ __global__ void layernorm_k(const bf16* x, int tokens, int C, const float* gamma
             float y[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) y[k] = (f[j][k] - mu) * rstd * gg[k] + be[k];
-            o[v] = pack8(y);
+            Vec8<T>::store(o + v * 8, Vec8<T>::pack(y));
         }
     }
 }
@@ -496,15 +534,19 @@ __global__ void concat_k(Cat2 x, long long pixels, bf16* out) {
 }
 
 // latent (fp32 or fp64, H*W*c_lat, HWC order) -> bf16 NHWC with cpad channels (zeros above c_lat)
-template <typename T>
-__global__ void pack_latent_k(const T* x, long long pixels, int c_lat, int cpad, bf16* out) {
+template <typename T, typename O = bf16>
+__global__ void pack_latent_k(const T* x, long long pixels, int c_lat, int cpad, O* out) {
     pdl_wait();
     const long long n = pixels * cpad;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long p = i / cpad;
         const int c = static_cast<int>(i % cpad);
-        out[i] = __float2bfloat16(c < c_lat ? static_cast<float>(x[p * c_lat + c]) : 0.f);
+        const float v = c < c_lat ? static_cast<float>(x[p * c_lat + c]) : 0.f;
+        if constexpr (sizeof(O) == 2)
+            out[i] = __float2bfloat16(v);
+        else
+            out[i] = v;
     }
 }
 
@@ -524,21 +566,98 @@ __global__ void transpose_head_k(const bf16* V, long long ldv, int L, int Lpad, 
     }
 }
 
+// split-bf16 operands of the ADX_F32 mode (see split3 in unet_kernels.cuh)
+__global__ void split3_k(const float* x, long long rows, int cols, long long ldx, int g, int pattern, bf16* out) {
+    pdl_wait();
+    const int nv = cols / 8;
+    const long long n = rows * nv;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long row = i / nv;
+        const int c = static_cast<int>(i - row * nv) * 8;
+        float f[8], hi[8], lo[8];
+        Vec8<float>::unpack(Vec8<float>::load(x + row * ldx + c), f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            hi[k] = __bfloat162float(__float2bfloat16(f[k]));
+            lo[k] = f[k] - hi[k];
+        }
+        const uint4 h = pack8(hi), l = pack8(lo);
+        const int grp = c / g, cg = c - grp * g;
+        bf16* o = out + row * 3LL * cols + 3LL * grp * g + cg;
+        *reinterpret_cast<uint4*>(o) = h;
+        *reinterpret_cast<uint4*>(o + g) = pattern ? l : h;
+        *reinterpret_cast<uint4*>(o + 2 * g) = pattern ? h : l;
+    }
+}
+
+// fp32 row softmax, in place (the ADX_F32 mode's unfused attention)
+__global__ void softmax_rows_f32_k(float* S, long long lds, int valid, int padded) {
+    pdl_wait();
+    float* r = S + static_cast<long long>(blockIdx.x) * lds;
+    __shared__ float red[32];
+    float mx = -INFINITY;
+    for (int c = threadIdx.x; c < valid; c += blockDim.x) mx = fmaxf(mx, r[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    mx = red[0];
+    __syncthreads();
+    float s = 0.f;
+    for (int c = threadIdx.x; c < valid; c += blockDim.x) s += expf(r[c] - mx);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        red[0] = t;
+    }
+    __syncthreads();
+    const float inv = 1.0f / red[0];
+    for (int c = threadIdx.x; c < padded; c += blockDim.x) r[c] = c < valid ? expf(r[c] - mx) * inv : 0.f;
+}
+
+__global__ void transpose_f32_k(const float* V, long long ldv, int L, int Lpad, int hd, float* VT) {
+    pdl_wait();
+    __shared__ float tile[32][33];
+    const int k0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int k = k0 + i, d = d0 + threadIdx.x;
+        tile[i][threadIdx.x] = (k < L && d < hd) ? V[static_cast<long long>(k) * ldv + d] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int d = d0 + i, k = k0 + threadIdx.x;
+        if (d < hd && k < Lpad) VT[static_cast<long long>(d) * Lpad + k] = tile[threadIdx.x][i];
+    }
+}
+
 int grid_for(long long n, int threads = 256) {
     return static_cast<int>(std::min<long long>((n + threads - 1) / threads, 148LL * 16));
 }
 
 }  // namespace
 
-void check_vec8(const Cat2& x, const char* who) {
+template <typename T>
+void check_vec8(const Cat2T<T>& x, const char* who) {
     if ((x.c0 % 8) || (x.c1 % 8))
         throw std::invalid_argument(std::string(who) + ": channel segments must be multiples of 8");
 }
 
 // one-launch cooperative GroupNorm when the chunk of every SM fits in SMEM (see gn_fused);
 // returns false (nothing launched) otherwise.  ADX_GN_FUSED=0 disables it.
-bool group_norm_fused(const Cat2& x, int HW, int groups, const float* gamma, const float* beta, float eps, int act,
-                      __nv_bfloat16* out, float2* scratch, cudaStream_t st) {
+template <typename T>
+bool group_norm_fused(const Cat2T<T>& x, int HW, int groups, const float* gamma, const float* beta, float eps, int act,
+                      T* out, float2* scratch, cudaStream_t st) {
     static const int mode = [] {
         const char* e = getenv("ADX_GN_FUSED");
         return e ? atoi(e) : 1;
@@ -553,12 +672,12 @@ bool group_norm_fused(const Cat2& x, int HW, int groups, const float* gamma, con
     const int G = (HW + chunk_pix - 1) / chunk_pix;
     const int rpb = std::max(1, 512 / nv), threads = rpb * nv;
     const int nsub = std::max(1, threads / groups);
-    const size_t smem = static_cast<size_t>(chunk_pix) * C * 2 + static_cast<size_t>(2) * rpb * C * 4 +
+    const size_t smem = static_cast<size_t>(chunk_pix) * C * sizeof(T) + static_cast<size_t>(2) * rpb * C * 4 +
                         static_cast<size_t>(C) * 8 + static_cast<size_t>(nsub) * groups * 16;
     if (smem > 200 * 1024) return false;
     static bool attr[64] = {};
     if (!attr[dev]) {
-        CKU(cudaFuncSetAttribute(gn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CKU(cudaFuncSetAttribute(gn_fused<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr[dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -571,12 +690,13 @@ bool group_norm_fused(const Cat2& x, int HW, int groups, const float* gamma, con
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CKU(cudaLaunchKernelEx(&cfg, gn_fused, x, HW, groups, chunk_pix, gamma, beta, eps, act, scratch, out));
+    CKU(cudaLaunchKernelEx(&cfg, gn_fused<T>, x, HW, groups, chunk_pix, gamma, beta, eps, act, scratch, out));
     return true;
 }
 
-void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
-                int silu_act, __nv_bfloat16* out, float2* scratch, cudaStream_t st) {
+template <typename T>
+void group_norm_t(const Cat2T<T>& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
+                  int silu_act, T* out, float2* scratch, cudaStream_t st) {
     const int C = x.c0 + x.c1;
     if (C % groups) throw std::invalid_argument("group_norm: channels not divisible by groups");
     check_vec8(x, "group_norm");
@@ -590,14 +710,23 @@ void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma
     size_t smem = static_cast<size_t>(2) * rpb * C * sizeof(float);
     smem = std::max(smem, static_cast<size_t>(nsub) * batch * groups * 2 * sizeof(double));
     if (smem > 48 * 1024) throw std::invalid_argument("group_norm: statistics tile exceeds 48 KB shared memory");
-    CKU(launch_pdl(gn_stats, dim3(chunks, batch), dim3(threads), smem, st, 1, x, HW, groups, chunk_pix, chunks, gamma,
+    CKU(launch_pdl(gn_stats<T>, dim3(chunks, batch), dim3(threads), smem, st, 1, x, HW, groups, chunk_pix, chunks, gamma,
                    beta, eps, scratch));
     CKU(cudaGetLastError());
     const GnLayout L = gn_layout(scratch, batch, C);
     const long long pixels = static_cast<long long>(batch) * HW;
-    CKU(launch_pdl(gn_apply, dim3(grid_for(pixels * nv)), dim3(256), 0, st, 1, x, pixels, HW,
+    CKU(launch_pdl(gn_apply<T>, dim3(grid_for(pixels * nv)), dim3(256), 0, st, 1, x, pixels, HW,
                    static_cast<const float2*>(L.ab), silu_act, out));
     CKU(cudaGetLastError());
+}
+
+void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
+                int silu_act, __nv_bfloat16* out, float2* scratch, cudaStream_t st) {
+    group_norm_t(x, batch, HW, groups, gamma, beta, eps, silu_act, out, scratch, st);
+}
+void group_norm(const Cat2F& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
+                int silu_act, float* out, float2* scratch, cudaStream_t st) {
+    group_norm_t(x, batch, HW, groups, gamma, beta, eps, silu_act, out, scratch, st);
 }
 
 size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C) {
@@ -609,7 +738,44 @@ size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C) {
 void layer_norm(const __nv_bfloat16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
                 __nv_bfloat16* out, cudaStream_t st) {
     if (C % 8 || C > 256 * kLnMaxVec) throw std::invalid_argument("layer_norm: C must be a multiple of 8, <= 2048");
-    CKU(launch_pdl(layernorm_k, dim3((tokens + 7) / 8), dim3(256), 0, st, 1, x, tokens, C, gamma, beta, eps, out));
+    CKU(launch_pdl(layernorm_k<bf16>, dim3((tokens + 7) / 8), dim3(256), 0, st, 1, x, tokens, C, gamma, beta, eps,
+                   out));
+    CKU(cudaGetLastError());
+}
+void layer_norm(const float* x, int tokens, int C, const float* gamma, const float* beta, float eps, float* out,
+                cudaStream_t st) {
+    if (C % 8 || C > 256 * kLnMaxVec) throw std::invalid_argument("layer_norm: C must be a multiple of 8, <= 2048");
+    CKU(launch_pdl(layernorm_k<float>, dim3((tokens + 7) / 8), dim3(256), 0, st, 1, x, tokens, C, gamma, beta, eps,
+                   out));
+    CKU(cudaGetLastError());
+}
+
+void split3(const float* x, long long rows, int cols, long long ldx, int g, int pattern, __nv_bfloat16* out,
+            cudaStream_t st) {
+    if (cols % g || g % 8) throw std::invalid_argument("split3: group width must divide cols and be a multiple of 8");
+    CKU(launch_pdl(split3_k, dim3(grid_for(rows * cols / 8)), dim3(256), 0, st, 1, x, rows, cols, ldx, g, pattern,
+                   out));
+    CKU(cudaGetLastError());
+}
+
+void softmax_rows_f32(float* S, long long lds, int rows, int valid, int padded, cudaStream_t st) {
+    CKU(launch_pdl(softmax_rows_f32_k, dim3(rows), dim3(256), 0, st, 1, S, lds, valid, padded));
+    CKU(cudaGetLastError());
+}
+
+void transpose_f32(const float* V, long long ldv, int L, int Lpad, int hd, float* VT, cudaStream_t st) {
+    CKU(launch_pdl(transpose_f32_k, dim3((Lpad + 31) / 32, (hd + 31) / 32), dim3(32, 8), 0, st, 1, V, ldv, L, Lpad,
+                   hd, VT));
+    CKU(cudaGetLastError());
+}
+
+void pack_latent_f32(const void* x, bool f64, long long pixels, int c_lat, int cpad, float* out, cudaStream_t st) {
+    if (f64)
+        pack_latent_k<double, float><<<grid_for(pixels * cpad), 256, 0, st>>>(static_cast<const double*>(x), pixels,
+                                                                             c_lat, cpad, out);
+    else
+        pack_latent_k<float, float><<<grid_for(pixels * cpad), 256, 0, st>>>(static_cast<const float*>(x), pixels,
+                                                                            c_lat, cpad, out);
     CKU(cudaGetLastError());
 }
 

@@ -3,5 +3,5 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import paper_2406_06911_b200 as adx
 m = adx.build_unet_denoiser(seed=0)
-ms, b, n = adx.time_model_pass(m, 50, 1, "f32", [0])
+ms, b, n = adx.time_model_pass(m, 50, 1, "bf16", [0])
 print("pass ms", ms)
