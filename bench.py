@@ -167,13 +167,15 @@ def config_block(args, cfg, N):
         desc = (f"{args.config}: SD-2.1-shaped UNet (random init; ch {list(u['ch'])}, {u['n_res']} resnets/level, "
                 f"transformers at levels {[i for i, a in enumerate(u['attn']) if a]}, 77x1024 synthetic context), "
                 f"{u['H']}x{u['W']}x4 latent, T={cfg['T']} DDIM")
-        l2 = "UNet weights 1.7 GB bf16 > 126 MB L2 (no flush needed)"
+        l2 = ("UNet weights 1.7 GB bf16 > 126 MB L2 (no flush needed)" if u["H"] >= 64 and u["ch"][0] >= 320 else
+              "small UNet: weights and activations largely L2-resident")
     else:
         desc = (f"{args.config}: reference MLP-stage denoiser (L={cfg['L']} unet-mirror, widths {cfg['widths'][1]}, "
                 f"E={cfg['E']}), d={cfg['widths'][0]} latent, T={cfg['T']} DDIM")
         l2 = "weights > 126 MB L2 for c1b (no flush needed); c1a is L2/launch-resident"
     return {"workload": f"{desc}, components N={N}, w={w}, S={cfg['S']}, batch 1", "global_batch": 1,
             "components": N, "T": cfg["T"], "w": w, "S": cfg["S"],
+            "partition": (getattr(args, "partition", "macs") + "-balanced min-max") if N > 1 else "single component",
             "parallelism": f"async-model-parallel n{N}" if N > 1 else "sequential (1 GPU)", "l2": l2}
 
 
@@ -263,6 +265,37 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def predict_scaling(m, s, cfg, prec, link_gbs=700.0, latency_s=10e-6):
+    """N = 2 / 4 / 8 (and N = 3 S = 2) latency predicted by the reference's cost model
+    (costsim.cpp:18-50 with the bytes-aware comm term) from per-stage device times measured
+    here, time-balanced partition (partition_by_cost); NVLink taken as 700 GB/s achieved
+    + 10 us per exchange round.  A prediction, not a measurement: this box has one GPU."""
+    import paper_2406_06911_b200 as adx
+    st = adx.stage_times(m, cfg["T"], 5, prec, [0])
+    out = {"model": "costsim (reference cost model) + bytes-aware comm", "link_gbs": link_gbs,
+           "comm_latency_s": latency_s, "stage_ms_sum": sum(st), "runs": []}
+    for N, S in ((2, 1), (4, 1), (3, 2), (8, 1)):
+        plan = adx.plan_async(cfg["T"], cfg["w"], N, S)
+        part = adx.partition_by_cost(m, N, st)
+        seg = [sum(st[i - 1] for i in sg) / 1e3 for sg in part.segments]
+        cm = adx.CostModel(segment_cost_s=seg, sampler_cost_s=5e-6, comm_latency_s=latency_s, link_gbs=link_gbs)
+        rep = adx.predict_async(plan, cm, adx.round_exchange_bytes(plan, part, m, prec))
+        out["runs"].append({"N": N, "S": S, "w": cfg["w"], "predicted_ms": rep.async_total_s * 1e3,
+                            "sequential_ms": rep.sequential_total_s * 1e3, "speedup": rep.speedup})
+    return out
+
+
+def make_partition(args, m, cfg, N, prec, dev, costs=None):
+    """partition_balanced (MACs, the reference) or partition_by_cost over measured stage
+    times; `costs` lets rank 0's measurement be shared so every rank builds the same split."""
+    import paper_2406_06911_b200 as adx
+    if args.partition == "macs" or N == 1:
+        return adx.partition_balanced(m, N), None
+    if costs is None:
+        costs = adx.stage_times(m, cfg["T"], 5, prec, [dev])
+    return adx.partition_by_cost(m, N, costs), costs
+
+
 def run_ours(args, cfg):
     import numpy as np
     import paper_2406_06911_b200 as adx
@@ -280,7 +313,7 @@ def run_ours(args, cfg):
         sess = seq
     else:
         plan = adx.plan_async(cfg["T"], cfg["w"], N, cfg["S"])
-        part = adx.partition_balanced(m, N)
+        part, _ = make_partition(args, m, cfg, N, prec, 0)
         sess = adx.Session(m, s, "parallel", plan=plan, partition=part, workers=plan.D, precision=prec,
                            devices=list(range(ngpu)))
     sess.upload(x)
@@ -313,6 +346,8 @@ def run_ours(args, cfg):
     }
     if cfg["family"] == "mlp":
         line["roofline"]["run_weight_bytes"] = sess.weight_bytes()
+    if cfg["family"] == "unet" and N == 1:
+        line["cost_model_prediction"] = predict_scaling(m, s, cfg, prec)
     if not args.no_cpu_baseline:
         cms, cores, sample = cpu_baseline(cfg, N, 1)
         line["cpu_baseline"] = {"value": cms, "unit": "ms", "cores": cores, "kind": "port", "sample": sample}
@@ -331,9 +366,12 @@ def run_ranks(args, cfg, ws, rank):
     N = ws
     m, s, x, d = build_model(cfg)
     plan = adx.plan_async(cfg["T"], cfg["w"], N, cfg["S"])
-    part = adx.partition_balanced(m, N)
-    box = [adx.nccl_unique_id() if rank == 0 else None]
+    costs = None
+    if rank == 0 and args.partition == "time":
+        _, costs = make_partition(args, m, cfg, N, prec, local)
+    box = [adx.nccl_unique_id() if rank == 0 else None, costs]
     dist.broadcast_object_list(box, src=0)
+    part, _ = make_partition(args, m, cfg, N, prec, local, box[1])
     sess = adx.RankSession(m, s, plan, part, rank, box[0], local, prec)
     for _ in range(args.warmup):
         sess.time(1)
@@ -386,9 +424,14 @@ def main():
                     help="MLP configs: engine precision (default f32); UNet configs: bf16 (default, bf16 "
                          "tensor-core stages) or f32 (fp32 activations, split-bf16 products, the 1e-3 parity mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", default=None, choices=["macs", "time"],
+                    help="N>1 component split: the reference's MAC-balanced min-max DP, or the same DP over "
+                         "per-stage device times measured on this GPU (default: time for UNet, macs for MLP)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    if args.partition is None:
+        args.partition = "time" if cfg["family"] == "unet" else "macs"
     if args.precision is None:
         args.precision = "bf16" if cfg["family"] == "unet" else "f32"  # UNet: bf16 stages, f32 latent
     if cfg["family"] == "unet" and args.precision == "f64":

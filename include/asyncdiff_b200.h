@@ -95,6 +95,9 @@ enum { ADX_SEQUENTIAL_BALANCED = 0, ADX_FIRST_LAST_GROUPED = 1 };
 
 /* partition_balanced: partition.hpp:39-40, partition.cpp:95-198 */
 int adx_partition_balanced(const adx_model* m, int N, int strategy, adx_partition** out);
+/* extension: the same min-max DP (partition.cpp:95-125 semantics, ties to the smallest
+ * cut) over measured per-stage costs (e.g. adx_engine_stage_times, in any unit) */
+int adx_partition_by_cost(const adx_model* m, int N, const double* stage_cost, adx_partition** out);
 /* explicit partition (tests' uniform_partition, plan_test.cpp:14-22):
  * seg_sizes[n_segments], stages[sum(seg_sizes)] 1-based, devices/macs per segment */
 int adx_partition_create(int n_segments, const int* seg_sizes, const int* stages,
@@ -161,6 +164,10 @@ int adx_engine_weight_bytes(const adx_engine* e, int ordinal_index, long long* b
  * algorithmic weight bytes one pass streams: the HBM roofline of the GEMV. */
 int adx_engine_time_eval(adx_engine* e, int t_embed, int iters, double* ms_per_pass,
                          long long* bytes_per_pass, int* launches_per_pass);
+/* device ms of every stage evaluated on its own (each stage captured into its own
+ * CUDA graph and replayed): stage_ms[L], the measured per-component costs that feed
+ * the cost model (costsim.hpp:13-19 segment_cost_s) */
+int adx_engine_stage_times(adx_engine* e, int t_embed, int iters, double* stage_ms);
 
 /* Microbenchmark of the stage GEMV kernel: a dependent chain of `chain` square
  * n x n GEMVs (distinct weights), one CUDA graph, `iters` launches; device ms

@@ -99,7 +99,7 @@ EXPORTS = [
     "adx_model_save_checkpoint", "adx_model_load_checkpoint", "adx_plan_to_json", "adx_plan_from_json",
     "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes", "adx_tc_gemm", "adx_tc_conv3x3",
     "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context", "adx_tc_attention",
-    "adx_engine_profile_pass", "adx_tc_plan_override",
+    "adx_engine_profile_pass", "adx_tc_plan_override", "adx_engine_stage_times", "adx_partition_by_cost",
 ]
 
 
@@ -216,6 +216,8 @@ def lib():
         "adx_tc_conv3x3": (i, [i, i, i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_float), i,
                                P(d)]),
         "adx_tc_plan_override": (i, [i, i]),
+        "adx_engine_stage_times": (i, [vp, i, i, P(d)]),
+        "adx_partition_by_cost": (i, [vp, i, P(d), P(vp)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

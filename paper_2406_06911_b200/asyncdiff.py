@@ -30,7 +30,8 @@ __all__ = [
     "Round", "ExecutionPlan", "plan_async", "validate_plan", "PlanCounts", "plan_counts", "shift_embeddings",
     "render_plan", "RunOptions", "RunStats", "InstrumentedDenoiser", "inject_delay", "run_serial",
     "run_parallel", "DivergenceReport", "compare_trajectories", "kWarmupRound", "set_default_precision",
-    "PRECISIONS", "Session", "time_model_pass", "profile_model_pass", "RankSession", "nccl_unique_id", "save_checkpoint",
+    "PRECISIONS", "Session", "time_model_pass", "profile_model_pass", "stage_times", "partition_by_cost",
+    "RankSession", "nccl_unique_id", "save_checkpoint",
     "load_checkpoint", "plan_to_json", "plan_from_json", "CostModel", "LatencyReport", "predict_sequential",
     "predict_async", "CostComparison", "calibrate_and_compare", "round_exchange_bytes", "SimilarityProfile",
     "similarity_profile", "build_unet_denoiser", "unet_stage_info", "unet_stage_params", "unet_context",
@@ -497,6 +498,17 @@ def partition_balanced(m: LayeredDenoiser, N: int, strategy: str = "sequential-b
         raise InvalidArgument(f"unknown partition strategy: {strategy}")
     h = C.c_void_p()
     check(lib().adx_partition_balanced(m._h, N, st, C.byref(h)))
+    return Partition(h.value)
+
+
+def partition_by_cost(m: LayeredDenoiser, N: int, stage_cost: Sequence[float]) -> Partition:
+    """Extension of partition_balanced: the same exact min-max DP (ties to the smallest
+    cut) over measured per-stage costs (e.g. stage_times) instead of MACs."""
+    c = _f64(list(stage_cost))
+    if c.size != m.num_stages():
+        raise InvalidArgument(f"partition_by_cost: need one cost per stage ({m.num_stages()})")
+    h = C.c_void_p()
+    check(lib().adx_partition_by_cost(m._h, N, _dp(c), C.byref(h)))
     return Partition(h.value)
 
 
@@ -1100,6 +1112,15 @@ def profile_model_pass(m: LayeredDenoiser, t_embed: int, precision: Optional[str
     check(lib().adx_engine_profile_pass(m.engine(precision, devices)._h, t_embed, _dp(out)))
     return {k: dict(launches=int(out[3 * i]), ms=float(out[3 * i + 1]), flops=float(out[3 * i + 2]))
             for i, k in enumerate(("conv3x3", "gemm", "attention"))}
+
+
+def stage_times(m: LayeredDenoiser, t_embed: int, iters: int = 10, precision: Optional[str] = None,
+                devices: Optional[Sequence[int]] = None) -> List[float]:
+    """Device ms of every stage evaluated on its own (own CUDA graph, `iters` replays):
+    the measured per-component costs for CostModel.segment_cost_s (costsim.hpp:13-19)."""
+    out = np.zeros(m.num_stages())
+    check(lib().adx_engine_stage_times(m.engine(precision, devices)._h, t_embed, iters, _dp(out)))
+    return out.tolist()
 
 
 def time_model_pass(m: LayeredDenoiser, t_embed: int, iters: int, precision: Optional[str] = None,

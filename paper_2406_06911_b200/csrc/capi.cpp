@@ -447,6 +447,15 @@ int adx_partition_balanced(const adx_model* m, int N, int strategy, adx_partitio
     });
 }
 
+int adx_partition_by_cost(const adx_model* m, int N, const double* stage_cost, adx_partition** out) {
+    return guard([&] {
+        need(m, "partition_by_cost");
+        std::vector<long long> c(m->m.L);
+        for (int i = 0; i < m->m.L; ++i) c[i] = std::llround(stage_cost[i] * 1e6);  // micro-units: exact ints
+        *out = new adx_partition{adx::partition_by_cost(m->m, N, c)};
+    });
+}
+
 int adx_partition_create(int n_segments, const int* seg_sizes, const int* stages, const int* devices,
                          const long long* macs, int strategy, adx_partition** out) {
     return guard([&] {
@@ -623,6 +632,13 @@ int adx_engine_time_eval(adx_engine* e, int t_embed, int iters, double* ms_per_p
         for (int i = 1; i <= m.L; ++i) b += static_cast<long long>(e->e->stage_weight_bytes(i));
         if (bytes_per_pass) *bytes_per_pass = b;
         *ms_per_pass = e->e->time_eval_ms(0, t_embed, iters, launches_per_pass);
+    });
+}
+
+int adx_engine_stage_times(adx_engine* e, int t_embed, int iters, double* stage_ms) {
+    return guard([&] {
+        need(e, "engine_stage_times");
+        e->e->time_eval_ms(0, t_embed, std::max(1, iters), nullptr, nullptr, stage_ms);
     });
 }
 

@@ -253,7 +253,7 @@ int Engine::enqueue_stage(int idx, int stage, const std::vector<Seg>& inputs, in
     return 2;
 }
 
-double Engine::time_eval_ms(int idx, int t_embed, int iters, int* launches, double (*profile)[3]) {
+double Engine::time_eval_ms(int idx, int t_embed, int iters, int* launches, double (*profile)[3], double* stage_ms) {
     const int ord = ordinal(idx);
     CK(cudaSetDevice(ord));
     const Model& m = model_;
@@ -300,6 +300,41 @@ double Engine::time_eval_ms(int idx, int t_embed, int iters, int* launches, doub
         tc_profile_enable(false);
         CK(cudaStreamSynchronize(st));
         tc_profile_collect(profile);
+    }
+    if (stage_ms) {  // every stage captured into its own graph, replayed `iters` times (device time)
+        pass();
+        CK(cudaStreamSynchronize(st));
+        for (int i = 1; i <= m.L; ++i) {
+            std::vector<Seg> in;
+            if (i == 1) {
+                in.push_back({x, m.data_dim()});
+                in.push_back({etab_row(idx, t_embed), m.E});
+            } else {
+                in.push_back({y[i - 1], m.widths[i - 1]});
+            }
+            for (auto& l : m.links_into(i)) in.push_back({y[l.first], m.widths[l.first]});
+            cudaGraph_t gs = nullptr;
+            cudaGraphExec_t gse = nullptr;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+            enqueue_stage(idx, i, in, t_embed, h[i], y[i], bad, i, st, true);
+            CK(cudaStreamEndCapture(st, &gs));
+            CK(cudaGraphInstantiate(&gse, gs, 0));
+            cudaEvent_t a0, b0;
+            CK(cudaEventCreate(&a0));
+            CK(cudaEventCreate(&b0));
+            for (int w = 0; w < 2; ++w) CK(cudaGraphLaunch(gse, st));
+            CK(cudaEventRecord(a0, st));
+            for (int it = 0; it < iters; ++it) CK(cudaGraphLaunch(gse, st));
+            CK(cudaEventRecord(b0, st));
+            CK(cudaEventSynchronize(b0));
+            float sms = 0.f;
+            CK(cudaEventElapsedTime(&sms, a0, b0));
+            stage_ms[i - 1] = sms / std::max(1, iters);
+            cudaEventDestroy(a0);
+            cudaEventDestroy(b0);
+            cudaGraphExecDestroy(gse);
+            cudaGraphDestroy(gs);
+        }
     }
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;

@@ -81,7 +81,10 @@ public:
     // HBM roofline of the stage GEMV kernel.
     // profile != nullptr: also run one eager pass with per-launch events around every
     // tensor-core kernel; per kind (conv, GEMM, attention): {launches, ms, flops}
-    double time_eval_ms(int idx, int t_embed, int iters, int* launches, double (*profile)[3] = nullptr);
+    // device ms of one full pass (graph of back-to-back passes); optionally the tensor-core
+    // family profile of an eager pass and the device ms of every stage on its own (stage_ms[L])
+    double time_eval_ms(int idx, int t_embed, int iters, int* launches, double (*profile)[3] = nullptr,
+                        double* stage_ms = nullptr);
     // element size of stage outputs (bf16 for the UNet family, the activation dtype otherwise)
     // bytes per stage-output element: UNet bf16 mode 2, UNet f32 mode 4, MLP the engine precision
     int stage_bytes() const { return model_.kind == 1 ? (prec_ == kF32 ? 4 : 2) : act_bytes(prec_); }

@@ -316,6 +316,33 @@ Partition partition_balanced(const Model& m, int N, int strategy) {
     return p;
 }
 
+// The same exact min-max DP (ties to the smallest cut) over caller-supplied per-stage
+// costs (e.g. measured device time, ns) instead of MACs; segment_macs still report MACs.
+Partition partition_by_cost(const Model& m, int N, const std::vector<long long>& stage_cost) {
+    const int L = m.L;
+    if (static_cast<int>(stage_cost.size()) != L)
+        throw std::invalid_argument("partition_by_cost: need one cost per stage (" + S(L) + ")");
+    if (N < 1 || N > L) throw std::invalid_argument("partition_by_cost: N=" + S(N) + " infeasible for L=" + S(L));
+    for (long long c : stage_cost)
+        if (c < 0) throw std::invalid_argument("partition_by_cost: negative stage cost");
+    const auto cuts = minmax_cuts(stage_cost, N);
+    Partition p;
+    p.strategy = 0;
+    for (int seg = 0; seg < N; ++seg) {
+        std::vector<int> st;
+        long long macs = 0;
+        for (int s = cuts[seg] + 1; s <= cuts[seg + 1]; ++s) {
+            st.push_back(s);
+            macs += m.stages[s - 1].cost_macs;
+        }
+        p.segments.push_back(std::move(st));
+        p.segment_macs.push_back(macs);
+        p.device_of_segment.push_back(seg);
+    }
+    p.validate(m);
+    return p;
+}
+
 // partition.cpp:200-208
 std::vector<std::pair<int, int>> crossing_links(const Model& m, const Partition& p) {
     std::vector<std::pair<int, int>> r;

@@ -98,6 +98,7 @@ struct Partition {
     void validate(const Model& m) const;
 };
 Partition partition_balanced(const Model& m, int N, int strategy);
+Partition partition_by_cost(const Model& m, int N, const std::vector<long long>& stage_cost);
 std::vector<std::pair<int, int>> crossing_links(const Model& m, const Partition& p);
 
 // ----------------------------------------------------------------- plan

@@ -161,3 +161,27 @@ def test_sinusoid_matches_oracle():
     for t in (1, 7, 50):
         assert np.array_equal(adx.sinusoid(t, 8), O.sinusoid(t, 8))
     assert np.abs(adx.sinusoid(7, 8)).max() <= 1.0
+
+
+def test_partition_by_cost_is_minmax_optimal():
+    """partition_by_cost (extension): the partition.cpp min-max DP over arbitrary stage
+    costs -- optimal against brute force, ties to the smallest cut, MACs still reported."""
+    import itertools
+    rng = np.random.default_rng(3)
+    m = adx.build_toy_denoiser(6, [2, 8, 8, 8, 8, 8, 2])
+    for _ in range(40):
+        costs = rng.integers(1, 6, size=6).astype(float) * 0.25
+        for N in (1, 2, 3, 4):
+            p = adx.partition_by_cost(m, N, costs)
+            segs = p.segments
+            got = max(sum(costs[s - 1] for s in sg) for sg in segs)
+            best = None
+            for cuts in itertools.combinations(range(1, 6), N - 1):
+                b = (0,) + cuts + (6,)
+                v = max(sum(costs[b[k]:b[k + 1]]) for k in range(N))
+                if best is None or v < best[0] - 1e-12:
+                    best = (v, cuts)
+            assert abs(got - best[0]) < 1e-12
+            assert sum(p.segment_macs) == m.total_macs()
+    with pytest.raises(adx.InvalidArgument):
+        adx.partition_by_cost(m, 2, [1.0, 2.0])
