@@ -156,3 +156,19 @@ def test_cmd_bench_style_calibration_on_gpu():  # experiment.cpp:391-455 with GP
     _, stats = adx.run_parallel(plan, adx.inject_delay(m, delays), part, adx.Latent(O.random_normals(12, 2), 12), s, 2)
     c = adx.calibrate_and_compare(plan, delays, stats)
     assert c.rel_error_total < 0.25
+
+
+def test_round_exchange_bytes_unet_stage_element_sizes():
+    """UNet stage outputs travel as bf16 in the bf16 mode and fp32 in the f32 mode;
+    eps (the last segment's output) at the fp32 trajectory size in both (host-only)."""
+    m = adx.build_unet_denoiser(H=16, W=16, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64,
+                                temb_dim=128, seed=5)
+    part = adx.partition_balanced(m, 2)
+    plan = adx.plan_async(4, 1, 2, 1)
+    b16 = adx.round_exchange_bytes(plan, part, m, "bf16")
+    b32 = adx.round_exchange_bytes(plan, part, m, "f32")
+    eps = m.data_dim() * 4
+    assert len(b16) == len(plan.rounds) and all(b > eps for b in b16[:-1])
+    for x, y in zip(b16, b32):
+        assert y - eps == 2 * (x - eps)  # stage payload doubles, the eps send does not
+    assert adx.round_exchange_bytes(plan, part, m) == b16  # the UNet default precision is bf16
