@@ -316,7 +316,8 @@ int adx_unet_context(const adx_model* m, float* out /* ctx_len * ctx_dim */);
  * (no reference function: builder-written oracle, SURVEY §8a extension list).
  * A/B/X/Wt are bf16 bit patterns (uint16), outputs fp32.  iters > 0 also times
  * `iters` back-to-back launches (CUDA events). */
-/* C[M x N] = act(A[M x K] . B[N x K]^T + bias); K % 64 == 0; bn in {0,32,64,80,96,128,160,192,256} */
+/* C[M x N] = act(A[M x K] . B[N x K]^T + bias); K % 64 == 0; bn in {0,32,64,80,96,128,160,192,256};
+ * act 0 none, 1 SiLU, 2 GEGLU over 256-row tiles of [128 hidden | 128 gate] rows (C is M x N/2) */
 int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B,
                 const float* bias, int act, float* C, int bn, int iters, double* ms_per_iter);
 /* fused multi-head attention (64-wide heads, scale 1/8): out[L x C] bf16 from Q [L x C],

@@ -993,12 +993,13 @@ int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint1
         p.bias = bias ? static_cast<const float*>(bi.p) : nullptr;
         p.act = act;
         p.out_f32 = static_cast<float*>(c.p);
-        p.ldo = N;
+        const int nout = act == 2 ? N / 2 : N;  // GEGLU writes hidden * gelu(gate): N/2 columns
+        p.ldo = nout;
         adx::tc_gemm(a.p, b.p, M, N, K, p, 0, bn);
         CKC(cudaDeviceSynchronize());
         if (iters > 0 && ms_per_iter)
             *ms_per_iter = time_graph_ms([&](cudaStream_t st) { adx::tc_gemm(a.p, b.p, M, N, K, p, st, bn); }, iters);
-        if (C) CKC(cudaMemcpy(C, c.p, static_cast<size_t>(M) * N * 4, cudaMemcpyDeviceToHost));
+        if (C) CKC(cudaMemcpy(C, c.p, static_cast<size_t>(M) * nout * 4, cudaMemcpyDeviceToHost));
     });
 }
 
