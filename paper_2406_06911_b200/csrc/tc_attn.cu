@@ -37,7 +37,12 @@ namespace adx {
 
 namespace {
 
-constexpr int QT = 128, KT = 128, HD = 64, STG = 3;
+// KT = 64 keys per KV block: 100 KB of SMEM and 256 TMEM columns per CTA, so two CTAs
+// (20 warps) share an SM and hide each other's barrier / TMEM / MUFU latencies
+constexpr int QT = 128, KT = 64, HD = 64, STG = 3;
+constexpr int HK = KT / 2;                            // keys per softmax warp (two warps per row)
+constexpr int NB64 = KT / 64;                         // 64-key (128-byte) column blocks per tile
+constexpr uint32_t TM_COLS = (2 * KT + HD) <= 256 ? 256 : 512;  // S[2] + O, power of two
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
@@ -114,6 +119,16 @@ __device__ __forceinline__ void tld64_nowait(uint32_t taddr, uint32_t* r) {
         : "r"(taddr));
 }
 __device__ __forceinline__ void tld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tld32_nowait(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -159,13 +174,21 @@ constexpr uint32_t idesc(int M, int N) {
            (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// this warp's HK columns of its S row
+__device__ __forceinline__ void tld_hk_nowait(uint32_t taddr, uint32_t* r) {
+    if constexpr (HK == 64)
+        tld64_nowait(taddr, r);
+    else
+        tld32_nowait(taddr, r);
+}
+
 struct AttnArgs {
     int L, Lk, C;  // query tokens, key tokens, model width (heads * 64)
     __nv_bfloat16* out;
     long long ldo;
 };
 
-__global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CUtensorMap tmQ,
+__global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                       const __grid_constant__ CUtensorMap tmK,
                                                       const __grid_constant__ CUtensorMap tmVT, const AttnArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -207,7 +230,8 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sa(tptr)) : "memory");
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tptr)), "n"(TM_COLS)
+                     : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -215,7 +239,7 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     pdl_wait();  // prologue done: wait for the producers of Q / K / V^T
     const uint32_t tmem = *tptr;
-    // TMEM columns: S buffers [0,128) and [128,256); O accumulator [256,320)
+    // TMEM columns: S buffers [0,KT) and [KT,2KT); O accumulator [2KT, 2KT+64)
 
     if (warp == 0 && lane == 0) {
         // ------------------------------------------------------------ TMA
@@ -226,9 +250,9 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
             bar_wait(&kv_empty[s], ((j / STG) & 1) ^ 1);
             bar_expect(&kv_full[s], K_B + V_B);
             tma2d(sK + s * K_B, &tmK, head * HD, j * KT, &kv_full[s]);
-            // V^T rows = this head's 64 dims, two 64-key halves (128-byte rows each)
-            tma2d(sV + s * V_B, &tmVT, j * KT, head * HD, &kv_full[s]);
-            tma2d(sV + s * V_B + V_B / 2, &tmVT, j * KT + 64, head * HD, &kv_full[s]);
+            // V^T rows = this head's 64 dims, one box per 64-key block (128-byte rows)
+            for (int blk = 0; blk < NB64; ++blk)
+                tma2d(sV + s * V_B + blk * (HD * 128), &tmVT, j * KT + 64 * blk, head * HD, &kv_full[s]);
         }
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------------------ MMA
@@ -240,7 +264,7 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < HD / 16; ++k)
-                mma(tmem + b * 128, sdesc(sQ + k * 32), sdesc(sK + s * K_B + k * 32), idesc(QT, KT), k > 0);
+                mma(tmem + b * KT, sdesc(sQ + k * 32), sdesc(sK + s * K_B + k * 32), idesc(QT, KT), k > 0);
             commit(&s_full[b]);
         };
         bar_wait(q_full, 0);
@@ -254,9 +278,9 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int k = 0; k < KT / 16; ++k) {
-                    const int half = k / 4, kk = k % 4;
-                    mma(tmem + 256, sdesc(sP + b * P_B + half * (P_B / 2) + kk * 32),
-                        sdesc(sV + s * V_B + half * (V_B / 2) + kk * 32), idesc(QT, HD), (jj | k) > 0);
+                    const int blk = k / 4, kk = k % 4;
+                    mma(tmem + 2 * KT, sdesc(sP + b * P_B + blk * (QT * 128) + kk * 32),
+                        sdesc(sV + s * V_B + blk * (HD * 128) + kk * 32), idesc(QT, HD), (jj | k) > 0);
                 }
                 commit(&pv_done[b]);
                 commit(&kv_empty[s]);
@@ -274,34 +298,34 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
         const int half = (warp - 2) >> 2;
         const int r = q * 32 + lane;  // query row within the tile
         const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
-        const uint32_t tO = tmem + 256 + lrow;
+        const uint32_t tO = tmem + 2 * KT + lrow;
         const float sl2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
         auto pair_sync = [&] { asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory"); };
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nkv; ++j) {
             const int b = j & 1;
-            const uint32_t tS = tmem + b * 128 + half * 64 + lrow;
+            const uint32_t tS = tmem + b * KT + half * HK + lrow;
             bar_wait(&s_full[b], (j >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t sr[64];
-            tld64_nowait(tS, sr);
+            uint32_t sr[HK];
+            tld_hk_nowait(tS, sr);
             tld_wait();
             // S_j is in registers: release its TMEM buffer to the MMA warp (S_{j+2}) now
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) bar_arrive(&s_free[b]);
             // ragged last tile: mask the dead keys to -inf once so the hot loops carry no predicates
-            const int valid = min(KT, p.Lk - j * KT) - half * 64;
-            if (valid < 64) {
+            const int valid = min(KT, p.Lk - j * KT) - half * HK;
+            if (valid < HK) {
 #pragma unroll
-                for (int i = 0; i < 64; ++i)
+                for (int i = 0; i < HK; ++i)
                     if (i >= valid) sr[i] = 0xff800000u;
             }
             float mp[8];  // 8 independent max chains
 #pragma unroll
             for (int a = 0; a < 8; ++a) mp[a] = __uint_as_float(sr[a]);
 #pragma unroll
-            for (int i = 8; i < 64; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(sr[i]));
+            for (int i = 8; i < HK; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(sr[i]));
             const float mh = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
                                    fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
             xmax[(b * 2 + half) * QT + r] = mh;
@@ -335,9 +359,12 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
             // P = exp2(s*scale*log2e - m*scale*log2e) -> SW128 K-major A tile in SMEM
             // (this warp's half = keys [64h, 64h+64), 16-byte chunk k of row r at k ^ (r & 7))
             float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent sum chains
-            uint8_t* row = sP + b * P_B + half * (P_B / 2) + r * 128;
+            // this warp's keys [half*HK, half*HK + HK): 64-key block (half*HK)/64, 16-byte chunks
+            // from ((half*HK) % 64) / 8 on, chunk k of row r stored at k ^ (r & 7)
+            uint8_t* row = sP + b * P_B + ((half * HK) / 64) * (QT * 128) + r * 128;
+            const int kbase = ((half * HK) % 64) / 8;
 #pragma unroll
-            for (int c = 0; c < 64; c += 16) {
+            for (int c = 0; c < HK; c += 16) {
                 float v[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
@@ -346,7 +373,7 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
                 }
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
-                    const int k = c / 8 + hh;
+                    const int k = kbase + c / 8 + hh;
                     uint4 u;
                     __nv_bfloat162 b0 = __floats2bfloat162_rn(v[hh * 8 + 0], v[hh * 8 + 1]);
                     __nv_bfloat162 b1 = __floats2bfloat162_rn(v[hh * 8 + 2], v[hh * 8 + 3]);
@@ -398,7 +425,8 @@ __global__ void __launch_bounds__(320, 1) attn_kernel(const __grid_constant__ CU
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TM_COLS) : "memory");
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
