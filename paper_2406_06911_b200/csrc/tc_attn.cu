@@ -42,7 +42,8 @@ namespace {
 constexpr int QT = 128, KT = 64, HD = 64, STG = 3;
 constexpr int HK = KT / 2;                            // keys per softmax warp (two warps per row)
 constexpr int NB64 = KT / 64;                         // 64-key (128-byte) column blocks per tile
-constexpr uint32_t TM_COLS = (2 * KT + HD) <= 256 ? 256 : 512;  // S[2] + O, power of two
+constexpr int TP_COL = 2 * KT + HD;                  // P[2] (bf16 pairs: KT/2 columns each) after S[2], O
+constexpr uint32_t TM_COLS = (TP_COL + KT) <= 256 ? 256 : 512;  // S[2] + O + P[2], power of two
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
@@ -182,6 +183,32 @@ __device__ __forceinline__ void tld_hk_nowait(uint32_t taddr, uint32_t* r) {
         tld32_nowait(taddr, r);
 }
 
+// D (+)= A . B^T with A (M x K bf16, K-major) read from TMEM: lane = row, one 32-bit
+// column = two consecutive K elements, 8 columns per K=16 instruction (checked by
+// _ab/ts_mma_test.cu); B from SMEM as usual
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tst_u32(uint32_t taddr, const uint32_t* r) {
+    static_assert(N == 16 || N == 32, "tst_u32: 16 or 32 columns");
+    if constexpr (N == 16) {
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                taddr),
+            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+            "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+            : "memory");
+    } else {
+        tst_u32<16>(taddr, r);
+        tst_u32<16>(taddr + 16, r + 16);
+    }
+}
+
 struct AttnArgs {
     int L, Lk, C;  // query tokens, key tokens, model width (heads * 64)
     __nv_bfloat16* out;
@@ -194,12 +221,12 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2, P_B = QT * KT * 2;
-    constexpr int XCH_OFF = Q_B + STG * (K_B + V_B) + 2 * P_B + 256;  // after the barriers
+    constexpr int XCH_OFF = Q_B + STG * (K_B + V_B) + 256;  // after the barriers
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + Q_B;        // STG x K_B
     uint8_t* sV = sK + STG * K_B;  // STG x (2 halves of [64 dims x 64 keys])
-    uint8_t* sP = sV + STG * V_B;  // 2 buffers x (2 halves of [128 rows x 64 keys])
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * P_B);
+    // P lives in TMEM (the PV MMA's A operand), not SMEM
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + STG * V_B);
     uint64_t* q_full = bars;
     uint64_t* kv_full = bars + 1;         // [STG]
     uint64_t* kv_empty = kv_full + STG;   // [STG]
@@ -279,8 +306,8 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
 #pragma unroll
                 for (int k = 0; k < KT / 16; ++k) {
                     const int blk = k / 4, kk = k % 4;
-                    mma(tmem + 2 * KT, sdesc(sP + b * P_B + blk * (QT * 128) + kk * 32),
-                        sdesc(sV + s * V_B + blk * (HD * 128) + kk * 32), idesc(QT, HD), (jj | k) > 0);
+                    mma_ts(tmem + 2 * KT, tmem + TP_COL + b * (KT / 2) + k * 8,
+                           sdesc(sV + s * V_B + blk * (HD * 128) + kk * 32), idesc(QT, HD), (jj | k) > 0);
                 }
                 commit(&pv_done[b]);
                 commit(&kv_empty[s]);
@@ -356,38 +383,22 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
                 }
             }
             const float off = -m * sl2;
-            // P = exp2(s*scale*log2e - m*scale*log2e) -> SW128 K-major A tile in SMEM
-            // (this warp's half = keys [64h, 64h+64), 16-byte chunk k of row r at k ^ (r & 7))
+            // P = exp2(s*scale*log2e - m*scale*log2e) as bf16 pairs (keys 2c, 2c+1 in one 32-bit
+            // column) straight into this row's TMEM lane: the PV MMA reads its A operand from there
             float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent sum chains
-            // this warp's keys [half*HK, half*HK + HK): 64-key block (half*HK)/64, 16-byte chunks
-            // from ((half*HK) % 64) / 8 on, chunk k of row r stored at k ^ (r & 7)
-            uint8_t* row = sP + b * P_B + ((half * HK) / 64) * (QT * 128) + r * 128;
-            const int kbase = ((half * HK) % 64) / 8;
+            uint32_t pk[HK / 2];
 #pragma unroll
-            for (int c = 0; c < HK; c += 16) {
-                float v[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    v[i] = ex2_mix(fmaf(__uint_as_float(sr[c + i]), sl2, off), i);
-                    sp[i & 7] += v[i];
-                }
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const int k = kbase + c / 8 + hh;
-                    uint4 u;
-                    __nv_bfloat162 b0 = __floats2bfloat162_rn(v[hh * 8 + 0], v[hh * 8 + 1]);
-                    __nv_bfloat162 b1 = __floats2bfloat162_rn(v[hh * 8 + 2], v[hh * 8 + 3]);
-                    __nv_bfloat162 b2 = __floats2bfloat162_rn(v[hh * 8 + 4], v[hh * 8 + 5]);
-                    __nv_bfloat162 b3 = __floats2bfloat162_rn(v[hh * 8 + 6], v[hh * 8 + 7]);
-                    u.x = *reinterpret_cast<uint32_t*>(&b0);
-                    u.y = *reinterpret_cast<uint32_t*>(&b1);
-                    u.z = *reinterpret_cast<uint32_t*>(&b2);
-                    u.w = *reinterpret_cast<uint32_t*>(&b3);
-                    *reinterpret_cast<uint4*>(row + ((k ^ (r & 7)) * 16)) = u;
-                }
+            for (int c = 0; c < HK; c += 2) {
+                const float v0 = ex2_mix(fmaf(__uint_as_float(sr[c]), sl2, off), c);
+                const float v1 = ex2_mix(fmaf(__uint_as_float(sr[c + 1]), sl2, off), c + 1);
+                sp[c & 7] += v0;
+                sp[(c + 1) & 7] += v1;
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
+                pk[c / 2] = *reinterpret_cast<uint32_t*>(&h2);
             }
+            tst_u32<HK / 2>(tmem + TP_COL + b * (KT / 2) + half * (HK / 2) + lrow, pk);
+            tst_wait();
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) bar_arrive(&p_full[b]);
             l += ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
@@ -472,8 +483,7 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
     const CUtensorMap mk = map2d(K, Lk, C, ldk, KT);
     const CUtensorMap mv = map2d(VT, C, Lk, ldvt, HD);  // rows = dims, cols = keys
     AttnArgs a{L, Lk, C, out, ldo};
-    constexpr size_t smem =
-        1024 + QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + 2 * QT * KT * 2 + 256 + 6 * QT * sizeof(float);
+    constexpr size_t smem = 1024 + QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + 256 + 6 * QT * sizeof(float);
     static bool attr[64] = {};
     int dev = 0;
     CKA(cudaGetDevice(&dev));
