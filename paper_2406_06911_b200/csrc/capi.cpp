@@ -1016,8 +1016,11 @@ int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const
         CKC(cudaMemcpy(q.p, Q, static_cast<size_t>(L) * C * 2, cudaMemcpyHostToDevice));
         CKC(cudaMemcpy(k.p, K, static_cast<size_t>(Lk) * C * 2, cudaMemcpyHostToDevice));
         CKC(cudaMemcpy(v.p, VT, static_cast<size_t>(C) * ldvt * 2, cudaMemcpyHostToDevice));
+        const size_t wsb = adx::tc_attention_ws_bytes(L, Lk, C);
+        DevBuf ws(std::max<size_t>(wsb, 256));
+        CKC(cudaMemset(ws.p, 0, std::max<size_t>(wsb, 256)));
         auto run = [&](cudaStream_t st) {
-            adx::tc_attention(q.p, C, k.p, C, v.p, ldvt, L, Lk, C, static_cast<__nv_bfloat16*>(o.p), C, st);
+            adx::tc_attention(q.p, C, k.p, C, v.p, ldvt, L, Lk, C, static_cast<__nv_bfloat16*>(o.p), C, st, ws.p, wsb);
         };
         run(0);
         CKC(cudaDeviceSynchronize());

@@ -213,7 +213,14 @@ struct AttnArgs {
     int L, Lk, C;  // query tokens, key tokens, model width (heads * 64)
     __nv_bfloat16* out;
     long long ldo;
+    // split-KV (load balance): nsplit CTAs share one (query tile, head) item, each over a
+    // contiguous range of KV blocks; partial O / row max / row sum go to `part`, and the
+    // last CTA of the item (ticket in `counters`) combines them in split order
+    int nsplit = 1;
+    float* part = nullptr;         // [item][split] records of kRecFloats
+    unsigned* counters = nullptr;  // [item], zero at allocation, re-armed by the combiner
 };
+constexpr int kRecFloats = QT * HD + 2 * QT;  // O [128][64] fp32, then m[128], l[128]
 
 __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                       const __grid_constant__ CUtensorMap tmK,
@@ -239,8 +246,10 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
                                                              // then [2 halves][128 rows] row sums
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qt = blockIdx.x, head = blockIdx.y;
-    const int nkv = (p.Lk + KT - 1) / KT;
+    const int qt = blockIdx.x / p.nsplit, split = blockIdx.x - qt * p.nsplit, head = blockIdx.y;
+    const int nkv_all = (p.Lk + KT - 1) / KT;
+    const int j0 = (nkv_all * split) / p.nsplit;  // this CTA's KV blocks [j0, j0 + nkv)
+    const int nkv = (nkv_all * (split + 1)) / p.nsplit - j0;
 
     if (warp == 0 && lane == 0) {
         bar_init(q_full, 1);
@@ -276,10 +285,10 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
             const int s = j % STG;
             bar_wait(&kv_empty[s], ((j / STG) & 1) ^ 1);
             bar_expect(&kv_full[s], K_B + V_B);
-            tma2d(sK + s * K_B, &tmK, head * HD, j * KT, &kv_full[s]);
+            tma2d(sK + s * K_B, &tmK, head * HD, (j0 + j) * KT, &kv_full[s]);
             // V^T rows = this head's 64 dims, one box per 64-key block (128-byte rows)
             for (int blk = 0; blk < NB64; ++blk)
-                tma2d(sV + s * V_B + blk * (HD * 128), &tmVT, j * KT + 64 * blk, head * HD, &kv_full[s]);
+                tma2d(sV + s * V_B + blk * (HD * 128), &tmVT, (j0 + j) * KT + 64 * blk, head * HD, &kv_full[s]);
         }
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------------------ MMA
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
             __syncwarp();
             if (lane == 0) bar_arrive(&s_free[b]);
             // ragged last tile: mask the dead keys to -inf once so the hot loops carry no predicates
-            const int valid = min(KT, p.Lk - j * KT) - half * HK;
+            const int valid = min(KT, p.Lk - (j0 + j) * KT) - half * HK;
             if (valid < HK) {
 #pragma unroll
                 for (int i = 0; i < HK; ++i)
@@ -408,14 +417,58 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
         float* xsum = xmax + 4 * QT;  // own region: the partner may still read tile nkv-1's maxima
         xsum[half * QT + r] = l;
         pair_sync();
-        const float lt = xsum[r] + xsum[QT + r];
+        float lt = xsum[r] + xsum[QT + r];
         bar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         float ov[HD / 2];
         tld16(tO + half * (HD / 2), ov);
         tld16(tO + half * (HD / 2) + 16, ov + 16);
         const long long row = static_cast<long long>(qt) * QT + r;
-        if (row < p.L) {
+        bool write_out = true;
+        if (p.nsplit > 1) {
+            // publish this split's partial: O (unnormalised), the row max m it used, row sum
+            const long long item = qt + static_cast<long long>(gridDim.x / p.nsplit) * head;
+            float* rec = p.part + (item * p.nsplit + split) * kRecFloats;
+#pragma unroll
+            for (int c = 0; c < HD / 2; c += 4)
+                *reinterpret_cast<float4*>(rec + r * HD + half * (HD / 2) + c) =
+                    make_float4(ov[c], ov[c + 1], ov[c + 2], ov[c + 3]);
+            if (half == 0) rec[QT * HD + r] = m, rec[QT * HD + QT + r] = lt;
+            __threadfence();
+            __shared__ unsigned last;
+            asm volatile("bar.sync 5, 256;" ::: "memory");  // the 8 softmax warps
+            if (threadIdx.x == 64)
+                last = atomicAdd(p.counters + item, 1u) == static_cast<unsigned>(p.nsplit - 1);
+            asm volatile("bar.sync 5, 256;" ::: "memory");
+            write_out = last != 0u;
+            if (write_out) {
+                __threadfence();
+                // combine in split order: M = max m_s, w_s = 2^((m_s - M) * scale * log2e),
+                // O = sum w_s O_s / sum w_s l_s (deterministic whichever split finishes last)
+                const float* base = p.part + item * p.nsplit * kRecFloats;
+                float M = -INFINITY;
+                for (int s2 = 0; s2 < p.nsplit; ++s2) M = fmaxf(M, __ldcg(base + s2 * kRecFloats + QT * HD + r));
+                float acc[HD / 2], den = 0.f;
+#pragma unroll
+                for (int c = 0; c < HD / 2; ++c) acc[c] = 0.f;
+                for (int s2 = 0; s2 < p.nsplit; ++s2) {
+                    const float* rs = base + s2 * kRecFloats;
+                    const float w = ex2((__ldcg(rs + QT * HD + r) - M) * sl2);
+                    den = fmaf(w, __ldcg(rs + QT * HD + QT + r), den);
+#pragma unroll
+                    for (int c = 0; c < HD / 2; c += 4) {
+                        const float4 o4 = __ldcg(reinterpret_cast<const float4*>(rs + r * HD + half * (HD / 2) + c));
+                        acc[c] = fmaf(w, o4.x, acc[c]), acc[c + 1] = fmaf(w, o4.y, acc[c + 1]);
+                        acc[c + 2] = fmaf(w, o4.z, acc[c + 2]), acc[c + 3] = fmaf(w, o4.w, acc[c + 3]);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < HD / 2; ++c) ov[c] = acc[c];
+                lt = den;
+                if (threadIdx.x == 64) p.counters[item] = 0u;  // re-arm for the next launch
+            }
+        }
+        if (write_out && row < p.L) {
             const float inv = 1.0f / lt;
             __nv_bfloat16* dst = p.out + row * p.ldo + head * HD + half * (HD / 2);
 #pragma unroll
@@ -475,14 +528,56 @@ CUtensorMap map2d(const void* base, long long rows, long long cols, long long ld
 
 }  // namespace
 
+namespace {
+// split-KV factor: the (query tile, head) items fill 2 CTAs per SM unevenly (e.g. 360
+// items over 296 slots = a 22% second wave); minimise rounds x (KV blocks per CTA + fixed
+// per-CTA cost, + the combine when split)
+int attn_splits(int L, int Lk, int C, int sms) {
+    const long long items = static_cast<long long>((L + QT - 1) / QT) * (C / HD);
+    const int nkv = (Lk + KT - 1) / KT, slots = 2 * sms;
+    int best_s = 1;
+    double best = 1e300;
+    for (int S = 1; S <= 8 && S <= nkv; ++S) {
+        const long long rounds = (items * S + slots - 1) / slots;
+        // the partial publish + fence + ticket + combine costs about ten KV blocks (measured:
+        // splitting the 100-item L=576 grid doubled its time), so only long grids with a bad
+        // wave tail split (level 0: 360 items over 296 slots)
+        const double t = static_cast<double>(rounds) * ((nkv + S - 1) / S + 3 + (S > 1 ? 10 : 0));
+        if (t < best - 1e-9) best = t, best_s = S;
+    }
+    return best_s;
+}
+int device_sms() {
+    int dev = 0, sms = 0;
+    CKA(cudaGetDevice(&dev));
+    CKA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return sms;
+}
+}  // namespace
+
+size_t tc_attention_ws_bytes(int L, int Lk, int C) {
+    const int S = attn_splits(L, Lk, C, device_sms());
+    if (S == 1) return 0;
+    const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD);
+    return 256 * ((items * 4 + 255) / 256) + items * S * kRecFloats * sizeof(float);
+}
+
 void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, const void* VT, long long ldvt, int L,
-                  int Lk, int C, __nv_bfloat16* out, long long ldo, cudaStream_t st) {
+                  int Lk, int C, __nv_bfloat16* out, long long ldo, cudaStream_t st, void* ws, size_t ws_bytes) {
     if (C % HD) throw std::invalid_argument("attention: C must be a multiple of 64");
     if ((ldq | ldk | ldvt | ldo) % 8) throw std::invalid_argument("attention: strides must be multiples of 8");
     const CUtensorMap mq = map2d(Q, L, C, ldq, QT);
     const CUtensorMap mk = map2d(K, Lk, C, ldk, KT);
     const CUtensorMap mv = map2d(VT, C, Lk, ldvt, HD);  // rows = dims, cols = keys
     AttnArgs a{L, Lk, C, out, ldo};
+    const int S = attn_splits(L, Lk, C, device_sms());
+    const size_t need = tc_attention_ws_bytes(L, Lk, C);
+    if (S > 1 && ws && ws_bytes >= need) {  // without a (large enough) workspace: unsplit
+        const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD);
+        a.nsplit = S;
+        a.counters = static_cast<unsigned*>(ws);
+        a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * ((items * 4 + 255) / 256));
+    }
     constexpr size_t smem = 1024 + QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + 256 + 6 * QT * sizeof(float);
     static bool attr[64] = {};
     int dev = 0;
@@ -491,7 +586,7 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
         CKA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr[dev] = true;
     }
-    dim3 grid((L + QT - 1) / QT, C / HD);
+    dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD);
     tc_profile_record_begin(st);
     CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, st, 1, mq, mk, mv, a));
     tc_profile_record_end(st, 2, 4.0 * L * Lk * C);

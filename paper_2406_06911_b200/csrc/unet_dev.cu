@@ -104,7 +104,7 @@ UNetDevice::~UNetDevice() {
                         static_cast<void*>(s.fa), static_cast<void*>(s.fb), static_cast<void*>(s.fc),
                         static_cast<void*>(s.fr), static_cast<void*>(s.fqkv), static_cast<void*>(s.fatt),
                         static_cast<void*>(s.fff), static_cast<void*>(s.fvt), static_cast<void*>(s.sa),
-                        static_cast<void*>(s.sq), static_cast<void*>(s.sk), static_cast<void*>(s.sv)})
+                        static_cast<void*>(s.sq), static_cast<void*>(s.sk), static_cast<void*>(s.sv), s.attn_ws})
             cudaFree(p);
     }
 }
@@ -255,6 +255,16 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
     s.S = static_cast<float*>(al(S * 4));
     s.VT = static_cast<bf16*>(al(vt * 2));
     s.gn = static_cast<float2*>(al(gn));
+    for (const UStage& stg : d_.st)
+        if (stg.attn) {
+            const int L = stg.H * stg.W;
+            s.attn_ws_bytes = std::max({s.attn_ws_bytes, tc_attention_ws_bytes(L, L, stg.cout),
+                                        tc_attention_ws_bytes(L, sp.ctx_len, stg.cout)});
+        }
+    if (s.attn_ws_bytes) {
+        s.attn_ws = al(s.attn_ws_bytes);
+        CKD(cudaMemsetAsync(s.attn_ws, 0, s.attn_ws_bytes, st));
+    }
     if (exact_) {
         size_t spl = 0, ffx = 0, vtx = 0;
         for (const UStage& st : d_.st) {
@@ -307,7 +317,7 @@ void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16
             transpose_head(v, ldv, Lk, Lkp, C, s.VT, st);
             vt = s.VT;
         }
-        tc_attention(q, ldq, k, ldk, vt, Lkp, L, Lk, C, out, C, st);
+        tc_attention(q, ldq, k, ldk, vt, Lkp, L, Lk, C, out, C, st, s.attn_ws, s.attn_ws_bytes);
         return;
     }
     for (int h = 0; h < C / 64; ++h) {

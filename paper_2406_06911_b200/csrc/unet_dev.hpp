@@ -28,6 +28,8 @@ struct UScratch {
                   *ff = nullptr, *ff2 = nullptr, *P = nullptr, *VT = nullptr;
     float* S = nullptr;
     float2* gn = nullptr;
+    void* attn_ws = nullptr;  // split-KV workspace of the fused attention (zeroed counters)
+    size_t attn_ws_bytes = 0;
     // ADX_F32 mode: fp32 activations and split-bf16 operands (3 columns per column)
     float *fa = nullptr, *fb = nullptr, *fc = nullptr, *fr = nullptr, *fqkv = nullptr, *fatt = nullptr, *fff = nullptr,
           *fvt = nullptr;

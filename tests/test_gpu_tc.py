@@ -97,7 +97,9 @@ def test_tc_conv3x3_matches_fp32_reference(batch, H, W, Cin, Cout):
 
 
 @pytest.mark.parametrize("L,Lk,C", [(256, 256, 64), (9216 // 16, 576, 128), (144, 144, 320), (300, 77, 128),
-                                     (1024, 1024, 640)])
+                                     (1024, 1024, 640),
+                                     # split-KV (ticketed combine of partial O / max / sum): level-1 shape, ragged Lk
+                                     (2304, 2304, 640), (700, 1000, 320)])
 def test_tc_attention_matches_fp32_reference(L, Lk, C):
     rng = np.random.default_rng(L + Lk + C)
     Q = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
@@ -118,3 +120,17 @@ def test_tc_attention_matches_fp32_reference(L, Lk, C):
     got = bits_f32(out)
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err < 2e-2, err
+
+
+def test_tc_attention_split_kv_is_deterministic():
+    rng = np.random.default_rng(9)
+    L, C = 1024, 640  # 80 (query tile, head) items -> split over KV
+    Q = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
+    VT = bf16_bits(rng.standard_normal((C, L)).astype(np.float32))
+    outs = []
+    for _ in range(2):
+        out = np.zeros((L, C), np.uint16)
+        _lib.check(adx.lib().adx_tc_attention(0, L, L, C, Q.ctypes.data_as(P16), Q.ctypes.data_as(P16),
+                                              VT.ctypes.data_as(P16), L, out.ctypes.data_as(P16), 3, None))
+        outs.append(out)
+    assert np.array_equal(outs[0], outs[1])
