@@ -166,7 +166,8 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float* v) {
 }
 
 // fused epilogue on 16 accumulator columns [nb, nb + 16) of output row m
-__device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int nb, float* v) {
+__device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int nb, float* v,
+                                      const uint4* rpre = nullptr) {
     const int nlim = p.n_store ? p.n_store : p.N;
     if ((((p.ldo | p.ldr) & 7) == 0) && nb + 16 <= nlim && !p.residual_f32) {
         // vectorised: 16-byte loads / stores
@@ -186,7 +187,7 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int
             for (int j = 0; j < 16; ++j) v[j] = silu(v[j]);
         }
         if (p.residual) {
-            const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + nb);
+            const uint4* rp = rpre ? rpre : reinterpret_cast<const uint4*>(p.residual + m * p.ldr + nb);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const uint4 u = rp[h];
@@ -449,10 +450,25 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
                         if (valid) epi_geglu16(p, m, n0, c, v, g);
                     }
                 } else {
+                    // the residual of chunk c+16 is requested before chunk c's TMEM read and
+                    // epilogue, so its L2 latency overlaps instead of stalling every chunk
+                    const int nlim = p.n_store ? p.n_store : p.N;
+                    const bool pre = valid && p.residual && (((p.ldo | p.ldr) & 7) == 0);
+                    uint4 rnext[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+                    if (pre && n0 + 16 <= nlim) {
+                        const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0);
+                        rnext[0] = rp[0], rnext[1] = rp[1];
+                    }
                     for (int c = 0; c < BN; c += 16) {
+                        const uint4 rcur[2] = {rnext[0], rnext[1]};
+                        const bool have = pre && n0 + c + 16 <= nlim;
+                        if (pre && c + 16 < BN && n0 + c + 32 <= nlim) {
+                            const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + c + 16);
+                            rnext[0] = rp[0], rnext[1] = rp[1];
+                        }
                         float v[16];
                         tmem_ld16(trow + c, v);
-                        if (valid) epi16(p, m, img, n0 + c, v);
+                        if (valid) epi16(p, m, img, n0 + c, v, have ? rcur : nullptr);
                     }
                 }
             }
