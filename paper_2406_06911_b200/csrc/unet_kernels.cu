@@ -351,11 +351,22 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
     const int nsub = max(1, static_cast<int>(blockDim.x) / groups);
     if (threadIdx.x < nsub * groups) {
         const int g = threadIdx.x % groups, sub = threadIdx.x / groups;
+        // all of this thread's partials are requested before any is summed (one L2
+        // round trip instead of one per partial); summed in k order (deterministic)
+        constexpr int kMaxPer = 16;
+        float2 pv[kMaxPer];
+#pragma unroll
+        for (int i = 0; i < kMaxPer; ++i) {
+            const int k = sub + i * nsub;
+            pv[i] = k < G ? __ldcg(&part[static_cast<long long>(k) * groups + g]) : make_float2(0.f, 0.f);
+        }
         double a = 0.0, b = 0.0;
-        for (int k = sub; k < G; k += nsub) {
-            const float2 pv = __ldcg(&part[static_cast<long long>(k) * groups + g]);
-            a += pv.x;
-            b += pv.y;
+#pragma unroll
+        for (int i = 0; i < kMaxPer; ++i) a += pv[i].x, b += pv[i].y;
+        for (int k = sub + kMaxPer * nsub; k < G; k += nsub) {  // (only for > 16 * nsub partials)
+            const float2 q = __ldcg(&part[static_cast<long long>(k) * groups + g]);
+            a += q.x;
+            b += q.y;
         }
         st[2 * (sub * groups + g)] = a;
         st[2 * (sub * groups + g) + 1] = b;
