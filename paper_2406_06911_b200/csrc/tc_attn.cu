@@ -185,7 +185,7 @@ __device__ __forceinline__ void tld_hk_nowait(uint32_t taddr, uint32_t* r) {
 
 // D (+)= A . B^T with A (M x K bf16, K-major) read from TMEM: lane = row, one 32-bit
 // column = two consecutive K elements, 8 columns per K=16 instruction (checked by
-// _ab/ts_mma_test.cu); B from SMEM as usual
+// tools/ts_mma_test.cu); B from SMEM as usual
 __device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"

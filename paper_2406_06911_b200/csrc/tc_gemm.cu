@@ -666,7 +666,7 @@ dim3 launch_grid(const TcArgs& p, int bn) {
 // bn_fixed != 0 pins the tile width.
 int g_override_bn = 0, g_override_splits = 0;
 
-// Measured plans (tools_tc_tune.py on B200: every (BN, S) timed per shape, best kept).
+// Measured plans (tools/tools_tc_tune.py on B200: every (BN, S) timed per shape, best kept).
 // GEMM rows: {0, M, N, K, 0, bn, S}; conv rows: {1, H, W, Cin, Cout, bn, S} (batch 1).
 struct PlanRow {
     int conv, a, b, c, d, bn, s;

@@ -1,6 +1,6 @@
 """One fused-attention launch (L=9216, C=320) for ncu."""
 import ctypes as C, numpy as np, sys, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2406_06911_b200 as adx
 from paper_2406_06911_b200 import _lib
 P16 = C.POINTER(C.c_uint16)

@@ -1,6 +1,6 @@
 """GEMV tuning sweep (run on the GPU box): ms/GEMV and GB/s per config."""
 import ctypes as C, json, os, subprocess, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     import paper_2406_06911_b200 as adx
     L = adx.lib()

@@ -9,7 +9,7 @@ same DP over the measured stage times ("time-balanced").
 NVLink model: 900 GB/s per direction nominal, taken as 700 GB/s achieved for the
 multi-MB activations, plus 10 us per exchange round (launch + NCCL group latency)."""
 import json, os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2406_06911_b200 as adx
 

@@ -1,6 +1,6 @@
 """tcgen05 GEMM / conv3x3 throughput sweep (run on the GPU box)."""
 import ctypes as C, json, sys, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2406_06911_b200 as adx
 from paper_2406_06911_b200 import _lib

@@ -1,7 +1,7 @@
 """ADX_F32 (and ADX_BF16) UNet modes vs the numpy oracle: per-step eps rel-L2 and the
 final-latent rel-L2 of a full trajectory, at two sizes; plus the f32-mode pass time at c2."""
 import json, sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2406_06911_b200 as adx
 from oracle import oracle as O

@@ -1,6 +1,6 @@
 """One level-0 conv3x3 (96x96, 320->320) and one level-0 self-attention (L=9216, C=320) for ncu --set full."""
 import ctypes as C, numpy as np, sys, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2406_06911_b200 as adx
 from paper_2406_06911_b200 import _lib
 P16 = C.POINTER(C.c_uint16); PF = C.POINTER(C.c_float)
