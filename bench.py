@@ -188,7 +188,9 @@ def roofline(m, cfg, prec, dev):
     pass_ms, pass_bytes, launches = adx.time_model_pass(m, cfg["T"], iters, prec, [dev])
     if cfg["family"] == "unet":
         # dominant kernel family = the tcgen05 conv3x3 / GEMM launches, timed per launch
-        # (CUDA events on the launching stream, one eager pass) against their algorithmic FLOPs
+        # (each launch of a profiled pass replayed in isolation from a CUDA graph and timed with CUDA
+        # events on its stream: device time per launch, warm inputs, no host gaps) against their
+        # algorithmic FLOPs
         prof = adx.profile_model_pass(m, cfg["T"], prec, [dev])
         peak, src = load_peak("tensor")
         cg_ms = prof["conv3x3"]["ms"] + prof["gemm"]["ms"]

@@ -1106,7 +1106,8 @@ class RankSession:
 
 def profile_model_pass(m: LayeredDenoiser, t_embed: int, precision: Optional[str] = None,
                        devices: Optional[Sequence[int]] = None) -> Dict[str, dict]:
-    """Per tensor-core kernel family, one eager pass: launches, device ms (CUDA
+    """Per tensor-core kernel family over one pass, every launch replayed in isolation from a CUDA
+    graph: launches, device ms (CUDA
     events per launch) and algorithmic FLOPs."""
     out = np.zeros(9)
     check(lib().adx_engine_profile_pass(m.engine(precision, devices)._h, t_embed, _dp(out)))

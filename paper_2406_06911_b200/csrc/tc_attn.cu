@@ -587,9 +587,10 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
         attr[dev] = true;
     }
     dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD);
-    tc_profile_record_begin(st);
     CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, st, 1, mq, mk, mv, a));
-    tc_profile_record_end(st, 2, 4.0 * L * Lk * C);
+    tc_profile_measure(st, 2, 4.0 * L * Lk * C, [&](cudaStream_t s2) {
+        CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, s2, 1, mq, mk, mv, a));
+    });
     CKA(cudaGetLastError());
 }
 

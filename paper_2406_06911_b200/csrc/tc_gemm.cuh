@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <functional>
+
 namespace adx {
 
 // fused epilogue: out = scale * (act(acc + bias[n] + chan_add[img][n]) + residual[m][n])
@@ -35,12 +37,11 @@ struct TcArgs {
 // force (bn, splits) for every following launch (tuning); (0, 0) restores the plan table / model
 void tc_plan_override(int bn, int splits);
 
-// In-run kernel profiling (eager passes only): when enabled, every tensor-core
-// launch is bracketed by CUDA events on its stream and recorded with its
-// algorithmic FLOPs; kind 0 conv3x3, 1 GEMM, 2 attention.
+// In-run kernel profiling (eager passes only): when enabled, every tensor-core launch is,
+// after it completes, replayed in isolation from a small CUDA graph and timed with events;
+// kind 0 conv3x3, 1 GEMM, 2 attention, with its algorithmic FLOPs.
 void tc_profile_enable(bool on);
-void tc_profile_record_begin(cudaStream_t st);
-void tc_profile_record_end(cudaStream_t st, int kind, double flops);
+void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::function<void(cudaStream_t)>& launch);
 // per kind: {launches, total ms, total flops}; clears the records
 void tc_profile_collect(double out[3][3]);
 
