@@ -755,6 +755,7 @@ void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::func
     float ms = 0.f;
     CKT(cudaEventElapsedTime(&ms, a, b));
     g_prof.push_back({kind, flops, ms / kRep});
+    if (tc_trace()) fprintf(stderr, "  prof kind=%d %.1f us %.1f TFLOP/s\n", kind, 1e3 * ms / kRep, flops / (ms / kRep) / 1e9);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaGraphExecDestroy(ge);
@@ -813,7 +814,8 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     p.n_tiles = (N + bn - 1) / bn;
     p.batch = 1;
     const dim3 grid = launch_grid<false>(p, bn);
-    if (tc_trace()) fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d grid=%ux%u\n", M, N, K, bn, S, grid.x, grid.y);
+    if (tc_trace())
+        fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d act=%d grid=%ux%u\n", M, N, K, bn, S, p.act, grid.x, grid.y);
     dispatch<false>(ma, mb, p, grid, bn, st);
     tc_profile_measure(st, 1, 2.0 * M * N * K, [&](cudaStream_t s2) { dispatch<false>(ma, mb, p, grid, bn, s2); });
 }
