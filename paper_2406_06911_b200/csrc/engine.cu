@@ -81,7 +81,6 @@ void* upload_act(int prec, const std::vector<double>& src) {
     return d;
 }
 
-const void* offset(const void* p, size_t bytes) { return static_cast<const char*>(p) + bytes; }
 void* offset(void* p, size_t bytes) { return static_cast<char*>(p) + bytes; }
 
 }  // namespace

@@ -103,7 +103,7 @@ template <typename WT, typename AT>
 __global__ void __launch_bounds__(kWarps * 32) gemv_kernel(const GemvArgs a) {
     using AccT = typename Acc<WT>::T;
     constexpr int VEC = 16 / sizeof(WT);
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     AT* sx = reinterpret_cast<AT*>(smem_raw);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -165,7 +165,8 @@ __device__ __forceinline__ float ex2_poly(float x) {
 constexpr int POLY_EVERY = ADX_ATTN_POLY_EVERY;
 __device__ __forceinline__ float ex2_mix(float x, int i) {
     if constexpr (POLY_EVERY > 0) {
-        if (i % POLY_EVERY == POLY_EVERY - 1) return ex2_poly(x);
+        constexpr int kEvery = POLY_EVERY > 0 ? POLY_EVERY : 1;
+        if (i % kEvery == kEvery - 1) return ex2_poly(x);
     }
     return ex2(x);
 }
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
                                                       const __grid_constant__ CUtensorMap tmVT, const AttnArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2, P_B = QT * KT * 2;
+    constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2;
     constexpr int XCH_OFF = Q_B + STG * (K_B + V_B) + 256;  // after the barriers
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + Q_B;        // STG x K_B

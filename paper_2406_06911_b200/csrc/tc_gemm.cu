@@ -259,11 +259,6 @@ __device__ __forceinline__ void epi_geglu16(const TcArgs& p, long long m, int n0
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
 // shared::cluster address of `local` in CTA `rank` of this cluster
 __device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
     uint32_t r;
