@@ -750,7 +750,9 @@ void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::func
     float ms = 0.f;
     CKT(cudaEventElapsedTime(&ms, a, b));
     g_prof.push_back({kind, flops, ms / kRep});
-    if (tc_trace()) fprintf(stderr, "  prof kind=%d %.1f us %.1f TFLOP/s\n", kind, 1e3 * ms / kRep, flops / (ms / kRep) / 1e9);
+    if (tc_trace())
+        fprintf(stderr, "  prof kind=%d %.1f us %.1f %s\n", kind, 1e3 * ms / kRep, flops / (ms / kRep) / 1e9,
+                kind > 2 ? "GB/s" : "TFLOP/s");
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaGraphExecDestroy(ge);
@@ -761,6 +763,7 @@ void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::func
 void tc_profile_collect(double out[3][3]) {
     for (int k = 0; k < 3; ++k) out[k][0] = out[k][1] = out[k][2] = 0.0;
     for (auto& r : g_prof) {
+        if (r.kind > 2) continue;  // bandwidth kernels (3 GroupNorm, 4 LayerNorm): trace only
         out[r.kind][0] += 1;
         out[r.kind][1] += r.ms;
         out[r.kind][2] += r.flops;

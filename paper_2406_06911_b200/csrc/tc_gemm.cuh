@@ -39,7 +39,8 @@ void tc_plan_override(int bn, int splits);
 
 // In-run kernel profiling (eager passes only): when enabled, every tensor-core launch is,
 // after it completes, replayed in isolation from a small CUDA graph and timed with events;
-// kind 0 conv3x3, 1 GEMM, 2 attention, with its algorithmic FLOPs.
+// kind 0 conv3x3, 1 GEMM, 2 attention, with its algorithmic FLOPs; kinds 3 (GroupNorm) and 4
+// (LayerNorm) with their algorithmic bytes are only traced (ADX_TC_TRACE=1).
 void tc_profile_enable(bool on);
 void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::function<void(cudaStream_t)>& launch);
 // per kind: {launches, total ms, total flops}; clears the records

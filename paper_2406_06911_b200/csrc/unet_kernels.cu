@@ -6,6 +6,7 @@
 #include "unet_kernels.cuh"
 
 #include "pdl.cuh"
+#include "tc_gemm.cuh"
 
 #include <cuda_bf16.h>
 
@@ -712,7 +713,12 @@ void group_norm_t(const Cat2T<T>& x, int batch, int HW, int groups, const float*
     check_vec8(x, "group_norm");
     const int nv = C / 8;
     if (nv > 1024) throw std::invalid_argument("group_norm: more than 8192 channels");
-    if (batch == 1 && group_norm_fused(x, HW, groups, gamma, beta, eps, silu_act, out, scratch, st)) return;
+    if (batch == 1 && group_norm_fused(x, HW, groups, gamma, beta, eps, silu_act, out, scratch, st)) {
+        tc_profile_measure(st, 3, 2.0 * HW * (x.c0 + x.c1) * sizeof(T), [&](cudaStream_t s2) {
+            group_norm_fused(x, HW, groups, gamma, beta, eps, silu_act, out, scratch, s2);
+        });
+        return;
+    }
     const int chunk_pix = (HW + kGnMaxChunks - 1) / kGnMaxChunks;
     const int chunks = (HW + chunk_pix - 1) / chunk_pix;
     const int rpb = std::max(1, 512 / nv);
@@ -751,6 +757,10 @@ void layer_norm(const __nv_bfloat16* x, int tokens, int C, const float* gamma, c
     CKU(launch_pdl(layernorm_k<bf16>, dim3((tokens + 7) / 8), dim3(256), 0, st, 1, x, tokens, C, gamma, beta, eps,
                    out));
     CKU(cudaGetLastError());
+    tc_profile_measure(st, 4, 2.0 * tokens * C * 2, [&](cudaStream_t s2) {
+        CKU(launch_pdl(layernorm_k<bf16>, dim3((tokens + 7) / 8), dim3(256), 0, s2, 1, x, tokens, C, gamma, beta,
+                       eps, out));
+    });
 }
 void layer_norm(const float* x, int tokens, int C, const float* gamma, const float* beta, float eps, float* out,
                 cudaStream_t st) {
