@@ -41,6 +41,13 @@ CONFIGS = {
                 beta=(0.01, 0.15), w=1, S=1, x_seed=12),
     # BASELINE configs[1], SD-2.1-shaped UNet, 96x96x4, 50-step DDIM, N=2 S=1 w=9
     "c2": dict(family="unet", unet=dict(H=96, W=96), seed=0, T=50, beta=(0.01, 0.19), w=9, S=1, x_seed=12),
+    # BASELINE configs[2], SD-2.1-shaped, stride denoising N=3 S=2 (D = 4 devices)
+    "c3": dict(family="unet", unet=dict(H=96, W=96), seed=0, T=50, beta=(0.01, 0.19), w=9, S=2, x_seed=12),
+    # BASELINE configs[3], SDXL-shaped UNet (3 levels 320/640/1280, transformer depth
+    # 0/2/10, mid 10, 77x2048 context), 128x128x4 latent, classifier-free guidance (batch 2, scale 5)
+    "c4": dict(family="unet", unet=dict(H=128, W=128, ch=(320, 640, 1280), attn=(0, 2, 10), mid_attn=10,
+                                        ctx_dim=2048, cfg=True, cfg_scale=5.0),
+               seed=0, T=50, beta=(0.01, 0.19), w=9, S=1, x_seed=12),
     # a small UNet for quick checks
     "c2s": dict(family="unet", unet=dict(H=32, W=32, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64,
                                          temb_dim=128), seed=0, T=10, beta=(0.01, 0.19), w=2, S=1, x_seed=12),
@@ -162,12 +169,15 @@ def build_model(cfg):
 def config_block(args, cfg, N):
     w = cfg["w"] if N > 1 else cfg["T"]
     if cfg["family"] == "unet":
-        u = dict(H=96, W=96, ch=(320, 640, 1280, 1280), attn=(1, 1, 1, 0), n_res=2)
+        u = dict(H=96, W=96, ch=(320, 640, 1280, 1280), attn=(1, 1, 1, 0), n_res=2, mid_attn=1, ctx_dim=1024,
+                 cfg=False, cfg_scale=5.0)
         u.update(cfg["unet"])
-        desc = (f"{args.config}: SD-2.1-shaped UNet (random init; ch {list(u['ch'])}, {u['n_res']} resnets/level, "
-                f"transformers at levels {[i for i, a in enumerate(u['attn']) if a]}, 77x1024 synthetic context), "
+        shape = "SDXL-shaped" if u["cfg"] or max(u["attn"]) > 1 else "SD-2.1-shaped"
+        desc = (f"{args.config}: {shape} UNet (random init; ch {list(u['ch'])}, {u['n_res']} resnets/level, "
+                f"transformer depth per level {list(u['attn'])} (mid {u['mid_attn']}), 77x{u['ctx_dim']} synthetic "
+                f"context{', CFG batch 2 scale %g' % u['cfg_scale'] if u['cfg'] else ''}), "
                 f"{u['H']}x{u['W']}x4 latent, T={cfg['T']} DDIM")
-        l2 = ("UNet weights 1.7 GB bf16 > 126 MB L2 (no flush needed)" if u["H"] >= 64 and u["ch"][0] >= 320 else
+        l2 = ("UNet weights (GBs of bf16) > 126 MB L2 (no flush needed)" if u["H"] >= 64 and u["ch"][0] >= 320 else
               "small UNet: weights and activations largely L2-resident")
     else:
         desc = (f"{args.config}: reference MLP-stage denoiser (L={cfg['L']} unet-mirror, widths {cfg['widths'][1]}, "

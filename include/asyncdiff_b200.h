@@ -300,9 +300,11 @@ typedef struct {
     int H, W, c_lat;
     int n_levels;
     int ch[8];
-    int attn[8];
+    int attn[8];          /* SpatialTransformer depth per level (0: none; SD-2.1 1, SDXL 0/2/10) */
     int n_res, head_dim, ctx_len, ctx_dim, temb_dim, groups, mid_attn;
     uint64_t seed;
+    int cfg;              /* classifier-free guidance: batch-2 stages, eps_u + scale (eps_c - eps_u) */
+    float cfg_scale;
 } adx_unet_spec;
 int adx_model_build_unet(const adx_unet_spec* spec, adx_model** out);
 /* kind (0 conv_in, 1 res, 2 down, 3 up, 4 out, 5 mid res), cin, cskip, cout, H, W, attn */
@@ -310,7 +312,7 @@ int adx_unet_stage_info(const adx_model* m, int stage, int* info7);
 /* stage parameters (stage 0 = shared time-embedding MLP) for the builder-written oracle */
 int adx_unet_stage_params(const adx_model* m, int stage, char* names, int names_cap, int* shapes,
                           int* n_params, float* data, long long data_cap, long long* n_data);
-int adx_unet_context(const adx_model* m, float* out /* ctx_len * ctx_dim */);
+int adx_unet_context(const adx_model* m, float* out /* batch x ctx_len x ctx_dim; CFG: [uncond, cond] */);
 
 /* --------------------------------- tcgen05 kernels of the UNet-shaped family
  * (no reference function: builder-written oracle, SURVEY §8a extension list).

@@ -54,7 +54,8 @@ class UNetOracle:
         self.links = model.skip_links
         self.info = {s: adx.unet_stage_info(model, s) for s in range(1, self.L + 1)}
         self.params = {s: adx.unet_stage_params(model, s) for s in range(0, self.L + 1)}
-        self.ctx = adx.unet_context(model)
+        self.ctxs = adx.unet_context(model)  # (batch, ctx_len, ctx_dim); CFG: [uncond, cond]
+        self.ci = self.ctxs.shape[0] - 1     # the context of the cascade being evaluated
         self._kv = {}
 
     # ---------------------------------------------------------- primitives
@@ -115,13 +116,15 @@ class UNetOracle:
         h = silu(p["temb.lin1.w"] @ sinusoid(t, self.sp["ch"][0]).astype(self.dt) + p["temb.lin1.b"])
         return p["temb.lin2.w"] @ h + p["temb.lin2.b"]
 
-    def cross_kv(self, stage):
-        if stage not in self._kv:
+    def cross_kv(self, stage, pre="tf."):
+        key = (stage, pre, self.ci)
+        if key not in self._kv:
             p = self.params[stage]
-            k2 = self.r(self.ctx.astype(self.dt) @ p["tf.k2.w"].T)
-            v2 = self.r(self.ctx.astype(self.dt) @ p["tf.v2.w"].T)
-            self._kv[stage] = (k2, v2)
-        return self._kv[stage]
+            ctx = self.ctxs[self.ci].astype(self.dt)
+            k2 = self.r(ctx @ p[pre + "k2.w"].T)
+            v2 = self.r(ctx @ p[pre + "v2.w"].T)
+            self._kv[key] = (k2, v2)
+        return self._kv[key]
 
     # -------------------------------------------------------------- stages
     def transformer(self, stage, x):
@@ -129,19 +132,21 @@ class UNetOracle:
         H, W, C = x.shape
         a = self.group_norm(x, p["tf.gn.gamma"], p["tf.gn.beta"], 1e-6, False).reshape(-1, C)
         h = self.r(self.lin(a, p["tf.proj_in.w"], p["tf.proj_in.b"]))
-        a = self.layer_norm(h, p["tf.ln1.gamma"], p["tf.ln1.beta"])
-        qkv = self.r(self.lin(a, p["tf.qkv.w"]))
-        att = self.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], H * W)
-        h = self.r(self.lin(att, p["tf.o1.w"], p["tf.o1.b"]) + h)
-        a = self.layer_norm(h, p["tf.ln2.gamma"], p["tf.ln2.beta"])
-        q2 = self.r(self.lin(a, p["tf.q2.w"]))
-        k2, v2 = self.cross_kv(stage)
-        att = self.attention(q2, k2, v2, self.sp["ctx_len"])
-        h = self.r(self.lin(att, p["tf.o2.w"], p["tf.o2.b"]) + h)
-        a = self.layer_norm(h, p["tf.ln3.gamma"], p["tf.ln3.beta"])
-        f = self.r(self.lin(a, p["tf.ff1.w"], p["tf.ff1.b"]))
-        g = self.r(f[:, :4 * C] * gelu(f[:, 4 * C:]))
-        h = self.r(self.lin(g, p["tf.ff2.w"], p["tf.ff2.b"]) + h)
+        for b in range(self.info[stage]["attn"]):  # transformer blocks (depth)
+            pre = "tf." if b == 0 else f"tf.b{b}."
+            a = self.layer_norm(h, p[pre + "ln1.gamma"], p[pre + "ln1.beta"])
+            qkv = self.r(self.lin(a, p[pre + "qkv.w"]))
+            att = self.attention(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], H * W)
+            h = self.r(self.lin(att, p[pre + "o1.w"], p[pre + "o1.b"]) + h)
+            a = self.layer_norm(h, p[pre + "ln2.gamma"], p[pre + "ln2.beta"])
+            q2 = self.r(self.lin(a, p[pre + "q2.w"]))
+            k2, v2 = self.cross_kv(stage, pre)
+            att = self.attention(q2, k2, v2, self.sp["ctx_len"])
+            h = self.r(self.lin(att, p[pre + "o2.w"], p[pre + "o2.b"]) + h)
+            a = self.layer_norm(h, p[pre + "ln3.gamma"], p[pre + "ln3.beta"])
+            f = self.r(self.lin(a, p[pre + "ff1.w"], p[pre + "ff1.b"]))
+            g = self.r(f[:, :4 * C] * gelu(f[:, 4 * C:]))
+            h = self.r(self.lin(g, p[pre + "ff2.w"], p[pre + "ff2.b"]) + h)
         y = self.r(self.lin(h, p["tf.proj_out.w"], p["tf.proj_out.b"]) + x.reshape(-1, C))
         return y.reshape(H, W, C)
 
@@ -178,7 +183,19 @@ class UNetOracle:
         return out
 
     def eval_full(self, x, t):
-        """one denoiser evaluation: eps (H*W*c_lat; fp32, or fp64 in the exact mode)"""
+        """one denoiser evaluation: eps (H*W*c_lat; fp32, or fp64 in the exact mode);
+        with CFG the cascade runs once per context and eps = eps_u + s * (eps_c - eps_u)"""
+        if self.ctxs.shape[0] == 1:
+            self.ci = 0
+            return self._cascade(x, t)
+        self.ci = 0
+        eu = self._cascade(x, t)
+        self.ci = 1
+        ec = self._cascade(x, t)
+        s = self.sp["cfg_scale"]
+        return eu + np.float32(s) * (ec - eu) if not self.exact else eu + s * (ec - eu)
+
+    def _cascade(self, x, t):
         outs = {}
         cur = x
         for s in range(1, self.L + 1):

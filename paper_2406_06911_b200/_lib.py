@@ -107,7 +107,7 @@ class adx_unet_spec(C.Structure):
     _fields_ = [("H", C.c_int), ("W", C.c_int), ("c_lat", C.c_int), ("n_levels", C.c_int), ("ch", C.c_int * 8),
                 ("attn", C.c_int * 8), ("n_res", C.c_int), ("head_dim", C.c_int), ("ctx_len", C.c_int),
                 ("ctx_dim", C.c_int), ("temb_dim", C.c_int), ("groups", C.c_int), ("mid_attn", C.c_int),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("cfg", C.c_int), ("cfg_scale", C.c_float)]
 
 
 class adx_latency_report(C.Structure):

@@ -290,13 +290,20 @@ UNET_KINDS = {0: "conv_in", 1: "res", 2: "down", 3: "up", 4: "out", 5: "mid_res"
 def build_unet_denoiser(H: int = 96, W: int = 96, c_lat: int = 4, ch: Sequence[int] = (320, 640, 1280, 1280),
                         attn: Sequence[int] = (1, 1, 1, 0), n_res: int = 2, head_dim: int = 64, ctx_len: int = 77,
                         ctx_dim: int = 1024, temb_dim: int = 1280, groups: int = 32, mid_attn: int = 1,
-                        seed: int = 0) -> LayeredDenoiser:
+                        seed: int = 0, cfg: bool = False, cfg_scale: float = 5.0) -> LayeredDenoiser:
     """UNet-shaped denoiser behind the reference's stage contract (defaults: the
     SD-2.1 UNet topology at a 96x96x4 latent, random init).  Works with every
     partition / plan / run entry point.  Engine precision "bf16" (the default for
     this family): bf16 activations on the tcgen05 kernels, fp32 latent; "f32": fp32
     activations with split-bf16 tensor-core products (the north_star's rel-L2 <=
-    1e-3 mode, checked against the fp64 oracle)."""
+    1e-3 mode, checked against the fp64 oracle).
+
+    attn[l] / mid_attn are SpatialTransformer depths (0: none).  cfg=True runs
+    classifier-free guidance inside the denoiser: every stage carries a batch of 2
+    (unconditional, conditional context) and the out stage returns
+    eps_u + cfg_scale * (eps_c - eps_u).  SDXL-shaped example (BASELINE config 4):
+    build_unet_denoiser(128, 128, ch=(320, 640, 1280), attn=(0, 2, 10), mid_attn=10,
+    ctx_dim=2048, cfg=True)."""
     from ._lib import adx_unet_spec
     s = adx_unet_spec()
     s.H, s.W, s.c_lat, s.n_levels = H, W, c_lat, len(ch)
@@ -304,13 +311,14 @@ def build_unet_denoiser(H: int = 96, W: int = 96, c_lat: int = 4, ch: Sequence[i
         s.ch[i], s.attn[i] = c, int(a)
     s.n_res, s.head_dim, s.ctx_len, s.ctx_dim = n_res, head_dim, ctx_len, ctx_dim
     s.temb_dim, s.groups, s.mid_attn, s.seed = temb_dim, groups, int(mid_attn), seed
+    s.cfg, s.cfg_scale = int(bool(cfg)), float(cfg_scale)
     h = C.c_void_p()
     check(lib().adx_model_build_unet(C.byref(s), C.byref(h)))
     m = LayeredDenoiser(h.value)
     m.default_precision = "bf16"
     m.unet_spec = dict(H=H, W=W, c_lat=c_lat, ch=list(ch), attn=list(attn), n_res=n_res, head_dim=head_dim,
                        ctx_len=ctx_len, ctx_dim=ctx_dim, temb_dim=temb_dim, groups=groups, mid_attn=mid_attn,
-                       seed=seed)
+                       seed=seed, cfg=int(bool(cfg)), cfg_scale=float(cfg_scale))
     return m
 
 
@@ -340,10 +348,12 @@ def unet_stage_params(m: LayeredDenoiser, stage: int) -> Dict[str, np.ndarray]:
 
 
 def unet_context(m: LayeredDenoiser) -> np.ndarray:
+    """(batch, ctx_len, ctx_dim) contexts: batch 1, or [uncond, cond] with CFG"""
     sp = m.unet_spec
-    out = np.zeros(sp["ctx_len"] * sp["ctx_dim"], np.float32)
+    b = 2 if sp.get("cfg") else 1
+    out = np.zeros(b * sp["ctx_len"] * sp["ctx_dim"], np.float32)
     check(lib().adx_unet_context(m._h, out.ctypes.data_as(C.POINTER(C.c_float))))
-    return out.reshape(sp["ctx_len"], sp["ctx_dim"])
+    return out.reshape(b, sp["ctx_len"], sp["ctx_dim"])
 
 
 def sinusoid(t: int, dim: int) -> np.ndarray:

@@ -928,6 +928,8 @@ int adx_model_build_unet(const adx_unet_spec* s, adx_model** out) {
         sp.groups = s->groups;
         sp.mid_attn = s->mid_attn;
         sp.seed = s->seed;
+        sp.cfg = s->cfg ? 1 : 0;
+        sp.cfg_scale = s->cfg_scale;
         *out = new adx_model{adx::build_unet_model(sp)};
     });
 }

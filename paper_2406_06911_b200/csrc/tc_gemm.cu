@@ -179,7 +179,8 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int
                 v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
             }
             if (p.chan_add) {
-                const float4 b = *reinterpret_cast<const float4*>(p.chan_add + static_cast<long long>(img) * p.N + nb + j);
+                const float4 b = *reinterpret_cast<const float4*>(
+                    p.chan_add + static_cast<long long>(p.chan_add_shared ? 0 : img) * p.N + nb + j);
                 v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
             }
         }
@@ -220,7 +221,7 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int
         if (n >= nlim) continue;
         float x = v[j];
         if (p.bias) x += p.bias[n];
-        if (p.chan_add) x += p.chan_add[static_cast<long long>(img) * p.N + n];
+        if (p.chan_add) x += p.chan_add[static_cast<long long>(p.chan_add_shared ? 0 : img) * p.N + n];
         if (p.act == 1) x = silu(x);
         if (p.residual) x += __bfloat162float(p.residual[m * p.ldr + n]);
         if (p.residual_f32) x += p.residual_f32[m * p.ldr + n];

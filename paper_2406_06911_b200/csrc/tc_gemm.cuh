@@ -19,6 +19,7 @@ struct TcArgs {
     // epilogue
     const float* bias = nullptr;          // [N]
     const float* chan_add = nullptr;      // [images][N] (e.g. time-embedding projection)
+    int chan_add_shared = 0;              // 1: every image uses row 0 (CFG batch at one timestep)
     const __nv_bfloat16* residual = nullptr;
     const float* residual_f32 = nullptr;  // fp32 residual (ADX_F32 mode); at most one of the two
     long long ldr = 0;

@@ -13,10 +13,11 @@ namespace {
 
 long long conv_macs(int H, int W, int cout, int cin) { return static_cast<long long>(H) * W * cout * 9 * cin; }
 
-long long attn_macs(int L, int C, int Lc, int ctx_dim) {
+// a SpatialTransformer of `depth` blocks: proj_in / proj_out once, per block QKV, self and
+// cross attention, o1 / q2 / o2, GEGLU FF (the context K / V projection is precomputed)
+long long attn_macs(int L, int C, int Lc, int depth) {
     const long long l = L, c = C;
-    return l * c * c * (1 + 3 + 1 + 1 + 1 + 8 + 4 + 1) + 2 * l * l * c + 2 * l * Lc * c +
-           2LL * Lc * c * ctx_dim;
+    return l * c * c * 2 + depth * (l * c * c * (3 + 1 + 1 + 1 + 8 + 4) + 2 * l * l * c + 2 * l * Lc * c);
 }
 
 }  // namespace
@@ -26,6 +27,10 @@ Model build_unet_model(const UNetSpec& sp) {
     for (int c : sp.ch)
         if (c % 64 || c % sp.groups) throw std::invalid_argument("unet: channels must be multiples of 64 and groups");
     if (sp.head_dim != 64) throw std::invalid_argument("unet: head_dim must be 64");
+    if (sp.ctx_dim % 64) throw std::invalid_argument("unet: ctx_dim must be a multiple of 64");
+    for (int a : sp.attn)
+        if (a < 0) throw std::invalid_argument("unet: transformer depth must be >= 0");
+    if (sp.mid_attn < 0) throw std::invalid_argument("unet: mid transformer depth must be >= 0");
     const int levels = static_cast<int>(sp.ch.size());
     if (sp.H % (1 << (levels - 1)) || sp.W % (1 << (levels - 1)))
         throw std::invalid_argument("unet: H, W must be divisible by 2^(levels-1)");
@@ -124,13 +129,22 @@ Model build_unet_model(const UNetSpec& sp) {
             default:
                 s.macs = conv_macs(s.H, s.W, s.cout, cin) + conv_macs(s.H, s.W, s.cout, s.cout) +
                          (cin != s.cout ? static_cast<long long>(s.H) * s.W * s.cout * cin : 0);
-                if (s.attn) s.macs += attn_macs(s.H * s.W, s.cout, sp.ctx_len, sp.ctx_dim);
+                if (s.attn) s.macs += attn_macs(s.H * s.W, s.cout, sp.ctx_len, s.attn);
         }
+        s.macs *= sp.batch();
     }
-    // synthetic cross-attention context ~ N(0, 1)
-    Rng rng(mix_seed(sp.seed, 1000003));
-    d->ctx.resize(static_cast<size_t>(sp.ctx_len) * sp.ctx_dim);
-    for (auto& v : d->ctx) v = static_cast<float>(rng.normal());
+    // synthetic cross-attention contexts ~ N(0, 1): the conditional one (seed 1000003) and,
+    // with CFG, an unconditional one (seed 1000004) placed first (image 0)
+    const size_t csz = static_cast<size_t>(sp.ctx_len) * sp.ctx_dim;
+    d->ctx.resize(csz * sp.batch());
+    {
+        Rng rng(mix_seed(sp.seed, 1000003));
+        for (size_t i = 0; i < csz; ++i) d->ctx[(sp.batch() - 1) * csz + i] = static_cast<float>(rng.normal());
+    }
+    if (sp.cfg) {
+        Rng rng(mix_seed(sp.seed, 1000004));
+        for (size_t i = 0; i < csz; ++i) d->ctx[i] = static_cast<float>(rng.normal());
+    }
 
     Model m;
     m.kind = 1;
@@ -141,7 +155,7 @@ Model build_unet_model(const UNetSpec& sp) {
     m.widths.push_back(sp.H * sp.W * sp.c_lat);
     for (size_t i = 0; i < st.size(); ++i) {
         const UStage& s = st[i];
-        m.widths.push_back(i + 1 == st.size() ? sp.H * sp.W * sp.c_lat : s.cout * s.Ho() * s.Wo());
+        m.widths.push_back(i + 1 == st.size() ? sp.H * sp.W * sp.c_lat : sp.batch() * s.cout * s.Ho() * s.Wo());
     }
     m.links = links;
     std::sort(m.links.begin(), m.links.end());
@@ -255,6 +269,22 @@ std::vector<UParam> unet_stage_params(const UNetDesc& d, int stage) {
                 lin_params(g, ps, "tf.ff1", 8 * C, C, true);
                 lin_params(g, ps, "tf.ff2", C, 4 * C, true);
                 lin_params(g, ps, "tf.proj_out", C, C, true);
+                // further transformer blocks (depth > 1), appended so depth-1 stages keep
+                // exactly the parameters above
+                for (int b = 1; b < s.attn; ++b) {
+                    const std::string pre = "tf.b" + std::to_string(b) + ".";
+                    norm_params(g, ps, pre + "ln1", C);
+                    lin_params(g, ps, pre + "qkv", 3 * C, C, false);
+                    lin_params(g, ps, pre + "o1", C, C, true);
+                    norm_params(g, ps, pre + "ln2", C);
+                    lin_params(g, ps, pre + "q2", C, C, false);
+                    lin_params(g, ps, pre + "k2", C, sp.ctx_dim, false);
+                    lin_params(g, ps, pre + "v2", C, sp.ctx_dim, false);
+                    lin_params(g, ps, pre + "o2", C, C, true);
+                    norm_params(g, ps, pre + "ln3", C);
+                    lin_params(g, ps, pre + "ff1", 8 * C, C, true);
+                    lin_params(g, ps, pre + "ff2", C, 4 * C, true);
+                }
             }
         }
     }

@@ -18,13 +18,20 @@ struct UNetSpec {
     int c_lat = 4;                            // latent channels
     std::vector<int> ch = {320, 640, 1280, 1280};
     int n_res = 2;                            // resnets per down level (up levels use n_res+1)
-    std::vector<int> attn = {1, 1, 1, 0};     // SpatialTransformer after the level's resnets
+    std::vector<int> attn = {1, 1, 1, 0};     // SpatialTransformer depth after the level's resnets
+                                              // (0: none; SD-2.1: 1, SDXL: 0 / 2 / 10 blocks)
     int head_dim = 64;
     int ctx_len = 77, ctx_dim = 1024;         // cross-attention context (synthetic, seeded)
     int temb_dim = 1280;
     int groups = 32;
-    int mid_attn = 1;
+    int mid_attn = 1;                         // mid-block transformer depth
     uint64_t seed = 0;
+    // classifier-free guidance: the stages run a batch of 2 (image 0 with the unconditional
+    // context, image 1 with the conditional one) and the out stage returns
+    // eps_u + cfg_scale * (eps_c - eps_u); the latent / eps stay one image
+    int cfg = 0;
+    float cfg_scale = 5.0f;
+    int batch() const { return cfg ? 2 : 1; }
 };
 
 enum UKind { kConvIn = 0, kRes = 1, kDown = 2, kUp = 3, kOut = 4, kMidRes = 5 };
@@ -35,7 +42,7 @@ struct UStage {
     int cskip = 0;    // concatenated skip channels (0: none)
     int cout = 0;
     int H = 0, W = 0; // input spatial size (DOWN halves it, UP doubles it)
-    int attn = 0;     // followed by a SpatialTransformer (RES / MidRes)
+    int attn = 0;     // depth of the following SpatialTransformer (RES / MidRes; 0: none)
     long long macs = 0;
     int Ho() const { return kind == kDown ? H / 2 : kind == kUp ? 2 * H : H; }
     int Wo() const { return kind == kDown ? W / 2 : kind == kUp ? 2 * W : W; }
@@ -44,7 +51,7 @@ struct UStage {
 struct UNetDesc {
     UNetSpec spec;
     std::vector<UStage> st;  // index 0 = stage 1
-    std::vector<float> ctx;  // ctx_len x ctx_dim context
+    std::vector<float> ctx;  // batch x ctx_len x ctx_dim contexts (CFG: [uncond, cond])
 };
 
 // Model (topology + costs, no MLP weights) for the engine / partitioner / plan

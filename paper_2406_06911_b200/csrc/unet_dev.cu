@@ -73,6 +73,45 @@ std::vector<uint16_t> split_b(const std::vector<float>& w, long long rows, int K
     return out;
 }
 
+bool ends_with(const std::string& s, const char* suf) {
+    const size_t n = std::strlen(suf);
+    return s.size() >= n && s.compare(s.size() - n, n, suf) == 0;
+}
+
+void* device_zeros(size_t bytes) {
+    void* d = nullptr;
+    CKD(cudaMalloc(&d, std::max<size_t>(bytes, 16)));
+    CKD(cudaMemset(d, 0, std::max<size_t>(bytes, 16)));
+    return d;
+}
+
+void* upload_bf16(const std::vector<float>& v);
+
+// K2 [Lp][C] = ctx . Wk^T and V2^T [C][Lp] = Wv . ctx^T on the tensor cores (private stream,
+// synchronous: runs at stage preparation, outside any capture); rows / columns >= Lc stay zero
+void ctx_projection(const float* ctx, int Lc, int Dc, const std::vector<float>& wk, const std::vector<float>& wv,
+                    int C, int Lp, __nv_bfloat16* k2, __nv_bfloat16* vt2) {
+    std::vector<float> c(ctx, ctx + static_cast<size_t>(Lc) * Dc);
+    void* dctx = upload_bf16(c);
+    void* dwk = upload_bf16(wk);
+    void* dwv = upload_bf16(wv);
+    cudaStream_t st;
+    CKD(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    TcArgs a;
+    a.out_bf16 = k2;
+    a.ldo = C;
+    tc_gemm(dctx, dwk, Lc, C, Dc, a, st);
+    TcArgs b;
+    b.out_bf16 = vt2;
+    b.ldo = Lp;
+    tc_gemm(dwv, dctx, C, Lc, Dc, b, st);
+    CKD(cudaStreamSynchronize(st));
+    CKD(cudaStreamDestroy(st));
+    cudaFree(dctx);
+    cudaFree(dwk);
+    cudaFree(dwv);
+}
+
 void* upload_u16(const std::vector<uint16_t>& h) {
     void* d = nullptr;
     CKD(cudaMalloc(&d, std::max<size_t>(h.size(), 8) * 2));
@@ -92,8 +131,8 @@ UNetDevice::~UNetDevice() {
     for (auto& s : st_) {
         for (auto& kv : s.p) cudaFree(kv.second);
         cudaFree(s.chan_add);
-        cudaFree(s.k2);
-        cudaFree(s.vt2);
+        for (auto* q : s.k2) cudaFree(q);
+        for (auto* q : s.vt2) cudaFree(q);
     }
     for (auto& kv : scratch_) {
         UScratch& s = kv.second;
@@ -104,7 +143,8 @@ UNetDevice::~UNetDevice() {
                         static_cast<void*>(s.fa), static_cast<void*>(s.fb), static_cast<void*>(s.fc),
                         static_cast<void*>(s.fr), static_cast<void*>(s.fqkv), static_cast<void*>(s.fatt),
                         static_cast<void*>(s.fff), static_cast<void*>(s.fvt), static_cast<void*>(s.sa),
-                        static_cast<void*>(s.sq), static_cast<void*>(s.sk), static_cast<void*>(s.sv), s.attn_ws})
+                        static_cast<void*>(s.sq), static_cast<void*>(s.sk), static_cast<void*>(s.sv), s.attn_ws,
+                        static_cast<void*>(s.eps2)})
             cudaFree(p);
     }
 }
@@ -123,12 +163,14 @@ void UNetDevice::ensure_stage(int stage) {
     auto ps = unet_stage_params(d_, stage);
     for (auto& p : ps) {
         const bool matrix = p.shape.size() == 2;
-        if (exact_ && matrix && p.name != "tf.k2.w" && p.name != "tf.v2.w" && p.name != "temb.w") {
+        const bool ctx_proj = ends_with(p.name, ".k2.w") || ends_with(p.name, ".v2.w");  // precomputed below
+        const bool ff1 = ends_with(p.name, ".ff1.w") || ends_with(p.name, ".ff1.b");
+        if (exact_ && matrix && !ctx_proj && p.name != "temb.w") {
             // ADX_F32: split-bf16 weights, [hi | lo | hi] per conv tap (g = Cin) or per row (g = K);
             // the GEGLU ff1 rows are tile-interleaved first, exactly as in the bf16 mode
             const int rows = p.shape[0], K = p.shape[1];
             std::vector<float> w = p.data;
-            if (p.name == "tf.ff1.w") {
+            if (ff1) {
                 const int H = rows / 2;
                 if (H % 128) throw std::invalid_argument("unet: GEGLU width must be a multiple of 128");
                 for (int t = 0; t < H / 128; ++t)
@@ -143,7 +185,7 @@ void UNetDevice::ensure_stage(int stage) {
             ds.bytes[p.name] = static_cast<long long>(w.size()) * 6;
             continue;
         }
-        if (p.name == "tf.ff1.w" || p.name == "tf.ff1.b") {
+        if (ff1) {
             // GEGLU fused into the ff1 GEMM epilogue: rows [hidden | gate] interleaved per
             // 256-wide N tile: tile t = hidden rows [128t, 128t+128) then gate rows 4C + same
             const int rows = p.shape[0], cols = matrix ? p.shape[1] : 1, H = rows / 2;
@@ -159,39 +201,48 @@ void UNetDevice::ensure_stage(int stage) {
             ds.bytes[p.name] = static_cast<long long>(p.data.size()) * (matrix ? 2 : 4);
             continue;
         }
-        if (p.name == "tf.k2.w" || p.name == "tf.v2.w" || p.name == "temb.w" || p.name == "temb.b") continue;
+        if (ctx_proj || p.name == "temb.w" || p.name == "temb.b") continue;
         ds.p[p.name] = matrix ? upload_bf16(p.data) : upload_f32(p.data);
         ds.bytes[p.name] = static_cast<long long>(p.data.size()) * (matrix ? 2 : 4);
     }
     const UStage& s = d_.st[stage - 1];
     if (s.attn) {
-        // cross-attention K2 = ctx . Wk2^T, V2 = ctx . Wv2^T are constant per run:
-        // precompute once (fp32), pad the context length to a multiple of 64
-        const int C = s.cout, Lc = sp.ctx_len, Lp = pad64(Lc), Dc = sp.ctx_dim;
-        const std::vector<float>* wk = nullptr;
-        const std::vector<float>* wv = nullptr;
-        for (auto& p : ps) {
-            if (p.name == "tf.k2.w") wk = &p.data;
-            if (p.name == "tf.v2.w") wv = &p.data;
-        }
-        std::vector<float> k2(static_cast<size_t>(Lp) * C, 0.f), vt2(static_cast<size_t>(C) * Lp, 0.f);
-        for (int l = 0; l < Lc; ++l)
-            for (int c = 0; c < C; ++c) {
-                float ak = 0.f, av = 0.f;
-                for (int k = 0; k < Dc; ++k) {
-                    const float x = d_.ctx[static_cast<size_t>(l) * Dc + k];
-                    ak += (*wk)[static_cast<size_t>(c) * Dc + k] * x;
-                    av += (*wv)[static_cast<size_t>(c) * Dc + k] * x;
-                }
-                k2[static_cast<size_t>(l) * C + c] = ak;
-                vt2[static_cast<size_t>(c) * Lp + l] = av;
+        // cross-attention K2 = ctx . Wk2^T and V2^T = Wv2 . ctx^T are constant per run: computed
+        // once per (block, context), context length padded to a multiple of 64 (zeros)
+        const int C = s.cout, Lc = sp.ctx_len, Lp = pad64(Lc), Dc = sp.ctx_dim, B = sp.batch();
+        const size_t csz = static_cast<size_t>(Lc) * Dc;
+        for (int b = 0; b < s.attn; ++b) {
+            const std::string pre = b == 0 ? "tf." : "tf.b" + std::to_string(b) + ".";
+            const std::vector<float>* wk = nullptr;
+            const std::vector<float>* wv = nullptr;
+            for (auto& p : ps) {
+                if (p.name == pre + "k2.w") wk = &p.data;
+                if (p.name == pre + "v2.w") wv = &p.data;
             }
-        if (exact_) {  // split operands: K2' per 64-wide head, V2'^T along the (padded) context keys
-            ds.k2 = static_cast<bf16*>(upload_u16(split_b(k2, Lp, C, 64)));
-            ds.vt2 = static_cast<bf16*>(upload_u16(split_b(vt2, C, Lp, Lp)));
-        } else {
-            ds.k2 = static_cast<bf16*>(upload_bf16(k2));
-            ds.vt2 = static_cast<bf16*>(upload_bf16(vt2));
+            if (!wk || !wv) throw std::logic_error("unet: missing cross-attention projection of " + pre);
+            for (int img = 0; img < B; ++img) {
+                const float* ctx = d_.ctx.data() + img * csz;
+                if (exact_) {  // fp32 on the host, then split operands (K2' per head, V2'^T along keys)
+                    std::vector<float> k2(static_cast<size_t>(Lp) * C, 0.f), vt2(static_cast<size_t>(C) * Lp, 0.f);
+                    for (int l = 0; l < Lc; ++l)
+                        for (int c = 0; c < C; ++c) {
+                            float ak = 0.f, av = 0.f;
+                            for (int k = 0; k < Dc; ++k) {
+                                const float x = ctx[static_cast<size_t>(l) * Dc + k];
+                                ak += (*wk)[static_cast<size_t>(c) * Dc + k] * x;
+                                av += (*wv)[static_cast<size_t>(c) * Dc + k] * x;
+                            }
+                            k2[static_cast<size_t>(l) * C + c] = ak;
+                            vt2[static_cast<size_t>(c) * Lp + l] = av;
+                        }
+                    ds.k2.push_back(static_cast<bf16*>(upload_u16(split_b(k2, Lp, C, 64))));
+                    ds.vt2.push_back(static_cast<bf16*>(upload_u16(split_b(vt2, C, Lp, Lp))));
+                } else {  // bf16 on the tensor cores: two GEMMs (SDXL: 10 blocks x 2 contexts per stage)
+                    ds.k2.push_back(static_cast<bf16*>(device_zeros(static_cast<size_t>(Lp) * C * 2)));
+                    ds.vt2.push_back(static_cast<bf16*>(device_zeros(static_cast<size_t>(C) * Lp * 2)));
+                    ctx_projection(ctx, Lc, Dc, *wk, *wv, C, Lp, ds.k2.back(), ds.vt2.back());
+                }
+            }
         }
     }
     ds.ready = true;
@@ -237,6 +288,11 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
             vt = std::max(vt, static_cast<size_t>(s.cout) * Lp);
         }
     }
+    // activations / GEMM operands hold the whole CFG batch; S, V^T and the attention work
+    // space are per image (attention runs image by image)
+    act *= sp.batch();
+    qkv *= sp.batch();
+    ff *= sp.batch();
     UScratch s;
     auto al = [](size_t bytes) {
         void* p = nullptr;
@@ -255,6 +311,7 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
     s.S = static_cast<float*>(al(S * 4));
     s.VT = static_cast<bf16*>(al(vt * 2));
     s.gn = static_cast<float2*>(al(gn));
+    s.eps2 = static_cast<float*>(al(static_cast<size_t>(sp.batch()) * sp.H * sp.W * sp.c_lat * 4));
     for (const UStage& stg : d_.st)
         if (stg.attn) {
             const int L = stg.H * stg.W;
@@ -277,6 +334,8 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
                 vtx = std::max(vtx, 64 * Lp);
             }
         }
+        spl *= sp.batch();  // split operands of whole-batch GEMMs (attention ones are per image)
+        ffx *= sp.batch();
         s.fa = static_cast<float*>(al(act * 4));
         s.fb = static_cast<float*>(al(act * 4));
         s.fc = static_cast<float*>(al(act * 4));
@@ -337,67 +396,82 @@ void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16
 }
 
 // SpatialTransformer: GN -> proj_in -> [LN self-attn] -> [LN cross-attn] -> [LN GEGLU FF] -> proj_out + x
+// SpatialTransformer: GN -> proj_in -> depth x ([LN self-attn] [LN cross-attn] [LN GEGLU FF])
+// -> proj_out + x.  With CFG the batch holds 2 images: GEMMs / LN run over both, GN and
+// attention per image (image i cross-attends to context i).
 void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16* y, cudaStream_t st) {
     UScratch& s = scratch(st);
     const UNetSpec& sp = d_.spec;
-    const int L = H * W;
-    Cat2 xc{x, C, nullptr, 0};
-    group_norm(xc, 1, L, sp.groups, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"), 1e-6f, 0, s.a, s.gn, st);
+    const int L = H * W, B = sp.batch(), BL = B * L, depth = d_.st[stage - 1].attn;
+    const long long img = static_cast<long long>(L) * C;
+    for (int b = 0; b < B; ++b)
+        group_norm(Cat2{x + b * img, C, nullptr, 0}, 1, L, sp.groups, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"),
+                   1e-6f, 0, s.a + b * img, s.gn, st);
     TcArgs pi;
     pi.bias = F(stage, "tf.proj_in.b");
     pi.out_bf16 = s.b;
     pi.ldo = C;
-    tc_gemm(s.a, P(stage, "tf.proj_in.w"), L, C, C, pi, st);  // h = s.b
-    // self attention
-    layer_norm(s.b, L, C, F(stage, "tf.ln1.gamma"), F(stage, "tf.ln1.beta"), 1e-5f, s.a, st);
-    TcArgs qk;
-    qk.out_bf16 = s.qkv;
-    qk.ldo = 3 * C;
-    tc_gemm(s.a, P(stage, "tf.qkv.w"), L, 3 * C, C, qk, st);
-    attention(s, s.qkv, 3 * C, s.qkv + C, 3 * C, s.qkv + 2 * C, 3 * C, nullptr, L, L, C, s.att, st);
-    TcArgs o1;
-    o1.bias = F(stage, "tf.o1.b");
-    o1.residual = s.b;
-    o1.ldr = C;
-    o1.out_bf16 = s.b;  // in place: each element is read and written by one epilogue thread
-    o1.ldo = C;
-    tc_gemm(s.att, P(stage, "tf.o1.w"), L, C, C, o1, st);
-    // cross attention against the fixed context
-    layer_norm(s.b, L, C, F(stage, "tf.ln2.gamma"), F(stage, "tf.ln2.beta"), 1e-5f, s.a, st);
-    TcArgs q2;
-    q2.out_bf16 = s.qkv;
-    q2.ldo = C;
-    tc_gemm(s.a, P(stage, "tf.q2.w"), L, C, C, q2, st);
-    attention(s, s.qkv, C, st_[stage].k2, C, nullptr, 0, st_[stage].vt2, L, sp.ctx_len, C, s.att, st);
-    TcArgs o2;
-    o2.bias = F(stage, "tf.o2.b");
-    o2.residual = s.b;
-    o2.ldr = C;
-    o2.out_bf16 = s.b;
-    o2.ldo = C;
-    tc_gemm(s.att, P(stage, "tf.o2.w"), L, C, C, o2, st);
-    // GEGLU feed-forward
-    layer_norm(s.b, L, C, F(stage, "tf.ln3.gamma"), F(stage, "tf.ln3.beta"), 1e-5f, s.a, st);
-    TcArgs f1;
-    f1.bias = F(stage, "tf.ff1.b");
-    f1.act = 2;  // GEGLU in the epilogue: s.ff2 = hidden * gelu(gate), 4C wide
-    f1.out_bf16 = s.ff2;
-    f1.ldo = 4 * C;
-    tc_gemm(s.a, P(stage, "tf.ff1.w"), L, 8 * C, C, f1, st);
-    TcArgs f2;
-    f2.bias = F(stage, "tf.ff2.b");
-    f2.residual = s.b;
-    f2.ldr = C;
-    f2.out_bf16 = s.b;
-    f2.ldo = C;
-    tc_gemm(s.ff2, P(stage, "tf.ff2.w"), L, C, 4 * C, f2, st);
+    tc_gemm(s.a, P(stage, "tf.proj_in.w"), BL, C, C, pi, st);  // h = s.b
+    for (int blk = 0; blk < depth; ++blk) {
+        const std::string pre = blk == 0 ? "tf." : "tf.b" + std::to_string(blk) + ".";
+        auto Pn = [&](const char* n) { return P(stage, (pre + n).c_str()); };
+        auto Fn = [&](const char* n) { return F(stage, (pre + n).c_str()); };
+        // self attention
+        layer_norm(s.b, BL, C, Fn("ln1.gamma"), Fn("ln1.beta"), 1e-5f, s.a, st);
+        TcArgs qk;
+        qk.out_bf16 = s.qkv;
+        qk.ldo = 3 * C;
+        tc_gemm(s.a, Pn("qkv.w"), BL, 3 * C, C, qk, st);
+        for (int b = 0; b < B; ++b) {
+            const bf16* q = s.qkv + b * 3 * img;
+            attention(s, q, 3 * C, q + C, 3 * C, q + 2 * C, 3 * C, nullptr, L, L, C, s.att + b * img, st);
+        }
+        TcArgs o1;
+        o1.bias = Fn("o1.b");
+        o1.residual = s.b;
+        o1.ldr = C;
+        o1.out_bf16 = s.b;  // in place: each element is read and written by one epilogue thread
+        o1.ldo = C;
+        tc_gemm(s.att, Pn("o1.w"), BL, C, C, o1, st);
+        // cross attention against the fixed context(s)
+        layer_norm(s.b, BL, C, Fn("ln2.gamma"), Fn("ln2.beta"), 1e-5f, s.a, st);
+        TcArgs q2;
+        q2.out_bf16 = s.qkv;
+        q2.ldo = C;
+        tc_gemm(s.a, Pn("q2.w"), BL, C, C, q2, st);
+        for (int b = 0; b < B; ++b)
+            attention(s, s.qkv + b * img, C, st_[stage].k2[blk * B + b], C, nullptr, 0, st_[stage].vt2[blk * B + b], L,
+                      sp.ctx_len, C, s.att + b * img, st);
+        TcArgs o2;
+        o2.bias = Fn("o2.b");
+        o2.residual = s.b;
+        o2.ldr = C;
+        o2.out_bf16 = s.b;
+        o2.ldo = C;
+        tc_gemm(s.att, Pn("o2.w"), BL, C, C, o2, st);
+        // GEGLU feed-forward
+        layer_norm(s.b, BL, C, Fn("ln3.gamma"), Fn("ln3.beta"), 1e-5f, s.a, st);
+        TcArgs f1;
+        f1.bias = Fn("ff1.b");
+        f1.act = 2;  // GEGLU in the epilogue: s.ff2 = hidden * gelu(gate), 4C wide
+        f1.out_bf16 = s.ff2;
+        f1.ldo = 4 * C;
+        tc_gemm(s.a, Pn("ff1.w"), BL, 8 * C, C, f1, st);
+        TcArgs f2;
+        f2.bias = Fn("ff2.b");
+        f2.residual = s.b;
+        f2.ldr = C;
+        f2.out_bf16 = s.b;
+        f2.ldo = C;
+        tc_gemm(s.ff2, Pn("ff2.w"), BL, C, 4 * C, f2, st);
+    }
     TcArgs po;
     po.bias = F(stage, "tf.proj_out.b");
     po.residual = x;
     po.ldr = C;
     po.out_bf16 = y;
     po.ldo = C;
-    tc_gemm(s.b, P(stage, "tf.proj_out.w"), L, C, C, po, st);
+    tc_gemm(s.b, P(stage, "tf.proj_out.w"), BL, C, C, po, st);
 }
 
 void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, bool latent_f64, cudaStream_t st) {
@@ -406,15 +480,18 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
     const UNetSpec& sp = d_.spec;
     const UStage& s = d_.st[stage - 1];
     UScratch& sc = scratch(st);
-    const int HW = s.H * s.W;
+    const int HW = s.H * s.W, B = sp.batch();
     switch (s.kind) {
         case kConvIn: {
             pack_latent(in[0].p, latent_f64, HW, sp.c_lat, 64, sc.a, st);
+            if (B == 2)  // both CFG images start from the same latent
+                CKD(cudaMemcpyAsync(sc.a + static_cast<long long>(HW) * 64, sc.a, static_cast<size_t>(HW) * 64 * 2,
+                                    cudaMemcpyDeviceToDevice, st));
             TcArgs a;
             a.bias = F(stage, "conv.b");
             a.out_bf16 = static_cast<bf16*>(y);
             a.ldo = s.cout;
-            tc_conv3x3(sc.a, P(stage, "conv.w"), 1, s.H, s.W, 64, s.cout, a, st);
+            tc_conv3x3(sc.a, P(stage, "conv.w"), B, s.H, s.W, 64, s.cout, a, st);
             break;
         }
         case kDown: {
@@ -423,56 +500,65 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
             a.out_bf16 = static_cast<bf16*>(y);
             a.ldo = s.cout;
             a.sub2 = 1;
-            tc_conv3x3(in[0].p, P(stage, "conv.w"), 1, s.H, s.W, s.cin, s.cout, a, st);
+            tc_conv3x3(in[0].p, P(stage, "conv.w"), B, s.H, s.W, s.cin, s.cout, a, st);
             break;
         }
         case kUp: {
-            upsample2x(static_cast<const bf16*>(in[0].p), 1, s.H, s.W, s.cin, sc.a, st);
+            upsample2x(static_cast<const bf16*>(in[0].p), B, s.H, s.W, s.cin, sc.a, st);
             TcArgs a;
             a.bias = F(stage, "conv.b");
             a.out_bf16 = static_cast<bf16*>(y);
             a.ldo = s.cout;
-            tc_conv3x3(sc.a, P(stage, "conv.w"), 1, 2 * s.H, 2 * s.W, s.cin, s.cout, a, st);
+            tc_conv3x3(sc.a, P(stage, "conv.w"), B, 2 * s.H, 2 * s.W, s.cin, s.cout, a, st);
             break;
         }
         case kOut: {
-            Cat2 x{static_cast<const bf16*>(in[0].p), s.cin, nullptr, 0};
-            group_norm(x, 1, HW, sp.groups, F(stage, "gn.gamma"), F(stage, "gn.beta"), 1e-5f, 1, sc.a, sc.gn, st);
+            if (latent_f64) throw std::invalid_argument("unet: the UNet family runs in f32 trajectory precision");
+            const bf16* x = static_cast<const bf16*>(in[0].p);
+            const long long img = static_cast<long long>(HW) * s.cin;
+            for (int b = 0; b < B; ++b)
+                group_norm(Cat2{x + b * img, s.cin, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn.gamma"),
+                           F(stage, "gn.beta"), 1e-5f, 1, sc.a + b * img, sc.gn, st);
             TcArgs a;
             a.bias = F(stage, "conv.b");
-            a.out_f32 = static_cast<float*>(y);
+            a.out_f32 = B == 1 ? static_cast<float*>(y) : sc.eps2;
             a.ldo = sp.c_lat;
             a.n_store = sp.c_lat;
-            if (latent_f64) throw std::invalid_argument("unet: the UNet family runs in f32 trajectory precision");
-            tc_conv3x3(sc.a, P(stage, "conv.w"), 1, s.H, s.W, s.cin, 32, a, st);
+            tc_conv3x3(sc.a, P(stage, "conv.w"), B, s.H, s.W, s.cin, 32, a, st);
+            if (B == 2) cfg_combine(sc.eps2, static_cast<long long>(HW) * sp.c_lat, sp.cfg_scale, static_cast<float*>(y), st);
             break;
         }
         default: {  // resnet (+ transformer)
             const int C = s.cout, cin = s.cin + s.cskip;
             const bf16* x0 = static_cast<const bf16*>(in[0].p);
             const bf16* x1 = s.cskip ? static_cast<const bf16*>(in[1].p) : nullptr;
-            Cat2 xc{x0, s.cin, x1, s.cskip};
-            group_norm(xc, 1, HW, sp.groups, F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.a, sc.gn, st);
+            const long long i0 = static_cast<long long>(HW) * s.cin, i1 = static_cast<long long>(HW) * s.cskip,
+                            ic = static_cast<long long>(HW) * cin, io = static_cast<long long>(HW) * C;
+            for (int b = 0; b < B; ++b)
+                group_norm(Cat2{x0 + b * i0, s.cin, x1 ? x1 + b * i1 : nullptr, s.cskip}, 1, HW, sp.groups,
+                           F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.a + b * ic, sc.gn, st);
             TcArgs c1;
             c1.bias = F(stage, "conv1.b");
             c1.chan_add = st_[stage].chan_add + static_cast<long long>(t) * C;
+            c1.chan_add_shared = 1;  // one timestep for every image of the batch
             c1.out_bf16 = sc.b;
             c1.ldo = C;
-            tc_conv3x3(sc.a, P(stage, "conv1.w"), 1, s.H, s.W, cin, C, c1, st);
-            Cat2 hc{sc.b, C, nullptr, 0};
-            group_norm(hc, 1, HW, sp.groups, F(stage, "gn2.gamma"), F(stage, "gn2.beta"), 1e-5f, 1, sc.a, sc.gn, st);
+            tc_conv3x3(sc.a, P(stage, "conv1.w"), B, s.H, s.W, cin, C, c1, st);
+            for (int b = 0; b < B; ++b)
+                group_norm(Cat2{sc.b + b * io, C, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn2.gamma"),
+                           F(stage, "gn2.beta"), 1e-5f, 1, sc.a + b * io, sc.gn, st);
             const bf16* res = x0;
             if (cin != C) {
                 const bf16* xin = x0;
                 if (s.cskip) {
-                    concat_channels(xc, HW, sc.c, st);
+                    concat_channels(Cat2{x0, s.cin, x1, s.cskip}, static_cast<long long>(B) * HW, sc.c, st);
                     xin = sc.c;
                 }
                 TcArgs sh;
                 sh.bias = F(stage, "short.b");
                 sh.out_bf16 = sc.r;
                 sh.ldo = C;
-                tc_gemm(xin, P(stage, "short.w"), HW, C, cin, sh, st);
+                tc_gemm(xin, P(stage, "short.w"), B * HW, C, cin, sh, st);
                 res = sc.r;
             }
             TcArgs c2;
@@ -482,7 +568,7 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
             bf16* out = s.attn ? sc.c : static_cast<bf16*>(y);
             c2.out_bf16 = out;
             c2.ldo = C;
-            tc_conv3x3(sc.a, P(stage, "conv2.w"), 1, s.H, s.W, C, C, c2, st);
+            tc_conv3x3(sc.a, P(stage, "conv2.w"), B, s.H, s.W, C, C, c2, st);
             if (s.attn) transformer(stage, sc.c, s.H, s.W, C, static_cast<bf16*>(y), st);
         }
     }
@@ -501,8 +587,9 @@ void UNetDevice::gemm_x(UScratch& s, const float* x, int M, int K, const char* w
 
 void UNetDevice::conv_x(UScratch& s, const float* x, int H, int W, int Cin, const char* wname, int stage, int Cout,
                         TcArgs a, cudaStream_t st) {
-    split3(x, static_cast<long long>(H) * W, Cin, Cin, Cin, 0, s.sa, st);
-    tc_conv3x3(s.sa, P(stage, wname), 1, H, W, 3 * Cin, Cout, a, st);
+    const int B = d_.spec.batch();
+    split3(x, static_cast<long long>(B) * H * W, Cin, Cin, Cin, 0, s.sa, st);
+    tc_conv3x3(s.sa, P(stage, wname), B, H, W, 3 * Cin, Cout, a, st);
 }
 
 // unfused attention, one 64-wide head at a time: S = Q'_h K'_h^T (K = 192), fp32 softmax in
@@ -535,62 +622,75 @@ void UNetDevice::attention_exact(UScratch& s, const float* q, long long ldq, con
 void UNetDevice::transformer_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st) {
     UScratch& s = scratch(st);
     const UNetSpec& sp = d_.spec;
-    const int L = H * W;
-    group_norm(Cat2F{x, C, nullptr, 0}, 1, L, sp.groups, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"), 1e-6f, 0,
-               s.fa, s.gn, st);
+    const int L = H * W, B = sp.batch(), BL = B * L, depth = d_.st[stage - 1].attn;
+    const long long img = static_cast<long long>(L) * C;
+    for (int b = 0; b < B; ++b)
+        group_norm(Cat2F{x + b * img, C, nullptr, 0}, 1, L, sp.groups, F(stage, "tf.gn.gamma"),
+                   F(stage, "tf.gn.beta"), 1e-6f, 0, s.fa + b * img, s.gn, st);
     TcArgs pi;
     pi.bias = F(stage, "tf.proj_in.b");
     pi.out_f32 = s.fb;
     pi.ldo = C;
-    gemm_x(s, s.fa, L, C, "tf.proj_in.w", stage, C, pi, st);  // h = fb
-    layer_norm(s.fb, L, C, F(stage, "tf.ln1.gamma"), F(stage, "tf.ln1.beta"), 1e-5f, s.fa, st);
-    TcArgs qk;
-    qk.out_f32 = s.fqkv;
-    qk.ldo = 3 * C;
-    gemm_x(s, s.fa, L, C, "tf.qkv.w", stage, 3 * C, qk, st);
-    split3(s.fqkv + C, L, C, 3LL * C, 64, 1, s.sk, st);
-    attention_exact(s, s.fqkv, 3LL * C, s.sk, s.fqkv + 2 * C, 3LL * C, nullptr, L, L, C, s.fatt, st);
-    TcArgs o1;
-    o1.bias = F(stage, "tf.o1.b");
-    o1.residual_f32 = s.fb;
-    o1.ldr = C;
-    o1.out_f32 = s.fb;
-    o1.ldo = C;
-    gemm_x(s, s.fatt, L, C, "tf.o1.w", stage, C, o1, st);
-    layer_norm(s.fb, L, C, F(stage, "tf.ln2.gamma"), F(stage, "tf.ln2.beta"), 1e-5f, s.fa, st);
-    TcArgs q2;
-    q2.out_f32 = s.fqkv;
-    q2.ldo = C;
-    gemm_x(s, s.fa, L, C, "tf.q2.w", stage, C, q2, st);
-    attention_exact(s, s.fqkv, C, st_[stage].k2, nullptr, 0, st_[stage].vt2, L, sp.ctx_len, C, s.fatt, st);
-    TcArgs o2;
-    o2.bias = F(stage, "tf.o2.b");
-    o2.residual_f32 = s.fb;
-    o2.ldr = C;
-    o2.out_f32 = s.fb;
-    o2.ldo = C;
-    gemm_x(s, s.fatt, L, C, "tf.o2.w", stage, C, o2, st);
-    layer_norm(s.fb, L, C, F(stage, "tf.ln3.gamma"), F(stage, "tf.ln3.beta"), 1e-5f, s.fa, st);
-    TcArgs f1;
-    f1.bias = F(stage, "tf.ff1.b");
-    f1.act = 2;  // GEGLU in the epilogue, fp32 out, 4C wide
-    f1.out_f32 = s.fff;
-    f1.ldo = 4 * C;
-    gemm_x(s, s.fa, L, C, "tf.ff1.w", stage, 8 * C, f1, st);
-    TcArgs f2;
-    f2.bias = F(stage, "tf.ff2.b");
-    f2.residual_f32 = s.fb;
-    f2.ldr = C;
-    f2.out_f32 = s.fb;
-    f2.ldo = C;
-    gemm_x(s, s.fff, L, 4 * C, "tf.ff2.w", stage, C, f2, st);
+    gemm_x(s, s.fa, BL, C, "tf.proj_in.w", stage, C, pi, st);  // h = fb
+    for (int blk = 0; blk < depth; ++blk) {
+        const std::string pre = blk == 0 ? "tf." : "tf.b" + std::to_string(blk) + ".";
+        const std::string n_qkv = pre + "qkv.w", n_o1 = pre + "o1.w", n_q2 = pre + "q2.w", n_o2 = pre + "o2.w",
+                          n_ff1 = pre + "ff1.w", n_ff2 = pre + "ff2.w";
+        auto Fn = [&](const char* n) { return F(stage, (pre + n).c_str()); };
+        layer_norm(s.fb, BL, C, Fn("ln1.gamma"), Fn("ln1.beta"), 1e-5f, s.fa, st);
+        TcArgs qk;
+        qk.out_f32 = s.fqkv;
+        qk.ldo = 3 * C;
+        gemm_x(s, s.fa, BL, C, n_qkv.c_str(), stage, 3 * C, qk, st);
+        for (int b = 0; b < B; ++b) {
+            const float* q = s.fqkv + b * 3 * img;
+            split3(q + C, L, C, 3LL * C, 64, 1, s.sk, st);
+            attention_exact(s, q, 3LL * C, s.sk, q + 2 * C, 3LL * C, nullptr, L, L, C, s.fatt + b * img, st);
+        }
+        TcArgs o1;
+        o1.bias = Fn("o1.b");
+        o1.residual_f32 = s.fb;
+        o1.ldr = C;
+        o1.out_f32 = s.fb;
+        o1.ldo = C;
+        gemm_x(s, s.fatt, BL, C, n_o1.c_str(), stage, C, o1, st);
+        layer_norm(s.fb, BL, C, Fn("ln2.gamma"), Fn("ln2.beta"), 1e-5f, s.fa, st);
+        TcArgs q2;
+        q2.out_f32 = s.fqkv;
+        q2.ldo = C;
+        gemm_x(s, s.fa, BL, C, n_q2.c_str(), stage, C, q2, st);
+        for (int b = 0; b < B; ++b)
+            attention_exact(s, s.fqkv + b * img, C, st_[stage].k2[blk * B + b], nullptr, 0,
+                            st_[stage].vt2[blk * B + b], L, sp.ctx_len, C, s.fatt + b * img, st);
+        TcArgs o2;
+        o2.bias = Fn("o2.b");
+        o2.residual_f32 = s.fb;
+        o2.ldr = C;
+        o2.out_f32 = s.fb;
+        o2.ldo = C;
+        gemm_x(s, s.fatt, BL, C, n_o2.c_str(), stage, C, o2, st);
+        layer_norm(s.fb, BL, C, Fn("ln3.gamma"), Fn("ln3.beta"), 1e-5f, s.fa, st);
+        TcArgs f1;
+        f1.bias = Fn("ff1.b");
+        f1.act = 2;  // GEGLU in the epilogue, fp32 out, 4C wide
+        f1.out_f32 = s.fff;
+        f1.ldo = 4 * C;
+        gemm_x(s, s.fa, BL, C, n_ff1.c_str(), stage, 8 * C, f1, st);
+        TcArgs f2;
+        f2.bias = Fn("ff2.b");
+        f2.residual_f32 = s.fb;
+        f2.ldr = C;
+        f2.out_f32 = s.fb;
+        f2.ldo = C;
+        gemm_x(s, s.fff, BL, 4 * C, n_ff2.c_str(), stage, C, f2, st);
+    }
     TcArgs po;
     po.bias = F(stage, "tf.proj_out.b");
     po.residual_f32 = x;
     po.ldr = C;
     po.out_f32 = y;
     po.ldo = C;
-    gemm_x(s, s.fb, L, C, "tf.proj_out.w", stage, C, po, st);
+    gemm_x(s, s.fb, BL, C, "tf.proj_out.w", stage, C, po, st);
 }
 
 void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, void* y, bool latent_f64,
@@ -598,11 +698,14 @@ void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, voi
     const UNetSpec& sp = d_.spec;
     const UStage& s = d_.st[stage - 1];
     UScratch& sc = scratch(st);
-    const int HW = s.H * s.W;
+    const int HW = s.H * s.W, B = sp.batch();
     float* yf = static_cast<float*>(y);
     switch (s.kind) {
         case kConvIn: {
             pack_latent_f32(in[0].p, latent_f64, HW, sp.c_lat, 64, sc.fa, st);
+            if (B == 2)
+                CKD(cudaMemcpyAsync(sc.fa + static_cast<long long>(HW) * 64, sc.fa, static_cast<size_t>(HW) * 64 * 4,
+                                    cudaMemcpyDeviceToDevice, st));
             TcArgs a;
             a.bias = F(stage, "conv.b");
             a.out_f32 = yf;
@@ -621,7 +724,7 @@ void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, voi
         }
         case kUp: {
             // nearest 2x of fp32 = the bf16 copy kernel over twice the channel count
-            upsample2x(static_cast<const bf16*>(in[0].p), 1, s.H, s.W, 2 * s.cin, reinterpret_cast<bf16*>(sc.fa), st);
+            upsample2x(static_cast<const bf16*>(in[0].p), B, s.H, s.W, 2 * s.cin, reinterpret_cast<bf16*>(sc.fa), st);
             TcArgs a;
             a.bias = F(stage, "conv.b");
             a.out_f32 = yf;
@@ -631,44 +734,53 @@ void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, voi
         }
         case kOut: {
             if (latent_f64) throw std::invalid_argument("unet: the UNet family runs in f32 trajectory precision");
-            Cat2F x{static_cast<const float*>(in[0].p), s.cin, nullptr, 0};
-            group_norm(x, 1, HW, sp.groups, F(stage, "gn.gamma"), F(stage, "gn.beta"), 1e-5f, 1, sc.fa, sc.gn, st);
+            const float* x = static_cast<const float*>(in[0].p);
+            const long long img = static_cast<long long>(HW) * s.cin;
+            for (int b = 0; b < B; ++b)
+                group_norm(Cat2F{x + b * img, s.cin, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn.gamma"),
+                           F(stage, "gn.beta"), 1e-5f, 1, sc.fa + b * img, sc.gn, st);
             TcArgs a;
             a.bias = F(stage, "conv.b");
-            a.out_f32 = yf;
+            a.out_f32 = B == 1 ? yf : sc.eps2;
             a.ldo = sp.c_lat;
             a.n_store = sp.c_lat;
             conv_x(sc, sc.fa, s.H, s.W, s.cin, "conv.w", stage, 32, a, st);
+            if (B == 2) cfg_combine(sc.eps2, static_cast<long long>(HW) * sp.c_lat, sp.cfg_scale, yf, st);
             break;
         }
         default: {  // resnet (+ transformer)
             const int C = s.cout, cin = s.cin + s.cskip;
             const float* x0 = static_cast<const float*>(in[0].p);
             const float* x1 = s.cskip ? static_cast<const float*>(in[1].p) : nullptr;
-            Cat2F xc{x0, s.cin, x1, s.cskip};
-            group_norm(xc, 1, HW, sp.groups, F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.fa, sc.gn, st);
+            const long long i0 = static_cast<long long>(HW) * s.cin, i1 = static_cast<long long>(HW) * s.cskip,
+                            ic = static_cast<long long>(HW) * cin, io = static_cast<long long>(HW) * C;
+            for (int b = 0; b < B; ++b)
+                group_norm(Cat2F{x0 + b * i0, s.cin, x1 ? x1 + b * i1 : nullptr, s.cskip}, 1, HW, sp.groups,
+                           F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.fa + b * ic, sc.gn, st);
             TcArgs c1;
             c1.bias = F(stage, "conv1.b");
             c1.chan_add = st_[stage].chan_add + static_cast<long long>(t) * C;
+            c1.chan_add_shared = 1;
             c1.out_f32 = sc.fb;
             c1.ldo = C;
             conv_x(sc, sc.fa, s.H, s.W, cin, "conv1.w", stage, C, c1, st);
-            group_norm(Cat2F{sc.fb, C, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn2.gamma"), F(stage, "gn2.beta"),
-                       1e-5f, 1, sc.fa, sc.gn, st);
+            for (int b = 0; b < B; ++b)
+                group_norm(Cat2F{sc.fb + b * io, C, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn2.gamma"),
+                           F(stage, "gn2.beta"), 1e-5f, 1, sc.fa + b * io, sc.gn, st);
             const float* res = x0;
             if (cin != C) {
                 const float* xin = x0;
                 if (s.cskip) {  // fp32 channel concat = the bf16 copy kernel over twice the channels
                     concat_channels(Cat2{reinterpret_cast<const bf16*>(x0), 2 * s.cin, reinterpret_cast<const bf16*>(x1),
                                          2 * s.cskip},
-                                    HW, reinterpret_cast<bf16*>(sc.fc), st);
+                                    static_cast<long long>(B) * HW, reinterpret_cast<bf16*>(sc.fc), st);
                     xin = sc.fc;
                 }
                 TcArgs sh;
                 sh.bias = F(stage, "short.b");
                 sh.out_f32 = sc.fr;
                 sh.ldo = C;
-                gemm_x(sc, xin, HW, cin, "short.w", stage, C, sh, st);
+                gemm_x(sc, xin, B * HW, cin, "short.w", stage, C, sh, st);
                 res = sc.fr;
             }
             TcArgs c2;

@@ -19,8 +19,9 @@ struct UDevStage {
     std::map<std::string, long long> bytes;
     float* chan_add = nullptr;       // [(T+1)][cout] time-embedding projection per t
     int chan_T = -1;
-    __nv_bfloat16* k2 = nullptr;     // cross-attention keys   [ctx_pad][C]
-    __nv_bfloat16* vt2 = nullptr;    // cross-attention values [C][ctx_pad] (transposed per head)
+    // cross-attention keys [ctx_pad][C] and values [C][ctx_pad] (transposed per head), per
+    // (transformer block, context): index block * batch + image
+    std::vector<__nv_bfloat16*> k2, vt2;
 };
 
 struct UScratch {
@@ -28,6 +29,7 @@ struct UScratch {
                   *ff = nullptr, *ff2 = nullptr, *P = nullptr, *VT = nullptr;
     float* S = nullptr;
     float2* gn = nullptr;
+    float* eps2 = nullptr;    // CFG: [eps_u | eps_c] before the guidance combine
     void* attn_ws = nullptr;  // split-KV workspace of the fused attention (zeroed counters)
     size_t attn_ws_bytes = 0;
     // ADX_F32 mode: fp32 activations and split-bf16 operands (3 columns per column)

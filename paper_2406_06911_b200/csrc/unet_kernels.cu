@@ -652,6 +652,13 @@ __global__ void transpose_f32_k(const float* V, long long ldv, int L, int Lpad, 
     }
 }
 
+__global__ void cfg_combine_k(const float* e, long long n, float scale, float* out) {
+    pdl_wait();
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = fmaf(scale, e[n + i] - e[i], e[i]);
+}
+
 int grid_for(long long n, int threads = 256) {
     return static_cast<int>(std::min<long long>((n + threads - 1) / threads, 148LL * 16));
 }
@@ -775,6 +782,11 @@ void split3(const float* x, long long rows, int cols, long long ldx, int g, int 
     if (cols % g || g % 8) throw std::invalid_argument("split3: group width must divide cols and be a multiple of 8");
     CKU(launch_pdl(split3_k, dim3(grid_for(rows * cols / 8)), dim3(256), 0, st, 1, x, rows, cols, ldx, g, pattern,
                    out));
+    CKU(cudaGetLastError());
+}
+
+void cfg_combine(const float* e, long long n, float scale, float* out, cudaStream_t st) {
+    CKU(launch_pdl(cfg_combine_k, dim3(grid_for(n)), dim3(256), 0, st, 1, e, n, scale, out));
     CKU(cudaGetLastError());
 }
 

@@ -36,6 +36,8 @@ void split3(const float* x, long long rows, int cols, long long ldx, int g, int 
 void softmax_rows_f32(float* S, long long lds, int rows, int valid, int padded, cudaStream_t st);
 // VT[d][k] = V[k * ldv + d] (k < L; 0 for L <= k < Lpad), fp32, hd rows
 void transpose_f32(const float* V, long long ldv, int L, int Lpad, int hd, float* VT, cudaStream_t st);
+// classifier-free guidance: out[i] = e[i] + scale * (e[n + i] - e[i])  (e = [eps_u | eps_c])
+void cfg_combine(const float* e, long long n, float scale, float* out, cudaStream_t st);
 // latent (fp32 / fp64, HWC) -> fp32 NHWC with cpad channels
 void pack_latent_f32(const void* x, bool f64, long long pixels, int c_lat, int cpad, float* out, cudaStream_t st);
 // scratch for group_norm; must be zeroed once at allocation (holds a self-resetting ticket counter)

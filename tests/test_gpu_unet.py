@@ -114,3 +114,45 @@ def test_unet_f32_async_invariants_bit_exact(small):
     ser, _ = adx.run_serial(plan, m, part, x, s, precision="f32")
     par, _ = adx.run_parallel(plan, m, part, x, s, plan.D, precision="f32")
     assert np.array_equal(ser.latent_matrix(), par.latent_matrix())  # parallel == serial
+
+
+# SDXL-shaped (BASELINE config 4) in miniature: 3 levels, transformer depths 0 / 2 / 3, mid
+# depth 2, classifier-free guidance (batch-2 stages, eps_u + s (eps_c - eps_u))
+SMALL_XL = dict(H=16, W=16, ch=(64, 128, 128), attn=(0, 2, 3), n_res=1, ctx_len=8, ctx_dim=64, temb_dim=128,
+                mid_attn=2, cfg=True, cfg_scale=4.0, seed=7)
+
+
+@pytest.fixture(scope="module")
+def small_xl():
+    m = adx.build_unet_denoiser(**SMALL_XL)
+    s = adx.build_schedule(3, 0.01, 0.15)
+    x = adx.Latent(O.random_normals(13, m.data_dim()).astype(np.float64), 3)
+    return m, s, x
+
+
+# guidance combines two evaluations with weights (1 - s, s): the bf16 error of the guided eps
+# grows with s (stated bf16-CFG tolerance TOL * s / 2); the f32 mode keeps the 1e-3 bar
+@pytest.mark.parametrize("prec,exact,tol", [("bf16", False, TOL * SMALL_XL["cfg_scale"] / 2), ("f32", True, TOL_F32)])
+def test_unet_xl_cfg_matches_oracle(small_xl, prec, exact, tol):
+    m, s, x = small_xl
+    traj = adx.sequential_denoise(m, x, s, precision=prec)
+    orc = UNetOracle(adx, m, exact=exact)
+    lat = x.values.astype(np.float64)
+    for k, t in enumerate(range(3, 0, -1)):
+        eps = orc.eval_full(lat if exact else traj.latents[k].values.astype(np.float32), t)
+        assert rel(traj.eps_used[k], eps) < tol, (prec, t, rel(traj.eps_used[k], eps))
+        lat = O.ddim_step(lat, np.asarray(eps, np.float64), t, s.alpha_bars)
+    if exact:
+        assert rel(traj.latents[-1].values, lat) < tol
+
+
+def test_unet_xl_cfg_async_invariants_bit_exact(small_xl):
+    m, s, x = small_xl
+    seq = adx.sequential_denoise(m, x, s)
+    part = adx.partition_balanced(m, 2)
+    full, _ = adx.run_serial(adx.plan_async(3, 3, 2, 1), m, part, x, s)
+    assert np.array_equal(full.latent_matrix(), seq.latent_matrix())
+    plan = adx.plan_async(3, 1, 2, 1)
+    ser, _ = adx.run_serial(plan, m, part, x, s)
+    par, _ = adx.run_parallel(plan, m, part, x, s, plan.D)
+    assert np.array_equal(ser.latent_matrix(), par.latent_matrix())

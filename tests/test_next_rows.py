@@ -172,3 +172,24 @@ def test_round_exchange_bytes_unet_stage_element_sizes():
     for x, y in zip(b16, b32):
         assert y - eps == 2 * (x - eps)  # stage payload doubles, the eps send does not
     assert adx.round_exchange_bytes(plan, part, m) == b16  # the UNet default precision is bf16
+
+
+def test_unet_sdxl_shape_and_cfg_build():
+    """SDXL-shaped builder (host only): transformer depth per level, CFG doubles the stage
+    widths (batch 2) and MACs but not the latent / eps, two contexts, per-block parameters."""
+    kw = dict(H=16, W=16, ch=(64, 128, 128), attn=(0, 2, 3), n_res=1, ctx_len=8, ctx_dim=64, temb_dim=128,
+              mid_attn=2, seed=7)
+    a = adx.build_unet_denoiser(**kw)
+    b = adx.build_unet_denoiser(cfg=True, **kw)
+    assert a.num_stages() == b.num_stages()
+    assert a.data_dim() == b.data_dim() == 16 * 16 * 4
+    assert b.total_macs() == 2 * a.total_macs()
+    assert adx.unet_context(a).shape == (1, 8, 64) and adx.unet_context(b).shape == (2, 8, 64)
+    assert np.array_equal(adx.unet_context(a)[0], adx.unet_context(b)[1])  # the conditional context
+    depths = {adx.unet_stage_info(a, i)["attn"] for i in range(1, a.num_stages() + 1)}
+    assert depths == {0, 2, 3}
+    st = next(i for i in range(1, a.num_stages() + 1) if adx.unet_stage_info(a, i)["attn"] == 3)
+    names = set(adx.unet_stage_params(a, st))
+    assert {"tf.qkv.w", "tf.b1.qkv.w", "tf.b2.ff2.w"} <= names and "tf.b3.qkv.w" not in names
+    with pytest.raises(adx.InvalidArgument):
+        adx.build_unet_denoiser(**dict(kw, ctx_dim=100))
