@@ -195,6 +195,22 @@ class UNetOracle:
         s = self.sp["cfg_scale"]
         return eu + np.float32(s) * (ec - eu) if not self.exact else eu + s * (ec - eu)
 
+    def timed_cascade(self, x, t, budget_s):
+        """bench CPU-baseline sample: run the conditional cascade stage by stage until
+        `budget_s` seconds have passed; returns (seconds, stages completed)"""
+        import time
+        self.ci = self.ctxs.shape[0] - 1
+        outs, cur, done = {}, x, []
+        t0 = time.perf_counter()
+        for s in range(1, self.L + 1):
+            ins = [cur] + [outs[pp] for pp, cc in self.links if cc == s]
+            cur = self.stage(s, ins, t)
+            outs[s] = cur
+            done.append(s)
+            if time.perf_counter() - t0 > budget_s:
+                break
+        return time.perf_counter() - t0, done
+
     def _cascade(self, x, t):
         outs = {}
         cur = x
