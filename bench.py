@@ -48,6 +48,11 @@ CONFIGS = {
     "c4": dict(family="unet", unet=dict(H=128, W=128, ch=(320, 640, 1280), attn=(0, 2, 10), mid_attn=10,
                                         ctx_dim=2048, cfg=True, cfg_scale=5.0),
                seed=0, T=50, beta=(0.01, 0.19), w=9, S=1, x_seed=12),
+    # BASELINE configs[4], AnimateDiff-shaped video UNet: SD-1.5-shaped spatial UNet
+    # (77x768 context) over 16 frames of a 64x64x4 latent, temporal-attention motion module after
+    # every resnet; one sample = one 16-frame clip
+    "c5": dict(family="unet", unet=dict(H=64, W=64, ctx_dim=768, frames=16, motion=True), seed=0, T=50,
+               beta=(0.01, 0.19), w=9, S=1, x_seed=12),
     # a small UNet for quick checks
     "c2s": dict(family="unet", unet=dict(H=32, W=32, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64,
                                          temb_dim=128), seed=0, T=10, beta=(0.01, 0.19), w=2, S=1, x_seed=12),
@@ -170,13 +175,16 @@ def config_block(args, cfg, N):
     w = cfg["w"] if N > 1 else cfg["T"]
     if cfg["family"] == "unet":
         u = dict(H=96, W=96, ch=(320, 640, 1280, 1280), attn=(1, 1, 1, 0), n_res=2, mid_attn=1, ctx_dim=1024,
-                 cfg=False, cfg_scale=5.0)
+                 cfg=False, cfg_scale=5.0, frames=1, motion=False)
         u.update(cfg["unet"])
-        shape = "SDXL-shaped" if u["cfg"] or max(u["attn"]) > 1 else "SD-2.1-shaped"
+        shape = ("AnimateDiff-shaped video" if u["motion"] else
+                 "SDXL-shaped" if u["cfg"] or max(u["attn"]) > 1 else "SD-2.1-shaped")
         desc = (f"{args.config}: {shape} UNet (random init; ch {list(u['ch'])}, {u['n_res']} resnets/level, "
                 f"transformer depth per level {list(u['attn'])} (mid {u['mid_attn']}), 77x{u['ctx_dim']} synthetic "
                 f"context{', CFG batch 2 scale %g' % u['cfg_scale'] if u['cfg'] else ''}), "
-                f"{u['H']}x{u['W']}x4 latent, T={cfg['T']} DDIM")
+                f"{u['H']}x{u['W']}x4 latent"
+                f"{' x %d frames (motion module after every resnet; one sample = one clip)' % u['frames'] if u['frames'] > 1 else ''}"
+                f", T={cfg['T']} DDIM")
         l2 = ("UNet weights (GBs of bf16) > 126 MB L2 (no flush needed)" if u["H"] >= 64 and u["ch"][0] >= 320 else
               "small UNet: weights and activations largely L2-resident")
     else:

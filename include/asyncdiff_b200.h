@@ -305,6 +305,8 @@ typedef struct {
     uint64_t seed;
     int cfg;              /* classifier-free guidance: batch-2 stages, eps_u + scale (eps_c - eps_u) */
     float cfg_scale;
+    int frames;           /* video: frames per sample (latent / eps = frames x H x W x c_lat); >= 1 */
+    int motion;           /* temporal-attention motion module after every resnet (frames >= 2) */
 } adx_unet_spec;
 int adx_model_build_unet(const adx_unet_spec* spec, adx_model** out);
 /* kind (0 conv_in, 1 res, 2 down, 3 up, 4 out, 5 mid res), cin, cskip, cout, H, W, attn */
@@ -326,6 +328,11 @@ int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint1
  * K [Lk x C] and V transposed VT [C x ldvt] (ldvt >= Lk, multiple of 8) */
 int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K,
                      const uint16_t* VT, int ldvt, uint16_t* out, int iters, double* ms_per_iter);
+/* video motion-module temporal attention: for every (pixel, 64-wide head) the frames
+ * attend to each other; qkv frame-major [frames][HW][3C] bf16 (q | k | v), out
+ * [frames][HW][C] bf16; 2 <= frames <= 32 */
+int adx_temporal_attention(int ordinal, int frames, int HW, int C, const uint16_t* qkv, uint16_t* out, int iters,
+                           double* ms_per_iter);
 /* conv3x3 / stride 1 / pad 1, NHWC: X [batch][H][W][Cin], Wt [Cout][9*Cin] ((r*3+s)*Cin+ci) */
 int adx_tc_conv3x3(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X,
                    const uint16_t* Wt, const float* bias, float* out, int iters, double* ms_per_iter);

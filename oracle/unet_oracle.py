@@ -150,7 +150,71 @@ class UNetOracle:
         y = self.r(self.lin(h, p["tf.proj_out.w"], p["tf.proj_out.b"]) + x.reshape(-1, C))
         return y.reshape(H, W, C)
 
+    def frame_pe(self, nf, C):
+        """frame positions of the motion modules (AnimateDiff's sinusoidal PositionalEncoding
+        layout: sin on even, cos on odd channels), (nf, C) float64"""
+        pe = np.zeros((nf, C))
+        w = np.exp(-(2.0 * np.arange(C // 2)) * math.log(10000.0) / C)
+        f = np.arange(nf)[:, None]
+        pe[:, 0::2] = np.sin(f * w)
+        pe[:, 1::2] = np.cos(f * w)
+        return pe
+
+    def temporal_attention(self, qkv, nf, HW, C):
+        """self-attention across the nf frames of every (pixel, 64-wide head); qkv frame-major
+        [nf*HW, 3C]; probabilities and the output accumulate unrounded (one rounding at the end)"""
+        def heads(x):
+            return x.reshape(nf, HW, C // 64, 64)
+        q, k, v = heads(qkv[:, :C]), heads(qkv[:, C:2 * C]), heads(qkv[:, 2 * C:])
+        S = np.einsum("fphd,gphd->phfg", q, k) * self.dt(0.125)
+        S = S - S.max(axis=-1, keepdims=True)
+        P = np.exp(S)
+        P = P / P.sum(axis=-1, keepdims=True)
+        return self.r(np.einsum("phfg,gphd->fphd", P, v).reshape(nf * HW, C))
+
+    def motion(self, stage, xs):
+        """temporal motion module over the frames (nf, H, W, C) of a stage output
+        (mirrors UNetDevice::motion in paper_2406_06911_b200/csrc/unet_dev.cu)"""
+        p = self.params[stage]
+        nf, H, W, C = xs.shape
+        a = np.stack([self.group_norm(xs[f], p["mm.gn.gamma"], p["mm.gn.beta"], 1e-6, False)
+                      for f in range(nf)]).reshape(-1, C)
+        h = self.r(self.lin(a, p["mm.proj_in.w"], p["mm.proj_in.b"]))
+        pe = self.frame_pe(nf, C)
+        for i in (1, 2):
+            pre = f"mm.a{i}."
+            n = self.layer_norm(h, p[pre + "ln.gamma"], p[pre + "ln.beta"])
+            w = p[pre + "qkv.w"]
+            pe_proj = (pe @ self.r(w).astype(np.float64).T).astype(self.dt)  # (a + pe) W^T, pe W^T per frame
+            qkv = self.r(self.lin(n, w) + np.repeat(pe_proj, H * W, axis=0))
+            att = self.temporal_attention(qkv, nf, H * W, C)
+            h = self.r(self.lin(att, p[pre + "o.w"], p[pre + "o.b"]) + h)
+        n = self.layer_norm(h, p["mm.ln3.gamma"], p["mm.ln3.beta"])
+        f = self.r(self.lin(n, p["mm.ff1.w"], p["mm.ff1.b"]))
+        g = self.r(f[:, :4 * C] * gelu(f[:, 4 * C:]))
+        h = self.r(self.lin(g, p["mm.ff2.w"], p["mm.ff2.b"]) + h)
+        y = self.r(self.lin(h, p["mm.proj_out.w"], p["mm.proj_out.b"]) + xs.reshape(-1, C))
+        return y.reshape(nf, H, W, C)
+
     def stage(self, stage, inputs, t):
+        """one stage; video models carry a leading frame axis (frames, H, W, C): the spatial
+        program runs frame by frame, then the motion module mixes the frames"""
+        nf = self.sp.get("frames", 1)
+        if nf == 1:
+            return self._stage1(stage, inputs, t)
+        kind = self.info[stage]["kind"]
+        if kind == "conv_in":
+            lat = np.asarray(inputs[0]).reshape(nf, -1)
+            return np.stack([self._stage1(stage, [lat[f]], t) for f in range(nf)])
+        outs = [self._stage1(stage, [x[f] for x in inputs], t) for f in range(nf)]
+        if kind == "out":
+            return np.concatenate(outs)
+        y = np.stack(outs)
+        if kind in ("res", "mid_res") and self.sp.get("motion"):
+            y = self.motion(stage, y)
+        return y
+
+    def _stage1(self, stage, inputs, t):
         """inputs: [main (H,W,C) bf16-valued, skip?]; stage 1 gets the fp32 latent (H*W*c_lat)."""
         info, p = self.info[stage], self.params[stage]
         kind = info["kind"]

@@ -98,7 +98,7 @@ EXPORTS = [
     "adx_rank_session_destroy", "adx_rank_session_run", "adx_rank_session_time", "adx_rank_session_kernel_count",
     "adx_model_save_checkpoint", "adx_model_load_checkpoint", "adx_plan_to_json", "adx_plan_from_json",
     "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes", "adx_tc_gemm", "adx_tc_conv3x3",
-    "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context", "adx_tc_attention",
+    "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context", "adx_tc_attention", "adx_temporal_attention",
     "adx_engine_profile_pass", "adx_tc_plan_override", "adx_engine_stage_times", "adx_partition_by_cost",
 ]
 
@@ -107,7 +107,8 @@ class adx_unet_spec(C.Structure):
     _fields_ = [("H", C.c_int), ("W", C.c_int), ("c_lat", C.c_int), ("n_levels", C.c_int), ("ch", C.c_int * 8),
                 ("attn", C.c_int * 8), ("n_res", C.c_int), ("head_dim", C.c_int), ("ctx_len", C.c_int),
                 ("ctx_dim", C.c_int), ("temb_dim", C.c_int), ("groups", C.c_int), ("mid_attn", C.c_int),
-                ("seed", C.c_uint64), ("cfg", C.c_int), ("cfg_scale", C.c_float)]
+                ("seed", C.c_uint64), ("cfg", C.c_int), ("cfg_scale", C.c_float), ("frames", C.c_int),
+                ("motion", C.c_int)]
 
 
 class adx_latency_report(C.Structure):
@@ -213,6 +214,7 @@ def lib():
         "adx_tc_gemm": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), i, P(C.c_float), i, i, P(d)]),
         "adx_tc_attention": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_uint16), i, P(C.c_uint16), i,
                                  P(d)]),
+        "adx_temporal_attention": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), i, P(d)]),
         "adx_tc_conv3x3": (i, [i, i, i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_float), i,
                                P(d)]),
         "adx_tc_plan_override": (i, [i, i]),

@@ -290,7 +290,8 @@ UNET_KINDS = {0: "conv_in", 1: "res", 2: "down", 3: "up", 4: "out", 5: "mid_res"
 def build_unet_denoiser(H: int = 96, W: int = 96, c_lat: int = 4, ch: Sequence[int] = (320, 640, 1280, 1280),
                         attn: Sequence[int] = (1, 1, 1, 0), n_res: int = 2, head_dim: int = 64, ctx_len: int = 77,
                         ctx_dim: int = 1024, temb_dim: int = 1280, groups: int = 32, mid_attn: int = 1,
-                        seed: int = 0, cfg: bool = False, cfg_scale: float = 5.0) -> LayeredDenoiser:
+                        seed: int = 0, cfg: bool = False, cfg_scale: float = 5.0, frames: int = 1,
+                        motion: bool = False) -> LayeredDenoiser:
     """UNet-shaped denoiser behind the reference's stage contract (defaults: the
     SD-2.1 UNet topology at a 96x96x4 latent, random init).  Works with every
     partition / plan / run entry point.  Engine precision "bf16" (the default for
@@ -303,7 +304,10 @@ def build_unet_denoiser(H: int = 96, W: int = 96, c_lat: int = 4, ch: Sequence[i
     (unconditional, conditional context) and the out stage returns
     eps_u + cfg_scale * (eps_c - eps_u).  SDXL-shaped example (BASELINE config 4):
     build_unet_denoiser(128, 128, ch=(320, 640, 1280), attn=(0, 2, 10), mid_attn=10,
-    ctx_dim=2048, cfg=True)."""
+    ctx_dim=2048, cfg=True).  frames > 1 with motion=True is the AnimateDiff-shaped video
+    UNet (BASELINE config 5): the latent holds every frame and a temporal-attention motion
+    module follows every resnet: build_unet_denoiser(64, 64, ctx_dim=768, frames=16,
+    motion=True)."""
     from ._lib import adx_unet_spec
     s = adx_unet_spec()
     s.H, s.W, s.c_lat, s.n_levels = H, W, c_lat, len(ch)
@@ -312,13 +316,15 @@ def build_unet_denoiser(H: int = 96, W: int = 96, c_lat: int = 4, ch: Sequence[i
     s.n_res, s.head_dim, s.ctx_len, s.ctx_dim = n_res, head_dim, ctx_len, ctx_dim
     s.temb_dim, s.groups, s.mid_attn, s.seed = temb_dim, groups, int(mid_attn), seed
     s.cfg, s.cfg_scale = int(bool(cfg)), float(cfg_scale)
+    s.frames, s.motion = int(frames), int(bool(motion))
     h = C.c_void_p()
     check(lib().adx_model_build_unet(C.byref(s), C.byref(h)))
     m = LayeredDenoiser(h.value)
     m.default_precision = "bf16"
     m.unet_spec = dict(H=H, W=W, c_lat=c_lat, ch=list(ch), attn=list(attn), n_res=n_res, head_dim=head_dim,
                        ctx_len=ctx_len, ctx_dim=ctx_dim, temb_dim=temb_dim, groups=groups, mid_attn=mid_attn,
-                       seed=seed, cfg=int(bool(cfg)), cfg_scale=float(cfg_scale))
+                       seed=seed, cfg=int(bool(cfg)), cfg_scale=float(cfg_scale), frames=int(frames),
+                       motion=int(bool(motion)))
     return m
 
 

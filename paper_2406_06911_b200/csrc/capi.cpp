@@ -10,6 +10,7 @@
 #include "tc_attn.cuh"
 #include "tc_gemm.cuh"
 #include "unet.hpp"
+#include "unet_kernels.cuh"
 
 #include <cuda_runtime.h>
 
@@ -930,6 +931,8 @@ int adx_model_build_unet(const adx_unet_spec* s, adx_model** out) {
         sp.seed = s->seed;
         sp.cfg = s->cfg ? 1 : 0;
         sp.cfg_scale = s->cfg_scale;
+        sp.frames = s->frames < 1 ? 1 : s->frames;
+        sp.motion = s->motion ? 1 : 0;
         *out = new adx_model{adx::build_unet_model(sp)};
     });
 }
@@ -1028,6 +1031,24 @@ int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const
         CKC(cudaDeviceSynchronize());
         if (iters > 0 && ms_per_iter) *ms_per_iter = time_graph_ms(run, iters);
         if (out) CKC(cudaMemcpy(out, o.p, static_cast<size_t>(L) * C * 2, cudaMemcpyDeviceToHost));
+    });
+}
+
+int adx_temporal_attention(int ordinal, int frames, int HW, int C, const uint16_t* qkv, uint16_t* out, int iters,
+                           double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        const size_t nin = static_cast<size_t>(frames) * HW * 3 * C, nout = static_cast<size_t>(frames) * HW * C;
+        DevBuf q(nin * 2), o(nout * 2);
+        CKC(cudaMemcpy(q.p, qkv, nin * 2, cudaMemcpyHostToDevice));
+        auto run = [&](cudaStream_t st) {
+            adx::temporal_attention(static_cast<const __nv_bfloat16*>(q.p), frames, HW, C,
+                                    static_cast<__nv_bfloat16*>(o.p), st);
+        };
+        run(0);
+        CKC(cudaDeviceSynchronize());
+        if (iters > 0 && ms_per_iter) *ms_per_iter = time_graph_ms(run, iters);
+        if (out) CKC(cudaMemcpy(out, o.p, nout * 2, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -166,6 +166,11 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float* v) {
     return make_uint4(w4[0], w4[1], w4[2], w4[3]);
 }
 
+// row of chan_add an output row reads: per row group (chan_add_rows), shared, or per image
+__device__ __forceinline__ long long chan_row(const TcArgs& p, long long m, int img) {
+    return p.chan_add_rows ? m / p.chan_add_rows : p.chan_add_shared ? 0 : img;
+}
+
 // fused epilogue on 16 accumulator columns [nb, nb + 16) of output row m
 __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int nb, float* v,
                                       const uint4* rpre = nullptr) {
@@ -180,7 +185,7 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int
             }
             if (p.chan_add) {
                 const float4 b = *reinterpret_cast<const float4*>(
-                    p.chan_add + static_cast<long long>(p.chan_add_shared ? 0 : img) * p.N + nb + j);
+                    p.chan_add + chan_row(p, m, img) * p.N + nb + j);
                 v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
             }
         }
@@ -221,7 +226,7 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int
         if (n >= nlim) continue;
         float x = v[j];
         if (p.bias) x += p.bias[n];
-        if (p.chan_add) x += p.chan_add[static_cast<long long>(p.chan_add_shared ? 0 : img) * p.N + n];
+        if (p.chan_add) x += p.chan_add[chan_row(p, m, img) * p.N + n];
         if (p.act == 1) x = silu(x);
         if (p.residual) x += __bfloat162float(p.residual[m * p.ldr + n]);
         if (p.residual_f32) x += p.residual_f32[m * p.ldr + n];

@@ -20,6 +20,8 @@ struct TcArgs {
     const float* bias = nullptr;          // [N]
     const float* chan_add = nullptr;      // [images][N] (e.g. time-embedding projection)
     int chan_add_shared = 0;              // 1: every image uses row 0 (CFG batch at one timestep)
+    int chan_add_rows = 0;                // > 0: output row m uses chan_add row m / chan_add_rows
+                                          //   (video: a per-frame add over frame-major GEMM rows)
     const __nv_bfloat16* residual = nullptr;
     const float* residual_f32 = nullptr;  // fp32 residual (ADX_F32 mode); at most one of the two
     long long ldr = 0;

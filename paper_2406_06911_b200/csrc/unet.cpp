@@ -28,6 +28,9 @@ Model build_unet_model(const UNetSpec& sp) {
         if (c % 64 || c % sp.groups) throw std::invalid_argument("unet: channels must be multiples of 64 and groups");
     if (sp.head_dim != 64) throw std::invalid_argument("unet: head_dim must be 64");
     if (sp.ctx_dim % 64) throw std::invalid_argument("unet: ctx_dim must be a multiple of 64");
+    if (sp.frames < 1 || sp.frames > 32) throw std::invalid_argument("unet: frames must be in 1..32");
+    if (sp.cfg && sp.frames > 1) throw std::invalid_argument("unet: CFG and video frames are exclusive");
+    if (sp.motion && sp.frames < 2) throw std::invalid_argument("unet: motion modules need frames >= 2");
     for (int a : sp.attn)
         if (a < 0) throw std::invalid_argument("unet: transformer depth must be >= 0");
     if (sp.mid_attn < 0) throw std::invalid_argument("unet: mid transformer depth must be >= 0");
@@ -118,6 +121,8 @@ Model build_unet_model(const UNetSpec& sp) {
     st.push_back(so);
     if (!skips.empty()) throw std::logic_error("unet: unbalanced skip stack");
 
+    for (UStage& s : st)
+        if (s.kind == kRes || s.kind == kMidRes) s.motion = sp.motion;
     // costs (implemented MACs: stride-2 convs run at full resolution)
     for (UStage& s : st) {
         const int cin = s.cin + s.cskip;
@@ -130,16 +135,19 @@ Model build_unet_model(const UNetSpec& sp) {
                 s.macs = conv_macs(s.H, s.W, s.cout, cin) + conv_macs(s.H, s.W, s.cout, s.cout) +
                          (cin != s.cout ? static_cast<long long>(s.H) * s.W * s.cout * cin : 0);
                 if (s.attn) s.macs += attn_macs(s.H * s.W, s.cout, sp.ctx_len, s.attn);
+                if (s.motion)  // proj_in / out, 2 x (QKV + out proj + F x F attention), GEGLU FF
+                    s.macs += static_cast<long long>(s.H) * s.W * s.cout *
+                              (2LL * s.cout + 2 * (4LL * s.cout + 2LL * sp.frames) + 12LL * s.cout);
         }
         s.macs *= sp.batch();
     }
     // synthetic cross-attention contexts ~ N(0, 1): the conditional one (seed 1000003) and,
     // with CFG, an unconditional one (seed 1000004) placed first (image 0)
     const size_t csz = static_cast<size_t>(sp.ctx_len) * sp.ctx_dim;
-    d->ctx.resize(csz * sp.batch());
+    d->ctx.resize(csz * sp.contexts());
     {
         Rng rng(mix_seed(sp.seed, 1000003));
-        for (size_t i = 0; i < csz; ++i) d->ctx[(sp.batch() - 1) * csz + i] = static_cast<float>(rng.normal());
+        for (size_t i = 0; i < csz; ++i) d->ctx[(sp.contexts() - 1) * csz + i] = static_cast<float>(rng.normal());
     }
     if (sp.cfg) {
         Rng rng(mix_seed(sp.seed, 1000004));
@@ -152,10 +160,11 @@ Model build_unet_model(const UNetSpec& sp) {
     m.L = static_cast<int>(st.size());
     m.E = 8;  // unused by the UNet stages; keeps the shared etab path trivial
     m.proj.assign(64, 0.0);
-    m.widths.push_back(sp.H * sp.W * sp.c_lat);
+    const int lat = sp.frames * sp.H * sp.W * sp.c_lat;  // latent / eps: every frame
+    m.widths.push_back(lat);
     for (size_t i = 0; i < st.size(); ++i) {
         const UStage& s = st[i];
-        m.widths.push_back(i + 1 == st.size() ? sp.H * sp.W * sp.c_lat : sp.batch() * s.cout * s.Ho() * s.Wo());
+        m.widths.push_back(i + 1 == st.size() ? lat : sp.batch() * s.cout * s.Ho() * s.Wo());
     }
     m.links = links;
     std::sort(m.links.begin(), m.links.end());
@@ -271,7 +280,7 @@ std::vector<UParam> unet_stage_params(const UNetDesc& d, int stage) {
                 lin_params(g, ps, "tf.proj_out", C, C, true);
                 // further transformer blocks (depth > 1), appended so depth-1 stages keep
                 // exactly the parameters above
-                for (int b = 1; b < s.attn; ++b) {
+                for (int b = 1; b < s.attn; ++b) {  // (motion-module parameters follow below)
                     const std::string pre = "tf.b" + std::to_string(b) + ".";
                     norm_params(g, ps, pre + "ln1", C);
                     lin_params(g, ps, pre + "qkv", 3 * C, C, false);
@@ -285,6 +294,20 @@ std::vector<UParam> unet_stage_params(const UNetDesc& d, int stage) {
                     lin_params(g, ps, pre + "ff1", 8 * C, C, true);
                     lin_params(g, ps, pre + "ff2", C, 4 * C, true);
                 }
+            }
+            if (s.motion) {  // temporal motion module: attention across the frames of each pixel
+                norm_params(g, ps, "mm.gn", C);
+                lin_params(g, ps, "mm.proj_in", C, C, true);
+                for (int a = 1; a <= 2; ++a) {
+                    const std::string pre = "mm.a" + std::to_string(a) + ".";
+                    norm_params(g, ps, pre + "ln", C);
+                    lin_params(g, ps, pre + "qkv", 3 * C, C, false);
+                    lin_params(g, ps, pre + "o", C, C, true);
+                }
+                norm_params(g, ps, "mm.ln3", C);
+                lin_params(g, ps, "mm.ff1", 8 * C, C, true);
+                lin_params(g, ps, "mm.ff2", C, 4 * C, true);
+                lin_params(g, ps, "mm.proj_out", C, C, true);
             }
         }
     }

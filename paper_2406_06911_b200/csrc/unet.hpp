@@ -31,7 +31,13 @@ struct UNetSpec {
     // eps_u + cfg_scale * (eps_c - eps_u); the latent / eps stay one image
     int cfg = 0;
     float cfg_scale = 5.0f;
-    int batch() const { return cfg ? 2 : 1; }
+    // video (AnimateDiff-shaped): `frames` latents per sample (the latent / eps are
+    // frames x H x W x c_lat) and, with motion = 1, a temporal-attention motion module after
+    // every resnet (attention across the frames of each pixel); CFG and frames exclusive
+    int frames = 1;
+    int motion = 0;
+    int batch() const { return cfg ? 2 : frames; }     // images every stage processes
+    int contexts() const { return cfg ? 2 : 1; }        // text contexts (video frames share one)
 };
 
 enum UKind { kConvIn = 0, kRes = 1, kDown = 2, kUp = 3, kOut = 4, kMidRes = 5 };
@@ -43,6 +49,7 @@ struct UStage {
     int cout = 0;
     int H = 0, W = 0; // input spatial size (DOWN halves it, UP doubles it)
     int attn = 0;     // depth of the following SpatialTransformer (RES / MidRes; 0: none)
+    int motion = 0;   // followed by a temporal motion module (RES / MidRes, video models)
     long long macs = 0;
     int Ho() const { return kind == kDown ? H / 2 : kind == kUp ? 2 * H : H; }
     int Wo() const { return kind == kDown ? W / 2 : kind == kUp ? 2 * W : W; }

@@ -73,6 +73,13 @@ std::vector<uint16_t> split_b(const std::vector<float>& w, long long rows, int K
     return out;
 }
 
+float bf16_to_float(uint16_t b) {
+    const uint32_t u = static_cast<uint32_t>(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
 bool ends_with(const std::string& s, const char* suf) {
     const size_t n = std::strlen(suf);
     return s.size() >= n && s.compare(s.size() - n, n, suf) == 0;
@@ -133,6 +140,7 @@ UNetDevice::~UNetDevice() {
         cudaFree(s.chan_add);
         for (auto* q : s.k2) cudaFree(q);
         for (auto* q : s.vt2) cudaFree(q);
+        for (auto* q : s.pe_proj) cudaFree(q);
     }
     for (auto& kv : scratch_) {
         UScratch& s = kv.second;
@@ -209,7 +217,7 @@ void UNetDevice::ensure_stage(int stage) {
     if (s.attn) {
         // cross-attention K2 = ctx . Wk2^T and V2^T = Wv2 . ctx^T are constant per run: computed
         // once per (block, context), context length padded to a multiple of 64 (zeros)
-        const int C = s.cout, Lc = sp.ctx_len, Lp = pad64(Lc), Dc = sp.ctx_dim, B = sp.batch();
+        const int C = s.cout, Lc = sp.ctx_len, Lp = pad64(Lc), Dc = sp.ctx_dim, B = sp.contexts();
         const size_t csz = static_cast<size_t>(Lc) * Dc;
         for (int b = 0; b < s.attn; ++b) {
             const std::string pre = b == 0 ? "tf." : "tf.b" + std::to_string(b) + ".";
@@ -243,6 +251,39 @@ void UNetDevice::ensure_stage(int stage) {
                     ctx_projection(ctx, Lc, Dc, *wk, *wv, C, Lp, ds.k2.back(), ds.vt2.back());
                 }
             }
+        }
+    }
+    if (s.motion) {
+        // frame positions (sinusoidal, AnimateDiff's PositionalEncoding layout: sin on even,
+        // cos on odd channels) are added to the normed tokens before the QKV projection:
+        // (a + pe) W^T = a W^T + pe W^T, the second term precomputed here with the weights the
+        // device multiplies by (bf16-rounded, or fp32 in the ADX_F32 mode)
+        const int C = s.cout, F = sp.frames;
+        std::vector<double> pe(static_cast<size_t>(F) * C);
+        for (int f = 0; f < F; ++f)
+            for (int i = 0; i < C / 2; ++i) {
+                const double w = std::exp(-(2.0 * i) * std::log(10000.0) / C);
+                pe[static_cast<size_t>(f) * C + 2 * i] = std::sin(f * w);
+                pe[static_cast<size_t>(f) * C + 2 * i + 1] = std::cos(f * w);
+            }
+        for (int a = 1; a <= 2; ++a) {
+            const std::string nm = "mm.a" + std::to_string(a) + ".qkv.w";
+            const std::vector<float>* w = nullptr;
+            for (auto& p : ps)
+                if (p.name == nm) w = &p.data;
+            if (!w) throw std::logic_error("unet: missing " + nm);
+            std::vector<float> proj(static_cast<size_t>(F) * 3 * C);
+            for (int f = 0; f < F; ++f)
+                for (int n = 0; n < 3 * C; ++n) {
+                    double acc = 0.0;
+                    for (int c = 0; c < C; ++c) {
+                        float wv = (*w)[static_cast<size_t>(n) * C + c];
+                        if (!exact_) wv = bf16_to_float(to_bf16_bits(wv));
+                        acc += pe[static_cast<size_t>(f) * C + c] * wv;
+                    }
+                    proj[static_cast<size_t>(f) * 3 * C + n] = static_cast<float>(acc);
+                }
+            ds.pe_proj.push_back(static_cast<float*>(upload_f32(proj)));
         }
     }
     ds.ready = true;
@@ -279,11 +320,14 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
         const size_t hw = static_cast<size_t>(s.H) * s.W;
         act = std::max({act, hw * (s.cin + s.cskip), static_cast<size_t>(s.Ho()) * s.Wo() * s.cout, hw * 64,
                         4 * hw * s.cin});
-        gn = std::max({gn, group_norm_scratch_bytes(1, static_cast<int>(4 * hw), sp.groups, s.cin + s.cskip + s.cout)});
+        gn = std::max({gn, group_norm_scratch_bytes(sp.batch(), static_cast<int>(4 * hw), sp.groups,
+                                                    s.cin + s.cskip + s.cout)});
+        if (s.attn || s.motion) {
+            qkv = std::max(qkv, hw * 3 * s.cout);
+            ff = std::max(ff, hw * 8 * s.cout);
+        }
         if (s.attn) {
             const size_t L = hw, Lp = pad64(static_cast<int>(L));
-            qkv = std::max(qkv, L * 3 * s.cout);
-            ff = std::max(ff, L * 8 * s.cout);
             S = std::max(S, L * std::max(Lp, static_cast<size_t>(pad64(sp.ctx_len))));
             vt = std::max(vt, static_cast<size_t>(s.cout) * Lp);
         }
@@ -316,7 +360,7 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
         if (stg.attn) {
             const int L = stg.H * stg.W;
             s.attn_ws_bytes = std::max({s.attn_ws_bytes, tc_attention_ws_bytes(L, L, stg.cout),
-                                        tc_attention_ws_bytes(L, sp.ctx_len, stg.cout)});
+                                        tc_attention_ws_bytes(sp.batch() * L, sp.ctx_len, stg.cout)});
         }
     if (s.attn_ws_bytes) {
         s.attn_ws = al(s.attn_ws_bytes);
@@ -327,10 +371,13 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
         for (const UStage& st : d_.st) {
             const size_t hw = static_cast<size_t>(st.H) * st.W;
             spl = std::max({spl, 3 * 4 * hw * st.cin, 3 * hw * (st.cin + st.cskip), 3 * hw * st.cout});
+            if (st.attn || st.motion) {
+                spl = std::max(spl, 3 * hw * 4 * st.cout);
+                ffx = std::max(ffx, hw * 4 * st.cout);
+            }
             if (st.attn) {
                 const size_t L = hw, Lp = pad64(static_cast<int>(L));
-                spl = std::max({spl, 3 * L * 4 * st.cout, 3 * L * Lp});
-                ffx = std::max(ffx, L * 4 * st.cout);
+                spl = std::max(spl, 3 * L * Lp);
                 vtx = std::max(vtx, 64 * Lp);
             }
         }
@@ -395,6 +442,128 @@ void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16
     }
 }
 
+template <typename T>
+void UNetDevice::gn_images(const Cat2T<T>& x, int HW, const float* gamma, const float* beta, float eps, int act,
+                           T* out, UScratch& s, cudaStream_t st) {
+    const int B = d_.spec.batch();
+    if (B > 2) {  // video frames: one batched stats + apply pair instead of B fused launches
+        group_norm(x, B, HW, d_.spec.groups, gamma, beta, eps, act, out, s.gn, st);
+        return;
+    }
+    const long long i0 = static_cast<long long>(HW) * x.c0, i1 = static_cast<long long>(HW) * x.c1;
+    for (int b = 0; b < B; ++b)
+        group_norm(Cat2T<T>{x.p0 + b * i0, x.c0, x.p1 ? x.p1 + b * i1 : nullptr, x.c1}, 1, HW, d_.spec.groups, gamma,
+                   beta, eps, act, out + b * (i0 + i1), s.gn, st);
+}
+
+// Temporal motion module (video UNets, AnimateDiff-shaped): GN (per frame) -> proj_in ->
+// 2 x [LN -> +frame positions -> self-attention across the frames of each pixel -> out
+// proj + residual] -> LN -> GEGLU FF + residual -> proj_out + x.  Tokens are frame-major
+// [F][HW][C]; the QKV GEMMs add PE . W^T per frame in the epilogue (chan_add_rows = HW).
+void UNetDevice::motion(int stage, const bf16* x, int H, int W, int C, bf16* y, cudaStream_t st) {
+    UScratch& s = scratch(st);
+    const UNetSpec& sp = d_.spec;
+    const int L = H * W, NF = sp.frames, FL = NF * L;
+    gn_images(Cat2{x, C, nullptr, 0}, L, F(stage, "mm.gn.gamma"), F(stage, "mm.gn.beta"), 1e-6f, 0, s.a, s, st);
+    TcArgs pi;
+    pi.bias = F(stage, "mm.proj_in.b");
+    pi.out_bf16 = s.b;
+    pi.ldo = C;
+    tc_gemm(s.a, P(stage, "mm.proj_in.w"), FL, C, C, pi, st);  // h = s.b
+    for (int a = 1; a <= 2; ++a) {
+        const std::string pre = "mm.a" + std::to_string(a) + ".";
+        layer_norm(s.b, FL, C, F(stage, (pre + "ln.gamma").c_str()), F(stage, (pre + "ln.beta").c_str()), 1e-5f, s.a,
+                   st);
+        TcArgs qk;
+        qk.chan_add = st_[stage].pe_proj[a - 1];
+        qk.chan_add_rows = L;  // row f * HW + p adds frame f's projected position
+        qk.out_bf16 = s.qkv;
+        qk.ldo = 3 * C;
+        tc_gemm(s.a, P(stage, (pre + "qkv.w").c_str()), FL, 3 * C, C, qk, st);
+        temporal_attention(s.qkv, NF, L, C, s.att, st);
+        TcArgs o;
+        o.bias = F(stage, (pre + "o.b").c_str());
+        o.residual = s.b;
+        o.ldr = C;
+        o.out_bf16 = s.b;
+        o.ldo = C;
+        tc_gemm(s.att, P(stage, (pre + "o.w").c_str()), FL, C, C, o, st);
+    }
+    layer_norm(s.b, FL, C, F(stage, "mm.ln3.gamma"), F(stage, "mm.ln3.beta"), 1e-5f, s.a, st);
+    TcArgs f1;
+    f1.bias = F(stage, "mm.ff1.b");
+    f1.act = 2;
+    f1.out_bf16 = s.ff2;
+    f1.ldo = 4 * C;
+    tc_gemm(s.a, P(stage, "mm.ff1.w"), FL, 8 * C, C, f1, st);
+    TcArgs f2;
+    f2.bias = F(stage, "mm.ff2.b");
+    f2.residual = s.b;
+    f2.ldr = C;
+    f2.out_bf16 = s.b;
+    f2.ldo = C;
+    tc_gemm(s.ff2, P(stage, "mm.ff2.w"), FL, C, 4 * C, f2, st);
+    TcArgs po;
+    po.bias = F(stage, "mm.proj_out.b");
+    po.residual = x;
+    po.ldr = C;
+    po.out_bf16 = y;
+    po.ldo = C;
+    tc_gemm(s.b, P(stage, "mm.proj_out.w"), FL, C, C, po, st);
+}
+
+void UNetDevice::motion_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st) {
+    UScratch& s = scratch(st);
+    const UNetSpec& sp = d_.spec;
+    const int L = H * W, NF = sp.frames, FL = NF * L;
+    gn_images(Cat2F{x, C, nullptr, 0}, L, F(stage, "mm.gn.gamma"), F(stage, "mm.gn.beta"), 1e-6f, 0, s.fa, s, st);
+    TcArgs pi;
+    pi.bias = F(stage, "mm.proj_in.b");
+    pi.out_f32 = s.fb;
+    pi.ldo = C;
+    gemm_x(s, s.fa, FL, C, "mm.proj_in.w", stage, C, pi, st);
+    for (int a = 1; a <= 2; ++a) {
+        const std::string pre = "mm.a" + std::to_string(a) + ".", n_qkv = pre + "qkv.w", n_o = pre + "o.w";
+        layer_norm(s.fb, FL, C, F(stage, (pre + "ln.gamma").c_str()), F(stage, (pre + "ln.beta").c_str()), 1e-5f,
+                   s.fa, st);
+        TcArgs qk;
+        qk.chan_add = st_[stage].pe_proj[a - 1];
+        qk.chan_add_rows = L;
+        qk.out_f32 = s.fqkv;
+        qk.ldo = 3 * C;
+        gemm_x(s, s.fa, FL, C, n_qkv.c_str(), stage, 3 * C, qk, st);
+        temporal_attention(s.fqkv, NF, L, C, s.fatt, st);
+        TcArgs o;
+        o.bias = F(stage, (pre + "o.b").c_str());
+        o.residual_f32 = s.fb;
+        o.ldr = C;
+        o.out_f32 = s.fb;
+        o.ldo = C;
+        gemm_x(s, s.fatt, FL, C, n_o.c_str(), stage, C, o, st);
+    }
+    layer_norm(s.fb, FL, C, F(stage, "mm.ln3.gamma"), F(stage, "mm.ln3.beta"), 1e-5f, s.fa, st);
+    TcArgs f1;
+    f1.bias = F(stage, "mm.ff1.b");
+    f1.act = 2;
+    f1.out_f32 = s.fff;
+    f1.ldo = 4 * C;
+    gemm_x(s, s.fa, FL, C, "mm.ff1.w", stage, 8 * C, f1, st);
+    TcArgs f2;
+    f2.bias = F(stage, "mm.ff2.b");
+    f2.residual_f32 = s.fb;
+    f2.ldr = C;
+    f2.out_f32 = s.fb;
+    f2.ldo = C;
+    gemm_x(s, s.fff, FL, 4 * C, "mm.ff2.w", stage, C, f2, st);
+    TcArgs po;
+    po.bias = F(stage, "mm.proj_out.b");
+    po.residual_f32 = x;
+    po.ldr = C;
+    po.out_f32 = y;
+    po.ldo = C;
+    gemm_x(s, s.fb, FL, C, "mm.proj_out.w", stage, C, po, st);
+}
+
 // SpatialTransformer: GN -> proj_in -> [LN self-attn] -> [LN cross-attn] -> [LN GEGLU FF] -> proj_out + x
 // SpatialTransformer: GN -> proj_in -> depth x ([LN self-attn] [LN cross-attn] [LN GEGLU FF])
 // -> proj_out + x.  With CFG the batch holds 2 images: GEMMs / LN run over both, GN and
@@ -404,9 +573,7 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
     const UNetSpec& sp = d_.spec;
     const int L = H * W, B = sp.batch(), BL = B * L, depth = d_.st[stage - 1].attn;
     const long long img = static_cast<long long>(L) * C;
-    for (int b = 0; b < B; ++b)
-        group_norm(Cat2{x + b * img, C, nullptr, 0}, 1, L, sp.groups, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"),
-                   1e-6f, 0, s.a + b * img, s.gn, st);
+    gn_images(Cat2{x, C, nullptr, 0}, L, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"), 1e-6f, 0, s.a, s, st);
     TcArgs pi;
     pi.bias = F(stage, "tf.proj_in.b");
     pi.out_bf16 = s.b;
@@ -439,9 +606,13 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
         q2.out_bf16 = s.qkv;
         q2.ldo = C;
         tc_gemm(s.a, Pn("q2.w"), BL, C, C, q2, st);
-        for (int b = 0; b < B; ++b)
-            attention(s, s.qkv + b * img, C, st_[stage].k2[blk * B + b], C, nullptr, 0, st_[stage].vt2[blk * B + b], L,
-                      sp.ctx_len, C, s.att + b * img, st);
+        if (sp.contexts() == 1)  // one shared context: every image's queries in one launch
+            attention(s, s.qkv, C, st_[stage].k2[blk], C, nullptr, 0, st_[stage].vt2[blk], BL, sp.ctx_len, C, s.att,
+                      st);
+        else
+            for (int b = 0; b < B; ++b)
+                attention(s, s.qkv + b * img, C, st_[stage].k2[blk * B + b], C, nullptr, 0,
+                          st_[stage].vt2[blk * B + b], L, sp.ctx_len, C, s.att + b * img, st);
         TcArgs o2;
         o2.bias = Fn("o2.b");
         o2.residual = s.b;
@@ -483,8 +654,8 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
     const int HW = s.H * s.W, B = sp.batch();
     switch (s.kind) {
         case kConvIn: {
-            pack_latent(in[0].p, latent_f64, HW, sp.c_lat, 64, sc.a, st);
-            if (B == 2)  // both CFG images start from the same latent
+            pack_latent(in[0].p, latent_f64, static_cast<long long>(sp.frames) * HW, sp.c_lat, 64, sc.a, st);
+            if (sp.cfg)  // both CFG images start from the same latent (video: one latent per frame)
                 CKD(cudaMemcpyAsync(sc.a + static_cast<long long>(HW) * 64, sc.a, static_cast<size_t>(HW) * 64 * 2,
                                     cudaMemcpyDeviceToDevice, st));
             TcArgs a;
@@ -515,28 +686,23 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
         case kOut: {
             if (latent_f64) throw std::invalid_argument("unet: the UNet family runs in f32 trajectory precision");
             const bf16* x = static_cast<const bf16*>(in[0].p);
-            const long long img = static_cast<long long>(HW) * s.cin;
-            for (int b = 0; b < B; ++b)
-                group_norm(Cat2{x + b * img, s.cin, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn.gamma"),
-                           F(stage, "gn.beta"), 1e-5f, 1, sc.a + b * img, sc.gn, st);
+            gn_images(Cat2{x, s.cin, nullptr, 0}, HW, F(stage, "gn.gamma"), F(stage, "gn.beta"), 1e-5f, 1, sc.a, sc, st);
             TcArgs a;
             a.bias = F(stage, "conv.b");
-            a.out_f32 = B == 1 ? static_cast<float*>(y) : sc.eps2;
+            a.out_f32 = sp.cfg ? sc.eps2 : static_cast<float*>(y);  // video: every frame's eps
             a.ldo = sp.c_lat;
             a.n_store = sp.c_lat;
             tc_conv3x3(sc.a, P(stage, "conv.w"), B, s.H, s.W, s.cin, 32, a, st);
-            if (B == 2) cfg_combine(sc.eps2, static_cast<long long>(HW) * sp.c_lat, sp.cfg_scale, static_cast<float*>(y), st);
+            if (sp.cfg)
+                cfg_combine(sc.eps2, static_cast<long long>(HW) * sp.c_lat, sp.cfg_scale, static_cast<float*>(y), st);
             break;
         }
         default: {  // resnet (+ transformer)
             const int C = s.cout, cin = s.cin + s.cskip;
             const bf16* x0 = static_cast<const bf16*>(in[0].p);
             const bf16* x1 = s.cskip ? static_cast<const bf16*>(in[1].p) : nullptr;
-            const long long i0 = static_cast<long long>(HW) * s.cin, i1 = static_cast<long long>(HW) * s.cskip,
-                            ic = static_cast<long long>(HW) * cin, io = static_cast<long long>(HW) * C;
-            for (int b = 0; b < B; ++b)
-                group_norm(Cat2{x0 + b * i0, s.cin, x1 ? x1 + b * i1 : nullptr, s.cskip}, 1, HW, sp.groups,
-                           F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.a + b * ic, sc.gn, st);
+            gn_images(Cat2{x0, s.cin, x1, s.cskip}, HW, F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.a, sc,
+                      st);
             TcArgs c1;
             c1.bias = F(stage, "conv1.b");
             c1.chan_add = st_[stage].chan_add + static_cast<long long>(t) * C;
@@ -544,9 +710,7 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
             c1.out_bf16 = sc.b;
             c1.ldo = C;
             tc_conv3x3(sc.a, P(stage, "conv1.w"), B, s.H, s.W, cin, C, c1, st);
-            for (int b = 0; b < B; ++b)
-                group_norm(Cat2{sc.b + b * io, C, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn2.gamma"),
-                           F(stage, "gn2.beta"), 1e-5f, 1, sc.a + b * io, sc.gn, st);
+            gn_images(Cat2{sc.b, C, nullptr, 0}, HW, F(stage, "gn2.gamma"), F(stage, "gn2.beta"), 1e-5f, 1, sc.a, sc, st);
             const bf16* res = x0;
             if (cin != C) {
                 const bf16* xin = x0;
@@ -565,11 +729,13 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
             c2.bias = F(stage, "conv2.b");
             c2.residual = res;
             c2.ldr = C;
-            bf16* out = s.attn ? sc.c : static_cast<bf16*>(y);
+            bf16* out = s.attn || s.motion ? sc.c : static_cast<bf16*>(y);
             c2.out_bf16 = out;
             c2.ldo = C;
             tc_conv3x3(sc.a, P(stage, "conv2.w"), B, s.H, s.W, C, C, c2, st);
-            if (s.attn) transformer(stage, sc.c, s.H, s.W, C, static_cast<bf16*>(y), st);
+            // resnet -> [spatial transformer] -> [temporal motion module]
+            if (s.attn) transformer(stage, sc.c, s.H, s.W, C, s.motion ? sc.r : static_cast<bf16*>(y), st);
+            if (s.motion) motion(stage, s.attn ? sc.r : sc.c, s.H, s.W, C, static_cast<bf16*>(y), st);
         }
     }
 }
@@ -624,9 +790,7 @@ void UNetDevice::transformer_exact(int stage, const float* x, int H, int W, int 
     const UNetSpec& sp = d_.spec;
     const int L = H * W, B = sp.batch(), BL = B * L, depth = d_.st[stage - 1].attn;
     const long long img = static_cast<long long>(L) * C;
-    for (int b = 0; b < B; ++b)
-        group_norm(Cat2F{x + b * img, C, nullptr, 0}, 1, L, sp.groups, F(stage, "tf.gn.gamma"),
-                   F(stage, "tf.gn.beta"), 1e-6f, 0, s.fa + b * img, s.gn, st);
+    gn_images(Cat2F{x, C, nullptr, 0}, L, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"), 1e-6f, 0, s.fa, s, st);
     TcArgs pi;
     pi.bias = F(stage, "tf.proj_in.b");
     pi.out_f32 = s.fb;
@@ -659,9 +823,11 @@ void UNetDevice::transformer_exact(int stage, const float* x, int H, int W, int 
         q2.out_f32 = s.fqkv;
         q2.ldo = C;
         gemm_x(s, s.fa, BL, C, n_q2.c_str(), stage, C, q2, st);
-        for (int b = 0; b < B; ++b)
-            attention_exact(s, s.fqkv + b * img, C, st_[stage].k2[blk * B + b], nullptr, 0,
-                            st_[stage].vt2[blk * B + b], L, sp.ctx_len, C, s.fatt + b * img, st);
+        for (int b = 0; b < B; ++b) {
+            const int ci = sp.contexts() == 1 ? blk : blk * B + b;  // video frames share one context
+            attention_exact(s, s.fqkv + b * img, C, st_[stage].k2[ci], nullptr, 0, st_[stage].vt2[ci], L, sp.ctx_len,
+                            C, s.fatt + b * img, st);
+        }
         TcArgs o2;
         o2.bias = Fn("o2.b");
         o2.residual_f32 = s.fb;
@@ -702,8 +868,8 @@ void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, voi
     float* yf = static_cast<float*>(y);
     switch (s.kind) {
         case kConvIn: {
-            pack_latent_f32(in[0].p, latent_f64, HW, sp.c_lat, 64, sc.fa, st);
-            if (B == 2)
+            pack_latent_f32(in[0].p, latent_f64, static_cast<long long>(sp.frames) * HW, sp.c_lat, 64, sc.fa, st);
+            if (sp.cfg)
                 CKD(cudaMemcpyAsync(sc.fa + static_cast<long long>(HW) * 64, sc.fa, static_cast<size_t>(HW) * 64 * 4,
                                     cudaMemcpyDeviceToDevice, st));
             TcArgs a;
@@ -735,28 +901,23 @@ void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, voi
         case kOut: {
             if (latent_f64) throw std::invalid_argument("unet: the UNet family runs in f32 trajectory precision");
             const float* x = static_cast<const float*>(in[0].p);
-            const long long img = static_cast<long long>(HW) * s.cin;
-            for (int b = 0; b < B; ++b)
-                group_norm(Cat2F{x + b * img, s.cin, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn.gamma"),
-                           F(stage, "gn.beta"), 1e-5f, 1, sc.fa + b * img, sc.gn, st);
+            gn_images(Cat2F{x, s.cin, nullptr, 0}, HW, F(stage, "gn.gamma"), F(stage, "gn.beta"), 1e-5f, 1, sc.fa, sc,
+                      st);
             TcArgs a;
             a.bias = F(stage, "conv.b");
-            a.out_f32 = B == 1 ? yf : sc.eps2;
+            a.out_f32 = sp.cfg ? sc.eps2 : yf;
             a.ldo = sp.c_lat;
             a.n_store = sp.c_lat;
             conv_x(sc, sc.fa, s.H, s.W, s.cin, "conv.w", stage, 32, a, st);
-            if (B == 2) cfg_combine(sc.eps2, static_cast<long long>(HW) * sp.c_lat, sp.cfg_scale, yf, st);
+            if (sp.cfg) cfg_combine(sc.eps2, static_cast<long long>(HW) * sp.c_lat, sp.cfg_scale, yf, st);
             break;
         }
         default: {  // resnet (+ transformer)
             const int C = s.cout, cin = s.cin + s.cskip;
             const float* x0 = static_cast<const float*>(in[0].p);
             const float* x1 = s.cskip ? static_cast<const float*>(in[1].p) : nullptr;
-            const long long i0 = static_cast<long long>(HW) * s.cin, i1 = static_cast<long long>(HW) * s.cskip,
-                            ic = static_cast<long long>(HW) * cin, io = static_cast<long long>(HW) * C;
-            for (int b = 0; b < B; ++b)
-                group_norm(Cat2F{x0 + b * i0, s.cin, x1 ? x1 + b * i1 : nullptr, s.cskip}, 1, HW, sp.groups,
-                           F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.fa + b * ic, sc.gn, st);
+            gn_images(Cat2F{x0, s.cin, x1, s.cskip}, HW, F(stage, "gn1.gamma"), F(stage, "gn1.beta"), 1e-5f, 1, sc.fa,
+                      sc, st);
             TcArgs c1;
             c1.bias = F(stage, "conv1.b");
             c1.chan_add = st_[stage].chan_add + static_cast<long long>(t) * C;
@@ -764,9 +925,8 @@ void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, voi
             c1.out_f32 = sc.fb;
             c1.ldo = C;
             conv_x(sc, sc.fa, s.H, s.W, cin, "conv1.w", stage, C, c1, st);
-            for (int b = 0; b < B; ++b)
-                group_norm(Cat2F{sc.fb + b * io, C, nullptr, 0}, 1, HW, sp.groups, F(stage, "gn2.gamma"),
-                           F(stage, "gn2.beta"), 1e-5f, 1, sc.fa + b * io, sc.gn, st);
+            gn_images(Cat2F{sc.fb, C, nullptr, 0}, HW, F(stage, "gn2.gamma"), F(stage, "gn2.beta"), 1e-5f, 1, sc.fa, sc,
+                      st);
             const float* res = x0;
             if (cin != C) {
                 const float* xin = x0;
@@ -787,11 +947,12 @@ void UNetDevice::enqueue_exact(int stage, const std::vector<Seg>& in, int t, voi
             c2.bias = F(stage, "conv2.b");
             c2.residual_f32 = res;
             c2.ldr = C;
-            float* out = s.attn ? sc.fc : yf;
+            float* out = s.attn || s.motion ? sc.fc : yf;
             c2.out_f32 = out;
             c2.ldo = C;
             conv_x(sc, sc.fa, s.H, s.W, C, "conv2.w", stage, C, c2, st);
-            if (s.attn) transformer_exact(stage, sc.fc, s.H, s.W, C, yf, st);
+            if (s.attn) transformer_exact(stage, sc.fc, s.H, s.W, C, s.motion ? sc.fr : yf, st);
+            if (s.motion) motion_exact(stage, s.attn ? sc.fr : sc.fc, s.H, s.W, C, yf, st);
         }
     }
 }

@@ -4,6 +4,7 @@
 #include "engine.hpp"
 #include "tc_gemm.cuh"
 #include "unet.hpp"
+#include "unet_kernels.cuh"
 
 #include <cuda_bf16.h>
 
@@ -22,6 +23,9 @@ struct UDevStage {
     // cross-attention keys [ctx_pad][C] and values [C][ctx_pad] (transposed per head), per
     // (transformer block, context): index block * batch + image
     std::vector<__nv_bfloat16*> k2, vt2;
+    // video motion module: per temporal attention, the frame positional encoding through the
+    // QKV projection, PE . Wqkv^T [frames][3C] fp32 (added per frame in the GEMM epilogue)
+    std::vector<float*> pe_proj;
 };
 
 struct UScratch {
@@ -59,6 +63,13 @@ private:
                    const __nv_bfloat16* v, long long ldv, const __nv_bfloat16* v_t, int L, int Lk, int C,
                    __nv_bfloat16* out, cudaStream_t st);
     void transformer(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
+    void motion(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
+    void motion_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st);
+    // GroupNorm of every image of the batch: per image (fused single launch) for 1-2 images,
+    // one batched two-kernel launch for video frames
+    template <typename T>
+    void gn_images(const Cat2T<T>& x, int HW, const float* gamma, const float* beta, float eps, int act, T* out,
+                   UScratch& s, cudaStream_t st);
     // ADX_F32 mode
     void enqueue_exact(int stage, const std::vector<Seg>& in, int t, void* y, bool latent_f64, cudaStream_t st);
     void transformer_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st);

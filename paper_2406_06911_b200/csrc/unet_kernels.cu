@@ -187,9 +187,10 @@ __global__ void gn_stats(Cat2T<T> x, int HW, int groups, int chunk_pix, int chun
     // fp64 merge of the chunk partials: nsub threads per (image, group), each over a fixed
     // strided subset with 4 loads in flight, then combined in sub order (fixed = deterministic)
     const int ngs = batch * groups, nsub = max(1, static_cast<int>(blockDim.x) / ngs);
+    // (loops: a video batch can hold more (image, group) pairs than the CTA has threads)
     double* red = reinterpret_cast<double*>(sm);  // [nsub][ngs][2], then [ngs][2] mean / rstd
-    if (threadIdx.x < nsub * ngs) {
-        const int ng = threadIdx.x % ngs, sub = threadIdx.x / ngs, nn = ng / groups, g = ng % groups;
+    for (int idx = threadIdx.x; idx < nsub * ngs; idx += blockDim.x) {
+        const int ng = idx % ngs, sub = idx / ngs, nn = ng / groups, g = ng % groups;
         const float2* pp = L.part + static_cast<long long>(nn) * chunks * groups + g;
         double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
         int k = sub;
@@ -208,20 +209,16 @@ __global__ void gn_stats(Cat2T<T> x, int HW, int groups, int chunk_pix, int chun
         red[2 * (sub * ngs + ng) + 1] = (b[0] + b[1]) + (b[2] + b[3]);
     }
     __syncthreads();
-    double mv[2] = {0.0, 0.0};
-    const int ng = threadIdx.x;
-    if (ng < ngs) {
+    double* st = red + 2 * nsub * ngs;  // [ngs][2] mean / rstd
+    for (int ng = threadIdx.x; ng < ngs; ng += blockDim.x) {
         double a = 0.0, b = 0.0;
         for (int sub = 0; sub < nsub; ++sub) a += red[2 * (sub * ngs + ng)], b += red[2 * (sub * ngs + ng) + 1];
         const double cnt = static_cast<double>(HW) * cpg;
         const double mu = a / cnt;
         const double var = fmax(b / cnt - mu * mu, 0.0);
-        mv[0] = mu;
-        mv[1] = 1.0 / sqrt(var + static_cast<double>(eps));
+        st[2 * ng] = mu;
+        st[2 * ng + 1] = 1.0 / sqrt(var + static_cast<double>(eps));
     }
-    __syncthreads();
-    double* st = red;
-    if (ng < ngs) st[2 * ng] = mv[0], st[2 * ng + 1] = mv[1];
     __syncthreads();
     for (int nc = threadIdx.x; nc < batch * C; nc += blockDim.x) {
         const int nn = nc / C, c = nc % C, g = c / cpg;
@@ -659,6 +656,112 @@ __global__ void cfg_combine_k(const float* e, long long n, float scale, float* o
         out[i] = fmaf(scale, e[n + i] - e[i], e[i]);
 }
 
+// Temporal self-attention of the video motion modules (AnimateDiff-shaped, BASELINE config
+// 5): for every (pixel, 64-wide head) the NF frames attend to each other.  qkv is the
+// frame-major packed projection [NF][HW][3C]; out [NF][HW][C].  Sequences are NF <= 32
+// long, far below a tensor-core tile, so this runs on the CUDA cores: one warp per (pixel,
+// head), K and V of all frames staged in shared memory as fp32, LPQ lanes per query frame
+// each owning 64 / LPQ dimensions (scores reduced over the LPQ lanes by xor shuffles).  fp32
+// scores / softmax / accumulation, one rounding at the store; fixed order (deterministic).
+template <int NF>
+struct TemporalShape {
+    static constexpr int LPQ = NF <= 4 ? 8 : NF <= 8 ? 4 : NF <= 16 ? 2 : 1;  // lanes per query
+    static constexpr int D = 64 / LPQ;                                         // dims per lane
+    static constexpr int WPB = NF > 16 ? 2 : 4;                                // warps per CTA
+    static constexpr int SMEM = WPB * NF * 128 * 4;                            // K + V, fp32
+};
+
+template <typename T, int NF>  // NF: frame capacity (4, 8, 16, 32); nf <= NF frames present
+__global__ void __launch_bounds__(128) temporal_attn_k(const T* qkv, int nf, int HW, int C, T* out) {
+    using S = TemporalShape<NF>;
+    constexpr int LPQ = S::LPQ, D = S::D;
+    pdl_wait();
+    extern __shared__ float tsm[];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, heads = C / 64;
+    const long long item = static_cast<long long>(blockIdx.x) * S::WPB + warp;  // (pixel, head)
+    if (item >= static_cast<long long>(HW) * heads) return;                    // warp-uniform
+    const int p = static_cast<int>(item / heads), h = static_cast<int>(item % heads);
+    float* Ks = tsm + warp * NF * 128;
+    float* Vs = Ks + NF * 64;
+    const long long ld = 3LL * C;
+    for (int i = lane; i < nf * 16; i += 32) {  // nf rows x (8 K + 8 V) vectors of 8
+        const int f = i / 16, v = i % 16, kv = v / 8, c8 = (v % 8) * 8;
+        float x[8];
+        Vec8<T>::unpack(Vec8<T>::load(qkv + (static_cast<long long>(f) * HW + p) * ld + (1 + kv) * C + h * 64 + c8),
+                        x);
+        float4* dst = reinterpret_cast<float4*>((kv ? Vs : Ks) + f * 64 + c8);
+        dst[0] = make_float4(x[0], x[1], x[2], x[3]);
+        dst[1] = make_float4(x[4], x[5], x[6], x[7]);
+    }
+    __syncwarp();
+    const int qf = lane / LPQ, sub = lane % LPQ;
+    const bool active = qf < nf;
+    const int qr = active ? qf : nf - 1;  // idle lanes shadow the last query (shuffles stay full-warp)
+    float q[D];
+    const T* qp = qkv + (static_cast<long long>(qr) * HW + p) * ld + h * 64 + sub * D;
+#pragma unroll
+    for (int d = 0; d < D; d += 8) Vec8<T>::unpack(Vec8<T>::load(qp + d), q + d);
+    float sc[NF];
+    float mx = -3.0e38f;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+        const float4* kr = reinterpret_cast<const float4*>(Ks + j * 64 + sub * D);
+        float a = 0.f;
+#pragma unroll
+        for (int d = 0; d < D / 4; ++d) {
+            const float4 k4 = kr[d];
+            a = fmaf(q[4 * d], k4.x, a);
+            a = fmaf(q[4 * d + 1], k4.y, a);
+            a = fmaf(q[4 * d + 2], k4.z, a);
+            a = fmaf(q[4 * d + 3], k4.w, a);
+        }
+#pragma unroll
+        for (int o = 1; o < LPQ; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        sc[j] = j < nf ? a * 0.125f : -3.0e38f;  // 1 / sqrt(64); absent frames weigh 0
+        mx = fmaxf(mx, sc[j]);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+        sc[j] = j < nf ? expf(sc[j] - mx) : 0.f;
+        sum += sc[j];
+    }
+    const float inv = 1.f / sum;
+    float o[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) o[d] = 0.f;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+        if (j >= nf) break;
+        const float pj = sc[j] * inv;
+        const float4* vr = reinterpret_cast<const float4*>(Vs + j * 64 + sub * D);
+#pragma unroll
+        for (int d = 0; d < D / 4; ++d) {
+            const float4 v4 = vr[d];
+            o[4 * d] = fmaf(pj, v4.x, o[4 * d]);
+            o[4 * d + 1] = fmaf(pj, v4.y, o[4 * d + 1]);
+            o[4 * d + 2] = fmaf(pj, v4.z, o[4 * d + 2]);
+            o[4 * d + 3] = fmaf(pj, v4.w, o[4 * d + 3]);
+        }
+    }
+    if (!active) return;
+    T* op = out + (static_cast<long long>(qf) * HW + p) * C + h * 64 + sub * D;
+#pragma unroll
+    for (int d = 0; d < D; d += 8) Vec8<T>::store(op + d, Vec8<T>::pack(o + d));
+}
+
+template <typename T, int NF>
+void temporal_launch(const T* qkv, int frames, int HW, int C, T* out, cudaStream_t st) {
+    if constexpr (NF > 4) {
+        if (2 * frames <= NF) return temporal_launch<T, NF / 2>(qkv, frames, HW, C, out, st);
+    }
+    using S = TemporalShape<NF>;
+    const long long items = static_cast<long long>(HW) * (C / 64);
+    CKU(launch_pdl(temporal_attn_k<T, NF>, dim3(static_cast<unsigned>((items + S::WPB - 1) / S::WPB)),
+                   dim3(32 * S::WPB), S::SMEM, st, 1, qkv, frames, HW, C, out));
+    CKU(cudaGetLastError());
+}
+
 int grid_for(long long n, int threads = 256) {
     return static_cast<int>(std::min<long long>((n + threads - 1) / threads, 148LL * 16));
 }
@@ -731,7 +834,7 @@ void group_norm_t(const Cat2T<T>& x, int batch, int HW, int groups, const float*
     const int rpb = std::max(1, 512 / nv);
     const int threads = rpb * nv, nsub = std::max(1, threads / (batch * groups));
     size_t smem = static_cast<size_t>(2) * rpb * C * sizeof(float);
-    smem = std::max(smem, static_cast<size_t>(nsub) * batch * groups * 2 * sizeof(double));
+    smem = std::max(smem, static_cast<size_t>(nsub + 1) * batch * groups * 2 * sizeof(double));
     if (smem > 48 * 1024) throw std::invalid_argument("group_norm: statistics tile exceeds 48 KB shared memory");
     CKU(launch_pdl(gn_stats<T>, dim3(chunks, batch), dim3(threads), smem, st, 1, x, HW, groups, chunk_pix, chunks, gamma,
                    beta, eps, scratch));
@@ -783,6 +886,19 @@ void split3(const float* x, long long rows, int cols, long long ldx, int g, int 
     CKU(launch_pdl(split3_k, dim3(grid_for(rows * cols / 8)), dim3(256), 0, st, 1, x, rows, cols, ldx, g, pattern,
                    out));
     CKU(cudaGetLastError());
+}
+
+template <typename T>
+void temporal_attention_t(const T* qkv, int frames, int HW, int C, T* out, cudaStream_t st) {
+    if (frames < 2 || frames > 32) throw std::invalid_argument("temporal_attention: frames must be in 2..32");
+    if (C % 64) throw std::invalid_argument("temporal_attention: channels must be a multiple of 64");
+    temporal_launch<T, 32>(qkv, frames, HW, C, out, st);
+}
+void temporal_attention(const __nv_bfloat16* qkv, int frames, int HW, int C, __nv_bfloat16* out, cudaStream_t st) {
+    temporal_attention_t(qkv, frames, HW, C, out, st);
+}
+void temporal_attention(const float* qkv, int frames, int HW, int C, float* out, cudaStream_t st) {
+    temporal_attention_t(qkv, frames, HW, C, out, st);
 }
 
 void cfg_combine(const float* e, long long n, float scale, float* out, cudaStream_t st) {

@@ -36,6 +36,10 @@ void split3(const float* x, long long rows, int cols, long long ldx, int g, int 
 void softmax_rows_f32(float* S, long long lds, int rows, int valid, int padded, cudaStream_t st);
 // VT[d][k] = V[k * ldv + d] (k < L; 0 for L <= k < Lpad), fp32, hd rows
 void transpose_f32(const float* V, long long ldv, int L, int Lpad, int hd, float* VT, cudaStream_t st);
+// video motion modules: self-attention across the frames of every (pixel, 64-wide head);
+// qkv frame-major [frames][HW][3C] (q | k | v), out [frames][HW][C]; 2 <= frames <= 32
+void temporal_attention(const __nv_bfloat16* qkv, int frames, int HW, int C, __nv_bfloat16* out, cudaStream_t st);
+void temporal_attention(const float* qkv, int frames, int HW, int C, float* out, cudaStream_t st);
 // classifier-free guidance: out[i] = e[i] + scale * (e[n + i] - e[i])  (e = [eps_u | eps_c])
 void cfg_combine(const float* e, long long n, float scale, float* out, cudaStream_t st);
 // latent (fp32 / fp64, HWC) -> fp32 NHWC with cpad channels

@@ -134,3 +134,20 @@ def test_tc_attention_split_kv_is_deterministic():
                                               VT.ctypes.data_as(P16), L, out.ctypes.data_as(P16), 3, None))
         outs.append(out)
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("frames,HW,C", [(16, 4096, 320), (16, 64, 1280), (3, 100, 128), (2, 37, 64), (9, 256, 640),
+                                          (32, 64, 320), (5, 1, 64)])
+def test_temporal_attention_matches_fp32_reference(frames, HW, C):
+    """video motion-module attention across frames, per (pixel, head), vs torch fp32"""
+    rng = np.random.default_rng(frames * 1000 + HW + C)
+    qkv = bf16_bits(rng.standard_normal((frames, HW, 3 * C)).astype(np.float32))
+    out = np.zeros((frames, HW, C), np.uint16)
+    _lib.check(adx.lib().adx_temporal_attention(0, frames, HW, C, qkv.ctypes.data_as(P16), out.ctypes.data_as(P16),
+                                                0, None))
+    x = torch.from_numpy(bits_f32(qkv)).view(frames, HW, 3, C // 64, 64)
+    q, k, v = (x[:, :, i].permute(1, 2, 0, 3) for i in range(3))  # (HW, heads, frames, 64)
+    ref = (torch.softmax(q @ k.transpose(-1, -2) / 8.0, dim=-1) @ v).permute(2, 0, 1, 3).reshape(frames, HW, C)
+    got = bits_f32(out)
+    err = np.abs(got - ref.numpy()).max() / np.abs(ref.numpy()).max()
+    assert err < 1e-2, err  # one bf16 rounding of the output

@@ -156,3 +156,54 @@ def test_unet_xl_cfg_async_invariants_bit_exact(small_xl):
     ser, _ = adx.run_serial(plan, m, part, x, s)
     par, _ = adx.run_parallel(plan, m, part, x, s, plan.D)
     assert np.array_equal(ser.latent_matrix(), par.latent_matrix())
+
+
+# AnimateDiff-shaped (BASELINE config 5) in miniature: the latent holds every frame, a
+# temporal-attention motion module follows every resnet; frames 3 exercises a partly
+# filled frame capacity of the temporal kernel, 16 the C5 frame count
+def small_video(frames):
+    m = adx.build_unet_denoiser(H=16, W=16, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64, temb_dim=128,
+                                frames=frames, motion=True, seed=9)
+    s = adx.build_schedule(3, 0.01, 0.15)
+    x = adx.Latent(O.random_normals(14, m.data_dim()).astype(np.float64), 3)
+    return m, s, x
+
+
+@pytest.mark.parametrize("frames", [3, 16])
+@pytest.mark.parametrize("prec,exact,tol", [("bf16", False, TOL), ("f32", True, TOL_F32)])
+def test_unet_video_motion_matches_oracle(frames, prec, exact, tol):
+    m, s, x = small_video(frames)
+    assert m.data_dim() == frames * 16 * 16 * 4
+    traj = adx.sequential_denoise(m, x, s, precision=prec)
+    orc = UNetOracle(adx, m, exact=exact)
+    lat = x.values.astype(np.float64)
+    for k, t in enumerate(range(3, 0, -1)):
+        eps = orc.eval_full(lat if exact else traj.latents[k].values.astype(np.float32), t)
+        assert rel(traj.eps_used[k], eps) < tol, (prec, frames, t, rel(traj.eps_used[k], eps))
+        lat = O.ddim_step(lat, np.asarray(eps, np.float64), t, s.alpha_bars)
+    if exact:
+        assert rel(traj.latents[-1].values, lat) < tol
+
+
+def test_unet_video_frames_are_mixed():
+    """the motion modules couple the frames: perturbing frame 0 of the input latent changes
+    every frame's eps (without them each frame would be denoised independently)"""
+    m, s, x = small_video(3)
+    e0 = adx.sequential_denoise(m, x, s).eps_used[0].reshape(3, -1)
+    v = x.values.copy().reshape(3, -1)
+    v[0] += 0.5
+    e1 = adx.sequential_denoise(m, adx.Latent(v.reshape(-1), 3), s).eps_used[0].reshape(3, -1)
+    for f in range(3):
+        assert rel(e1[f], e0[f]) > 1e-4, f
+
+
+def test_unet_video_async_invariants_bit_exact():
+    m, s, x = small_video(4)
+    seq = adx.sequential_denoise(m, x, s)
+    part = adx.partition_balanced(m, 2)
+    full, _ = adx.run_serial(adx.plan_async(3, 3, 2, 1), m, part, x, s)
+    assert np.array_equal(full.latent_matrix(), seq.latent_matrix())
+    plan = adx.plan_async(3, 1, 2, 1)
+    ser, _ = adx.run_serial(plan, m, part, x, s)
+    par, _ = adx.run_parallel(plan, m, part, x, s, plan.D)
+    assert np.array_equal(ser.latent_matrix(), par.latent_matrix())

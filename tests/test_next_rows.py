@@ -193,3 +193,31 @@ def test_unet_sdxl_shape_and_cfg_build():
     assert {"tf.qkv.w", "tf.b1.qkv.w", "tf.b2.ff2.w"} <= names and "tf.b3.qkv.w" not in names
     with pytest.raises(adx.InvalidArgument):
         adx.build_unet_denoiser(**dict(kw, ctx_dim=100))
+
+
+def test_unet_video_motion_build():
+    """AnimateDiff-shaped builder (host only): the latent / eps and every stage carry all
+    frames, motion modules add parameters to every resnet stage (not to conv / down / up /
+    out), frames share one context, invalid combinations are rejected."""
+    kw = dict(H=16, W=16, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64, temb_dim=128, seed=9)
+    a = adx.build_unet_denoiser(**kw)
+    v = adx.build_unet_denoiser(frames=4, motion=True, **kw)
+    assert v.num_stages() == a.num_stages() and v.skip_links == a.skip_links
+    assert v.data_dim() == 4 * a.data_dim()
+    assert adx.unet_context(v).shape == (1, 8, 64)
+    assert v.total_macs() > 4 * a.total_macs()  # + the motion modules
+    for i in range(1, v.num_stages() + 1):
+        kind = adx.unet_stage_info(v, i)["kind"]
+        names = set(adx.unet_stage_params(v, i))
+        has = {"mm.gn.gamma", "mm.a1.qkv.w", "mm.a2.o.w", "mm.ff1.w", "mm.proj_out.w"} <= names
+        assert has == (kind in ("res", "mid_res")), (i, kind)
+        assert names >= set(adx.unet_stage_params(a, i))  # the spatial parameters are unchanged
+    for i in range(1, a.num_stages() + 1):
+        for k, w in adx.unet_stage_params(a, i).items():
+            assert np.array_equal(w, adx.unet_stage_params(v, i)[k])
+    with pytest.raises(adx.InvalidArgument):
+        adx.build_unet_denoiser(frames=4, cfg=True, **kw)
+    with pytest.raises(adx.InvalidArgument):
+        adx.build_unet_denoiser(frames=1, motion=True, **kw)
+    with pytest.raises(adx.InvalidArgument):
+        adx.build_unet_denoiser(frames=33, motion=True, **kw)
