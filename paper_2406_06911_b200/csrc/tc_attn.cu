@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
                                                              // then [2 halves][128 rows] row sums
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qt = blockIdx.x / p.nsplit, split = blockIdx.x - qt * p.nsplit, head = blockIdx.y;
+    const int qt = blockIdx.x / p.nsplit, split = blockIdx.x - qt * p.nsplit, head = blockIdx.y, img = blockIdx.z;
     const int nkv_all = (p.Lk + KT - 1) / KT;
     const int j0 = (nkv_all * split) / p.nsplit;  // this CTA's KV blocks [j0, j0 + nkv)
     const int nkv = (nkv_all * (split + 1)) / p.nsplit - j0;
@@ -281,15 +281,17 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
     if (warp == 0 && lane == 0) {
         // ------------------------------------------------------------ TMA
         bar_expect(q_full, Q_B);
-        tma2d(sQ, &tmQ, head * HD, qt * QT, q_full);
+        tma2d(sQ, &tmQ, head * HD, img * p.L + qt * QT, q_full);  // (a ragged tile reads the next
+                                                                   // image's rows; never stored)
         for (int j = 0; j < nkv; ++j) {
             const int s = j % STG;
             bar_wait(&kv_empty[s], ((j / STG) & 1) ^ 1);
             bar_expect(&kv_full[s], K_B + V_B);
-            tma2d(sK + s * K_B, &tmK, head * HD, (j0 + j) * KT, &kv_full[s]);
+            tma2d(sK + s * K_B, &tmK, head * HD, img * p.Lk + (j0 + j) * KT, &kv_full[s]);  // (masked past Lk)
             // V^T rows = this head's 64 dims, one box per 64-key block (128-byte rows)
             for (int blk = 0; blk < NB64; ++blk)
-                tma2d(sV + s * V_B + blk * (HD * 128), &tmVT, (j0 + j) * KT + 64 * blk, head * HD, &kv_full[s]);
+                tma2d(sV + s * V_B + blk * (HD * 128), &tmVT, (j0 + j) * KT + 64 * blk, img * p.C + head * HD,
+                      &kv_full[s]);
         }
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------------------ MMA
@@ -428,7 +430,8 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
         bool write_out = true;
         if (p.nsplit > 1) {
             // publish this split's partial: O (unnormalised), the row max m it used, row sum
-            const long long item = qt + static_cast<long long>(gridDim.x / p.nsplit) * head;
+            const long long item =
+                qt + static_cast<long long>(gridDim.x / p.nsplit) * (head + static_cast<long long>(gridDim.y) * img);
             float* rec = p.part + (item * p.nsplit + split) * kRecFloats;
 #pragma unroll
             for (int c = 0; c < HD / 2; c += 4)
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
         }
         if (write_out && row < p.L) {
             const float inv = 1.0f / lt;
-            __nv_bfloat16* dst = p.out + row * p.ldo + head * HD + half * (HD / 2);
+            __nv_bfloat16* dst = p.out + (static_cast<long long>(img) * p.L + row) * p.ldo + head * HD + half * (HD / 2);
 #pragma unroll
             for (int c = 0; c < HD / 2; c += 8) {
                 uint4 v;
@@ -533,8 +536,8 @@ namespace {
 // split-KV factor: the (query tile, head) items fill 2 CTAs per SM unevenly (e.g. 360
 // items over 296 slots = a 22% second wave); minimise rounds x (KV blocks per CTA + fixed
 // per-CTA cost, + the combine when split)
-int attn_splits(int L, int Lk, int C, int sms) {
-    const long long items = static_cast<long long>((L + QT - 1) / QT) * (C / HD);
+int attn_splits(int L, int Lk, int C, int sms, int batch) {
+    const long long items = static_cast<long long>((L + QT - 1) / QT) * (C / HD) * batch;
     const int nkv = (Lk + KT - 1) / KT, slots = 2 * sms;
     int best_s = 1;
     double best = 1e300;
@@ -556,25 +559,27 @@ int device_sms() {
 }
 }  // namespace
 
-size_t tc_attention_ws_bytes(int L, int Lk, int C) {
-    const int S = attn_splits(L, Lk, C, device_sms());
+size_t tc_attention_ws_bytes(int L, int Lk, int C, int batch) {
+    const int S = attn_splits(L, Lk, C, device_sms(), batch);
     if (S == 1) return 0;
-    const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD);
+    const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD) * batch;
     return 256 * ((items * 4 + 255) / 256) + items * S * kRecFloats * sizeof(float);
 }
 
 void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, const void* VT, long long ldvt, int L,
-                  int Lk, int C, __nv_bfloat16* out, long long ldo, cudaStream_t st, void* ws, size_t ws_bytes) {
+                  int Lk, int C, __nv_bfloat16* out, long long ldo, cudaStream_t st, void* ws, size_t ws_bytes,
+                  int batch) {
     if (C % HD) throw std::invalid_argument("attention: C must be a multiple of 64");
     if ((ldq | ldk | ldvt | ldo) % 8) throw std::invalid_argument("attention: strides must be multiples of 8");
-    const CUtensorMap mq = map2d(Q, L, C, ldq, QT);
-    const CUtensorMap mk = map2d(K, Lk, C, ldk, KT);
-    const CUtensorMap mv = map2d(VT, C, Lk, ldvt, HD);  // rows = dims, cols = keys
+    if (batch < 1 || batch > 65535) throw std::invalid_argument("attention: batch must be in 1..65535");
+    const CUtensorMap mq = map2d(Q, static_cast<long long>(batch) * L, C, ldq, QT);
+    const CUtensorMap mk = map2d(K, static_cast<long long>(batch) * Lk, C, ldk, KT);
+    const CUtensorMap mv = map2d(VT, static_cast<long long>(batch) * C, Lk, ldvt, HD);  // rows = dims, cols = keys
     AttnArgs a{L, Lk, C, out, ldo};
-    const int S = attn_splits(L, Lk, C, device_sms());
-    const size_t need = tc_attention_ws_bytes(L, Lk, C);
+    const int S = attn_splits(L, Lk, C, device_sms(), batch);
+    const size_t need = tc_attention_ws_bytes(L, Lk, C, batch);
     if (S > 1 && ws && ws_bytes >= need) {  // without a (large enough) workspace: unsplit
-        const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD);
+        const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD) * batch;
         a.nsplit = S;
         a.counters = static_cast<unsigned*>(ws);
         a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * ((items * 4 + 255) / 256));
@@ -587,9 +592,9 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
         CKA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr[dev] = true;
     }
-    dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD);
+    dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD, batch);
     CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, st, 1, mq, mk, mv, a));
-    tc_profile_measure(st, 2, 4.0 * L * Lk * C, [&](cudaStream_t s2) {
+    tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, [&](cudaStream_t s2) {
         CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, s2, 1, mq, mk, mv, a));
     });
     CKA(cudaGetLastError());

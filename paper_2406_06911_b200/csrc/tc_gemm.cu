@@ -166,13 +166,16 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float* v) {
     return make_uint4(w4[0], w4[1], w4[2], w4[3]);
 }
 
-// row of chan_add an output row reads: per row group (chan_add_rows), shared, or per image
-__device__ __forceinline__ long long chan_row(const TcArgs& p, long long m, int img) {
-    return p.chan_add_rows ? m / p.chan_add_rows : p.chan_add_shared ? 0 : img;
+// the chan_add row output row m reads (per row group, shared, or per image); resolved once
+// per tile row by the caller, outside the column loop
+__device__ __forceinline__ const float* chan_row(const TcArgs& p, long long m, int img) {
+    if (!p.chan_add) return nullptr;
+    const int r = p.chan_add_rows ? static_cast<int>(m) / p.chan_add_rows : p.chan_add_shared ? 0 : img;
+    return p.chan_add + static_cast<long long>(r) * p.N;
 }
 
 // fused epilogue on 16 accumulator columns [nb, nb + 16) of output row m
-__device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int nb, float* v,
+__device__ __forceinline__ void epi16(const TcArgs& p, long long m, const float* ca, int nb, float* v,
                                       const uint4* rpre = nullptr) {
     const int nlim = p.n_store ? p.n_store : p.N;
     if ((((p.ldo | p.ldr) & 7) == 0) && nb + 16 <= nlim && !p.residual_f32) {
@@ -183,9 +186,8 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int
                 const float4 b = *reinterpret_cast<const float4*>(p.bias + nb + j);
                 v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
             }
-            if (p.chan_add) {
-                const float4 b = *reinterpret_cast<const float4*>(
-                    p.chan_add + chan_row(p, m, img) * p.N + nb + j);
+            if (ca) {
+                const float4 b = *reinterpret_cast<const float4*>(ca + nb + j);
                 v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
             }
         }
@@ -226,7 +228,7 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, int img, int
         if (n >= nlim) continue;
         float x = v[j];
         if (p.bias) x += p.bias[n];
-        if (p.chan_add) x += p.chan_add[chan_row(p, m, img) * p.N + n];
+        if (ca) x += ca[n];
         if (p.act == 1) x = silu(x);
         if (p.residual) x += __bfloat162float(p.residual[m * p.ldr + n]);
         if (p.residual_f32) x += p.residual_f32[m * p.ldr + n];
@@ -461,6 +463,7 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
                         const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0);
                         rnext[0] = rp[0], rnext[1] = rp[1];
                     }
+                    const float* ca = valid ? chan_row(p, m, img) : nullptr;
                     for (int c = 0; c < BN; c += 16) {
                         const uint4 rcur[2] = {rnext[0], rnext[1]};
                         const bool have = pre && n0 + c + 16 <= nlim;
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
                         }
                         float v[16];
                         tmem_ld16(trow + c, v);
-                        if (valid) epi16(p, m, img, n0 + c, v, have ? rcur : nullptr);
+                        if (valid) epi16(p, m, ca, n0 + c, v, have ? rcur : nullptr);
                     }
                 }
             }
@@ -518,7 +521,7 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
                 if (p.act == 2)
                     epi_geglu16(p, m, n0, c, v, g);
                 else
-                    epi16(p, m, img, n0 + c, v);
+                    epi16(p, m, chan_row(p, m, img), n0 + c, v);
             }
         }
         __syncwarp();

@@ -329,7 +329,7 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
         if (s.attn) {
             const size_t L = hw, Lp = pad64(static_cast<int>(L));
             S = std::max(S, L * std::max(Lp, static_cast<size_t>(pad64(sp.ctx_len))));
-            vt = std::max(vt, static_cast<size_t>(s.cout) * Lp);
+            vt = std::max(vt, static_cast<size_t>(s.cout) * Lp * sp.batch());  // every image's V^T
         }
     }
     // activations / GEMM operands hold the whole CFG batch; S, V^T and the attention work
@@ -359,7 +359,7 @@ UScratch& UNetDevice::scratch(cudaStream_t st) {
     for (const UStage& stg : d_.st)
         if (stg.attn) {
             const int L = stg.H * stg.W;
-            s.attn_ws_bytes = std::max({s.attn_ws_bytes, tc_attention_ws_bytes(L, L, stg.cout),
+            s.attn_ws_bytes = std::max({s.attn_ws_bytes, tc_attention_ws_bytes(L, L, stg.cout, sp.batch()),
                                         tc_attention_ws_bytes(sp.batch() * L, sp.ctx_len, stg.cout)});
         }
     if (s.attn_ws_bytes) {
@@ -411,7 +411,8 @@ const float* UNetDevice::F(int stage, const char* name) const { return static_ca
 // multi-head attention out[L x C] = softmax(q k^T / 8) v, one head (64) at a time;
 // v_t != nullptr: pre-transposed values [C x Lkp] (cross attention)
 void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16* k, long long ldk, const bf16* v,
-                           long long ldv, const bf16* v_t, int L, int Lk, int C, bf16* out, cudaStream_t st) {
+                           long long ldv, const bf16* v_t, int L, int Lk, int C, bf16* out, cudaStream_t st,
+                           int batch) {
     const int Lkp = pad64(Lk);
     static const bool unfused = [] {
         const char* e = getenv("ADX_ATTN");
@@ -420,10 +421,16 @@ void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16
     if (!unfused) {  // fused tcgen05 flash attention (tc_attn.cu): S stays in TMEM
         const bf16* vt = v_t;
         if (!vt) {
-            transpose_head(v, ldv, Lk, Lkp, C, s.VT, st);
+            transpose_head(v, ldv, Lk, Lkp, C, s.VT, st, batch);
             vt = s.VT;
         }
-        tc_attention(q, ldq, k, ldk, vt, Lkp, L, Lk, C, out, C, st, s.attn_ws, s.attn_ws_bytes);
+        tc_attention(q, ldq, k, ldk, vt, Lkp, L, Lk, C, out, C, st, s.attn_ws, s.attn_ws_bytes, batch);
+        return;
+    }
+    if (batch > 1) {  // the unfused debugging path runs image by image
+        for (int b = 0; b < batch; ++b)
+            attention(s, q + b * L * ldq, ldq, k + b * Lk * ldk, ldk, v ? v + b * Lk * ldv : nullptr, ldv, v_t, L, Lk,
+                      C, out + static_cast<long long>(b) * L * C, st, 1);
         return;
     }
     for (int h = 0; h < C / 64; ++h) {
@@ -589,10 +596,8 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
         qk.out_bf16 = s.qkv;
         qk.ldo = 3 * C;
         tc_gemm(s.a, Pn("qkv.w"), BL, 3 * C, C, qk, st);
-        for (int b = 0; b < B; ++b) {
-            const bf16* q = s.qkv + b * 3 * img;
-            attention(s, q, 3 * C, q + C, 3 * C, q + 2 * C, 3 * C, nullptr, L, L, C, s.att + b * img, st);
-        }
+        // self attention of every image in one launch (stacked rows)
+        attention(s, s.qkv, 3 * C, s.qkv + C, 3 * C, s.qkv + 2 * C, 3 * C, nullptr, L, L, C, s.att, st, B);
         TcArgs o1;
         o1.bias = Fn("o1.b");
         o1.residual = s.b;

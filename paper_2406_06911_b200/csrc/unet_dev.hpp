@@ -61,7 +61,7 @@ private:
     const float* F(int stage, const char* name) const;
     void attention(UScratch& s, const __nv_bfloat16* q, long long ldq, const __nv_bfloat16* k, long long ldk,
                    const __nv_bfloat16* v, long long ldv, const __nv_bfloat16* v_t, int L, int Lk, int C,
-                   __nv_bfloat16* out, cudaStream_t st);
+                   __nv_bfloat16* out, cudaStream_t st, int batch = 1);
     void transformer(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
     void motion(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
     void motion_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st);

@@ -10,6 +10,7 @@
 
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 #include <utility>
@@ -99,6 +100,9 @@ __device__ __forceinline__ typename Vec8<T>::raw cat_vec(const Cat2T<T>& x, long
 
 // GroupNorm scratch: [ticket counter (64 B)][per-channel (scale, shift) float2, batch*C][partials]
 constexpr int kGnMaxChunks = 148;  // one statistics CTA per SM
+// pixel chunks per image: one per SM for 1-2 images; a video batch shares ~2 CTAs per SM so
+// the last CTA's merge reads few partials per (image, group)
+inline int gn_chunk_cap(int batch) { return batch <= 2 ? kGnMaxChunks : std::max(4, 2 * kGnMaxChunks / batch); }
 struct GnLayout {
     unsigned* counter;
     float2* ab;
@@ -229,26 +233,48 @@ __global__ void gn_stats(Cat2T<T> x, int HW, int groups, int chunk_pix, int chun
     if (threadIdx.x == 0) *L.counter = 0u;  // re-arm for the next launch on this scratch
 }
 
-// GroupNorm pass 2: y = x * a[c] + b[c] (+SiLU), 8 channels per thread
+// GroupNorm pass 2: y = x * a[c] + b[c] (+SiLU).  Thread (r, v) owns the 8 channels of
+// vector v for pixel rows r, r + rpb, ... of its CTA's contiguous pixel range, so its (scale,
+// shift) pairs are loaded once per image, not per element; 4 rows in flight per thread
 template <typename T>
-__global__ void gn_apply(Cat2T<T> x, long long pixels, int HW, const float2* __restrict__ ab, int act, T* out) {
+__global__ void gn_apply(Cat2T<T> x, int pixels, int HW, const float2* __restrict__ ab, int act, T* out) {
     pdl_wait();
-    const int C = x.c0 + x.c1, nv = C / 8;
-    const long long n = pixels * nv;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long pix = i / nv;
-        const int v = static_cast<int>(i - pix * nv);
-        const float2* abv = ab + (pix / HW) * C + v * 8;
-        float f[8];
-        Vec8<T>::unpack(cat_vec(x, pix, v), f);
+    const int C = x.c0 + x.c1, nv = C / 8, rpb = blockDim.x / nv;
+    const int r = threadIdx.x / nv, v = threadIdx.x - (threadIdx.x / nv) * nv;
+    if (r >= rpb) return;
+    const int per = (pixels + gridDim.x - 1) / gridDim.x;
+    const int p0 = blockIdx.x * per, p1 = min(pixels, p0 + per);
+    int cur = -1;
+    float2 q[8];
+    for (int pix = p0 + r; pix < p1; pix += 4 * rpb) {
+        typename Vec8<T>::raw u[4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float2 q = __ldg(abv + k);
-            f[k] = fmaf(f[k], q.x, q.y);
-            if (act) f[k] = silu(f[k]);
+        for (int k = 0; k < 4; ++k)
+            if (pix + k * rpb < p1) u[k] = cat_vec(x, pix + k * rpb, v);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int pk = pix + k * rpb;
+            if (pk >= p1) break;
+            const int img = pk / HW;
+            if (img != cur) {
+                cur = img;
+                const float4* a4 = reinterpret_cast<const float4*>(ab + static_cast<long long>(img) * C + v * 8);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 t = __ldg(a4 + j);
+                    q[2 * j] = make_float2(t.x, t.y);
+                    q[2 * j + 1] = make_float2(t.z, t.w);
+                }
+            }
+            float f[8];
+            Vec8<T>::unpack(u[k], f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                f[j] = fmaf(f[j], q[j].x, q[j].y);
+                if (act) f[j] = silu(f[j]);
+            }
+            Vec8<T>::store(out + (static_cast<long long>(pk) * nv + v) * 8, Vec8<T>::pack(f));
         }
-        Vec8<T>::store(out + i * 8, Vec8<T>::pack(f));
     }
 }
 
@@ -404,8 +430,10 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
 }
 
 // LayerNorm over C per token, one warp per token, row held in registers (C <= 2048)
+// (NV: vectors of 8 per lane the instantiation holds -- C <= 256 NV; fewer registers for
+// narrow rows = more warps resident = more bytes in flight)
 constexpr int kLnMaxVec = 8;
-template <typename T>
+template <typename T, int NV = kLnMaxVec>
 __global__ void layernorm_k(const T* x, int tokens, int C, const float* gamma, const float* beta, float eps,
                             T* out) {
     pdl_wait();
@@ -413,10 +441,10 @@ __global__ void layernorm_k(const T* x, int tokens, int C, const float* gamma, c
     if (warp >= tokens) return;
     const int nv = C / 8;
     const T* r = x + static_cast<long long>(warp) * C;
-    float f[kLnMaxVec][8];
+    float f[NV][8];
     float s = 0.f;
 #pragma unroll
-    for (int j = 0; j < kLnMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
         const int v = lane + 32 * j;
         if (v < nv) {
             Vec8<T>::unpack(Vec8<T>::load(r + v * 8), f[j]);
@@ -427,7 +455,7 @@ __global__ void layernorm_k(const T* x, int tokens, int C, const float* gamma, c
     const float mu = warp_sum(s) / C;
     float ss = 0.f;
 #pragma unroll
-    for (int j = 0; j < kLnMaxVec; ++j)
+    for (int j = 0; j < NV; ++j)
         if (lane + 32 * j < nv) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -438,7 +466,7 @@ __global__ void layernorm_k(const T* x, int tokens, int C, const float* gamma, c
     const float rstd = rsqrtf(warp_sum(ss) / C + eps);
     T* o = out + static_cast<long long>(warp) * C;
 #pragma unroll
-    for (int j = 0; j < kLnMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
         const int v = lane + 32 * j;
         if (v < nv) {
             const float4* g4 = reinterpret_cast<const float4*>(gamma + v * 8);
@@ -561,6 +589,8 @@ __global__ void pack_latent_k(const T* x, long long pixels, int c_lat, int cpad,
 // VT[d][k] = V[k * ldv + d] for k < L, 0 for L <= k < Lpad  (one head, head_dim rows)
 __global__ void transpose_head_k(const bf16* V, long long ldv, int L, int Lpad, int hd, bf16* VT) {
     pdl_wait();
+    V += static_cast<long long>(blockIdx.z) * L * ldv;  // image z of a stacked batch
+    VT += static_cast<long long>(blockIdx.z) * hd * Lpad;
     __shared__ bf16 tile[32][33];
     const int k0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -684,14 +714,24 @@ __global__ void __launch_bounds__(128) temporal_attn_k(const T* qkv, int nf, int
     float* Ks = tsm + warp * NF * 128;
     float* Vs = Ks + NF * 64;
     const long long ld = 3LL * C;
-    for (int i = lane; i < nf * 16; i += 32) {  // nf rows x (8 K + 8 V) vectors of 8
-        const int f = i / 16, v = i % 16, kv = v / 8, c8 = (v % 8) * 8;
-        float x[8];
-        Vec8<T>::unpack(Vec8<T>::load(qkv + (static_cast<long long>(f) * HW + p) * ld + (1 + kv) * C + h * 64 + c8),
-                        x);
-        float4* dst = reinterpret_cast<float4*>((kv ? Vs : Ks) + f * 64 + c8);
-        dst[0] = make_float4(x[0], x[1], x[2], x[3]);
-        dst[1] = make_float4(x[4], x[5], x[6], x[7]);
+    {  // nf rows x (8 K + 8 V) vectors of 8: every load issued before the first store
+        constexpr int IT = NF / 2;  // NF * 16 vectors / 32 lanes
+        typename Vec8<T>::raw u[IT];
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int i = lane + 32 * it, f = i / 16, v = i % 16, kv = v / 8, c8 = (v % 8) * 8;
+            if (f < nf) u[it] = Vec8<T>::load(qkv + (static_cast<long long>(f) * HW + p) * ld + (1 + kv) * C + h * 64 + c8);
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int i = lane + 32 * it, f = i / 16, v = i % 16, kv = v / 8, c8 = (v % 8) * 8;
+            if (f >= nf) continue;
+            float x[8];
+            Vec8<T>::unpack(u[it], x);
+            float4* dst = reinterpret_cast<float4*>((kv ? Vs : Ks) + f * 64 + c8);
+            dst[0] = make_float4(x[0], x[1], x[2], x[3]);
+            dst[1] = make_float4(x[4], x[5], x[6], x[7]);
+        }
     }
     __syncwarp();
     const int qf = lane / LPQ, sub = lane % LPQ;
@@ -829,7 +869,7 @@ void group_norm_t(const Cat2T<T>& x, int batch, int HW, int groups, const float*
         });
         return;
     }
-    const int chunk_pix = (HW + kGnMaxChunks - 1) / kGnMaxChunks;
+    const int chunk_pix = (HW + gn_chunk_cap(batch) - 1) / gn_chunk_cap(batch);
     const int chunks = (HW + chunk_pix - 1) / chunk_pix;
     const int rpb = std::max(1, 512 / nv);
     const int threads = rpb * nv, nsub = std::max(1, threads / (batch * groups));
@@ -840,8 +880,10 @@ void group_norm_t(const Cat2T<T>& x, int batch, int HW, int groups, const float*
                    beta, eps, scratch));
     CKU(cudaGetLastError());
     const GnLayout L = gn_layout(scratch, batch, C);
-    const long long pixels = static_cast<long long>(batch) * HW;
-    CKU(launch_pdl(gn_apply<T>, dim3(grid_for(pixels * nv)), dim3(256), 0, st, 1, x, pixels, HW,
+    const int pixels = batch * HW;
+    const int arpb = std::max(1, 256 / nv);
+    const int ablocks = static_cast<int>(std::min<long long>(148LL * 8, (pixels + 4LL * arpb - 1) / (4LL * arpb)));
+    CKU(launch_pdl(gn_apply<T>, dim3(ablocks), dim3(arpb * nv), 0, st, 1, x, pixels, HW,
                    static_cast<const float2*>(L.ab), silu_act, out));
     CKU(cudaGetLastError());
 }
@@ -856,28 +898,30 @@ void group_norm(const Cat2F& x, int batch, int HW, int groups, const float* gamm
 }
 
 size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C) {
-    const int chunk_pix = (std::max(HW, 1) + kGnMaxChunks - 1) / kGnMaxChunks;
+    const int chunk_pix = (std::max(HW, 1) + gn_chunk_cap(batch) - 1) / gn_chunk_cap(batch);
     const int chunks = (HW + chunk_pix - 1) / chunk_pix;
     return (8 + static_cast<size_t>(batch) * C + static_cast<size_t>(batch) * chunks * groups) * sizeof(float2);
 }
 
+template <typename T>
+void layer_norm_t(const T* x, int tokens, int C, const float* gamma, const float* beta, float eps, T* out,
+                  cudaStream_t st) {
+    if (C % 8 || C > 256 * kLnMaxVec) throw std::invalid_argument("layer_norm: C must be a multiple of 8, <= 2048");
+    auto k = C <= 256 ? layernorm_k<T, 1> : C <= 512 ? layernorm_k<T, 2> : C <= 1024 ? layernorm_k<T, 4>
+                                                                                  : layernorm_k<T, kLnMaxVec>;
+    CKU(launch_pdl(k, dim3((tokens + 7) / 8), dim3(256), 0, st, 1, x, tokens, C, gamma, beta, eps, out));
+    CKU(cudaGetLastError());
+    tc_profile_measure(st, 4, 2.0 * tokens * C * sizeof(T), [&](cudaStream_t s2) {
+        CKU(launch_pdl(k, dim3((tokens + 7) / 8), dim3(256), 0, s2, 1, x, tokens, C, gamma, beta, eps, out));
+    });
+}
 void layer_norm(const __nv_bfloat16* x, int tokens, int C, const float* gamma, const float* beta, float eps,
                 __nv_bfloat16* out, cudaStream_t st) {
-    if (C % 8 || C > 256 * kLnMaxVec) throw std::invalid_argument("layer_norm: C must be a multiple of 8, <= 2048");
-    CKU(launch_pdl(layernorm_k<bf16>, dim3((tokens + 7) / 8), dim3(256), 0, st, 1, x, tokens, C, gamma, beta, eps,
-                   out));
-    CKU(cudaGetLastError());
-    tc_profile_measure(st, 4, 2.0 * tokens * C * 2, [&](cudaStream_t s2) {
-        CKU(launch_pdl(layernorm_k<bf16>, dim3((tokens + 7) / 8), dim3(256), 0, s2, 1, x, tokens, C, gamma, beta,
-                       eps, out));
-    });
+    layer_norm_t(x, tokens, C, gamma, beta, eps, out, st);
 }
 void layer_norm(const float* x, int tokens, int C, const float* gamma, const float* beta, float eps, float* out,
                 cudaStream_t st) {
-    if (C % 8 || C > 256 * kLnMaxVec) throw std::invalid_argument("layer_norm: C must be a multiple of 8, <= 2048");
-    CKU(launch_pdl(layernorm_k<float>, dim3((tokens + 7) / 8), dim3(256), 0, st, 1, x, tokens, C, gamma, beta, eps,
-                   out));
-    CKU(cudaGetLastError());
+    layer_norm_t(x, tokens, C, gamma, beta, eps, out, st);
 }
 
 void split3(const float* x, long long rows, int cols, long long ldx, int g, int pattern, __nv_bfloat16* out,
@@ -964,9 +1008,9 @@ void pack_latent(const void* x, bool f64, long long pixels, int c_lat, int cpad,
 }
 
 void transpose_head(const __nv_bfloat16* V, long long ldv, int L, int Lpad, int hd, __nv_bfloat16* VT,
-                    cudaStream_t st) {
-    CKU(launch_pdl(transpose_head_k, dim3((Lpad + 31) / 32, (hd + 31) / 32), dim3(32, 8), 0, st, 1, V, ldv, L, Lpad, hd,
-                   VT));
+                    cudaStream_t st, int batch) {
+    CKU(launch_pdl(transpose_head_k, dim3((Lpad + 31) / 32, (hd + 31) / 32, batch), dim3(32, 8), 0, st, 1, V, ldv, L,
+                   Lpad, hd, VT));
     CKU(cudaGetLastError());
 }
 

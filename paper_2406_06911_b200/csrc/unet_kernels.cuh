@@ -55,7 +55,8 @@ void upsample2x(const __nv_bfloat16* x, int batch, int H, int W, int C, __nv_bfl
 void concat_channels(const Cat2& x, long long pixels, __nv_bfloat16* out, cudaStream_t st);
 void pack_latent(const void* x, bool f64, long long pixels, int c_lat, int cpad, __nv_bfloat16* out,
                  cudaStream_t st);
+// VT[d][k] = V[k * ldv + d] per image of a stacked batch (V rows b * L.., VT [b][hd][Lpad])
 void transpose_head(const __nv_bfloat16* V, long long ldv, int L, int Lpad, int hd, __nv_bfloat16* VT,
-                    cudaStream_t st);
+                    cudaStream_t st, int batch = 1);
 
 }  // namespace adx
