@@ -22,6 +22,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdio>
+
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -593,6 +595,7 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
         attr[dev] = true;
     }
     dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD, batch);
+    if (tc_trace()) fprintf(stderr, "tc_attention L=%d Lk=%d C=%d batch=%d S=%d\n", L, Lk, C, batch, a.nsplit);
     CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, st, 1, mq, mk, mv, a));
     tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, [&](cudaStream_t s2) {
         CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, s2, 1, mq, mk, mv, a));

@@ -295,8 +295,18 @@ __device__ __forceinline__ float4 reduce_dsmem4(const uint32_t* a, int S, int of
 }
 
 // ------------------------------------------------------------------ kernel
+// epilogue warps: EPW / 4 per TMEM lane quadrant, each over its share of the tile's
+// 16-column chunks (more loads / stores in flight for the 1-tile-per-CTA small GEMMs)
+constexpr int EPW = 8;
+constexpr int kGemmThreads = 64 + 32 * EPW;
+__device__ __forceinline__ void epi_chunks(int nch, int part, int& c0, int& c1) {
+    constexpr int P = EPW / 4;
+    c0 = (nch * part) / P * 16;
+    c1 = (nch * (part + 1)) / P * 16;
+}
+
 template <int BN, bool CONV>
-__global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB, const TcArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment of the swizzled tiles
@@ -351,7 +361,7 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
         }
         for (int a = 0; a < 2; ++a) {
             bar_init(&tfull[a], 1);
-            bar_init(&tempty[a], 4);  // one arrival per epilogue warp
+            bar_init(&tempty[a], EPW);  // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -421,7 +431,8 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
         }
     } else if (warp >= 2) {
         // --------------------------------------------------------- epilogue
-        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        const int q = warp & 3;             // TMEM lane quadrant this warp may access
+        const int part = (warp - 2) >> 2;   // which share of the tile's column chunks
         const int row = q * 32 + lane;
         int lu = 0;
         for (int u = u0; u < uend; u += ustride, ++lu) {
@@ -436,7 +447,9 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
                 // stage this CTA's fp32 partial in its own SMEM (the drained pipeline
                 // buffers), rows padded by 4 floats so 8 lanes' float4 stores hit 32 banks
                 float* stg = reinterpret_cast<float*>(smem) + row * (BN + 4);
-                for (int c = 0; c < BN; c += 16) {
+                int cb, ce;
+                epi_chunks(BN / 16, part, cb, ce);
+                for (int c = cb; c < ce; c += 16) {
                     float v[16];
                     tmem_ld16(trow + c, v);
 #pragma unroll
@@ -447,7 +460,9 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
                 long long m;
                 const bool valid = row_to_m<CONV>(p, tile_m, img, h0, w0, row, m);
                 if (p.act == 2) {
-                    for (int c = 0; c < BN / 2; c += 16) {
+                    int cb, ce;
+                    epi_chunks(BN / 32, part, cb, ce);
+                    for (int c = cb; c < ce; c += 16) {
                         float v[16], g[16];
                         tmem_ld16(trow + c, v);
                         tmem_ld16(trow + BN / 2 + c, g);
@@ -458,16 +473,18 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
                     // epilogue, so its L2 latency overlaps instead of stalling every chunk
                     const int nlim = p.n_store ? p.n_store : p.N;
                     const bool pre = valid && p.residual && (((p.ldo | p.ldr) & 7) == 0);
+                    int cb, ce;
+                    epi_chunks(BN / 16, part, cb, ce);
                     uint4 rnext[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-                    if (pre && n0 + 16 <= nlim) {
-                        const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0);
+                    if (pre && cb < ce && n0 + cb + 16 <= nlim) {
+                        const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + cb);
                         rnext[0] = rp[0], rnext[1] = rp[1];
                     }
                     const float* ca = valid ? chan_row(p, m, img) : nullptr;
-                    for (int c = 0; c < BN; c += 16) {
+                    for (int c = cb; c < ce; c += 16) {
                         const uint4 rcur[2] = {rnext[0], rnext[1]};
                         const bool have = pre && n0 + c + 16 <= nlim;
-                        if (pre && c + 16 < BN && n0 + c + 32 <= nlim) {
+                        if (pre && c + 16 < ce && n0 + c + 32 <= nlim) {
                             const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + c + 16);
                             rnext[0] = rp[0], rnext[1] = rp[1];
                         }
@@ -494,9 +511,9 @@ __global__ void __launch_bounds__(192, 1) tc_gemm_kernel(const __grid_constant__
             const int n0 = tile_n * BN;
             const int r0 = (BM * split) / S, r1 = (BM * (split + 1)) / S;
             const uint32_t base = sa(smem);
-            const int et = threadIdx.x - 64;  // 0..127
+            const int et = threadIdx.x - 64;  // 0 .. 32 EPW - 1
             const int cols = p.act == 2 ? BN / 2 : BN, chunks = cols / 16;
-            for (int it = et; it < (r1 - r0) * chunks; it += 128) {
+            for (int it = et; it < (r1 - r0) * chunks; it += 32 * EPW) {
                 const int row = r0 + it / chunks, c = (it % chunks) * 16;
                 long long m;
                 const bool valid = row_to_m<CONV>(p, tile_m, img, h0, w0, row, m);
@@ -577,7 +594,8 @@ void launch_t(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 
         CKT(cudaFuncSetAttribute(tc_gemm_kernel<BN, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr[dev] = true;
     }
-    CKT(launch_pdl(tc_gemm_kernel<BN, CONV>, grid, dim3(192), smem, st, static_cast<unsigned>(p.splits), a, b, p));
+    CKT(launch_pdl(tc_gemm_kernel<BN, CONV>, grid, dim3(kGemmThreads), smem, st, static_cast<unsigned>(p.splits), a,
+                   b, p));
 }
 
 template <bool CONV>
@@ -598,7 +616,7 @@ void dispatch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 
 constexpr int kSMs = 148;
 
 // ADX_TC_TRACE=1: print every launch's tile plan to stderr
-bool tc_trace() {
+bool tc_trace_on() {
     static const bool on = [] {
         const char* e = getenv("ADX_TC_TRACE");
         return e && *e == '1';
@@ -622,7 +640,7 @@ int cluster_capacity_t(int S) {
     CKT(cudaFuncSetAttribute(tc_gemm_kernel<BN, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(S * 64, 1, 1);
-    cfg.blockDim = dim3(192, 1, 1);
+    cfg.blockDim = dim3(kGemmThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -759,7 +777,7 @@ void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::func
     float ms = 0.f;
     CKT(cudaEventElapsedTime(&ms, a, b));
     g_prof.push_back({kind, flops, ms / kRep});
-    if (tc_trace())
+    if (tc_trace_on())
         fprintf(stderr, "  prof kind=%d %.1f us %.1f %s\n", kind, 1e3 * ms / kRep, flops / (ms / kRep) / 1e9,
                 kind > 2 ? "GB/s" : "TFLOP/s");
     cudaEventDestroy(a);
@@ -821,7 +839,7 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     p.n_tiles = (N + bn - 1) / bn;
     p.batch = 1;
     const dim3 grid = launch_grid<false>(p, bn);
-    if (tc_trace())
+    if (tc_trace_on())
         fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d act=%d grid=%ux%u\n", M, N, K, bn, S, p.act, grid.x, grid.y);
     dispatch<false>(ma, mb, p, grid, bn, st);
     tc_profile_measure(st, 1, 2.0 * M * N * K, [&](cudaStream_t s2) { dispatch<false>(ma, mb, p, grid, bn, s2); });
@@ -884,7 +902,7 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     p.n_tiles = (Cout + bn - 1) / bn;
     p.batch = batch;
     const dim3 grid = launch_grid<true>(p, bn);
-    if (tc_trace())
+    if (tc_trace_on())
         fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u\n", H, W, Cin, Cout, bw, bh, bn, S,
                 grid.x, grid.y, grid.z);
     dispatch<true>(ma, mb, p, grid, bn, st);
@@ -892,5 +910,7 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     tc_profile_measure(st, 0, 2.0 * batch * H * W * Cout * 9.0 * Cin / (p.sub2 ? 4.0 : 1.0),
                        [&](cudaStream_t s2) { dispatch<true>(ma, mb, p, grid, bn, s2); });
 }
+
+bool tc_trace() { return tc_trace_on(); }
 
 }  // namespace adx

@@ -39,6 +39,8 @@ struct TcArgs {
 
 // force (bn, splits) for every following launch (tuning); (0, 0) restores the plan table / model
 void tc_plan_override(int bn, int splits);
+// ADX_TC_TRACE=1: print every launch's shape / plan (and, when profiling, its isolated time)
+bool tc_trace();
 
 // In-run kernel profiling (eager passes only): when enabled, every tensor-core launch is,
 // after it completes, replayed in isolation from a small CUDA graph and timed with events;
