@@ -846,11 +846,23 @@ bool group_norm_fused(const Cat2T<T>& x, int HW, int groups, const float* gamma,
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
+    unsigned n = 1;
+    // PDL as well: the CTAs may launch while the producer drains (they wait in pdl_wait);
+    // the producer never waits on them, so the co-residency the grid barrier needs follows
+    static const bool pdl_coop = [] {
+        const char* e = getenv("ADX_GN_PDL");
+        return !(e && *e == '0');
+    }();
+    if (pdl_enabled() && pdl_coop) {
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        n = 2;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = n;
     CKU(cudaLaunchKernelEx(&cfg, gn_fused<T>, x, HW, groups, chunk_pix, gamma, beta, eps, act, scratch, out));
     return true;
 }
