@@ -818,6 +818,29 @@ void Session::enqueue_all(bool capture) {
     (void)capture;
 }
 
+// kernels of this library in a captured graph (kernel nodes, NCCL's own excluded): the
+// bench's gpu_launches claim is counted from the graph itself, not from the enqueue calls
+int graph_kernel_nodes(cudaGraph_t g) {
+    size_t n = 0;
+    CK(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(g, nodes.data(), &n));
+    int k = 0;
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        CK(cudaGraphNodeGetType(nd, &t));
+        if (t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp = {};
+        const char* name = nullptr;
+        if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func &&
+            cudaFuncGetName(&name, kp.func) == cudaSuccess && name && std::strncmp(name, "nccl", 4) == 0)
+            continue;
+        cudaGetLastError();
+        ++k;
+    }
+    return k;
+}
+
 void Session::build_graph() {
     VDev& v0 = vd_[0];
     setdev(v0.ordinal);
@@ -833,7 +856,7 @@ void Session::build_graph() {
     }
     CK(cudaStreamEndCapture(v0.comp, &graph_));
     CK(cudaGraphInstantiate(&gexec_, graph_, 0));
-    kernel_count_ = enq_kernels_;
+    kernel_count_ = graph_kernel_nodes(graph_);
 }
 
 void Session::launch() {

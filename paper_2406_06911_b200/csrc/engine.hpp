@@ -125,7 +125,7 @@ public:
     void run(const double* x_T, double* lat, double* eps, RunStatsOut* stats);
     double time_runs(int iters);  // device-resident, ms per run
     void download(double* lat, double* eps);
-    int kernel_count() const { return kernel_count_; }
+    int kernel_count() const { return kernel_count_; }  // graph mode: kernel nodes of the graph
     long long weight_bytes_per_run() const { return weight_bytes_per_run_; }
     int T() const { return T_; }
     int d() const { return d_; }
@@ -200,5 +200,8 @@ void rank_session_destroy(void* s);
 void rank_session_run(void* s, const double* x, double* lat, double* eps);
 double rank_session_time(void* s, int iters);
 int rank_session_kernels(void* s);
+
+// kernel nodes of this library in a captured CUDA graph (NCCL kernels excluded)
+int graph_kernel_nodes(cudaGraph_t g);
 
 }  // namespace adx

@@ -325,6 +325,7 @@ private:
         CKR(cudaStreamWaitEvent(comp_, ev_join_, 0));
         CKR(cudaStreamEndCapture(comp_, &graph_));
         CKR(cudaGraphInstantiate(&gexec_, graph_, 0));
+        kernels_ = graph_kernel_nodes(graph_);
     }
 
     Engine* E_;
