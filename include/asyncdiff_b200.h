@@ -325,9 +325,9 @@ int adx_unet_context(const adx_model* m, float* out /* batch x ctx_len x ctx_dim
 int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B,
                 const float* bias, int act, float* C, int bn, int iters, double* ms_per_iter);
 /* fused multi-head attention (64-wide heads, scale 1/8): out[L x C] bf16 from Q [L x C],
- * K [Lk x C] and V transposed VT [C x ldvt] (ldvt >= Lk, multiple of 8) */
+ * K [Lk x C] and V [Lk x ldv] (row-major, ldv >= C, multiple of 8) */
 int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K,
-                     const uint16_t* VT, int ldvt, uint16_t* out, int iters, double* ms_per_iter);
+                     const uint16_t* V, int ldv, uint16_t* out, int iters, double* ms_per_iter);
 /* video motion-module temporal attention: for every (pixel, 64-wide head) the frames
  * attend to each other; qkv frame-major [frames][HW][3C] bf16 (q | k | v), out
  * [frames][HW][C] bf16; 2 <= frames <= 32 */

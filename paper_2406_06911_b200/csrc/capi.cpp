@@ -1012,20 +1012,21 @@ int adx_tc_plan_override(int bn, int splits) {
     return guard([&] { adx::tc_plan_override(bn, splits); });
 }
 
-int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K, const uint16_t* VT,
-                     int ldvt, uint16_t* out, int iters, double* ms_per_iter) {
+int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K, const uint16_t* V,
+                     int ldv, uint16_t* out, int iters, double* ms_per_iter) {
     return guard([&] {
         CKC(cudaSetDevice(ordinal));
+        if (ldv < C) throw std::invalid_argument("tc_attention: ldv < C");
         DevBuf q(static_cast<size_t>(L) * C * 2), k(static_cast<size_t>(Lk) * C * 2),
-            v(static_cast<size_t>(C) * ldvt * 2), o(static_cast<size_t>(L) * C * 2);
+            v(static_cast<size_t>(Lk) * ldv * 2), o(static_cast<size_t>(L) * C * 2);
         CKC(cudaMemcpy(q.p, Q, static_cast<size_t>(L) * C * 2, cudaMemcpyHostToDevice));
         CKC(cudaMemcpy(k.p, K, static_cast<size_t>(Lk) * C * 2, cudaMemcpyHostToDevice));
-        CKC(cudaMemcpy(v.p, VT, static_cast<size_t>(C) * ldvt * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(v.p, V, static_cast<size_t>(Lk) * ldv * 2, cudaMemcpyHostToDevice));
         const size_t wsb = adx::tc_attention_ws_bytes(L, Lk, C);
         DevBuf ws(std::max<size_t>(wsb, 256));
         CKC(cudaMemset(ws.p, 0, std::max<size_t>(wsb, 256)));
         auto run = [&](cudaStream_t st) {
-            adx::tc_attention(q.p, C, k.p, C, v.p, ldvt, L, Lk, C, static_cast<__nv_bfloat16*>(o.p), C, st, ws.p, wsb);
+            adx::tc_attention(q.p, C, k.p, C, v.p, ldv, L, Lk, C, static_cast<__nv_bfloat16*>(o.p), C, st, ws.p, wsb);
         };
         run(0);
         CKC(cudaDeviceSynchronize());

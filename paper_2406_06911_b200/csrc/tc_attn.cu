@@ -43,7 +43,9 @@ namespace {
 // (20 warps) share an SM and hide each other's barrier / TMEM / MUFU latencies
 constexpr int QT = 128, KT = 64, HD = 64, STG = 3;
 constexpr int HK = KT / 2;                            // keys per softmax warp (two warps per row)
-constexpr int NB64 = KT / 64;                         // 64-key (128-byte) column blocks per tile
+// V tiles are [KT keys][64 dims] straight from the V rows (SW128, dims contiguous) and feed
+// the PV MMA as an MN-major B operand (idesc bit 16; a K=16 step = 16 key rows = 2048 B,
+// SBO 1024 B between 8-row swizzle atoms; checked by tools/mn_mma_test.cu): no V^T pass
 constexpr int TP_COL = 2 * KT + HD;                  // P[2] (bf16 pairs: KT/2 columns each) after S[2], O
 constexpr uint32_t TM_COLS = (TP_COL + KT) <= 256 ? 256 : 512;  // S[2] + O + P[2], power of two
 
@@ -227,7 +229,7 @@ constexpr int kRecFloats = QT * HD + 2 * QT;  // O [128][64] fp32, then m[128], 
 
 __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                       const __grid_constant__ CUtensorMap tmK,
-                                                      const __grid_constant__ CUtensorMap tmVT, const AttnArgs p) {
+                                                      const __grid_constant__ CUtensorMap tmV, const AttnArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2;
@@ -291,9 +293,7 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
             bar_expect(&kv_full[s], K_B + V_B);
             tma2d(sK + s * K_B, &tmK, head * HD, img * p.Lk + (j0 + j) * KT, &kv_full[s]);  // (masked past Lk)
             // V^T rows = this head's 64 dims, one box per 64-key block (128-byte rows)
-            for (int blk = 0; blk < NB64; ++blk)
-                tma2d(sV + s * V_B + blk * (HD * 128), &tmVT, (j0 + j) * KT + 64 * blk, img * p.C + head * HD,
-                      &kv_full[s]);
+            tma2d(sV + s * V_B, &tmV, head * HD, img * p.Lk + (j0 + j) * KT, &kv_full[s]);  // (P = 0 past Lk)
         }
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------------------ MMA
@@ -318,11 +318,9 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
                 bar_wait(&p_full[b], (jj >> 1) & 1);  // P_jj in SMEM (and O rescaled if needed)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-                for (int k = 0; k < KT / 16; ++k) {
-                    const int blk = k / 4, kk = k % 4;
-                    mma_ts(tmem + 2 * KT, tmem + TP_COL + b * (KT / 2) + k * 8,
-                           sdesc(sV + s * V_B + blk * (HD * 128) + kk * 32), idesc(QT, HD), (jj | k) > 0);
-                }
+                for (int k = 0; k < KT / 16; ++k)
+                    mma_ts(tmem + 2 * KT, tmem + TP_COL + b * (KT / 2) + k * 8, sdesc(sV + s * V_B + k * 2048),
+                           idesc(QT, HD) | (1u << 16), (jj | k) > 0);
                 commit(&pv_done[b]);
                 commit(&kv_empty[s]);
             }
@@ -568,15 +566,15 @@ size_t tc_attention_ws_bytes(int L, int Lk, int C, int batch) {
     return 256 * ((items * 4 + 255) / 256) + items * S * kRecFloats * sizeof(float);
 }
 
-void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, const void* VT, long long ldvt, int L,
+void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, const void* V, long long ldv, int L,
                   int Lk, int C, __nv_bfloat16* out, long long ldo, cudaStream_t st, void* ws, size_t ws_bytes,
                   int batch) {
     if (C % HD) throw std::invalid_argument("attention: C must be a multiple of 64");
-    if ((ldq | ldk | ldvt | ldo) % 8) throw std::invalid_argument("attention: strides must be multiples of 8");
+    if ((ldq | ldk | ldv | ldo) % 8) throw std::invalid_argument("attention: strides must be multiples of 8");
     if (batch < 1 || batch > 65535) throw std::invalid_argument("attention: batch must be in 1..65535");
     const CUtensorMap mq = map2d(Q, static_cast<long long>(batch) * L, C, ldq, QT);
     const CUtensorMap mk = map2d(K, static_cast<long long>(batch) * Lk, C, ldk, KT);
-    const CUtensorMap mv = map2d(VT, static_cast<long long>(batch) * C, Lk, ldvt, HD);  // rows = dims, cols = keys
+    const CUtensorMap mv = map2d(V, static_cast<long long>(batch) * Lk, C, ldv, KT);  // rows = keys, like K
     AttnArgs a{L, Lk, C, out, ldo};
     const int S = attn_splits(L, Lk, C, device_sms(), batch);
     const size_t need = tc_attention_ws_bytes(L, Lk, C, batch);

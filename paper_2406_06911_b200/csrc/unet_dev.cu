@@ -94,10 +94,10 @@ void* device_zeros(size_t bytes) {
 
 void* upload_bf16(const std::vector<float>& v);
 
-// K2 [Lp][C] = ctx . Wk^T and V2^T [C][Lp] = Wv . ctx^T on the tensor cores (private stream,
-// synchronous: runs at stage preparation, outside any capture); rows / columns >= Lc stay zero
+// K2 [Lp][C] = ctx . Wk^T and V2 [Lp][C] = ctx . Wv^T on the tensor cores (private stream,
+// synchronous: runs at stage preparation, outside any capture); rows >= Lc stay zero
 void ctx_projection(const float* ctx, int Lc, int Dc, const std::vector<float>& wk, const std::vector<float>& wv,
-                    int C, int Lp, __nv_bfloat16* k2, __nv_bfloat16* vt2) {
+                    int C, __nv_bfloat16* k2, __nv_bfloat16* v2) {
     std::vector<float> c(ctx, ctx + static_cast<size_t>(Lc) * Dc);
     void* dctx = upload_bf16(c);
     void* dwk = upload_bf16(wk);
@@ -109,9 +109,9 @@ void ctx_projection(const float* ctx, int Lc, int Dc, const std::vector<float>& 
     a.ldo = C;
     tc_gemm(dctx, dwk, Lc, C, Dc, a, st);
     TcArgs b;
-    b.out_bf16 = vt2;
-    b.ldo = Lp;
-    tc_gemm(dwv, dctx, C, Lc, Dc, b, st);
+    b.out_bf16 = v2;
+    b.ldo = C;
+    tc_gemm(dctx, dwv, Lc, C, Dc, b, st);
     CKD(cudaStreamSynchronize(st));
     CKD(cudaStreamDestroy(st));
     cudaFree(dctx);
@@ -247,8 +247,8 @@ void UNetDevice::ensure_stage(int stage) {
                     ds.vt2.push_back(static_cast<bf16*>(upload_u16(split_b(vt2, C, Lp, Lp))));
                 } else {  // bf16 on the tensor cores: two GEMMs (SDXL: 10 blocks x 2 contexts per stage)
                     ds.k2.push_back(static_cast<bf16*>(device_zeros(static_cast<size_t>(Lp) * C * 2)));
-                    ds.vt2.push_back(static_cast<bf16*>(device_zeros(static_cast<size_t>(C) * Lp * 2)));
-                    ctx_projection(ctx, Lc, Dc, *wk, *wv, C, Lp, ds.k2.back(), ds.vt2.back());
+                    ds.vt2.push_back(static_cast<bf16*>(device_zeros(static_cast<size_t>(Lp) * C * 2)));
+                    ctx_projection(ctx, Lc, Dc, *wk, *wv, C, ds.k2.back(), ds.vt2.back());  // V2 row-major
                 }
             }
         }
@@ -408,29 +408,22 @@ const void* UNetDevice::P(int stage, const char* name) const {
 }
 const float* UNetDevice::F(int stage, const char* name) const { return static_cast<const float*>(P(stage, name)); }
 
-// multi-head attention out[L x C] = softmax(q k^T / 8) v, one head (64) at a time;
-// v_t != nullptr: pre-transposed values [C x Lkp] (cross attention)
+// multi-head attention out[L x C] = softmax(q k^T / 8) v (64-wide heads), q / k / v row-major
 void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16* k, long long ldk, const bf16* v,
-                           long long ldv, const bf16* v_t, int L, int Lk, int C, bf16* out, cudaStream_t st,
-                           int batch) {
+                           long long ldv, int L, int Lk, int C, bf16* out, cudaStream_t st, int batch) {
     const int Lkp = pad64(Lk);
     static const bool unfused = [] {
         const char* e = getenv("ADX_ATTN");
         return e && std::string(e) == "unfused";
     }();
-    if (!unfused) {  // fused tcgen05 flash attention (tc_attn.cu): S stays in TMEM
-        const bf16* vt = v_t;
-        if (!vt) {
-            transpose_head(v, ldv, Lk, Lkp, C, s.VT, st, batch);
-            vt = s.VT;
-        }
-        tc_attention(q, ldq, k, ldk, vt, Lkp, L, Lk, C, out, C, st, s.attn_ws, s.attn_ws_bytes, batch);
+    if (!unfused) {  // fused tcgen05 flash attention (tc_attn.cu): S and P stay in TMEM
+        tc_attention(q, ldq, k, ldk, v, ldv, L, Lk, C, out, C, st, s.attn_ws, s.attn_ws_bytes, batch);
         return;
     }
     if (batch > 1) {  // the unfused debugging path runs image by image
         for (int b = 0; b < batch; ++b)
-            attention(s, q + b * L * ldq, ldq, k + b * Lk * ldk, ldk, v ? v + b * Lk * ldv : nullptr, ldv, v_t, L, Lk,
-                      C, out + static_cast<long long>(b) * L * C, st, 1);
+            attention(s, q + b * L * ldq, ldq, k + b * Lk * ldk, ldk, v + b * Lk * ldv, ldv, L, Lk, C,
+                      out + static_cast<long long>(b) * L * C, st, 1);
         return;
     }
     for (int h = 0; h < C / 64; ++h) {
@@ -440,12 +433,11 @@ void UNetDevice::attention(UScratch& s, const bf16* q, long long ldq, const bf16
         a.out_scale = 0.125f;  // 1/sqrt(64)
         tc_gemm_strided(q + h * 64, ldq, k + h * 64, ldk, L, Lk, 64, a, st);
         softmax_rows(s.S, Lkp, L, Lk, s.P, Lkp, Lkp, st);
-        const bf16* vt = v_t ? v_t + static_cast<long long>(h) * 64 * Lkp : s.VT;
-        if (!v_t) transpose_head(v + h * 64, ldv, Lk, Lkp, 64, s.VT, st);
+        transpose_head(v + h * 64, ldv, Lk, Lkp, 64, s.VT, st);
         TcArgs o;
         o.out_bf16 = out + h * 64;
         o.ldo = C;
-        tc_gemm(s.P, vt, L, 64, Lkp, o, st);
+        tc_gemm(s.P, s.VT, L, 64, Lkp, o, st);
     }
 }
 
@@ -597,7 +589,7 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
         qk.ldo = 3 * C;
         tc_gemm(s.a, Pn("qkv.w"), BL, 3 * C, C, qk, st);
         // self attention of every image in one launch (stacked rows)
-        attention(s, s.qkv, 3 * C, s.qkv + C, 3 * C, s.qkv + 2 * C, 3 * C, nullptr, L, L, C, s.att, st, B);
+        attention(s, s.qkv, 3 * C, s.qkv + C, 3 * C, s.qkv + 2 * C, 3 * C, L, L, C, s.att, st, B);
         TcArgs o1;
         o1.bias = Fn("o1.b");
         o1.residual = s.b;
@@ -612,12 +604,11 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
         q2.ldo = C;
         tc_gemm(s.a, Pn("q2.w"), BL, C, C, q2, st);
         if (sp.contexts() == 1)  // one shared context: every image's queries in one launch
-            attention(s, s.qkv, C, st_[stage].k2[blk], C, nullptr, 0, st_[stage].vt2[blk], BL, sp.ctx_len, C, s.att,
-                      st);
+            attention(s, s.qkv, C, st_[stage].k2[blk], C, st_[stage].vt2[blk], C, BL, sp.ctx_len, C, s.att, st);
         else
             for (int b = 0; b < B; ++b)
-                attention(s, s.qkv + b * img, C, st_[stage].k2[blk * B + b], C, nullptr, 0,
-                          st_[stage].vt2[blk * B + b], L, sp.ctx_len, C, s.att + b * img, st);
+                attention(s, s.qkv + b * img, C, st_[stage].k2[blk * B + b], C, st_[stage].vt2[blk * B + b], C, L,
+                          sp.ctx_len, C, s.att + b * img, st);
         TcArgs o2;
         o2.bias = Fn("o2.b");
         o2.residual = s.b;

@@ -20,8 +20,9 @@ struct UDevStage {
     std::map<std::string, long long> bytes;
     float* chan_add = nullptr;       // [(T+1)][cout] time-embedding projection per t
     int chan_T = -1;
-    // cross-attention keys [ctx_pad][C] and values [C][ctx_pad] (transposed per head), per
-    // (transformer block, context): index block * batch + image
+    // cross-attention keys [ctx_pad][C] and values, per (transformer block, context): index
+    // block * contexts + context; values row-major [ctx_pad][C] (bf16 mode) or V^T split
+    // along the keys [C][3 ctx_pad] (ADX_F32 mode)
     std::vector<__nv_bfloat16*> k2, vt2;
     // video motion module: per temporal attention, the frame positional encoding through the
     // QKV projection, PE . Wqkv^T [frames][3C] fp32 (added per frame in the GEMM epilogue)
@@ -60,8 +61,8 @@ private:
     const void* P(int stage, const char* name) const;
     const float* F(int stage, const char* name) const;
     void attention(UScratch& s, const __nv_bfloat16* q, long long ldq, const __nv_bfloat16* k, long long ldk,
-                   const __nv_bfloat16* v, long long ldv, const __nv_bfloat16* v_t, int L, int Lk, int C,
-                   __nv_bfloat16* out, cudaStream_t st, int batch = 1);
+                   const __nv_bfloat16* v, long long ldv, int L, int Lk, int C, __nv_bfloat16* out, cudaStream_t st,
+                   int batch = 1);
     void transformer(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
     void motion(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
     void motion_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st);

@@ -104,17 +104,13 @@ def test_tc_attention_matches_fp32_reference(L, Lk, C):
     rng = np.random.default_rng(L + Lk + C)
     Q = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
     K = bf16_bits(rng.standard_normal((Lk, C)).astype(np.float32))
-    V = rng.standard_normal((Lk, C)).astype(np.float32)
-    ldvt = (Lk + 63) // 64 * 64
-    VT = np.zeros((C, ldvt), np.float32)
-    VT[:, :Lk] = V.T
-    VTb = bf16_bits(VT)
+    Vb = bf16_bits(rng.standard_normal((Lk, C)).astype(np.float32))
     out = np.zeros((L, C), np.uint16)
     _lib.check(adx.lib().adx_tc_attention(0, L, Lk, C, Q.ctypes.data_as(P16), K.ctypes.data_as(P16),
-                                          VTb.ctypes.data_as(P16), ldvt, out.ctypes.data_as(P16), 0, None))
+                                          Vb.ctypes.data_as(P16), C, out.ctypes.data_as(P16), 0, None))
     q = torch.from_numpy(bits_f32(Q)).view(L, C // 64, 64).transpose(0, 1)
     k = torch.from_numpy(bits_f32(K)).view(Lk, C // 64, 64).transpose(0, 1)
-    v = torch.from_numpy(bits_f32(VTb)[:, :Lk].T.copy()).view(Lk, C // 64, 64).transpose(0, 1)
+    v = torch.from_numpy(bits_f32(Vb)).view(Lk, C // 64, 64).transpose(0, 1)
     ref = torch.softmax(q @ k.transpose(1, 2) / 8.0, dim=-1) @ v
     ref = ref.transpose(0, 1).reshape(L, C).numpy()
     got = bits_f32(out)
@@ -126,12 +122,12 @@ def test_tc_attention_split_kv_is_deterministic():
     rng = np.random.default_rng(9)
     L, C = 1024, 640  # 80 (query tile, head) items -> split over KV
     Q = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
-    VT = bf16_bits(rng.standard_normal((C, L)).astype(np.float32))
+    V = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
     outs = []
     for _ in range(2):
         out = np.zeros((L, C), np.uint16)
         _lib.check(adx.lib().adx_tc_attention(0, L, L, C, Q.ctypes.data_as(P16), Q.ctypes.data_as(P16),
-                                              VT.ctypes.data_as(P16), L, out.ctypes.data_as(P16), 3, None))
+                                              V.ctypes.data_as(P16), C, out.ctypes.data_as(P16), 3, None))
         outs.append(out)
     assert np.array_equal(outs[0], outs[1])
 

@@ -9,5 +9,5 @@ rng = np.random.default_rng(0)
 q = (rng.standard_normal((L, C_)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
 vt = (rng.standard_normal((C_, L)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
 out = np.zeros((L, C_), np.uint16)
-_lib.check(adx.lib().adx_tc_attention(0, L, L, C_, q.ctypes.data_as(P16), q.ctypes.data_as(P16), vt.ctypes.data_as(P16), L, out.ctypes.data_as(P16), 0, None))
+_lib.check(adx.lib().adx_tc_attention(0, L, L, C_, q.ctypes.data_as(P16), q.ctypes.data_as(P16), vt.ctypes.data_as(P16), C_, out.ctypes.data_as(P16), 0, None))
 print("ok")

@@ -13,5 +13,5 @@ _lib.check(adx.lib().adx_tc_conv3x3(0, 1, 96, 96, 320, 320, X.ctypes.data_as(P16
 L, Cc = 9216, 320
 q = bf(rng.standard_normal((L, Cc))); vt = bf(rng.standard_normal((Cc, L))); o = np.zeros((L, Cc), np.uint16)
 _lib.check(adx.lib().adx_tc_attention(0, L, L, Cc, q.ctypes.data_as(P16), q.ctypes.data_as(P16), vt.ctypes.data_as(P16),
-                                      L, o.ctypes.data_as(P16), 0, None))
+                                      Cc, o.ctypes.data_as(P16), 0, None))
 print("ok")
