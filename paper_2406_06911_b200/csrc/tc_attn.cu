@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include <mutex>
 #include <stdexcept>
@@ -537,19 +538,27 @@ namespace {
 // items over 296 slots = a 22% second wave); minimise rounds x (KV blocks per CTA + fixed
 // per-CTA cost, + the combine when split)
 int attn_splits(int L, int Lk, int C, int sms, int batch) {
+    static const int forced = [] {  // ADX_ATTN_SPLITS=S forces the split factor (tuning)
+        const char* e = getenv("ADX_ATTN_SPLITS");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced > 0) return std::min(forced, std::max(1, (Lk + KT - 1) / KT));
     const long long items = static_cast<long long>((L + QT - 1) / QT) * (C / HD) * batch;
     const int nkv = (Lk + KT - 1) / KT, slots = 2 * sms;
-    int best_s = 1;
+    // the partial publish + fence + ticket + combine costs about ten KV blocks (measured:
+    // splitting the 100-item L=576 grid doubled its time), so only long grids with a bad
+    // wave tail split (level 0: 360 items over 296 slots); the smallest S within 5% of the
+    // best modelled time wins (level 0 measured: S=1 227 us, S=2 200 us, S=3 206 us)
+    double t[9] = {};
     double best = 1e300;
     for (int S = 1; S <= 8 && S <= nkv; ++S) {
         const long long rounds = (items * S + slots - 1) / slots;
-        // the partial publish + fence + ticket + combine costs about ten KV blocks (measured:
-        // splitting the 100-item L=576 grid doubled its time), so only long grids with a bad
-        // wave tail split (level 0: 360 items over 296 slots)
-        const double t = static_cast<double>(rounds) * ((nkv + S - 1) / S + 3 + (S > 1 ? 10 : 0));
-        if (t < best - 1e-9) best = t, best_s = S;
+        t[S] = static_cast<double>(rounds) * ((nkv + S - 1) / S + 3 + (S > 1 ? 10 : 0));
+        best = std::min(best, t[S]);
     }
-    return best_s;
+    for (int S = 1; S <= 8 && S <= nkv; ++S)
+        if (t[S] <= 1.05 * best) return S;
+    return 1;
 }
 int device_sms() {
     int dev = 0, sms = 0;
