@@ -43,6 +43,8 @@ namespace adx {
             throw cuda_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x); \
     } while (0)
 
+bool n_fast_order(long long a_bytes);
+
 namespace {
 
 constexpr int BM = 128, BK = 64, STAGES = 4;
@@ -342,10 +344,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
     const int kb0 = (p.k_blocks * split) / S, kb1 = (p.k_blocks * (split + 1)) / S;
     const int nkb = kb1 - kb0;
     auto coords = [&](int u, int& tile_m, int& tile_n, int& img, int& h0, int& w0) {
-        tile_m = u % p.m_tiles;
-        const int r = u / p.m_tiles;
-        tile_n = r % p.n_tiles;
-        img = r / p.n_tiles;
+        if (p.n_fast) {  // the CTAs in flight share the A (activation) tile
+            tile_n = u % p.n_tiles;
+            const int r = u / p.n_tiles;
+            tile_m = r % p.m_tiles;
+            img = r / p.m_tiles;
+        } else {  // the CTAs in flight share the B (weight) tile
+            tile_m = u % p.m_tiles;
+            const int r = u / p.m_tiles;
+            tile_n = r % p.n_tiles;
+            img = r / p.n_tiles;
+        }
         h0 = w0 = 0;
         if constexpr (CONV) {  // conv tile origin: box_h rows x box_w cols of one image
             const int tiles_w = p.W / p.box_w;
@@ -838,6 +847,7 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     p.m_tiles = (M + BM - 1) / BM;
     p.n_tiles = (N + bn - 1) / bn;
     p.batch = 1;
+    p.n_fast = S == 1 && p.n_tiles > 1 && n_fast_order(2LL * M * K);
     const dim3 grid = launch_grid<false>(p, bn);
     if (tc_trace_on())
         fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d act=%d grid=%ux%u\n", M, N, K, bn, S, p.act, grid.x, grid.y);
@@ -901,6 +911,7 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     p.m_tiles = m_tiles;
     p.n_tiles = (Cout + bn - 1) / bn;
     p.batch = batch;
+    p.n_fast = S == 1 && p.n_tiles > 1 && n_fast_order(2LL * batch * H * W * Cin);
     const dim3 grid = launch_grid<true>(p, bn);
     if (tc_trace_on())
         fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u\n", H, W, Cin, Cout, bw, bh, bn, S,
@@ -912,5 +923,18 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
 }
 
 bool tc_trace() { return tc_trace_on(); }
+
+// persistent tile order: n fastest, so the CTAs in flight share (and L2-hit) one A
+// (activation) tile and each A tile is consumed while hot -- with m fastest the CTAs sweep
+// every A tile once per N tile.  Measured per pass: c2 5.85 -> 5.81 ms, c4 21.68 -> 21.39,
+// c5 30.81 -> 30.55 (the weights are small enough to stay L2-resident either way).
+// ADX_TC_NFAST=0 restores m-fastest.
+bool n_fast_order(long long /*a_bytes*/) {
+    static const bool on = [] {
+        const char* e = getenv("ADX_TC_NFAST");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
 
 }  // namespace adx

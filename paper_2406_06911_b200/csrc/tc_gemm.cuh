@@ -35,6 +35,8 @@ struct TcArgs {
     int sub2 = 0;                         // conv: write only even (h, w) at (h/2, w/2) -> stride-2 conv
     int n_store = 0;                      // store only the first n_store columns (0: all N)
     int splits = 1;                       // filled by the launcher: split-K factor (cluster size)
+    int n_fast = 0;                       // filled by the launcher: persistent tile order n-fastest
+                                          //   (A tiles reused while L2-hot when A is the big operand)
 };
 
 // force (bn, splits) for every following launch (tuning); (0, 0) restores the plan table / model
