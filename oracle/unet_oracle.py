@@ -162,15 +162,20 @@ class UNetOracle:
 
     def temporal_attention(self, qkv, nf, HW, C):
         """self-attention across the nf frames of every (pixel, 64-wide head); qkv frame-major
-        [nf*HW, 3C]; probabilities and the output accumulate unrounded (one rounding at the end)"""
+        [nf*HW, 3C].  bf16 mode (temporal_mma_k, <= 16 frames): unnormalised P = exp(S - max)
+        rounded to bf16 for the P.V product, divided by the fp32 row sum; more frames and the
+        exact mode (CUDA-core kernel): P unrounded.  One rounding of the output."""
         def heads(x):
             return x.reshape(nf, HW, C // 64, 64)
         q, k, v = heads(qkv[:, :C]), heads(qkv[:, C:2 * C]), heads(qkv[:, 2 * C:])
         S = np.einsum("fphd,gphd->phfg", q, k) * self.dt(0.125)
         S = S - S.max(axis=-1, keepdims=True)
         P = np.exp(S)
-        P = P / P.sum(axis=-1, keepdims=True)
-        return self.r(np.einsum("phfg,gphd->fphd", P, v).reshape(nf * HW, C))
+        lsum = P.sum(axis=-1, keepdims=True)
+        if nf <= 16:
+            P = self.r(P)
+        O = np.einsum("phfg,gphd->fphd", P / lsum, v)
+        return self.r(O.reshape(nf * HW, C))
 
     def motion(self, stage, xs):
         """temporal motion module over the frames (nf, H, W, C) of a stage output

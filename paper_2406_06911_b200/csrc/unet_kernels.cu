@@ -790,6 +790,128 @@ __global__ void __launch_bounds__(128) temporal_attn_k(const T* qkv, int nf, int
     for (int d = 0; d < D; d += 8) Vec8<T>::store(op + d, Vec8<T>::pack(o + d));
 }
 
+// bf16 motion-module attention for up to 16 frames on the tensor cores (mma.sync m16n8k16):
+// per (pixel, head) item one warp computes S = Q K^T (16 x 16, K = 64 dims: 2 n8 tiles x 4
+// k16 steps) from fragments loaded straight from the packed QKV rows, the row softmax in
+// registers (quad shuffles), then O = P V (P re-used from the S accumulators as the A
+// fragment, rounded to bf16; V via ldmatrix.trans from a swizzled 2 KB SMEM copy) and
+// O / rowsum.  Frames >= nf are zero rows / masked keys.
+__device__ __forceinline__ uint32_t ld_b32(const bf16* p) { return *reinterpret_cast<const uint32_t*>(p); }
+__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(128) temporal_mma_k(const bf16* qkv, int nf, int HW, int C, bf16* out) {
+    pdl_wait();
+    __shared__ __align__(128) uint8_t vsm[4][16 * 128];  // per warp: V [16 frames][64 dims] bf16, swizzled
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, heads = C / 64;
+    const long long item = static_cast<long long>(blockIdx.x) * 4 + warp;
+    if (item >= static_cast<long long>(HW) * heads) return;  // warp-uniform
+    const int p = static_cast<int>(item / heads), h = static_cast<int>(item % heads);
+    const long long fs = static_cast<long long>(HW) * 3 * C;  // frame stride (elements)
+    const bf16* qb = qkv + static_cast<long long>(p) * 3 * C + h * 64;
+    const int g = lane >> 2, t = lane & 3;
+    // V rows -> SMEM (16-byte chunks, chunk c of frame r at (c ^ (r & 7))), zero past nf
+    uint8_t* vs = vsm[warp];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        const int i = lane + 32 * it, r = i >> 3, c = i & 7;
+        uint4 u = make_uint4(0, 0, 0, 0);
+        if (r < nf) u = *reinterpret_cast<const uint4*>(qb + r * fs + 2 * C + c * 8);
+        *reinterpret_cast<uint4*>(vs + r * 128 + ((c ^ (r & 7)) << 4)) = u;
+    }
+    // S = Q K^T
+    float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    const bool r0ok = g < nf, r1ok = g + 8 < nf;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+        const int c = ks * 16 + 2 * t;
+        uint32_t a[4];
+        a[0] = r0ok ? ld_b32(qb + g * fs + c) : 0u;
+        a[1] = r1ok ? ld_b32(qb + (g + 8) * fs + c) : 0u;
+        a[2] = r0ok ? ld_b32(qb + g * fs + c + 8) : 0u;
+        a[3] = r1ok ? ld_b32(qb + (g + 8) * fs + c + 8) : 0u;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int kf = nt * 8 + g;  // key frame of this lane's B column
+            const bool ok = kf < nf;
+            const uint32_t b0 = ok ? ld_b32(qb + kf * fs + C + c) : 0u;
+            const uint32_t b1 = ok ? ld_b32(qb + kf * fs + C + c + 8) : 0u;
+            mma16816(sacc[nt], a, b0, b1);
+        }
+    }
+    // softmax over the 16 keys of rows g and g + 8 (quad lanes hold 4 keys each)
+    const float sl2 = 0.125f * 1.4426950408889634f;
+    float m0 = -3.0e38f, m1 = -3.0e38f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const bool kok = nt * 8 + 2 * t + e < nf;
+            sacc[nt][e] = kok ? sacc[nt][e] * sl2 : -3.0e38f;
+            sacc[nt][2 + e] = kok ? sacc[nt][2 + e] * sl2 : -3.0e38f;
+            m0 = fmaxf(m0, sacc[nt][e]);
+            m1 = fmaxf(m1, sacc[nt][2 + e]);
+        }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            sacc[nt][e] = exp2f(sacc[nt][e] - m0);
+            sacc[nt][2 + e] = exp2f(sacc[nt][2 + e] - m1);
+            l0 += sacc[nt][e];
+            l1 += sacc[nt][2 + e];
+        }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    const uint32_t pa[4] = {pack_bf2(sacc[0][0], sacc[0][1]), pack_bf2(sacc[0][2], sacc[0][3]),
+                            pack_bf2(sacc[1][0], sacc[1][1]), pack_bf2(sacc[1][2], sacc[1][3])};
+    __syncwarp();
+    // O = P V: 8 dim tiles; ldmatrix.x4.trans yields (b0, b1) of two dim tiles
+    float oacc[8][4];
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) oacc[dt][0] = oacc[dt][1] = oacc[dt][2] = oacc[dt][3] = 0.f;
+    const uint32_t vbase = static_cast<uint32_t>(__cvta_generic_to_shared(vs));
+#pragma unroll
+    for (int d2 = 0; d2 < 4; ++d2) {
+        const int mtx = lane >> 3, fr = (mtx & 1) * 8 + (lane & 7), ch = 2 * d2 + (mtx >> 1);
+        const uint32_t addr = vbase + fr * 128 + ((ch ^ (fr & 7)) << 4);
+        uint32_t b[4];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+                     : "r"(addr));
+        mma16816(oacc[2 * d2], pa, b[0], b[1]);
+        mma16816(oacc[2 * d2 + 1], pa, b[2], b[3]);
+    }
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+    bf16* ob = out + static_cast<long long>(p) * C + h * 64 + 2 * t;
+    const long long os = static_cast<long long>(HW) * C;
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+        if (r0ok)
+            *reinterpret_cast<uint32_t*>(ob + g * os + dt * 8) = pack_bf2(oacc[dt][0] * i0, oacc[dt][1] * i0);
+        if (r1ok)
+            *reinterpret_cast<uint32_t*>(ob + (g + 8) * os + dt * 8) = pack_bf2(oacc[dt][2] * i1, oacc[dt][3] * i1);
+    }
+}
+
 template <typename T, int NF>
 void temporal_launch(const T* qkv, int frames, int HW, int C, T* out, cudaStream_t st) {
     if constexpr (NF > 4) {
@@ -951,6 +1073,17 @@ void temporal_attention_t(const T* qkv, int frames, int HW, int C, T* out, cudaS
     temporal_launch<T, 32>(qkv, frames, HW, C, out, st);
 }
 void temporal_attention(const __nv_bfloat16* qkv, int frames, int HW, int C, __nv_bfloat16* out, cudaStream_t st) {
+    static const bool cuda_cores = [] {  // ADX_TEMPORAL=cc: the CUDA-core kernel for every frame count
+        const char* e = getenv("ADX_TEMPORAL");
+        return e && std::string(e) == "cc";
+    }();
+    if (frames <= 16 && frames >= 2 && C % 64 == 0 && !cuda_cores) {  // tensor-core path
+        const long long items = static_cast<long long>(HW) * (C / 64);
+        CKU(launch_pdl(temporal_mma_k, dim3(static_cast<unsigned>((items + 3) / 4)), dim3(128), 0, st, 1, qkv, frames,
+                       HW, C, out));
+        CKU(cudaGetLastError());
+        return;
+    }
     temporal_attention_t(qkv, frames, HW, C, out, st);
 }
 void temporal_attention(const float* qkv, int frames, int HW, int C, float* out, cudaStream_t st) {
