@@ -207,3 +207,24 @@ def test_unet_video_async_invariants_bit_exact():
     ser, _ = adx.run_serial(plan, m, part, x, s)
     par, _ = adx.run_parallel(plan, m, part, x, s, plan.D)
     assert np.array_equal(ser.latent_matrix(), par.latent_matrix())
+
+
+@pytest.mark.parametrize("family", ["video", "xl_cfg"])
+def test_unet_batched_families_rank_session_matches_sequential(family):
+    """the one-process-per-GPU program (rank.cu) with one rank on the batched families
+    (16-frame video stages, CFG batch-2 stages): bit-exact with sequential_denoise"""
+    if family == "video":
+        m, s, x = small_video(16)
+    else:
+        m = adx.build_unet_denoiser(**SMALL_XL)
+        s = adx.build_schedule(3, 0.01, 0.15)
+        x = adx.Latent(O.random_normals(13, m.data_dim()).astype(np.float64), 3)
+    T = 3
+    plan = adx.plan_async(T, 1, 1, 1)
+    part = adx.partition_balanced(m, 1)
+    sess = adx.RankSession(m, s, plan, part, 0, adx.nccl_unique_id(), 0, "bf16")
+    d = m.data_dim()
+    lat, eps = np.zeros((T + 1, d)), np.zeros((T, d))
+    sess.run_into(np.ascontiguousarray(x.values, np.float64), lat, eps)
+    seq = adx.sequential_denoise(m, x, s, precision="bf16")
+    assert np.array_equal(lat, seq.latent_matrix())
