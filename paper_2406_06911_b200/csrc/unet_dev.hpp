@@ -66,8 +66,8 @@ private:
     void transformer(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
     void motion(int stage, const __nv_bfloat16* x, int H, int W, int C, __nv_bfloat16* y, cudaStream_t st);
     void motion_exact(int stage, const float* x, int H, int W, int C, float* y, cudaStream_t st);
-    // GroupNorm of every image of the batch: per image (fused single launch) for 1-2 images,
-    // one batched two-kernel launch for video frames
+    // GroupNorm of every image of the batch: the fused single launch for one image, one
+    // batched two-kernel launch for CFG pairs and video frames
     template <typename T>
     void gn_images(const Cat2T<T>& x, int HW, const float* gamma, const float* beta, float eps, int act, T* out,
                    UScratch& s, cudaStream_t st);
