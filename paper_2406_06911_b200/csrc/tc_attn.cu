@@ -232,7 +232,9 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
                                                       const __grid_constant__ CUtensorMap tmK,
                                                       const __grid_constant__ CUtensorMap tmV, const AttnArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned by offsetting the __shared__ array itself (not through an integer
+    // cast), so every access through `smem` stays a shared-space LDS / STS, not a generic LD / ST
+    uint8_t* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
     constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2;
     constexpr int XCH_OFF = Q_B + STG * (K_B + V_B) + 256;  // after the barriers
     uint8_t* sQ = smem;

@@ -312,7 +312,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                                                          const __grid_constant__ CUtensorMap tmB, const TcArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment of the swizzled tiles
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned by offsetting the __shared__ array itself (not through an integer
+    // cast), so every access through `smem` stays a shared-space LDS / STS, not a generic LD / ST
+    uint8_t* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
     constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
     constexpr uint32_t ACC_COLS = tmem_cols<BN>();  // one accumulator; two are allocated
     uint8_t* sA = smem;
