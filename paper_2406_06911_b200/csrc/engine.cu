@@ -1058,14 +1058,25 @@ void Session::download(double* lat, double* eps) {
     CK(cudaMemcpyAsync(out_host_, traj_lat_, nl * ab_bytes_, cudaMemcpyDeviceToHost, v0.comp));
     CK(cudaMemcpyAsync(offset(out_host_, nl * ab_bytes_), traj_eps_, ne * ab_bytes_, cudaMemcpyDeviceToHost, v0.comp));
     CK(cudaStreamSynchronize(v0.comp));
+    // pinned staging -> caller's fp64 arrays; large trajectories (UNet: 2T+1 latents of
+    // 37K-262K values) are widened on several host threads -- single-threaded this was
+    // ~2% of the c2 end-to-end time
     auto conv = [&](const void* src, double* dst, size_t n) {
         if (!dst) return;
-        if (ab_bytes_ == 8) {
-            std::memcpy(dst, src, n * 8);
-        } else {
-            const float* f = static_cast<const float*>(src);
-            for (size_t i = 0; i < n; ++i) dst[i] = f[i];
-        }
+        auto part = [&](size_t b, size_t e) {
+            if (ab_bytes_ == 8) {
+                std::memcpy(dst + b, static_cast<const double*>(src) + b, (e - b) * 8);
+            } else {
+                const float* f = static_cast<const float*>(src);
+                for (size_t i = b; i < e; ++i) dst[i] = f[i];
+            }
+        };
+        const size_t nt = n < (1u << 20) ? 1 : std::min<size_t>(8, std::max(1u, std::thread::hardware_concurrency()));
+        if (nt == 1) return part(0, n);
+        std::vector<std::thread> th;
+        for (size_t k = 1; k < nt; ++k) th.emplace_back(part, n * k / nt, n * (k + 1) / nt);
+        part(0, n / nt);
+        for (auto& t : th) t.join();
     };
     conv(out_host_, lat, nl);
     conv(offset(out_host_, nl * ab_bytes_), eps, ne);
