@@ -1050,6 +1050,26 @@ void Session::run(const double* x_T, double* lat, double* eps, RunStatsOut* stat
     }
 }
 
+// pinned staging -> the caller's fp64 arrays; large trajectories (UNet: 2T+1 latents of
+// 37K-262K values) are widened on several host threads -- single-threaded this was ~2% of
+// the c2 end-to-end time
+void widen_to_f64(const void* src, int bytes, double* dst, size_t n) {
+    auto part = [&](size_t b, size_t e) {
+        if (bytes == 8) {
+            std::memcpy(dst + b, static_cast<const double*>(src) + b, (e - b) * 8);
+        } else {
+            const float* f = static_cast<const float*>(src);
+            for (size_t i = b; i < e; ++i) dst[i] = f[i];
+        }
+    };
+    const size_t nt = n < (1u << 20) ? 1 : std::min<size_t>(8, std::max(1u, std::thread::hardware_concurrency()));
+    if (nt == 1) return part(0, n);
+    std::vector<std::thread> th;
+    for (size_t k = 1; k < nt; ++k) th.emplace_back(part, n * k / nt, n * (k + 1) / nt);
+    part(0, n / nt);
+    for (auto& t : th) t.join();
+}
+
 void Session::download(double* lat, double* eps) {
     VDev& v0 = vd_[0];
     setdev(v0.ordinal);
@@ -1058,28 +1078,8 @@ void Session::download(double* lat, double* eps) {
     CK(cudaMemcpyAsync(out_host_, traj_lat_, nl * ab_bytes_, cudaMemcpyDeviceToHost, v0.comp));
     CK(cudaMemcpyAsync(offset(out_host_, nl * ab_bytes_), traj_eps_, ne * ab_bytes_, cudaMemcpyDeviceToHost, v0.comp));
     CK(cudaStreamSynchronize(v0.comp));
-    // pinned staging -> caller's fp64 arrays; large trajectories (UNet: 2T+1 latents of
-    // 37K-262K values) are widened on several host threads -- single-threaded this was
-    // ~2% of the c2 end-to-end time
-    auto conv = [&](const void* src, double* dst, size_t n) {
-        if (!dst) return;
-        auto part = [&](size_t b, size_t e) {
-            if (ab_bytes_ == 8) {
-                std::memcpy(dst + b, static_cast<const double*>(src) + b, (e - b) * 8);
-            } else {
-                const float* f = static_cast<const float*>(src);
-                for (size_t i = b; i < e; ++i) dst[i] = f[i];
-            }
-        };
-        const size_t nt = n < (1u << 20) ? 1 : std::min<size_t>(8, std::max(1u, std::thread::hardware_concurrency()));
-        if (nt == 1) return part(0, n);
-        std::vector<std::thread> th;
-        for (size_t k = 1; k < nt; ++k) th.emplace_back(part, n * k / nt, n * (k + 1) / nt);
-        part(0, n / nt);
-        for (auto& t : th) t.join();
-    };
-    conv(out_host_, lat, nl);
-    conv(offset(out_host_, nl * ab_bytes_), eps, ne);
+    if (lat) widen_to_f64(out_host_, ab_bytes_, lat, nl);
+    if (eps) widen_to_f64(offset(out_host_, nl * ab_bytes_), ab_bytes_, eps, ne);
 }
 
 double Session::time_runs(int iters) {

@@ -204,4 +204,7 @@ int rank_session_kernels(void* s);
 // kernel nodes of this library in a captured CUDA graph (NCCL kernels excluded)
 int graph_kernel_nodes(cudaGraph_t g);
 
+// fp32 / fp64 host staging -> fp64 (multi-threaded for large arrays)
+void widen_to_f64(const void* src, int bytes, double* dst, size_t n);
+
 }  // namespace adx

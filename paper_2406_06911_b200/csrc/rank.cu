@@ -132,6 +132,7 @@ public:
             cudaFree(kv.second[1]);
         }
         for (auto& kv : H_) cudaFree(kv.second);
+        if (host_stage_) cudaFreeHost(host_stage_);
         cudaFree(EPS_[0]);
         cudaFree(EPS_[1]);
         cudaFree(traj_lat_);
@@ -157,23 +158,12 @@ public:
             throw std::domain_error("predict_x0: non-finite eps at t=" + std::to_string(T_ - h[1]));
         if (rank_ == 0 && (lat || eps)) {
             const size_t nl = static_cast<size_t>(T_ + 1) * d_, ne = static_cast<size_t>(T_) * d_;
-            std::vector<unsigned char> buf((nl + ne) * ab_bytes_);
-            CKR(cudaMemcpy(buf.data(), traj_lat_, nl * ab_bytes_, cudaMemcpyDeviceToHost));
-            CKR(cudaMemcpy(buf.data() + nl * ab_bytes_, traj_eps_, ne * ab_bytes_, cudaMemcpyDeviceToHost));
-            auto conv = [&](const unsigned char* src, double* dst, size_t n) {
-                if (!dst) return;
-                for (size_t i = 0; i < n; ++i) {
-                    if (ab_bytes_ == 8) {
-                        std::memcpy(&dst[i], src + i * 8, 8);
-                    } else {
-                        float f;
-                        std::memcpy(&f, src + i * 4, 4);
-                        dst[i] = f;
-                    }
-                }
-            };
-            conv(buf.data(), lat, nl);
-            conv(buf.data() + nl * ab_bytes_, eps, ne);
+            if (!host_stage_) CKR(cudaMallocHost(&host_stage_, (nl + ne) * ab_bytes_));  // pinned, reused
+            unsigned char* buf = static_cast<unsigned char*>(host_stage_);
+            CKR(cudaMemcpy(buf, traj_lat_, nl * ab_bytes_, cudaMemcpyDeviceToHost));
+            CKR(cudaMemcpy(buf + nl * ab_bytes_, traj_eps_, ne * ab_bytes_, cudaMemcpyDeviceToHost));
+            if (lat) widen_to_f64(buf, ab_bytes_, lat, nl);
+            if (eps) widen_to_f64(buf + nl * ab_bytes_, ab_bytes_, eps, ne);
         }
     }
 
@@ -333,6 +323,7 @@ private:
     Partition part_;
     std::vector<double> ab_;
     int rank_, T_ = 0, d_ = 0, ab_bytes_ = 0, kernels_ = 0;
+    void* host_stage_ = nullptr;  // pinned trajectory staging (rank 0)
     RunOptions opts_;
     std::vector<RankOp> ops_;
     std::vector<int> seg_first_, seg_last_, stage_seg_;
