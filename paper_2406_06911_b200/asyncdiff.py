@@ -34,7 +34,7 @@ __all__ = [
     "RankSession", "nccl_unique_id", "save_checkpoint",
     "load_checkpoint", "plan_to_json", "plan_from_json", "CostModel", "LatencyReport", "predict_sequential",
     "predict_async", "CostComparison", "calibrate_and_compare", "round_exchange_bytes", "SimilarityProfile",
-    "similarity_profile", "build_unet_denoiser", "unet_stage_info", "unet_stage_params", "unet_context",
+    "similarity_profile", "warmup_sweep", "build_unet_denoiser", "unet_stage_info", "unet_stage_params", "unet_context",
 ]
 
 PRECISIONS = {"f64": 0, "f32": 1, "bf16": 2}
@@ -1155,6 +1155,34 @@ class DivergenceReport:
     per_step_mse: List[float]
     final_mse: float
     final_max_abs: float
+
+
+def warmup_sweep(m: LayeredDenoiser, x_T: Latent, schedule: NoiseSchedule,
+                 matrix: Sequence[Tuple[int, int, int]], precision: Optional[str] = None,
+                 devices: Optional[Sequence[int]] = None) -> List[dict]:
+    """The warm-up sweep of experiment.cpp:312-389 (cmd_sweep) on the GPU -- the paper's
+    Table-2 analogue, quality of the async trajectory against the warm-up length.  The
+    reference scores each cell against its Gaussian-mixture oracle (final MSE / NLL,
+    out of scope here); this scores it against the sequential trajectory of the same model
+    and x_T (the divergence of metrics.cpp:9-30).  For every (N, w, S) of `matrix`:
+    MAC-balanced partition (partition.cpp:133), plan_async, the async run through
+    run_serial (identical numerics to run_parallel on N GPUs), plan_counts; one row each
+    with the sweep CSV's columns (experiment.cpp:368-383) plus the divergence."""
+    seq = sequential_denoise(m, x_T, schedule, precision=precision)
+    ref = seq.latents[-1].values
+    rows = []
+    for N, w, S in matrix:
+        part = partition_balanced(m, N)
+        plan = plan_async(schedule.T, w, N, S)
+        traj, _ = run_serial(plan, m, part, x_T, schedule, precision=precision, devices=devices)
+        rep = compare_trajectories(seq, traj)
+        cnt = plan_counts(plan, part)
+        fin = traj.latents[-1].values
+        rows.append(dict(config=f"N{N}_w{w}_S{S}", N=N, w=w, S=S, per_device_macs=cnt.max_device_macs,
+                         device_count=plan.D, broadcast_count=cnt.broadcasts_paper_convention,
+                         final_mse=rep.final_mse, final_max_abs=rep.final_max_abs,
+                         final_rel_l2=float(np.linalg.norm(fin - ref) / (np.linalg.norm(ref) + 1e-300))))
+    return rows
 
 
 def compare_trajectories(seq: Trajectory, async_traj: Trajectory) -> DivergenceReport:

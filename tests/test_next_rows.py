@@ -221,3 +221,18 @@ def test_unet_video_motion_build():
         adx.build_unet_denoiser(frames=1, motion=True, **kw)
     with pytest.raises(adx.InvalidArgument):
         adx.build_unet_denoiser(frames=33, motion=True, **kw)
+
+
+@pytest.mark.gpu
+def test_warmup_sweep_on_gpu():  # experiment.cpp:312-389 (cmd_sweep), scored against the sequential run
+    m = adx.build_toy_denoiser(6, [2, 8, 8, 8, 8, 8, 2], "unet-mirror", 11)
+    s = adx.build_schedule(20, 0.01, 0.15)
+    x = adx.Latent(O.random_normals(12, 2), 20)
+    rows = adx.warmup_sweep(m, x, s, [(2, 20, 1), (2, 1, 1), (3, 3, 1), (3, 1, 2)], precision="f64")
+    assert [r["config"] for r in rows] == ["N2_w20_S1", "N2_w1_S1", "N3_w3_S1", "N3_w1_S2"]
+    assert rows[0]["final_mse"] == 0.0 and rows[0]["final_rel_l2"] == 0.0  # w = T: sequential
+    for r in rows[1:]:
+        assert np.isfinite(r["final_mse"]) and r["final_rel_l2"] > 0.0
+    plan = adx.plan_async(20, 1, 3, 2)
+    assert rows[3]["device_count"] == plan.D == 4
+    assert rows[3]["per_device_macs"] == adx.plan_counts(plan, adx.partition_balanced(m, 3)).max_device_macs
