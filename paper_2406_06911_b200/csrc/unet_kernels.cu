@@ -102,7 +102,13 @@ __device__ __forceinline__ typename Vec8<T>::raw cat_vec(const Cat2T<T>& x, long
 constexpr int kGnMaxChunks = 148;  // one statistics CTA per SM
 // pixel chunks per image: one per SM for 1-2 images; a video batch shares ~2 CTAs per SM so
 // the last CTA's merge reads few partials per (image, group)
-inline int gn_chunk_cap(int batch) { return batch <= 2 ? kGnMaxChunks : std::max(4, 2 * kGnMaxChunks / batch); }
+inline int gn_chunk_cap(int batch) {
+    static const int per_sm = [] {  // ADX_GN_CTAS_PER_SM: statistics CTAs per SM for batches > 2
+        const char* e = getenv("ADX_GN_CTAS_PER_SM");
+        return e ? std::max(1, atoi(e)) : 2;
+    }();
+    return batch <= 2 ? kGnMaxChunks : std::max(4, per_sm * kGnMaxChunks / batch);
+}
 struct GnLayout {
     unsigned* counter;
     float2* ab;
