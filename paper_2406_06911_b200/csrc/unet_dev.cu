@@ -773,8 +773,7 @@ void UNetDevice::attention_exact(UScratch& s, const float* q, long long ldq, con
         a.ldo = Lkp;
         a.out_scale = 0.125f;
         tc_gemm_strided(s.sq + h * 192, 3LL * C, ks + h * 192, 3LL * C, L, Lk, 192, a, st);
-        softmax_rows_f32(s.S, Lkp, L, Lk, Lkp, st);
-        split3(s.S, L, Lkp, Lkp, Lkp, 0, s.sa, st);
+        softmax_split_rows(s.S, Lkp, L, Lk, Lkp, s.sa, st);  // P' = split(softmax(S)), S read once
         const bf16* vt = vts ? vts + static_cast<long long>(h) * 64 * 3 * Lkp : s.sv;
         if (!vts) {
             transpose_f32(v + h * 64, ldv, Lk, Lkp, 64, s.fvt, st);

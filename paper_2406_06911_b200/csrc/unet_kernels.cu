@@ -670,6 +670,56 @@ __global__ void softmax_rows_f32_k(float* S, long long lds, int valid, int padde
     for (int c = threadIdx.x; c < padded; c += blockDim.x) r[c] = c < valid ? expf(r[c] - mx) * inv : 0.f;
 }
 
+// the ADX_F32 attention's softmax fused with the split of P: row softmax over the first
+// `valid` columns (same reductions as softmax_rows_f32_k) written straight as the A-side
+// split operand [hi | hi | lo] (3 x padded bf16 per row): S is read, never written back
+__global__ void softmax_split_rows_k(const float* S, long long lds, int valid, int padded, bf16* out) {
+    pdl_wait();
+    const float* r = S + static_cast<long long>(blockIdx.x) * lds;
+    __shared__ float red[32];
+    float mx = -INFINITY;
+    for (int c = threadIdx.x; c < valid; c += blockDim.x) mx = fmaxf(mx, r[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    mx = red[0];
+    __syncthreads();
+    float s = 0.f;
+    for (int c = threadIdx.x; c < valid; c += blockDim.x) s += expf(r[c] - mx);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        red[0] = t;
+    }
+    __syncthreads();
+    const float inv = 1.0f / red[0];
+    bf16* o = out + static_cast<long long>(blockIdx.x) * 3 * padded;
+    for (int c = threadIdx.x * 8; c < padded; c += blockDim.x * 8) {
+        float hi[8], lo[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float p = c + k < valid ? expf(r[c + k] - mx) * inv : 0.f;
+            hi[k] = __bfloat162float(__float2bfloat16(p));
+            lo[k] = p - hi[k];
+        }
+        const uint4 h = pack8(hi), l = pack8(lo);
+        *reinterpret_cast<uint4*>(o + c) = h;
+        *reinterpret_cast<uint4*>(o + padded + c) = h;
+        *reinterpret_cast<uint4*>(o + 2 * padded + c) = l;
+    }
+}
+
 __global__ void transpose_f32_k(const float* V, long long ldv, int L, int Lpad, int hd, float* VT) {
     pdl_wait();
     __shared__ float tile[32][33];
@@ -1103,6 +1153,13 @@ void cfg_combine(const float* e, long long n, float scale, float* out, cudaStrea
 
 void softmax_rows_f32(float* S, long long lds, int rows, int valid, int padded, cudaStream_t st) {
     CKU(launch_pdl(softmax_rows_f32_k, dim3(rows), dim3(256), 0, st, 1, S, lds, valid, padded));
+    CKU(cudaGetLastError());
+}
+
+void softmax_split_rows(const float* S, long long lds, int rows, int valid, int padded, __nv_bfloat16* out,
+                        cudaStream_t st) {
+    if (padded % 8) throw std::invalid_argument("softmax_split_rows: padded width must be a multiple of 8");
+    CKU(launch_pdl(softmax_split_rows_k, dim3(rows), dim3(256), 0, st, 1, S, lds, valid, padded, out));
     CKU(cudaGetLastError());
 }
 

@@ -32,6 +32,10 @@ void layer_norm(const float* x, int tokens, int C, const float* gamma, const flo
 // A'.B'^T = hi.hi + hi.lo + lo.hi (the lo.lo term is ~2^-16 relative)
 void split3(const float* x, long long rows, int cols, long long ldx, int g, int pattern, __nv_bfloat16* out,
             cudaStream_t st);
+// fp32 row softmax over the first `valid` columns written as the split-bf16 A operand
+// [hi | hi | lo] (3 x padded per row; split3 pattern 0 with g = padded); S is not modified
+void softmax_split_rows(const float* S, long long lds, int rows, int valid, int padded, __nv_bfloat16* out,
+                        cudaStream_t st);
 // fp32 row softmax over the first `valid` columns, in place, zeros in [valid, padded)
 void softmax_rows_f32(float* S, long long lds, int rows, int valid, int padded, cudaStream_t st);
 // VT[d][k] = V[k * ldv + d] (k < L; 0 for L <= k < Lpad), fp32, hd rows
