@@ -1,6 +1,6 @@
 """Per-shape isolated launch times of one UNet pass (ADX_TC_TRACE=1 + profile_model_pass):
 aggregates GEMM / conv / attention / norm launches by shape, sorted by total time.
-usage: tools_shape_profile.py [bench config, default c2]"""
+usage: tools_shape_profile.py [bench config, default c2] [precision, default bf16]"""
 import collections, os, re, subprocess, sys
 HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if len(sys.argv) > 2 and sys.argv[2] == "--child":
@@ -9,10 +9,11 @@ if len(sys.argv) > 2 and sys.argv[2] == "--child":
     from bench import CONFIGS
     cfg = CONFIGS[sys.argv[1]]
     m = adx.build_unet_denoiser(seed=cfg["seed"], **cfg["unet"])
-    adx.profile_model_pass(m, cfg["T"])
+    adx.profile_model_pass(m, cfg["T"], sys.argv[3])
     sys.exit(0)
 conf = sys.argv[1] if len(sys.argv) > 1 else "c2"
-err = subprocess.run([sys.executable, __file__, conf, "--child"], env=dict(os.environ, ADX_TC_TRACE="1"),
+prec = sys.argv[2] if len(sys.argv) > 2 else "bf16"
+err = subprocess.run([sys.executable, __file__, conf, "--child", prec], env=dict(os.environ, ADX_TC_TRACE="1"),
                      capture_output=True, text=True).stderr.splitlines()
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
 last = None
