@@ -43,6 +43,7 @@ namespace adx {
             throw cuda_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x); \
     } while (0)
 
+bool tma_store_enabled();
 bool n_fast_order(long long a_bytes);
 
 namespace {
@@ -76,6 +77,13 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, int c0, i
             sa(dst)),
         "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(sa(b))
         : "memory");
+}
+// SMEM -> global bulk tensor store (bulk-group completion)
+__device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(sa(src))
+                 : "memory");
 }
 __device__ __forceinline__ void tma4d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, uint64_t* b) {
     asm volatile(
@@ -178,7 +186,7 @@ __device__ __forceinline__ const float* chan_row(const TcArgs& p, long long m, i
 
 // fused epilogue on 16 accumulator columns [nb, nb + 16) of output row m
 __device__ __forceinline__ void epi16(const TcArgs& p, long long m, const float* ca, int nb, float* v,
-                                      const uint4* rpre = nullptr) {
+                                      const uint4* rpre = nullptr, uint4* sdst = nullptr) {
     const int nlim = p.n_store ? p.n_store : p.N;
     if ((((p.ldo | p.ldr) & 7) == 0) && nb + 16 <= nlim && !p.residual_f32) {
         // vectorised: 16-byte loads / stores
@@ -218,7 +226,7 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, const float*
 #pragma unroll
             for (int j = 0; j < 4; ++j) op[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         } else {
-            uint4* op = reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + nb);
+            uint4* op = sdst ? sdst : reinterpret_cast<uint4*>(p.out_bf16 + m * p.ldo + nb);
             op[0] = pack_bf16x8(v);
             op[1] = pack_bf16x8(v + 8);
         }
@@ -296,6 +304,11 @@ __device__ __forceinline__ float4 reduce_dsmem4(const uint32_t* a, int S, int of
     return acc;
 }
 
+// TMA-store staging chunks per epilogue warp (its share of the BN / 16 column chunks);
+// BN = 256 tiles do not use the TMA store (no SMEM left beside their pipeline)
+template <int BN>
+constexpr int kStageChunks() { return BN > 192 ? 0 : (BN / 16 + 1) / 2; }
+
 // ------------------------------------------------------------------ kernel
 // epilogue warps: EPW / 4 per TMEM lane quadrant, each over its share of the tile's
 // 16-column chunks (more loads / stores in flight for the 1-tile-per-CTA small GEMMs)
@@ -309,7 +322,8 @@ __device__ __forceinline__ void epi_chunks(int nch, int part, int& c0, int& c1) 
 
 template <int BN, bool CONV>
 __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                         const __grid_constant__ CUtensorMap tmB, const TcArgs p) {
+                                                         const __grid_constant__ CUtensorMap tmB,
+                                                         const __grid_constant__ CUtensorMap tmC, const TcArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment of the swizzled tiles
     // 1024-byte aligned by offsetting the __shared__ array itself (not through an integer
@@ -445,12 +459,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
         const int q = warp & 3;             // TMEM lane quadrant this warp may access
         const int part = (warp - 2) >> 2;   // which share of the tile's column chunks
         const int row = q * 32 + lane;
+        // TMA-store staging: per warp, one 32-row x 16-column bf16 block (1 KB) per chunk of its share
+        uint8_t* stage = sB + STAGES * B_BYTES + 256 + (warp - 2) * kStageChunks<BN>() * 1024;
         int lu = 0;
         for (int u = u0; u < uend; u += ustride, ++lu) {
             int tile_m, tile_n, img, h0, w0;
             coords(u, tile_m, tile_n, img, h0, w0);
             const int n0 = tile_n * BN;
             const int acc = lu & 1;
+            if (p.tma_store && lu > 0) {  // the previous tile's stores have read their staging blocks
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+            }
             bar_wait(&tfull[acc], (lu >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t trow = tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16);
@@ -501,7 +521,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                         }
                         float v[16];
                         tmem_ld16(trow + c, v);
-                        if (valid) epi16(p, m, ca, n0 + c, v, have ? rcur : nullptr);
+                        if (p.tma_store) {
+                            // rows past M are clipped by the TMA; their staging content is unused
+                            uint4* sd = reinterpret_cast<uint4*>(stage + ((c - cb) >> 4) * 1024 + lane * 32);
+                            if (valid) epi16(p, m, ca, n0 + c, v, have ? rcur : nullptr, sd);
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            __syncwarp();
+                            if (lane == 0) {
+                                tma_store2d(&tmC, stage + ((c - cb) >> 4) * 1024, n0 + c, tile_m * BM + q * 32);
+                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            }
+                        } else if (valid) {
+                            epi16(p, m, ca, n0 + c, v, have ? rcur : nullptr);
+                        }
                     }
                 }
             }
@@ -510,6 +542,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             __syncwarp();
             if (lane == 0) bar_arrive1(&tempty[acc]);
         }
+        if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     if (S > 1) {
         // split-K reduction: CTA `split` owns tile rows [r0, r1) and sums the S staged
@@ -583,19 +616,20 @@ EncodeTiledFn encode_fn() {
 }
 
 CUtensorMap make_map(const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-                     const cuuint32_t* box) {
+                     const cuuint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     CUtensorMap m;
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims,
-                                   strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return m;
 }
 
 template <int BN, bool CONV>
-void launch_t(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 grid, cudaStream_t st) {
-    constexpr size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256;
+void launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcArgs& p, dim3 grid,
+              cudaStream_t st) {
+    constexpr size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256 + EPW * kStageChunks<BN>() * 1024;
     static_assert(static_cast<size_t>(BM) * (BN + 4) * 4 <= STAGES * (BM * BK * 2 + BN * BK * 2),
                   "split-K staging must fit in the pipeline buffers");
     static bool attr[64] = {};
@@ -606,20 +640,21 @@ void launch_t(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 
         attr[dev] = true;
     }
     CKT(launch_pdl(tc_gemm_kernel<BN, CONV>, grid, dim3(kGemmThreads), smem, st, static_cast<unsigned>(p.splits), a,
-                   b, p));
+                   b, c, p));
 }
 
 template <bool CONV>
-void dispatch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& p, dim3 grid, int bn, cudaStream_t st) {
+void dispatch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcArgs& p, dim3 grid, int bn,
+              cudaStream_t st) {
     switch (bn) {
-        case 32: launch_t<32, CONV>(a, b, p, grid, st); break;
-        case 64: launch_t<64, CONV>(a, b, p, grid, st); break;
-        case 80: launch_t<80, CONV>(a, b, p, grid, st); break;
-        case 96: launch_t<96, CONV>(a, b, p, grid, st); break;
-        case 128: launch_t<128, CONV>(a, b, p, grid, st); break;
-        case 160: launch_t<160, CONV>(a, b, p, grid, st); break;
-        case 192: launch_t<192, CONV>(a, b, p, grid, st); break;
-        case 256: launch_t<256, CONV>(a, b, p, grid, st); break;
+        case 32: launch_t<32, CONV>(a, b, c, p, grid, st); break;
+        case 64: launch_t<64, CONV>(a, b, c, p, grid, st); break;
+        case 80: launch_t<80, CONV>(a, b, c, p, grid, st); break;
+        case 96: launch_t<96, CONV>(a, b, c, p, grid, st); break;
+        case 128: launch_t<128, CONV>(a, b, c, p, grid, st); break;
+        case 160: launch_t<160, CONV>(a, b, c, p, grid, st); break;
+        case 192: launch_t<192, CONV>(a, b, c, p, grid, st); break;
+        case 256: launch_t<256, CONV>(a, b, c, p, grid, st); break;
         default: throw std::invalid_argument("tc_gemm: BN must be 32/64/80/96/128/160/192/256");
     }
 }
@@ -647,7 +682,7 @@ int cluster_capacity_t(int S) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find({dev, S});
     if (it != cache.end()) return it->second;
-    constexpr size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256;
+    constexpr size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256 + EPW * kStageChunks<BN>() * 1024;
     CKT(cudaFuncSetAttribute(tc_gemm_kernel<BN, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(S * 64, 1, 1);
@@ -850,11 +885,23 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     p.n_tiles = (N + bn - 1) / bn;
     p.batch = 1;
     p.n_fast = S == 1 && p.n_tiles > 1 && n_fast_order(2LL * M * K);
+    // bf16 output through SMEM + TMA bulk stores (32 rows x 16 columns per store): full-line
+    // writes instead of 32 row-scattered 16-byte stores per warp instruction
+    CUtensorMap mc = ma;
+    p.tma_store = 0;
+    if (tma_store_enabled() && S == 1 && bn <= 192 && p.act != 2 && p.out_bf16 && !p.out_f32 && !p.n_store &&
+        N % 16 == 0 && p.ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(p.out_bf16) & 15) == 0) {
+        const cuuint64_t dc[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+        const cuuint64_t sc[1] = {static_cast<cuuint64_t>(p.ldo) * 2};
+        const cuuint32_t bc[2] = {16, 32};
+        mc = make_map(p.out_bf16, 2, dc, sc, bc, CU_TENSOR_MAP_SWIZZLE_NONE);
+        p.tma_store = 1;
+    }
     const dim3 grid = launch_grid<false>(p, bn);
     if (tc_trace_on())
         fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d act=%d grid=%ux%u\n", M, N, K, bn, S, p.act, grid.x, grid.y);
-    dispatch<false>(ma, mb, p, grid, bn, st);
-    tc_profile_measure(st, 1, 2.0 * M * N * K, [&](cudaStream_t s2) { dispatch<false>(ma, mb, p, grid, bn, s2); });
+    dispatch<false>(ma, mb, mc, p, grid, bn, st);
+    tc_profile_measure(st, 1, 2.0 * M * N * K, [&](cudaStream_t s2) { dispatch<false>(ma, mb, mc, p, grid, bn, s2); });
 }
 
 // 3x3 conv, stride 1, pad 1, as an implicit GEMM over NHWC bf16:
@@ -918,13 +965,22 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     if (tc_trace_on())
         fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u\n", H, W, Cin, Cout, bw, bh, bn, S,
                 grid.x, grid.y, grid.z);
-    dispatch<true>(ma, mb, p, grid, bn, st);
+    dispatch<true>(ma, mb, ma, p, grid, bn, st);  // (no TMA store for convs: tmC unused)
     // algorithmic FLOPs (a stride-2 conv does a quarter of the work it launches)
     tc_profile_measure(st, 0, 2.0 * batch * H * W * Cout * 9.0 * Cin / (p.sub2 ? 4.0 : 1.0),
-                       [&](cudaStream_t s2) { dispatch<true>(ma, mb, p, grid, bn, s2); });
+                       [&](cudaStream_t s2) { dispatch<true>(ma, mb, ma, p, grid, bn, s2); });
 }
 
 bool tc_trace() { return tc_trace_on(); }
+
+// ADX_TC_TMA_STORE=0: the GEMM epilogue stores straight from registers
+bool tma_store_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("ADX_TC_TMA_STORE");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
 
 // persistent tile order: n fastest, so the CTAs in flight share (and L2-hit) one A
 // (activation) tile and each A tile is consumed while hot -- with m fastest the CTAs sweep

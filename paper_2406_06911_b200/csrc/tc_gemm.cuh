@@ -35,6 +35,8 @@ struct TcArgs {
     int sub2 = 0;                         // conv: write only even (h, w) at (h/2, w/2) -> stride-2 conv
     int n_store = 0;                      // store only the first n_store columns (0: all N)
     int splits = 1;                       // filled by the launcher: split-K factor (cluster size)
+    int tma_store = 0;                    // filled by the launcher: bf16 output written per 32x16
+                                          //   chunk from SMEM by the TMA (GEMM, S = 1, BN <= 192)
     int n_fast = 0;                       // filled by the launcher: persistent tile order n-fastest
                                           //   (A tiles reused while L2-hot when A is the big operand)
 };
