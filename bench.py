@@ -197,6 +197,24 @@ def config_block(args, cfg, N):
             "parallelism": f"async-model-parallel n{N}" if N > 1 else "sequential (1 GPU)", "l2": l2}
 
 
+def measured_traffic(cfg, prec, kernel, launches):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel's launches over one
+    pass, from the committed ncu capture profiles/r01_<config>_dram_traffic.json
+    (tools/tools_ncu_traffic.py; same per-pass basis as `achieved`).  None when this config /
+    precision has no capture."""
+    name = next((k for k, v in CONFIGS.items() if v is cfg), None)
+    path = os.path.join(ROOT, "profiles", f"r01_{name}_dram_traffic.json")
+    if prec != "bf16" or not os.path.exists(path):
+        return None, None
+    fam = json.load(open(path))["families"].get(kernel)
+    if not fam:
+        return None, None
+    return fam["dram_bytes_per_pass"], (f"{kernel}: dram__bytes_read.sum + dram__bytes_write.sum per pass, summed "
+                                        f"over its {fam['launches_per_pass']:.0f} launches in the ncu capture "
+                                        f"{os.path.basename(path)} (cold cache per launch; {launches} of them are "
+                                        f"the conv/GEMM launches timed for `achieved`)")
+
+
 def roofline(m, cfg, prec, dev):
     """dominant kernel family over one full-model pass (CUDA events, graph of
     back-to-back passes): HBM GB/s of the stage GEMV (MLP) or TFLOP/s of the
@@ -216,8 +234,10 @@ def roofline(m, cfg, prec, dev):
         ach = cg_fl / (cg_ms * 1e-3) / 1e12
         fam = {k: dict(v, tflops=v["flops"] / (v["ms"] * 1e-3) / 1e12 if v["ms"] else 0.0) for k, v in prof.items()}
         whole = 2.0 * sum(st.cost_macs for st in m.stages) / (pass_ms * 1e-3) / 1e12
+        traffic, tnote = measured_traffic(cfg, prec, "tc_gemm_kernel", prof["conv3x3"]["launches"] + prof["gemm"]["launches"])
         return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": None, "peak_source": src,
+                "traffic": traffic, "traffic_note": tnote,
+                "flop_per_dram_byte": cg_fl / traffic if traffic else None, "peak_source": src,
                 "kernel": "tc_gemm_kernel (tcgen05 conv3x3 + GEMM launches of one UNet pass)",
                 "families": fam, "ms_per_pass": pass_ms, "whole_pass_tflops": whole,
                 "stage_launches_per_pass": launches}
