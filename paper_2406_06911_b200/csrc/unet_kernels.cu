@@ -98,8 +98,9 @@ __device__ __forceinline__ typename Vec8<T>::raw cat_vec(const Cat2T<T>& x, long
     return c < x.c0 ? Vec8<T>::load(x.p0 + pix * x.c0 + c) : Vec8<T>::load(x.p1 + pix * x.c1 + (c - x.c0));
 }
 
-// GroupNorm scratch: [ticket counter (64 B)][per-channel (scale, shift) float2, batch*C][partials]
+// GroupNorm scratch: [ticket counters (64 B)][gn_fused grid barrier (64 B)][per-channel (scale, shift) float2, batch*C][partials]
 constexpr int kGnMaxChunks = 148;  // one statistics CTA per SM
+constexpr int kGnImageTickets = 16;  // per-image ticket counters in the scratch's first 64 B
 // pixel chunks per image: one per SM for 1-2 images; a video batch shares ~2 CTAs per SM so
 // the last CTA's merge reads few partials per (image, group)
 inline int gn_chunk_cap(int batch) {
@@ -117,7 +118,7 @@ struct GnLayout {
 __host__ __device__ inline GnLayout gn_layout(float2* scratch, int batch, int C) {
     GnLayout l;
     l.counter = reinterpret_cast<unsigned*>(scratch);
-    l.ab = scratch + 8;
+    l.ab = scratch + 16;
     l.part = l.ab + static_cast<long long>(batch) * C;
     return l;
 }
@@ -132,7 +133,7 @@ template <typename T>
 __global__ void gn_stats(Cat2T<T> x, int HW, int groups, int chunk_pix, int chunks, const float* gamma,
                          const float* beta, float eps, float2* scratch) {
     pdl_wait();
-    extern __shared__ float sm[];  // [2][rpb][C]
+    extern __shared__ __align__(16) float sm[];  // [2][rpb][C]
     const int n = blockIdx.y, ch = blockIdx.x, batch = gridDim.y;
     const int C = x.c0 + x.c1, nv = C / 8, cpg = C / groups;
     const int rpb = blockDim.x / nv, r = threadIdx.x / nv, v = threadIdx.x % nv;
@@ -160,11 +161,14 @@ __global__ void gn_stats(Cat2T<T> x, int HW, int groups, int chunk_pix, int chun
                 }
             }
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            sm[r * C + v * 8 + i] = s[i];
-            sm[(rpb + r) * C + v * 8 + i] = ss[i];
-        }
+        // 16-byte stores (C % 8 == 0: 32-byte aligned): scalar stores at a 32-byte thread
+        // stride were 8-way bank conflicts
+        float4* w0 = reinterpret_cast<float4*>(sm + r * C + v * 8);
+        float4* w1 = reinterpret_cast<float4*>(sm + (rpb + r) * C + v * 8);
+        w0[0] = make_float4(s[0], s[1], s[2], s[3]);
+        w0[1] = make_float4(s[4], s[5], s[6], s[7]);
+        w1[0] = make_float4(ss[0], ss[1], ss[2], ss[3]);
+        w1[1] = make_float4(ss[4], ss[5], ss[6], ss[7]);
     }
     __syncthreads();
     // rows -> per channel (one thread per channel), then channels -> per group; fixed order
@@ -186,21 +190,26 @@ __global__ void gn_stats(Cat2T<T> x, int HW, int groups, int chunk_pix, int chun
         }
         L.part[(static_cast<long long>(n) * chunks + ch) * groups + g] = make_float2(a, b);
     }
-    // ticket: the last CTA of the grid finalises every image
+    // ticket: up to kGnImageTickets images, the last CTA of each image finalises that image
+    // (the merges of a video batch run in parallel); larger batches: the last CTA of the grid
+    // finalises every image
     __shared__ unsigned last;
+    const bool per_image = batch <= kGnImageTickets;
+    const int n0 = per_image ? n : 0, nb = per_image ? 1 : batch;
+    unsigned* counter = L.counter + (per_image ? n : 0);
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(L.counter, 1u) == static_cast<unsigned>(chunks * batch - 1);
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == static_cast<unsigned>(chunks * nb - 1);
     __syncthreads();
     if (!last) return;
     __threadfence();
     // fp64 merge of the chunk partials: nsub threads per (image, group), each over a fixed
     // strided subset with 4 loads in flight, then combined in sub order (fixed = deterministic)
-    const int ngs = batch * groups, nsub = max(1, static_cast<int>(blockDim.x) / ngs);
+    const int ngs = nb * groups, nsub = max(1, static_cast<int>(blockDim.x) / ngs);
     // (loops: a video batch can hold more (image, group) pairs than the CTA has threads)
     double* red = reinterpret_cast<double*>(sm);  // [nsub][ngs][2], then [ngs][2] mean / rstd
     for (int idx = threadIdx.x; idx < nsub * ngs; idx += blockDim.x) {
-        const int ng = idx % ngs, sub = idx / ngs, nn = ng / groups, g = ng % groups;
+        const int ng = idx % ngs, sub = idx / ngs, nn = n0 + ng / groups, g = ng % groups;
         const float2* pp = L.part + static_cast<long long>(nn) * chunks * groups + g;
         double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
         int k = sub;
@@ -230,13 +239,13 @@ __global__ void gn_stats(Cat2T<T> x, int HW, int groups, int chunk_pix, int chun
         st[2 * ng + 1] = 1.0 / sqrt(var + static_cast<double>(eps));
     }
     __syncthreads();
-    for (int nc = threadIdx.x; nc < batch * C; nc += blockDim.x) {
+    for (int nc = threadIdx.x; nc < nb * C; nc += blockDim.x) {
         const int nn = nc / C, c = nc % C, g = c / cpg;
         const double mu = st[2 * (nn * groups + g)], rs = st[2 * (nn * groups + g) + 1];
         const float a = static_cast<float>(rs * gamma[c]);
-        L.ab[nc] = make_float2(a, static_cast<float>(beta[c] - mu * rs * gamma[c]));
+        L.ab[static_cast<long long>(n0) * C + nc] = make_float2(a, static_cast<float>(beta[c] - mu * rs * gamma[c]));
     }
-    if (threadIdx.x == 0) *L.counter = 0u;  // re-arm for the next launch on this scratch
+    if (threadIdx.x == 0) *counter = 0u;  // re-arm for the next launch on this scratch
 }
 
 // GroupNorm pass 2: y = x * a[c] + b[c] (+SiLU).  Thread (r, v) owns the 8 channels of
@@ -304,8 +313,9 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
     float* red = reinterpret_cast<float*>(gsm + static_cast<size_t>(chunk_pix) * nv * sizeof(Raw));  // [2][rpb][C]
     float2* ab = reinterpret_cast<float2*>(red + 2 * rpb * C);               // [C]
     double* st = reinterpret_cast<double*>(ab + C);                          // [nsub][groups][2], then [groups][2]
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(scratch + 1);
-    float2* part = scratch + 8;
+    // header words 18-19 (bytes 72-79): clear of gn_stats' ticket counters (words 0-15)
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(scratch + 9);
+    float2* part = scratch + 16;
     if (r < rpb) {
         float s[8], ss[8];
 #pragma unroll
@@ -328,11 +338,14 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
                 }
             }
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            red[r * C + v * 8 + i] = s[i];
-            red[(rpb + r) * C + v * 8 + i] = ss[i];
-        }
+        // 16-byte stores (C % 8 == 0: 32-byte aligned): scalar stores at a 32-byte thread
+        // stride were 8-way bank conflicts
+        float4* w0 = reinterpret_cast<float4*>(red + r * C + v * 8);
+        float4* w1 = reinterpret_cast<float4*>(red + (rpb + r) * C + v * 8);
+        w0[0] = make_float4(s[0], s[1], s[2], s[3]);
+        w0[1] = make_float4(s[4], s[5], s[6], s[7]);
+        w1[0] = make_float4(ss[0], ss[1], ss[2], ss[3]);
+        w1[1] = make_float4(ss[4], ss[5], ss[6], ss[7]);
     }
     __syncthreads();
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
@@ -419,16 +432,27 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
         ab[c] = make_float2(static_cast<float>(rs * gamma[c]), static_cast<float>(beta[c] - st[2 * g] * rs * gamma[c]));
     }
     __syncthreads();
-    // normalise the SMEM copy, 16-byte coalesced stores
+    // normalise the SMEM copy, 16-byte coalesced stores.  blockDim.x = rpb * nv, so the
+    // vector index i % nv of a thread is the same every iteration: its 8 (a, b) pairs are
+    // read from SMEM once (per-iteration reads at a 64-byte thread stride were 16-way
+    // bank conflicts, the kernel's top stall)
     T* o = out + static_cast<long long>(p0) * C;
+    float2 q[8];
+    {
+        const float4* a4 = reinterpret_cast<const float4*>(ab + (threadIdx.x % nv) * 8);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float4 t = a4[j];
+            q[2 * j] = make_float2(t.x, t.y);
+            q[2 * j + 1] = make_float2(t.z, t.w);
+        }
+    }
     for (int i = threadIdx.x; i < np * nv; i += blockDim.x) {
-        const int vv = i % nv;
         float f[8];
         Vec8<T>::unpack(tile[i], f);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const float2 q = ab[vv * 8 + k];
-            f[k] = fmaf(f[k], q.x, q.y);
+            f[k] = fmaf(f[k], q[k].x, q[k].y);
             if (act) f[k] = silu(f[k]);
         }
         Vec8<T>::store(o + static_cast<long long>(i) * 8, Vec8<T>::pack(f));
@@ -1065,6 +1089,8 @@ void group_norm_t(const Cat2T<T>& x, int batch, int HW, int groups, const float*
     const int threads = rpb * nv, nsub = std::max(1, threads / (batch * groups));
     size_t smem = static_cast<size_t>(2) * rpb * C * sizeof(float);
     smem = std::max(smem, static_cast<size_t>(nsub + 1) * batch * groups * 2 * sizeof(double));
+    if (batch <= kGnImageTickets)  // per-image merge (gn_stats): nsub over one image's groups
+        smem = std::max(smem, static_cast<size_t>(std::max(1, threads / groups) + 1) * groups * 2 * sizeof(double));
     if (smem > 48 * 1024) throw std::invalid_argument("group_norm: statistics tile exceeds 48 KB shared memory");
     CKU(launch_pdl(gn_stats<T>, dim3(chunks, batch), dim3(threads), smem, st, 1, x, HW, groups, chunk_pix, chunks, gamma,
                    beta, eps, scratch));
@@ -1090,7 +1116,7 @@ void group_norm(const Cat2F& x, int batch, int HW, int groups, const float* gamm
 size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C) {
     const int chunk_pix = (std::max(HW, 1) + gn_chunk_cap(batch) - 1) / gn_chunk_cap(batch);
     const int chunks = (HW + chunk_pix - 1) / chunk_pix;
-    return (8 + static_cast<size_t>(batch) * C + static_cast<size_t>(batch) * chunks * groups) * sizeof(float2);
+    return (16 + static_cast<size_t>(batch) * C + static_cast<size_t>(batch) * chunks * groups) * sizeof(float2);
 }
 
 template <typename T>
