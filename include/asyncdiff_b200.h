@@ -199,8 +199,8 @@ int adx_eval_segment(adx_engine* e, const adx_partition* p, int seg, const doubl
 /* RunOptions: executor.hpp:44-49 (+ InstrumentedDenoiser delays, executor.hpp:53-59) */
 typedef struct {
     double round_timeout_s;        /* default 30 */
-    uint64_t jitter_seed;          /* accepted for API parity; GPU start order is event-driven */
-    double max_jitter_s;
+    uint64_t jitter_seed;          /* executor.cpp:445-449: device d's stream starts with a GPU */
+    double max_jitter_s;           /* sleep of Rng(mix_seed(jitter_seed, d)).uniform() * max_jitter_s */
     const double* segment_delay_s; /* NULL or n_delays (must equal N) per-segment GPU sleeps */
     int n_delays;
     int use_graph;                 /* 1: capture the whole run in one CUDA graph (default) */

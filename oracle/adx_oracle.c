@@ -122,6 +122,20 @@ void or_random_normals(uint64_t seed, int n, double* out) {
     for (int i = 0; i < n; ++i) out[i] = or_rng_normal(&r);
 }
 
+/* Bulk draws for the UNet-family oracle (oracle/unet_model.py, test
+ * infrastructure): n consecutive float32 values (float)(lo + (hi-lo)*uniform())
+ * or (float)normal() from one Rng state -- the same stream a C++ caller gets
+ * from static_cast<float>(rng.uniform(lo, hi)) / static_cast<float>(rng.normal()). */
+long long or_rng_sizeof(void) { return (long long)sizeof(or_rng); }
+
+void or_rng_fill_uniform_f32(or_rng* r, long long n, double lo, double hi, float* out) {
+    for (long long i = 0; i < n; ++i) out[i] = (float)uniform_lohi(r, lo, hi);
+}
+
+void or_rng_fill_normal_f32(or_rng* r, long long n, float* out) {
+    for (long long i = 0; i < n; ++i) out[i] = (float)or_rng_normal(r);
+}
+
 /* ================================================================ schedule
  * proj/src/diffusion.cpp:39-77 */
 int or_build_schedule(int T, double beta_start, double beta_end, int kind, double* betas,

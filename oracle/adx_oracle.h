@@ -59,6 +59,11 @@ uint64_t or_mix_seed(uint64_t a, uint64_t b);
 /* convenience: n normals from Rng(seed) (test_util.hpp random_vec) */
 void or_random_normals(uint64_t seed, int n, double* out);
 
+/* bulk float32 draws for the UNet-family oracle (oracle/unet_model.py) */
+long long or_rng_sizeof(void);
+void or_rng_fill_uniform_f32(or_rng* r, long long n, double lo, double hi, float* out);
+void or_rng_fill_normal_f32(or_rng* r, long long n, float* out);
+
 /* ---- schedule + sampler: proj/src/diffusion.cpp:39-142 ---- */
 enum { OR_LINEAR = 0, OR_SCALED_LINEAR = 1 };
 int or_build_schedule(int T, double beta_start, double beta_end, int kind,

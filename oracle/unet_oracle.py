@@ -1,31 +1,55 @@
 """CPU numpy oracle of the UNet-shaped denoiser family.
 
-TEST INFRASTRUCTURE ONLY (tests/ and smoke(); never imported by the product).
-The reference has no UNet (its denoiser is an MLP stage list),
-so this is a BUILDER-WRITTEN oracle -- parity of the UNet family is
-*unpinned* by reference vectors; what is pinned is the stage/skip/plan
-contract it shares with the reference family.  It restates the stage programs
-of paper_2406_06911_b200/csrc/unet_dev.cu in fp32 numpy (float64 for norm
-statistics), rounding to bf16 exactly where the GPU stores bf16 tensors, and
-reads the same deterministic parameters through adx_unet_stage_params.
+TEST INFRASTRUCTURE ONLY (tests/, smoke() and bench.py's CPU legs; never
+imported by the product).  The reference has no UNet (its
+denoiser is an MLP stage list), so this is a BUILDER-WRITTEN oracle -- parity
+of the UNet family is *unpinned* by reference vectors; what is pinned is the
+stage/skip/plan contract it shares with the reference family.
 
-exact=True is the fp64 oracle of the fp32 (ADX_F32) GPU mode ("the
-builder's CPU fp64 UNet oracle defines the rel-L2 <= 1e-3 check"): float64
-everywhere, no rounding.
+Independence: the model (stage list, skip links, parameters, contexts) comes
+from oracle/unet_model.py, which draws its own parameters from the oracle's
+MT19937-64 -- nothing here calls the product library.  tests/test_unet_model.py
+checks that the product's model builder produces the same parameters
+bit-for-bit.
+
+Arithmetic: the stage programs of paper_2406_06911_b200/csrc/unet_dev.cu
+restated in fp32 numpy (float64 for norm statistics), rounding to bf16 exactly
+where the GPU stores bf16 tensors.  exact=True is the fp64 oracle of the fp32
+(ADX_F32) GPU mode ("the builder's CPU fp64 UNet oracle defines the
+rel-L2 <= 1e-3 check"): float64 everywhere, no rounding.
 """
 from __future__ import annotations
 
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
+_NT = max(1, min(32, os.cpu_count() or 1))
+_POOL = ThreadPoolExecutor(_NT)
+
+
+def _par(fn, n: int, min_chunk: int = 1 << 16):
+    """run fn(slice) over [0, n) in parallel chunks (numpy ufuncs release the GIL)"""
+    k = max(1, min(_NT, n // min_chunk))
+    bounds = [n * i // k for i in range(k + 1)]
+    list(_POOL.map(lambda i: fn(slice(bounds[i], bounds[i + 1])), range(k)))
+
 
 def bf(x: np.ndarray) -> np.ndarray:
-    """round-to-nearest-even fp32 -> bf16 -> fp32"""
-    x = np.ascontiguousarray(x, np.float32)
-    u = x.view(np.uint32).astype(np.uint64)
-    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
-    return r.astype(np.uint32).view(np.float32).reshape(x.shape)
+    """round-to-nearest-even fp32 -> bf16 -> fp32 (finite inputs: no uint32 overflow)"""
+    x = np.array(x, np.float32, order="C", copy=True)
+    u = x.reshape(-1).view(np.uint32)
+
+    def work(sl):
+        v = u[sl]
+        t = (v >> 16) & 1
+        t += 0x7FFF
+        v += t
+        v &= np.uint32(0xFFFF0000)
+    _par(work, u.size)
+    return x
 
 
 def silu(x):
@@ -44,19 +68,37 @@ def sinusoid(t, dim):
     return np.concatenate([np.cos(t * f), np.sin(t * f)])
 
 
+class _LazyParams:
+    """stage -> parameter dict, generated on first use (c2 holds ~0.87 G parameters)"""
+
+    def __init__(self, model):
+        self.m = model
+
+    def __getitem__(self, stage):
+        return self.m.params(stage)
+
+
 class UNetOracle:
-    def __init__(self, adx, model, exact: bool = False):
-        self.adx, self.m = adx, model
+    def __init__(self, model, exact: bool = False):
+        """model: an oracle.unet_model.UNetModel, or the build_unet_denoiser keyword
+        arguments (dict) to build one"""
+        from .unet_model import build_unet_model
+        if isinstance(model, dict):
+            model = build_unet_model(**model)
+        self.m = model
         self.exact = exact
         self.dt = np.float64 if exact else np.float32
-        self.sp = model.unet_spec
-        self.L = model.num_stages()
-        self.links = model.skip_links
-        self.info = {s: adx.unet_stage_info(model, s) for s in range(1, self.L + 1)}
-        self.params = {s: adx.unet_stage_params(model, s) for s in range(0, self.L + 1)}
-        self.ctxs = adx.unet_context(model)  # (batch, ctx_len, ctx_dim); CFG: [uncond, cond]
+        sp = model.spec
+        self.sp = dict(groups=sp.groups, ch=list(sp.ch), c_lat=sp.c_lat, ctx_len=sp.ctx_len,
+                       cfg_scale=sp.cfg_scale, frames=sp.frames, motion=int(sp.motion))
+        self.L = model.L
+        self.links = model.links
+        self.info = {s: model.info(s) for s in range(1, self.L + 1)}
+        self.params = _LazyParams(model)
+        self.ctxs = model.contexts()         # (batch, ctx_len, ctx_dim); CFG: [uncond, cond]
         self.ci = self.ctxs.shape[0] - 1     # the context of the cascade being evaluated
         self._kv = {}
+        self._rw = {}
 
     # ---------------------------------------------------------- primitives
     def r(self, x):
@@ -66,7 +108,7 @@ class UNetOracle:
     def conv3x3(self, x, w, b, stride2=False):
         H, W, Ci = x.shape
         Co = w.shape[0]
-        wt = self.r(w).reshape(Co, 3, 3, Ci)
+        wt = self.rw(w).reshape(Co, 3, 3, Ci)
         xp = np.zeros((H + 2, W + 2, Ci), self.dt)
         xp[1:-1, 1:-1] = x
         acc = np.zeros((H, W, Co), self.dt)
@@ -94,8 +136,18 @@ class UNetOracle:
         var = ((x - mu) ** 2).mean(axis=1, keepdims=True)
         return self.r((x - mu) / np.sqrt(var + eps) * gamma + beta)
 
+    def rw(self, w):
+        """a weight in the GPU's storage precision (bf16 mode: rounded once and cached;
+        weights are immutable)"""
+        if self.exact:
+            return np.asarray(w, np.float64)
+        k = id(w)
+        if k not in self._rw:
+            self._rw[k] = (w, self.r(w))
+        return self._rw[k][1]
+
     def lin(self, x, w, b=None):
-        y = x @ self.r(w).T
+        y = x @ self.rw(w).T
         return y + b if b is not None else y
 
     def attention(self, q, k, v, Lk):
@@ -105,10 +157,14 @@ class UNetOracle:
         for h in range(C // 64):
             sl = slice(64 * h, 64 * h + 64)
             S = (q[:, sl] @ k[:Lk, sl].T) * self.dt(0.125)
-            S = S - S.max(axis=1, keepdims=True)
-            P = np.exp(S)
-            P = self.r(P / P.sum(axis=1, keepdims=True))
-            out[:, sl] = self.r(P @ v[:Lk, sl])
+
+            def softmax(rows):
+                Sr = S[rows]
+                Sr -= Sr.max(axis=1, keepdims=True)
+                np.exp(Sr, out=Sr)
+                Sr /= Sr.sum(axis=1, keepdims=True)
+            _par(softmax, L, 64)
+            out[:, sl] = self.r(self.r(S) @ v[:Lk, sl])
         return out
 
     def temb(self, t):

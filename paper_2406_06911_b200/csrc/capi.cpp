@@ -229,6 +229,9 @@ adx::RunOptions to_opts(const adx_run_options* o) {
     adx::RunOptions r;
     if (!o) return r;
     r.round_timeout_s = o->round_timeout_s;
+    if (o->max_jitter_s < 0.0) throw std::invalid_argument("RunOptions: max_jitter_s must be >= 0");
+    r.jitter_seed = o->jitter_seed;
+    r.max_jitter_s = o->max_jitter_s;
     if (o->segment_delay_s && o->n_delays > 0) {
         r.segment_delay_s.assign(o->segment_delay_s, o->segment_delay_s + o->n_delays);
         for (double d : r.segment_delay_s)

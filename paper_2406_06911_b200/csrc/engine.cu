@@ -721,7 +721,21 @@ void Session::enqueue_all(bool capture) {
         if (v.v != 0) CK(cudaStreamWaitEvent(v.comp, fork_, 0));
         CK(cudaStreamWaitEvent(v.comm, fork_, 0));
         CK(cudaMemsetAsync(v.bad, 0x7f, 2 * sizeof(int), v.comp));
+        if (opts_.max_jitter_s > 0.0 && mode_ == kParallel) {  // executor.cpp:445-449
+            Rng rng(mix_seed(opts_.jitter_seed, static_cast<uint64_t>(v.v)));
+            launch_delay(rng.uniform() * opts_.max_jitter_s, v.comp);
+            ++enq_kernels_;
+        }
     }
+
+    // BundleStore ledger (executor.cpp:28-62): the bundles this enqueue commits
+    std::set<std::pair<int, int>> store;  // (segment, round)
+    ledger_entries_.clear();
+    auto put = [&](int seg, int r) {
+        if (!store.insert({seg, r}).second)
+            throw std::logic_error("BundleStore: entry (" + std::to_string(seg) + ", " + std::to_string(r) +
+                                   ") already written");
+    };
 
     auto record_eval = [&](VDev& v, int rslot) {
         CK(cudaEventRecord(v.eval_done, v.comp));
@@ -755,6 +769,8 @@ void Session::enqueue_all(bool capture) {
             }
         }
         enqueue_ddim(step, t);
+        if (wi + 1 == plan_.warmup_steps.size())  // executor.cpp:540-541
+            for (int n = 1; n < N_; ++n) put(n, -1);
     }
     if (timing) {
         setdev(v0.ordinal);
@@ -773,6 +789,11 @@ void Session::enqueue_all(bool capture) {
         }
         for (size_t k = 0; k < rd.evals.size(); ++k) {
             const Eval& ev = rd.evals[k];
+            if (ev.input.kind == 1 && !store.count({ev.input.producer_segment, ev.input.producer_round}))
+                throw std::logic_error("executor: unresolvable cached ref (segment " +
+                                       std::to_string(ev.input.producer_segment) + ", round " +
+                                       std::to_string(ev.input.producer_round) + ") in round " +
+                                       std::to_string(r));
             VDev& v = vd_[vdev_of_eval(ev)];
             setdev(v.ordinal);
             wait_inputs(v, ev.segment, rslot);
@@ -798,6 +819,12 @@ void Session::enqueue_all(bool capture) {
             enqueue_ddim(T_ - t, t);
         }
         if (timing) CK(cudaEventRecord(round_end_[ri], v0.comp));
+        // commit in produced_by order, prune to the warm-up tail + rounds >= r-1 (executor.cpp:574-581)
+        for (const Eval& ev : rd.evals)
+            if (ev.segment < N_) put(ev.segment, r);
+        for (auto it = store.begin(); it != store.end();)
+            it = it->second != -1 && it->second < r + 1 - 2 ? store.erase(it) : std::next(it);
+        ledger_entries_.push_back(static_cast<int>(store.size()));
     }
 
     // ---- join every stream back into vdev 0's compute stream
@@ -1017,9 +1044,7 @@ void Session::run(const double* x_T, double* lat, double* eps, RunStatsOut* stat
         for (int n = 0; n < N_; ++n) s.device_evals[part_.device_of_segment[n]] += plan_.w;
         for (auto& r : plan_.rounds)
             for (auto& ev : r.evals) s.device_evals[ev.device] += 1;
-        // logical BundleStore occupancy (executor.cpp:53-62): warm-up tail + rounds r-1, r
-        s.store_entries.clear();
-        for (size_t ri = 0; ri < plan_.rounds.size(); ++ri) s.store_entries.push_back((N_ - 1) * (ri == 0 ? 2 : 3));
+        s.store_entries = ledger_entries_;
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, t_start_, t_stop_));
         s.total_wall_s = ms * 1e-3;

@@ -100,6 +100,10 @@ private:
 
 struct RunOptions {
     double round_timeout_s = 30.0;
+    // executor.cpp:445-449: worker d starts after uniform() * max_jitter_s drawn from
+    // Rng(mix_seed(jitter_seed, d)); here a GPU sleep at the head of vdev d's compute stream
+    uint64_t jitter_seed = 0;
+    double max_jitter_s = 0.0;
     std::vector<double> segment_delay_s;
     bool use_graph = true;
     bool instrument = false;
@@ -187,6 +191,10 @@ private:
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t gexec_ = nullptr;
     bool instrumented_enqueue_ = false;
+    // BundleStore bookkeeping (executor.cpp:28-62) replayed from the bundles the enqueue
+    // actually commits: put per (segment, round) written, prune to the warm-up tail and
+    // rounds >= r-1; occupancy after every round
+    std::vector<int> ledger_entries_;
     int kernel_count_ = 0;
     long long weight_bytes_per_run_ = 0;
     int enq_kernels_ = 0;

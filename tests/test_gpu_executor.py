@@ -101,12 +101,38 @@ def test_rejects_invalid_plans_and_partitions():  # test_executor.cpp:116-133
 
 
 def test_store_retention_flat():  # test_executor.cpp:135-160
+    """the engine's BundleStore ledger (replayed from the bundles its enqueue commits) equals
+    the oracle's BundleStore occupancy round by round, flat at 3 (N - 1) after round 0"""
     f = Fixture()
-    plan = adx.plan_async(20, 2, 3, 1)
+    om = O.Model.build_toy(6, [2, 8, 8, 8, 8, 8, 2], "unet-mirror", 11, 8)
+    for N, S, w in [(3, 1, 2), (2, 2, 1), (4, 1, 1), (3, 2, 3), (1, 1, 2)]:
+        plan = adx.plan_async(20, w, N, S)
+        p = adx.partition_balanced(f.model, N)
+        _, stats = adx.run_serial(plan, f.model, p, f.x_T, f.schedule)
+        _, pst = adx.run_parallel(plan, f.model, p, f.x_T, f.schedule, plan.D)
+        ss, _ = O.partition_balanced(om.costs(), N)
+        _, _, entries, _ = O.run_serial(om, ss, N, O.plan_async_flat(20, w, N, S), f.schedule.alpha_bars,
+                                        f.x_T.values)
+        assert stats.store_entries_per_round == entries == pst.store_entries_per_round, (N, S, w)
+        assert set(entries[1:]) <= {3 * (N - 1)}
+
+
+def test_start_jitter_delays_devices_not_results():  # executor.cpp:445-449
+    """max_jitter_s delays each device's first work by Rng(mix_seed(seed, d)).uniform() * max;
+    the trajectory is unchanged and the instrumented wall time grows by the largest draw"""
+    f = Fixture()
+    plan = adx.plan_async(20, 1, 3, 1)
     p = adx.partition_balanced(f.model, 3)
-    _, stats = adx.run_serial(plan, f.model, p, f.x_T, f.schedule)
-    assert len(stats.store_entries_per_round) == len(plan.rounds)
-    assert set(stats.store_entries_per_round[1:]) == {3 * (3 - 1)}
+    base, bst = adx.run_parallel(plan, f.model, p, f.x_T, f.schedule, 3,
+                                 adx.RunOptions(use_graph=False, instrument=True))
+    seed, mx = 99, 0.05
+    jit, jst = adx.run_parallel(plan, f.model, p, f.x_T, f.schedule, 3,
+                                adx.RunOptions(jitter_seed=seed, max_jitter_s=mx, use_graph=False, instrument=True))
+    assert np.array_equal(base.latent_matrix(), jit.latent_matrix())
+    draws = [O.Rng(O.mix_seed(seed, d)).uniform() * mx for d in range(3)]
+    assert jst.total_wall_s >= bst.total_wall_s + 0.8 * max(draws)
+    with pytest.raises(adx.InvalidArgument):
+        adx.run_parallel(plan, f.model, p, f.x_T, f.schedule, 3, adx.RunOptions(max_jitter_s=-1.0))
 
 
 def test_zero_delays_identical():  # test_executor.cpp:162-173

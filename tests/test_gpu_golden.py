@@ -86,3 +86,28 @@ def test_gpu_matches_oracle_trajectory(N, S, w):
     olat, oeps, _, _ = O.run_serial(om, ss, N, O.plan_async_flat(20, w, N, S), s.alpha_bars, x_T.values)
     assert np.abs(traj.latent_matrix() - olat).max() < 1e-12
     assert np.abs(np.stack(traj.eps_used) - oeps).max() < 1e-12
+
+
+def test_c1b_f32_async_trajectory_matches_oracle():
+    """SURVEY §7 minimum slice: C1b (the reference's MLP-stage model at d=4096, square widths,
+    seed 11, T=20, N=2 w=1 S=1) in fp32 within rel-L2 1e-3 of the fp64 C oracle (final latent
+    and every step), and async-vs-sequential divergence equal to the oracle's"""
+    widths = [4096] * 7
+    m = adx.build_toy_denoiser(6, widths, "unet-mirror", 11)
+    s = adx.build_schedule(20, 0.01, 0.15)
+    x = adx.Latent(O.random_normals(12, 4096), 20)
+    part = adx.partition_balanced(m, 2)
+    plan = adx.plan_async(20, 1, 2, 1)
+    par, _ = adx.run_parallel(plan, m, part, x, s, plan.D, precision="f32")
+    seq = adx.sequential_denoise(m, x, s, precision="f32")
+    O.set_threads(16)
+    om = O.Model.build_toy(6, widths, "unet-mirror", 11, 8)
+    ss, _ = O.partition_balanced(om.costs(), 2)
+    olat, _, _, _ = O.run_serial(om, ss, 2, O.plan_async_flat(20, 1, 2, 1), s.alpha_bars, x.values)
+    oseq, _ = O.sequential_denoise(om, s.alpha_bars, x.values)
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    assert max(rel(par.latent_matrix()[k], olat[k]) for k in range(21)) < 1e-3
+    assert rel(seq.latent_matrix()[-1], oseq[-1]) < 1e-3
+    _, g, _ = O.compare_trajectories(seq.latent_matrix(), par.latent_matrix())
+    _, o, _ = O.compare_trajectories(oseq, olat)
+    assert abs(g - o) <= 1e-2 * o, (g, o)

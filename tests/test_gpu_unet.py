@@ -1,7 +1,8 @@
 """UNet-shaped family on the sm_100a path (tcgen05 conv/GEMM/attention stages):
-numerics vs the builder-written numpy oracle (oracle/unet_oracle.py -- parity
-unpinned by reference vectors), and the reference's executor
-invariants, which are model-agnostic and exact.
+numerics vs the builder-written numpy oracle (oracle/unet_oracle.py over the
+independent model restatement oracle/unet_model.py -- parity unpinned by
+reference vectors), and the reference's executor invariants,
+which are model-agnostic and exact.
   precision "bf16": bf16 activations, fp32 latent     -> TOL 3e-2 vs the bf16-rounding oracle
   precision "f32":  fp32 activations, split-bf16 MMAs -> TOL_F32 1e-3 vs the fp64 oracle
                     (the north_star's rel-L2 <= 1e-3 bar)"""
@@ -34,7 +35,7 @@ def small():
 def test_unet_sequential_matches_oracle(small):
     m, s, x = small
     traj = adx.sequential_denoise(m, x, s, precision="bf16")
-    orc = UNetOracle(adx, m)
+    orc = UNetOracle(SMALL)
     xv = x.values.astype(np.float32)
     lat = [xv]
     for k, t in enumerate(range(4, 0, -1)):
@@ -95,7 +96,7 @@ def test_unet_f32_mode_matches_fp64_oracle(small):
     the fp64 oracle (no bf16 rounding anywhere on either side)."""
     m, s, x = small
     traj = adx.sequential_denoise(m, x, s, precision="f32")
-    orc = UNetOracle(adx, m, exact=True)
+    orc = UNetOracle(SMALL, exact=True)
     lat = x.values.astype(np.float64)
     for k, t in enumerate(range(4, 0, -1)):
         eps = orc.eval_full(lat, t)
@@ -136,7 +137,7 @@ def small_xl():
 def test_unet_xl_cfg_matches_oracle(small_xl, prec, exact, tol):
     m, s, x = small_xl
     traj = adx.sequential_denoise(m, x, s, precision=prec)
-    orc = UNetOracle(adx, m, exact=exact)
+    orc = UNetOracle(SMALL_XL, exact=exact)
     lat = x.values.astype(np.float64)
     for k, t in enumerate(range(3, 0, -1)):
         eps = orc.eval_full(lat if exact else traj.latents[k].values.astype(np.float32), t)
@@ -161,9 +162,13 @@ def test_unet_xl_cfg_async_invariants_bit_exact(small_xl):
 # AnimateDiff-shaped (BASELINE config 5) in miniature: the latent holds every frame, a
 # temporal-attention motion module follows every resnet; frames 3 exercises a partly
 # filled frame capacity of the temporal kernel, 16 the C5 frame count
+def video_spec(frames):
+    return dict(H=16, W=16, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64, temb_dim=128,
+                frames=frames, motion=True, seed=9)
+
+
 def small_video(frames):
-    m = adx.build_unet_denoiser(H=16, W=16, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64, temb_dim=128,
-                                frames=frames, motion=True, seed=9)
+    m = adx.build_unet_denoiser(**video_spec(frames))
     s = adx.build_schedule(3, 0.01, 0.15)
     x = adx.Latent(O.random_normals(14, m.data_dim()).astype(np.float64), 3)
     return m, s, x
@@ -175,7 +180,7 @@ def test_unet_video_motion_matches_oracle(frames, prec, exact, tol):
     m, s, x = small_video(frames)
     assert m.data_dim() == frames * 16 * 16 * 4
     traj = adx.sequential_denoise(m, x, s, precision=prec)
-    orc = UNetOracle(adx, m, exact=exact)
+    orc = UNetOracle(video_spec(frames), exact=exact)
     lat = x.values.astype(np.float64)
     for k, t in enumerate(range(3, 0, -1)):
         eps = orc.eval_full(lat if exact else traj.latents[k].values.astype(np.float32), t)

@@ -18,7 +18,7 @@ for name, spec, T in (("small", dict(H=16, W=16, ch=(64, 128), attn=(1, 0), n_re
     x = adx.Latent(O.random_normals(12, m.data_dim()).astype(np.float64), T)
     for prec, exact in (("f32", True), ("bf16", False)):
         traj = adx.sequential_denoise(m, x, s, precision=prec)
-        orc = UNetOracle(adx, m, exact=exact)
+        orc = UNetOracle(spec, exact=exact)
         lat = x.values.astype(np.float64)
         eps_rel = []
         for k, t in enumerate(range(T, 0, -1)):
