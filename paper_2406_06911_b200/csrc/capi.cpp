@@ -12,6 +12,7 @@
 #include "unet.hpp"
 #include "unet_kernels.cuh"
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -96,27 +97,36 @@ struct DevBuf {
     DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
 };
 
-void to_act(int prec, const double* src, size_t n, std::vector<unsigned char>& out) {
-    const int ab = adx::act_bytes(prec);
-    out.resize(n * ab);
+// fp64 host values <-> device elements of `eb` bytes (8: fp64, 4: fp32, 2: bf16 RNE)
+void to_dev(int eb, const double* src, size_t n, std::vector<unsigned char>& out) {
+    out.resize(n * eb);
     for (size_t i = 0; i < n; ++i) {
-        if (ab == 8) {
+        if (eb == 8) {
             std::memcpy(&out[i * 8], &src[i], 8);
-        } else {
+        } else if (eb == 4) {
             const float f = static_cast<float>(src[i]);
             std::memcpy(&out[i * 4], &f, 4);
+        } else {
+            const __nv_bfloat16 b = __float2bfloat16_rn(static_cast<float>(src[i]));
+            std::memcpy(&out[i * 2], &b, 2);
         }
     }
 }
 
-void from_act(int prec, const unsigned char* src, size_t n, double* dst) {
-    if (adx::act_bytes(prec) == 8) {
+void from_dev(int eb, const unsigned char* src, size_t n, double* dst) {
+    if (eb == 8) {
         std::memcpy(dst, src, n * 8);
-    } else {
+    } else if (eb == 4) {
         for (size_t i = 0; i < n; ++i) {
             float f;
             std::memcpy(&f, src + i * 4, 4);
             dst[i] = f;
+        }
+    } else {
+        for (size_t i = 0; i < n; ++i) {
+            __nv_bfloat16 b;
+            std::memcpy(&b, src + i * 2, 2);
+            dst[i] = __bfloat162float(b);
         }
     }
 }
@@ -129,7 +139,10 @@ std::vector<double> run_range_device(adx::Engine& E, int first, int last, const 
                                      bool stage1_latent) {
     const adx::Model& m = E.model();
     const int prec = E.prec();
-    const int ab = adx::act_bytes(prec);
+    // latent / eps elements (act_bytes) vs stage-output elements (stage_bytes: bf16 UNet
+    // activations in the bf16 mode) -- the stage kernels read and write the latter
+    const int ab = adx::act_bytes(prec), sb = E.stage_bytes();
+    auto out_bytes = [&](int stage) { return stage == m.L ? ab : sb; };
     CKC(cudaSetDevice(E.ordinal(0)));
     for (int i = first; i <= last; ++i) E.stage_on(0, i);
     E.ensure_tables(0, std::max(t_embed, 1));
@@ -144,15 +157,15 @@ std::vector<double> run_range_device(adx::Engine& E, int first, int last, const 
         }
     } sg{st};
     std::vector<unsigned char> tmp;
-    auto upload = [&](const std::vector<double>& v) {
-        DevBuf b(v.size() * ab);
-        to_act(prec, v.data(), v.size(), tmp);
+    auto upload = [&](const std::vector<double>& v, int eb) {
+        DevBuf b(v.size() * eb);
+        to_dev(eb, v.data(), v.size(), tmp);
         CKC(cudaMemcpy(b.p, tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
         return b;
     };
     DevBuf bad(2 * sizeof(int));
     CKC(cudaMemset(bad.p, 0x7f, 2 * sizeof(int)));
-    DevBuf cur_d = upload(cur);
+    DevBuf cur_d = upload(cur, stage1_latent ? ab : out_bytes(first - 1));
     std::map<int, DevBuf> y;      // stage outputs
     std::map<std::pair<int, int>, DevBuf> skip_d;
     std::vector<DevBuf> hs;
@@ -179,7 +192,7 @@ std::vector<double> run_range_device(adx::Engine& E, int first, int last, const 
             if (it == skips.end())
                 throw std::runtime_error("eval: missing skip feature for link (" + std::to_string(l.first) + " -> " +
                                          std::to_string(l.second) + ")");
-            if (!skip_d.count(l)) skip_d.emplace(l, upload(it->second));
+            if (!skip_d.count(l)) skip_d.emplace(l, upload(it->second, out_bytes(l.first)));
             in.push_back({skip_d.at(l).p, static_cast<int>(it->second.size())});
         }
         DevBuf h(static_cast<size_t>(m.stages[i - 1].hidden) * ab);
@@ -196,10 +209,10 @@ std::vector<double> run_range_device(adx::Engine& E, int first, int last, const 
     if (flags[0] != 0x7f7f7f7f) throw std::domain_error("eval: non-finite activation at stage " + std::to_string(flags[0]));
     auto down = [&](int stage) {
         const int n = m.widths[stage];
-        std::vector<unsigned char> h(static_cast<size_t>(n) * ab);
+        std::vector<unsigned char> h(static_cast<size_t>(n) * out_bytes(stage));
         CKC(cudaMemcpy(h.data(), y.at(stage).p, h.size(), cudaMemcpyDeviceToHost));
         std::vector<double> out(n);
-        from_act(prec, h.data(), n, out.data());
+        from_dev(out_bytes(stage), h.data(), n, out.data());
         return out;
     };
     for (int i = first; i <= last; ++i)
@@ -313,9 +326,9 @@ int adx_ddim_step(int ordinal, int precision, const double* x, const double* eps
         DevBuf xd(static_cast<size_t>(d) * ab), ed(static_cast<size_t>(d) * ab), od(static_cast<size_t>(d) * ab),
             bad(2 * sizeof(int));
         std::vector<unsigned char> tmp;
-        to_act(precision, x, d, tmp);
+        to_dev(adx::act_bytes(precision), x, d, tmp);
         CKC(cudaMemcpy(xd.p, tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
-        to_act(precision, eps, d, tmp);
+        to_dev(adx::act_bytes(precision), eps, d, tmp);
         CKC(cudaMemcpy(ed.p, tmp.data(), tmp.size(), cudaMemcpyHostToDevice));
         CKC(cudaMemset(bad.p, 0x7f, 2 * sizeof(int)));
         adx::DdimArgs a = {};
@@ -336,7 +349,7 @@ int adx_ddim_step(int ordinal, int precision, const double* x, const double* eps
         if (flags[0] != 0x7f7f7f7f) throw std::domain_error("predict_x0: non-finite eps at t=" + std::to_string(t));
         tmp.resize(static_cast<size_t>(d) * ab);
         CKC(cudaMemcpy(tmp.data(), od.p, tmp.size(), cudaMemcpyDeviceToHost));
-        from_act(precision, tmp.data(), d, out);
+        from_dev(adx::act_bytes(precision), tmp.data(), d, out);
     });
 }
 

@@ -233,3 +233,19 @@ def test_unet_batched_families_rank_session_matches_sequential(family):
     sess.run_into(np.ascontiguousarray(x.values, np.float64), lat, eps)
     seq = adx.sequential_denoise(m, x, s, precision="bf16")
     assert np.array_equal(lat, seq.latent_matrix())
+
+
+@pytest.mark.parametrize("prec,tol", [("bf16", TOL), ("f32", TOL_F32)])
+@pytest.mark.parametrize("spec", [SMALL, SMALL_XL, dict(video_spec(3))], ids=["sd", "xl_cfg", "video"])
+def test_every_stage_through_eval_segment_matches_oracle(spec, prec, tol):
+    """every stage of the miniatures on its own one-stage segment (eval_segment with a host
+    HiddenBundle in and out: the bundle wire format in both precisions) vs the oracle stage
+    on the same inputs"""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gpu_unet_full import stage_parity
+    from oracle.unet_model import build_unet_model
+    L = build_unet_model(**spec).L
+    for st in range(1, L + 1):
+        e, info, _ = stage_parity(repr(spec), spec, st, prec)
+        assert e < tol, (st, info, e)

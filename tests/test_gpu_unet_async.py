@@ -59,7 +59,7 @@ def test_unet_async_matches_oracle_async(spec, N, S, w, prec, exact, tol):
     par, st = adx.run_parallel(plan, m, part, adx.Latent(x, T), s, plan.D, precision=prec)
     olat, ss, entries, bc = oracle_async(spec, N, S, w, x, s.alpha_bars, exact)
     # same partition and schedule on both sides
-    assert part.segments() == [[i + 1 for i in range(len(ss)) if ss[i] == n] for n in range(1, N + 1)]
+    assert part.segments == [[i + 1 for i in range(len(ss)) if ss[i] == n] for n in range(1, N + 1)]
     assert st.broadcast_count == bc
     assert st.store_entries_per_round == entries
     e = rel(par.latent_matrix()[-1], olat[-1])
