@@ -203,3 +203,45 @@ def unet_stage_fn(orc) -> StageFn:
             return eu + s * (ec - eu) if orc.exact else eu + np.float32(s) * (ec - eu)
         return tuple(ys)
     return fn_cfg
+
+
+def similarity_profile(ex: AsyncOracle, stage_segment, latents, timesteps):
+    """metrics.cpp:73-101 restated: boundary activations of segments 1..N-1 at every latent
+    with timestep >= 1 (fresh chaining, boundaries_at metrics.cpp:46-60), then cosine and
+    rel-L2 (metrics.cpp:32-44) between adjacent steps.  -> (pair_t, cosine[N-1][], rel_l2[N-1][])"""
+    segs = ex._segments(stage_segment)
+    N = len(segs)
+    cos = [[] for _ in range(max(0, N - 1))]
+    rl = [[] for _ in range(max(0, N - 1))]
+    pair_t = []
+    if len(latents) < 3 or N < 2:
+        return pair_t, cos, rl
+    per_step, ts = [], []
+    for x, t in zip(latents, timesteps):
+        if t < 1:
+            break
+        sk, out = {}, []
+        kind, o = ex.eval_segment(segs, 1, np.asarray(x, np.float64), sk, t)
+        for seg in range(2, N + 1):
+            out.append(np.asarray(o[0], np.float64).reshape(-1))
+            sk.update(o[1])
+            kind, o = ex.eval_segment(segs, seg, o[0], sk, t)
+        per_step.append(out)
+        ts.append(t)
+
+    def cosine(a, b):
+        na, nb = np.linalg.norm(a), np.linalg.norm(b)
+        if na == 0.0 or nb == 0.0:
+            return 1.0 if np.linalg.norm(a - b) == 0.0 else 0.0
+        return float(np.dot(a, b) / (na * nb))
+
+    def rel_l2(a, b):
+        den = max(np.linalg.norm(a), np.linalg.norm(b))
+        return 0.0 if den == 0.0 else float(np.linalg.norm(a - b) / den)
+
+    for i in range(len(per_step) - 1):
+        pair_t.append(ts[i])
+        for b in range(N - 1):
+            cos[b].append(cosine(per_step[i][b], per_step[i + 1][b]))
+            rl[b].append(rel_l2(per_step[i][b], per_step[i + 1][b]))
+    return pair_t, cos, rl

@@ -28,7 +28,7 @@ static std::vector<double> normals(uint64_t seed, int n) {  // rng.hpp Box-Mulle
 
 int main(int argc, char** argv) {
     const bool gpu = argc > 1 && std::strcmp(argv[1], "gpu") == 0;
-    auto model = ad::LayeredDenoiser::build_toy(6, {2, 8, 8, 8, 8, 8, 2}, ADX_SKIP_UNET_MIRROR, 11);
+    auto model = ad::build_toy_denoiser(6, {2, 8, 8, 8, 8, 8, 2}, ad::SkipSpec::UnetMirror, 11);
     auto part = ad::partition_balanced(model, 2);
     auto plan = ad::plan_async(20, 1, 2, 1);
     if (!ad::validate_plan(plan).empty() || plan.num_rounds() != 19 || part.num_segments() != 2) {
@@ -47,9 +47,8 @@ int main(int argc, char** argv) {
     }
     auto s = ad::build_schedule(20, 0.01, 0.15);
     ad::Latent x{normals(12, 2), 20};
-    ad::Engine eng(model, ADX_F64);
-    auto seq = ad::sequential_denoise(eng, x, s);
-    auto [traj, stats] = ad::run_parallel(plan, eng, part, x, s, plan.D());
+    auto seq = ad::sequential_denoise(model, x, s);
+    auto [traj, stats] = ad::run_parallel(plan, model, part, x, s, plan.D);
     double mse = 0;
     for (int k = 0; k < 2; ++k) {
         const double d = traj.final_latent().values[k] - seq.final_latent().values[k];

@@ -144,7 +144,35 @@ def test_similarity_profile_on_gpu():  # metrics.cpp:73-101
     seq = adx.sequential_denoise(m, adx.Latent(O.random_normals(12, 2), 20), s, precision="f64")
     prof = adx.similarity_profile(m, adx.partition_balanced(m, 3), seq, s, precision="f64")
     assert len(prof.cosine) == 2 and len(prof.pair_t) == 19
+    # against the oracle restatement of metrics.cpp:73-101 on the oracle's own model
+    from oracle.async_exec import AsyncOracle, mlp_stage_fn, similarity_profile
+    om = O.Model.build_toy(6, [2, 8, 8, 8, 8, 8, 2], "unet-mirror", 11, 8)
+    ss, _ = O.partition_balanced(om.costs(), 3)
+    pt, cos, rl = similarity_profile(AsyncOracle(om.L, om.links, mlp_stage_fn(om)), ss,
+                                     [x.values for x in seq.latents], [x.timestep for x in seq.latents])
+    assert prof.pair_t == pt
+    assert np.allclose(prof.cosine, cos, rtol=0, atol=1e-12) and np.allclose(prof.rel_l2, rl, rtol=1e-9, atol=1e-14)
     assert prof.median_cosine() > 0.9
+
+
+@pytest.mark.gpu
+def test_similarity_profile_unet_matches_oracle():  # metrics.cpp:73-101 on the UNet family (bf16)
+    from oracle.async_exec import AsyncOracle, similarity_profile, unet_stage_fn
+    from oracle.unet_model import build_unet_model
+    from oracle.unet_oracle import UNetOracle
+    spec = dict(H=16, W=16, ch=(64, 128), attn=(1, 0), n_res=1, ctx_len=8, ctx_dim=64, temb_dim=128, seed=5)
+    m = adx.build_unet_denoiser(**spec)
+    s = adx.build_schedule(4, 0.01, 0.15)
+    seq = adx.sequential_denoise(m, adx.Latent(O.random_normals(12, m.data_dim()), 4), s, precision="f32")
+    prof = adx.similarity_profile(m, adx.partition_balanced(m, 3), seq, s, precision="f32")
+    om = build_unet_model(**spec)
+    ss, _ = O.partition_balanced(om.costs(), 3)
+    orc = UNetOracle(om, exact=True)
+    pt, cos, rl = similarity_profile(AsyncOracle(om.L, om.links, unet_stage_fn(orc)), ss,
+                                     [x.values for x in seq.latents], [x.timestep for x in seq.latents])
+    assert prof.pair_t == pt
+    assert np.allclose(prof.cosine, cos, rtol=0, atol=1e-5)
+    assert np.allclose(prof.rel_l2, rl, rtol=1e-2, atol=1e-5)
 
 
 @pytest.mark.gpu
@@ -231,6 +259,10 @@ def test_warmup_sweep_on_gpu():  # experiment.cpp:312-389 (cmd_sweep), scored ag
     rows = adx.warmup_sweep(m, x, s, [(2, 20, 1), (2, 1, 1), (3, 3, 1), (3, 1, 2)], precision="f64")
     assert [r["config"] for r in rows] == ["N2_w20_S1", "N2_w1_S1", "N3_w3_S1", "N3_w1_S2"]
     assert rows[0]["final_mse"] == 0.0 and rows[0]["final_rel_l2"] == 0.0  # w = T: sequential
+    # the (N=2, w=1) row is the reference's golden G1 (test_executor.cpp:66-81): its final MSE
+    # is compare_trajectories' mean over d=2 -- the golden's |delta|^2 / 2
+    gold = 0.0011860077151787584
+    assert abs(rows[1]["final_mse"] - gold) <= 1e-9 * gold, rows[1]["final_mse"]
     for r in rows[1:]:
         assert np.isfinite(r["final_mse"]) and r["final_rel_l2"] > 0.0
     plan = adx.plan_async(20, 1, 3, 2)
