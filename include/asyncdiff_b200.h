@@ -340,6 +340,17 @@ int adx_tc_conv3x3(int ordinal, int batch, int H, int W, int Cin, int Cout, cons
  * launch in this process uses N tile `bn` and split-K factor `splits` (0, 0:
  * back to the measured plan table, then the model) */
 int adx_tc_plan_override(int bn, int splits);
+/* bf16-output epilogue (the UNet pass's: TMA-store staging, bf16 residual with row stride ldr,
+ * output row stride ldo >= N, columns past N untouched); bn / splits force a tile plan */
+int adx_tc_gemm_bf16(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B, const float* bias,
+                     const uint16_t* residual, int ldr, uint16_t* out, int ldo, int bn, int splits, int iters,
+                     double* ms_per_iter);
+int adx_tc_conv3x3_bf16(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X,
+                        const uint16_t* Wt, const float* bias, const uint16_t* residual, uint16_t* out, int bn,
+                        int splits, int iters, double* ms_per_iter);
+/* per-CTA %globaltimer stamps (8 per CTA) of the last tc_gemm / conv launch: diagnostics of
+ * -DADX_TC_TIMELINE builds (tools/tools_tc_timeline.py); zeros in the product build */
+int adx_tc_timeline(unsigned long long* out, int n_ctas);
 
 /* ------------------------------------------------------ §8(f) next rows */
 /* save_checkpoint / load_checkpoint: proj/include/asyncdiff/serialize.hpp:35-36,

@@ -1024,6 +1024,80 @@ int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint1
     });
 }
 
+// bf16-output epilogue variants (TMA-store path): optional bf16 residual (row stride ldr),
+// output row stride ldo >= N; bn / splits force a tile plan (0, 0: the launcher's choice)
+int adx_tc_gemm_bf16(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B, const float* bias,
+                     const uint16_t* residual, int ldr, uint16_t* out, int ldo, int bn, int splits, int iters,
+                     double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        if (ldo < N || (residual && ldr < N)) throw std::invalid_argument("tc_gemm_bf16: ldo / ldr < N");
+        DevBuf a(static_cast<size_t>(M) * K * 2), b(static_cast<size_t>(N) * K * 2), o(static_cast<size_t>(M) * ldo * 2),
+            r(residual ? static_cast<size_t>(M) * ldr * 2 : 16), bi(static_cast<size_t>(N) * 4);
+        CKC(cudaMemcpy(a.p, A, static_cast<size_t>(M) * K * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(b.p, B, static_cast<size_t>(N) * K * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(o.p, out, static_cast<size_t>(M) * ldo * 2, cudaMemcpyHostToDevice));  // untouched columns kept
+        if (residual) CKC(cudaMemcpy(r.p, residual, static_cast<size_t>(M) * ldr * 2, cudaMemcpyHostToDevice));
+        if (bias) CKC(cudaMemcpy(bi.p, bias, static_cast<size_t>(N) * 4, cudaMemcpyHostToDevice));
+        adx::TcArgs p;
+        p.bias = bias ? static_cast<const float*>(bi.p) : nullptr;
+        p.residual = residual ? static_cast<const __nv_bfloat16*>(r.p) : nullptr;
+        p.ldr = ldr;
+        p.out_bf16 = static_cast<__nv_bfloat16*>(o.p);
+        p.ldo = ldo;
+        if (bn) adx::tc_plan_override(bn, std::max(1, splits));
+        try {
+            adx::tc_gemm(a.p, b.p, M, N, K, p, 0, 0);
+            CKC(cudaDeviceSynchronize());
+            if (iters > 0 && ms_per_iter)
+                *ms_per_iter = time_graph_ms([&](cudaStream_t st) { adx::tc_gemm(a.p, b.p, M, N, K, p, st, 0); }, iters);
+        } catch (...) {
+            adx::tc_plan_override(0, 0);
+            throw;
+        }
+        if (bn) adx::tc_plan_override(0, 0);
+        CKC(cudaMemcpy(out, o.p, static_cast<size_t>(M) * ldo * 2, cudaMemcpyDeviceToHost));
+    });
+}
+
+int adx_tc_conv3x3_bf16(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X, const uint16_t* Wt,
+                        const float* bias, const uint16_t* residual, uint16_t* out, int bn, int splits, int iters,
+                        double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        const size_t nx = static_cast<size_t>(batch) * H * W * Cin, nw = static_cast<size_t>(Cout) * 9 * Cin,
+                     no = static_cast<size_t>(batch) * H * W * Cout;
+        DevBuf x(nx * 2), w(nw * 2), o(no * 2), r(residual ? no * 2 : 16), bi(static_cast<size_t>(Cout) * 4);
+        CKC(cudaMemcpy(x.p, X, nx * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(w.p, Wt, nw * 2, cudaMemcpyHostToDevice));
+        if (residual) CKC(cudaMemcpy(r.p, residual, no * 2, cudaMemcpyHostToDevice));
+        if (bias) CKC(cudaMemcpy(bi.p, bias, static_cast<size_t>(Cout) * 4, cudaMemcpyHostToDevice));
+        adx::TcArgs p;
+        p.bias = bias ? static_cast<const float*>(bi.p) : nullptr;
+        p.residual = residual ? static_cast<const __nv_bfloat16*>(r.p) : nullptr;
+        p.ldr = Cout;
+        p.out_bf16 = static_cast<__nv_bfloat16*>(o.p);
+        p.ldo = Cout;
+        if (bn) adx::tc_plan_override(bn, std::max(1, splits));
+        try {
+            adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, 0);
+            CKC(cudaDeviceSynchronize());
+            if (iters > 0 && ms_per_iter)
+                *ms_per_iter = time_graph_ms(
+                    [&](cudaStream_t st) { adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, st); }, iters);
+        } catch (...) {
+            adx::tc_plan_override(0, 0);
+            throw;
+        }
+        if (bn) adx::tc_plan_override(0, 0);
+        CKC(cudaMemcpy(out, o.p, no * 2, cudaMemcpyDeviceToHost));
+    });
+}
+
+int adx_tc_timeline(unsigned long long* out, int n_ctas) {
+    return guard([&] { adx::tc_timeline(out, n_ctas); });
+}
+
 int adx_tc_plan_override(int bn, int splits) {
     return guard([&] { adx::tc_plan_override(bn, splits); });
 }

@@ -42,7 +42,10 @@ namespace {
 
 // KT = 64 keys per KV block: 100 KB of SMEM and 256 TMEM columns per CTA, so two CTAs
 // (20 warps) share an SM and hide each other's barrier / TMEM / MUFU latencies
-constexpr int QT = 128, KT = 64, HD = 64, STG = 3;
+#ifndef ADX_ATTN_STG
+#define ADX_ATTN_STG 3
+#endif
+constexpr int QT = 128, KT = 64, HD = 64, STG = ADX_ATTN_STG;
 constexpr int HK = KT / 2;                            // keys per softmax warp (two warps per row)
 // V tiles are [KT keys][64 dims] straight from the V rows (SW128, dims contiguous) and feed
 // the PV MMA as an MN-major B operand (idesc bit 16; a K=16 step = 16 key rows = 2048 B,
@@ -500,6 +503,262 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TM_COLS) : "memory");
 }
 
+// ---------------------------------------------------------------------------- v2
+// Same CTA shape (one 128-query tile x one head x KV split, 10 warps, 2 CTAs per SM, 64-key
+// KV blocks), but the two softmax warps of a TMEM lane quadrant no longer meet every block:
+// warp half h owns keys [32h, 32h + 32) of every block with its OWN running max m_h, sum l_h
+// and O accumulator O_h (TMEM [2KT + 64h, 2KT + 64h + 64)).  O_h = sum_j P_j,h V_j,h is the
+// product over that half's keys only; the two partial softmaxes are merged once, after the
+// last block (the split-KV combine rule inside the CTA).  P_j,h (bf16 pairs) is written over
+// the half's own S_j columns (TMEM budget: S[2] 128 + O[2] 128 = 256 columns).  S_{j+2}
+// reuses that buffer: the MMA warp issues it after PV_j (tcgen05.mma from one thread
+// execute in issue order), and after the softmax has read S_j (p_full_j precedes PV_j).
+__global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__ CUtensorMap tmQ,
+                                                         const __grid_constant__ CUtensorMap tmK,
+                                                         const __grid_constant__ CUtensorMap tmV, const AttnArgs p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
+    constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2;
+    constexpr int XCH_OFF = Q_B + STG * (K_B + V_B) + 256;
+    uint8_t* sQ = smem;
+    uint8_t* sK = sQ + Q_B;
+    uint8_t* sV = sK + STG * K_B;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + STG * V_B);
+    uint64_t* q_full = bars;
+    uint64_t* kv_full = bars + 1;        // [STG]
+    uint64_t* kv_empty = kv_full + STG;  // [STG]
+    uint64_t* s_full = kv_empty + STG;   // [2]
+    uint64_t* p_full = s_full + 2;       // [2 buffers][2 halves]
+    uint64_t* pv_done = p_full + 4;      // [2 buffers][2 halves]
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(pv_done + 4);
+    float* xml = reinterpret_cast<float*>(smem + XCH_OFF);  // [2 halves][2 (m, l)][128 rows]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qt = blockIdx.x / p.nsplit, split = blockIdx.x - qt * p.nsplit, head = blockIdx.y, img = blockIdx.z;
+    const int nkv_all = (p.Lk + KT - 1) / KT;
+    const int j0 = (nkv_all * split) / p.nsplit;
+    const int nkv = (nkv_all * (split + 1)) / p.nsplit - j0;
+
+    if (warp == 0 && lane == 0) {
+        bar_init(q_full, 1);
+        for (int s = 0; s < STG; ++s) {
+            bar_init(&kv_full[s], 1);
+            bar_init(&kv_empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) bar_init(&s_full[b], 1);
+        for (int i = 0; i < 4; ++i) {
+            bar_init(&p_full[i], 4);  // the 4 warps of one half
+            bar_init(&pv_done[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tptr)), "n"(256)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    pdl_wait();
+    const uint32_t tmem = *tptr;
+
+    if (warp == 0 && lane == 0) {
+        bar_expect(q_full, Q_B);
+        tma2d(sQ, &tmQ, head * HD, img * p.L + qt * QT, q_full);
+        for (int j = 0; j < nkv; ++j) {
+            const int s = j % STG;
+            bar_wait(&kv_empty[s], ((j / STG) & 1) ^ 1);
+            bar_expect(&kv_full[s], K_B + V_B);
+            tma2d(sK + s * K_B, &tmK, head * HD, img * p.Lk + (j0 + j) * KT, &kv_full[s]);
+            tma2d(sV + s * V_B, &tmV, head * HD, img * p.Lk + (j0 + j) * KT, &kv_full[s]);
+        }
+    } else if (warp == 1 && lane == 0) {
+        auto issue_s = [&](int j) {
+            const int s = j % STG, b = j & 1;
+            bar_wait(&kv_full[s], (j / STG) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < HD / 16; ++k)
+                mma(tmem + b * KT, sdesc(sQ + k * 32), sdesc(sK + s * K_B + k * 32), idesc(QT, KT), k > 0);
+            commit(&s_full[b]);
+        };
+        bar_wait(q_full, 0);
+        issue_s(0);
+        for (int j = 1; j <= nkv; ++j) {
+            if (j < nkv) issue_s(j);  // after PV_{j-2} in issue order: S_j may overwrite P_{j-2}
+            const int jj = j - 1, s = jj % STG, b = jj & 1;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                bar_wait(&p_full[b * 2 + h], (jj >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int k = 2 * h; k < 2 * h + 2; ++k)  // keys [16k, 16k + 16) of the block
+                    mma_ts(tmem + 2 * KT + h * HD, tmem + b * KT + h * HK + (k & 1) * 8,
+                           sdesc(sV + s * V_B + k * 2048), idesc(QT, HD) | (1u << 16), (jj > 0 || (k & 1)) ? 1u : 0u);
+                commit(&pv_done[b * 2 + h]);
+            }
+            commit(&kv_empty[s]);
+        }
+    } else if (warp >= 2) {
+        const int q = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int r = q * 32 + lane;
+        const uint32_t lrow = static_cast<uint32_t>(q * 32) << 16;
+        const float sl2 = 0.125f * 1.4426950408889634f;
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+            const int b = j & 1;
+            const uint32_t tS = tmem + b * KT + half * HK + lrow;
+            bar_wait(&s_full[b], (j >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t sr[HK];
+            tld_hk_nowait(tS, sr);
+            tld_wait();
+            const int valid = min(KT, p.Lk - (j0 + j) * KT) - half * HK;
+            if (valid < HK) {
+#pragma unroll
+                for (int i = 0; i < HK; ++i)
+                    if (i >= valid) sr[i] = 0xff800000u;
+            }
+            float mp[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) mp[a] = __uint_as_float(sr[a]);
+#pragma unroll
+            for (int i = 8; i < HK; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(sr[i]));
+            const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                                   fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+            // lazy rescale of this half's O: only when its row max grows by > 2^8
+            const bool need = mx > m && (m == -INFINITY || (mx - m) * sl2 > 8.f);
+            if (__any_sync(0xffffffffu, need)) {
+                if (j > 0) {  // O_h must hold PV_{j-1},h
+                    bar_wait(&pv_done[((j - 1) & 1) * 2 + half], ((j - 1) >> 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const float alpha = need ? (m == -INFINITY ? 0.f : ex2((m - mx) * sl2)) : 1.f;
+                    const uint32_t tO = tmem + 2 * KT + half * HD + lrow;
+#pragma unroll
+                    for (int c = 0; c < HD; c += 16) {
+                        float ov[16];
+                        tld16(tO + c, ov);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) ov[i] *= alpha;
+                        tst16(tO + c, ov);
+                    }
+                    tst_wait();
+                    l *= alpha;
+                }
+                if (need) m = mx;
+            }
+            const float off = m == -INFINITY ? 0.f : -m * sl2;  // (a fully masked half: P = 0)
+            float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            uint32_t pk[HK / 2];
+#pragma unroll
+            for (int c = 0; c < HK; c += 2) {
+                const float v0 = ex2_mix(fmaf(__uint_as_float(sr[c]), sl2, off), c);
+                const float v1 = ex2_mix(fmaf(__uint_as_float(sr[c + 1]), sl2, off), c + 1);
+                sp[c & 7] += v0;
+                sp[(c + 1) & 7] += v1;
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
+                pk[c / 2] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            tst_u32<HK / 2>(tS, pk);  // P_j,h over the S_j,h columns just read
+            tst_wait();
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) bar_arrive(&p_full[b * 2 + half]);
+            l += ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
+        }
+        // merge the two halves: M = max(m0, m1), w_h = 2^((m_h - M) log2e / 8), O = w0 O0 + w1 O1,
+        // row sum w0 l0 + w1 l1; warp half h finishes output columns [32h, 32h + 32)
+        xml[(half * 2 + 0) * QT + r] = m;
+        xml[(half * 2 + 1) * QT + r] = l;
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        const float m0 = xml[0 * QT + r], l0 = xml[1 * QT + r], m1 = xml[2 * QT + r], l1 = xml[3 * QT + r];
+        const float M = fmaxf(m0, m1);
+        const float w0 = m0 == -INFINITY ? 0.f : ex2((m0 - M) * sl2);
+        const float w1 = m1 == -INFINITY ? 0.f : ex2((m1 - M) * sl2);
+        float lt = w0 * l0 + w1 * l1;
+        const int lb = (nkv - 1) & 1;
+        bar_wait(&pv_done[lb * 2 + 0], ((nkv - 1) >> 1) & 1);
+        bar_wait(&pv_done[lb * 2 + 1], ((nkv - 1) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float ov[HD / 2], o1[HD / 2];
+        const uint32_t tO0 = tmem + 2 * KT + lrow + half * (HD / 2);
+        tld16(tO0, ov);
+        tld16(tO0 + 16, ov + 16);
+        tld16(tO0 + HD, o1);
+        tld16(tO0 + HD + 16, o1 + 16);
+#pragma unroll
+        for (int c = 0; c < HD / 2; ++c) ov[c] = w0 * ov[c] + w1 * o1[c];
+        const float mrow = M;
+        const long long row = static_cast<long long>(qt) * QT + r;
+        bool write_out = true;
+        if (p.nsplit > 1) {
+            const long long item =
+                qt + static_cast<long long>(gridDim.x / p.nsplit) * (head + static_cast<long long>(gridDim.y) * img);
+            float* rec = p.part + (item * p.nsplit + split) * kRecFloats;
+#pragma unroll
+            for (int c = 0; c < HD / 2; c += 4)
+                *reinterpret_cast<float4*>(rec + r * HD + half * (HD / 2) + c) =
+                    make_float4(ov[c], ov[c + 1], ov[c + 2], ov[c + 3]);
+            if (half == 0) rec[QT * HD + r] = mrow, rec[QT * HD + QT + r] = lt;
+            __threadfence();
+            __shared__ unsigned last2;
+            asm volatile("bar.sync 5, 256;" ::: "memory");
+            if (threadIdx.x == 64)
+                last2 = atomicAdd(p.counters + item, 1u) == static_cast<unsigned>(p.nsplit - 1);
+            asm volatile("bar.sync 5, 256;" ::: "memory");
+            write_out = last2 != 0u;
+            if (write_out) {
+                __threadfence();
+                const float* base = p.part + item * p.nsplit * kRecFloats;
+                float MM = -INFINITY;
+                for (int s2 = 0; s2 < p.nsplit; ++s2) MM = fmaxf(MM, __ldcg(base + s2 * kRecFloats + QT * HD + r));
+                float acc[HD / 2], den = 0.f;
+#pragma unroll
+                for (int c = 0; c < HD / 2; ++c) acc[c] = 0.f;
+                for (int s2 = 0; s2 < p.nsplit; ++s2) {
+                    const float* rs = base + s2 * kRecFloats;
+                    const float ms = __ldcg(rs + QT * HD + r);
+                    const float w = ms == -INFINITY ? 0.f : ex2((ms - MM) * sl2);
+                    den = fmaf(w, __ldcg(rs + QT * HD + QT + r), den);
+#pragma unroll
+                    for (int c = 0; c < HD / 2; c += 4) {
+                        const float4 o4 = __ldcg(reinterpret_cast<const float4*>(rs + r * HD + half * (HD / 2) + c));
+                        acc[c] = fmaf(w, o4.x, acc[c]), acc[c + 1] = fmaf(w, o4.y, acc[c + 1]);
+                        acc[c + 2] = fmaf(w, o4.z, acc[c + 2]), acc[c + 3] = fmaf(w, o4.w, acc[c + 3]);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < HD / 2; ++c) ov[c] = acc[c];
+                lt = den;
+                if (threadIdx.x == 64) p.counters[item] = 0u;
+            }
+        }
+        if (write_out && row < p.L) {
+            const float inv = 1.0f / lt;
+            __nv_bfloat16* dst = p.out + (static_cast<long long>(img) * p.L + row) * p.ldo + head * HD + half * (HD / 2);
+#pragma unroll
+            for (int c = 0; c < HD / 2; c += 8) {
+                uint4 v;
+                __nv_bfloat162 b0 = __floats2bfloat162_rn(ov[c] * inv, ov[c + 1] * inv);
+                __nv_bfloat162 b1 = __floats2bfloat162_rn(ov[c + 2] * inv, ov[c + 3] * inv);
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(ov[c + 4] * inv, ov[c + 5] * inv);
+                __nv_bfloat162 b3 = __floats2bfloat162_rn(ov[c + 6] * inv, ov[c + 7] * inv);
+                v.x = *reinterpret_cast<uint32_t*>(&b0);
+                v.y = *reinterpret_cast<uint32_t*>(&b1);
+                v.z = *reinterpret_cast<uint32_t*>(&b2);
+                v.w = *reinterpret_cast<uint32_t*>(&b3);
+                *reinterpret_cast<uint4*>(dst + c) = v;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256) : "memory");
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -603,11 +862,21 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
         CKA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr[dev] = true;
     }
+    static bool attr2[64] = {};
+    if (!attr2[dev]) {
+        CKA(cudaFuncSetAttribute(attn_kernel_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr2[dev] = true;
+    }
+    static const int ver = [] {  // ADX_ATTN_V=1: the round-1 kernel (per-block max exchange)
+        const char* e = getenv("ADX_ATTN_V");
+        return e && *e == '1' ? 1 : 2;
+    }();
+    auto kern = ver == 1 ? attn_kernel : attn_kernel_v2;
     dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD, batch);
-    if (tc_trace()) fprintf(stderr, "tc_attention L=%d Lk=%d C=%d batch=%d S=%d\n", L, Lk, C, batch, a.nsplit);
-    CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, st, 1, mq, mk, mv, a));
+    if (tc_trace()) fprintf(stderr, "tc_attention L=%d Lk=%d C=%d batch=%d S=%d v%d\n", L, Lk, C, batch, a.nsplit, ver);
+    CKA(launch_pdl(kern, grid, dim3(320), smem, st, 1, mq, mk, mv, a));
     tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, [&](cudaStream_t s2) {
-        CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, s2, 1, mq, mk, mv, a));
+        CKA(launch_pdl(kern, grid, dim3(320), smem, s2, 1, mq, mk, mv, a));
     });
     CKA(cudaGetLastError());
 }

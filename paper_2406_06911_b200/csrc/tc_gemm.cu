@@ -44,12 +44,27 @@ namespace adx {
     } while (0)
 
 bool tma_store_enabled();
+bool tma_res_enabled();
 bool n_fast_order(long long a_bytes);
 
 namespace {
 
-constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
+
+// -DADX_TC_TIMELINE: %globaltimer stamps per CTA (tools/tools_tc_timeline.py; diagnostics only)
+#ifdef ADX_TC_TIMELINE
+__device__ unsigned long long g_tl[2048][8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL(k) (g_tl[blockIdx.x + gridDim.x * blockIdx.y][k] = gtime())
+#else
+#define TL(k) ((void)0)
+#endif
 constexpr int kMaxSplitsDev = 8;  // split-K cluster size bound (portable cluster size)
+constexpr int EPW_ = 8;           // epilogue warps
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -85,6 +100,12 @@ __device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* sr
                  "r"(c0), "r"(c1), "r"(sa(src))
                  : "memory");
 }
+__device__ __forceinline__ void tma_store4d(const CUtensorMap* m, const void* src, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(sa(src))
+                 : "memory");
+}
 __device__ __forceinline__ void tma4d(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, uint64_t* b) {
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
@@ -108,6 +129,31 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t a, uint64_t b, 
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// one 64-deep k block (4 x K16) issued by the elected lane of a converged warp, then the commit
+// that releases its SMEM stage: one asm block, descriptors precomputed by every lane (so the
+// compiler keeps them warp-uniform), no per-instruction election loop
+__device__ __forceinline__ void mma_kblock_commit(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                  uint32_t acc0, uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %6, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %8, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %9, %10, %3, t;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n}\n" ::"r"(tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc0), "l"(a + 2), "l"(b + 2), "l"(a + 4), "l"(b + 4), "l"(a + 6),
+        "l"(b + 6), "r"(sa(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* b) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(sa(b))
         : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* b) {
@@ -185,15 +231,18 @@ __device__ __forceinline__ const float* chan_row(const TcArgs& p, long long m, i
 }
 
 // fused epilogue on 16 accumulator columns [nb, nb + 16) of output row m
+// bias_base: column-indexed bias (p.bias, or the tile's SMEM-staged copy offset by -n0)
 __device__ __forceinline__ void epi16(const TcArgs& p, long long m, const float* ca, int nb, float* v,
-                                      const uint4* rpre = nullptr, uint4* sdst = nullptr) {
+                                      const uint4* rpre = nullptr, uint4* sdst = nullptr,
+                                      const float* bias_base = nullptr) {
     const int nlim = p.n_store ? p.n_store : p.N;
+    const float* bias = bias_base ? bias_base : p.bias;
     if ((((p.ldo | p.ldr) & 7) == 0) && nb + 16 <= nlim && !p.residual_f32) {
         // vectorised: 16-byte loads / stores
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
-            if (p.bias) {
-                const float4 b = *reinterpret_cast<const float4*>(p.bias + nb + j);
+            if (bias) {
+                const float4 b = *reinterpret_cast<const float4*>(bias + nb + j);
                 v[j] += b.x, v[j + 1] += b.y, v[j + 2] += b.z, v[j + 3] += b.w;
             }
             if (ca) {
@@ -237,7 +286,7 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, const float*
         const int n = nb + j;
         if (n >= nlim) continue;
         float x = v[j];
-        if (p.bias) x += p.bias[n];
+        if (bias) x += bias[n];
         if (ca) x += ca[n];
         if (p.act == 1) x = silu(x);
         if (p.residual) x += __bfloat162float(p.residual[m * p.ldr + n]);
@@ -245,6 +294,8 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, const float*
         x *= p.out_scale;
         if (p.out_f32)
             p.out_f32[m * p.ldo + n] = x;
+        else if (sdst)  // TMA-store staging: the bulk store writes this block
+            reinterpret_cast<__nv_bfloat16*>(sdst)[j] = __float2bfloat16(x);
         else
             p.out_bf16[m * p.ldo + n] = __float2bfloat16(x);
     }
@@ -309,10 +360,39 @@ __device__ __forceinline__ float4 reduce_dsmem4(const uint32_t* a, int S, int of
 template <int BN>
 constexpr int kStageChunks() { return BN > 192 ? 0 : (BN / 16 + 1) / 2; }
 
+// SMEM ring depth: as many (A, B) stages as fit one CTA per SM (max dynamic SMEM 227 KB), up to
+// 8.  The mainloop is latency-bound, not MMA-bound: a k-block's TMA round trip is ~1 us under
+// load (tools/tools_tc_timeline.py), so throughput ~ stages x stage bytes / 1 us; with the
+// round-1 ring of 4 every conv / GEMM ran at ~250 ns per k-block whatever its tile width.
+// ADX_TC_STAGES (compile time) caps it for A/B runs.
+#ifndef ADX_TC_STAGES
+#define ADX_TC_STAGES 8
+#endif
+// PDL: the first ring of weight (B) tiles is requested before griddepcontrol.wait, and the
+// MMA warp triggers the dependent launch once its last MMA is issued (A/B switches)
+#ifndef ADX_TC_EARLY_B
+#define ADX_TC_EARLY_B 0
+#endif
+#ifndef ADX_TC_TRIGGER
+#define ADX_TC_TRIGGER 0
+#endif
+template <int BN>
+constexpr int kStages() {
+    constexpr int fixed = 1024 + 256 + EPW_ * kStageChunks<BN>() * 1024 + 16 * BN;
+    constexpr int per = BM * BK * 2 + BN * BK * 2;
+    constexpr int fit = (227 * 1024 - fixed) / per;
+    return fit < ADX_TC_STAGES ? fit : ADX_TC_STAGES;
+}
+template <int BN>
+constexpr size_t kGemmSmem() {
+    return 1024 + static_cast<size_t>(kStages<BN>()) * (BM * BK * 2 + BN * BK * 2) + 256 +
+           static_cast<size_t>(EPW_) * kStageChunks<BN>() * 1024 + 16 * BN;
+}
+
 // ------------------------------------------------------------------ kernel
 // epilogue warps: EPW / 4 per TMEM lane quadrant, each over its share of the tile's
 // 16-column chunks (more loads / stores in flight for the 1-tile-per-CTA small GEMMs)
-constexpr int EPW = 8;
+constexpr int EPW = EPW_;
 constexpr int kGemmThreads = 64 + 32 * EPW;
 __device__ __forceinline__ void epi_chunks(int nch, int part, int& c0, int& c1) {
     constexpr int P = EPW / 4;
@@ -323,13 +403,15 @@ __device__ __forceinline__ void epi_chunks(int nch, int part, int& c0, int& c1) 
 template <int BN, bool CONV>
 __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB,
-                                                         const __grid_constant__ CUtensorMap tmC, const TcArgs p) {
+                                                         const __grid_constant__ CUtensorMap tmC,
+                                                         const __grid_constant__ CUtensorMap tmR, const TcArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+    if (threadIdx.x == 0) TL(0);
     // 1024-byte alignment of the swizzled tiles
     // 1024-byte aligned by offsetting the __shared__ array itself (not through an integer
     // cast), so every access through `smem` stays a shared-space LDS / STS, not a generic LD / ST
     uint8_t* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
-    constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2;
+    constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGES = kStages<BN>();
     constexpr uint32_t ACC_COLS = tmem_cols<BN>();  // one accumulator; two are allocated
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
@@ -337,7 +419,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
     uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* rbar = tempty + 2;       // [EPW] residual chunks landed in an epilogue warp's staging
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(rbar + EPW);
+    // per accumulator: [bias | chan_add] of the tile's BN columns, staged by the epilogue warps
+    float* sepi = reinterpret_cast<float*>(sB + STAGES * B_BYTES + 256 + EPW * kStageChunks<BN>() * 1024);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // Work units.  S == 1: persistent -- CTA b takes output tiles b, b + G, ... (m fastest,
@@ -388,6 +473,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             bar_init(&tfull[a], 1);
             bar_init(&tempty[a], EPW);  // one arrival per epilogue warp
         }
+        for (int w = 0; w < EPW; ++w) bar_init(&rbar[w], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -402,10 +488,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tptr;
-    pdl_wait();  // prologue done: wait for the producers of A / residual
+    if (threadIdx.x == 0) TL(1);
+    // prologue done: wait for the producers of A / residual (the TMA thread waits below, after
+    // requesting the first weight tiles, which no predecessor writes)
+    if (!(warp == 0 && lane == 0)) pdl_wait();
+    if (threadIdx.x == 0) TL(2);
 
     if (warp == 0 && lane == 0) {
         // ---------------------------------------------------------- producer
+        constexpr int kEarly = ADX_TC_EARLY_B ? STAGES : 0;
+        const int early = u0 < uend ? (nkb < kEarly ? nkb : kEarly) : 0;
+        {
+            int tile_m, tile_n, img, h0, w0;
+            coords(u0, tile_m, tile_n, img, h0, w0);
+            for (int i = 0; i < early; ++i) {  // fresh ring: no empty wait
+                bar_expect(&full[i], (CONV ? p.box_w * p.box_h * BK * 2 : A_BYTES) + B_BYTES);
+                tma2d(sB + i * B_BYTES, &tmB, (kb0 + i) * BK, tile_n * BN, &full[i]);
+            }
+        }
+        pdl_wait();
         int it = 0;  // ring position, continuous across tiles
         for (int u = u0; u < uend; u += ustride) {
             int tile_m, tile_n, img, h0, w0;
@@ -414,8 +515,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             for (int i = 0; i < nkb; ++i, ++it) {
                 const int kb = kb0 + i, s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
-                bar_wait(&empty[s], ph ^ 1);
-                bar_expect(&full[s], (CONV ? p.box_w * p.box_h * BK * 2 : A_BYTES) + B_BYTES);
+                const bool pre = it < early;  // B already requested (and the bytes expected)
+                if (!pre) {
+                    bar_wait(&empty[s], ph ^ 1);
+                    bar_expect(&full[s], (CONV ? p.box_w * p.box_h * BK * 2 : A_BYTES) + B_BYTES);
+                }
                 if constexpr (CONV) {
                     // k block kb -> tap (r, s) and channel block; A box at the
                     // tap-shifted window (OOB rows/cols are zero-filled = padding)
@@ -423,16 +527,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                     const int tap = kb / cpb, cb = kb - tap * cpb;
                     const int dr = tap / 3 - 1, ds = tap % 3 - 1;
                     tma4d(sA + s * A_BYTES, &tmA, cb * BK, w0 + ds, h0 + dr, img, &full[s]);
-                    tma2d(sB + s * B_BYTES, &tmB, kb * BK, n0, &full[s]);
                 } else {
                     tma2d(sA + s * A_BYTES, &tmA, kb * BK, tile_m * BM, &full[s]);
-                    tma2d(sB + s * B_BYTES, &tmB, kb * BK, n0, &full[s]);
                 }
+                if (!pre) tma2d(sB + s * B_BYTES, &tmB, kb * BK, n0, &full[s]);
             }
         }
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer
+        // the whole warp runs the loop (warp-uniform control flow and descriptors); one elected
+        // lane issues each k block's 4 MMAs and the commit releasing its stage
         constexpr uint32_t idesc = idesc_bf16<BN>();
+        const uint64_t da0 = sdesc(sA), db0 = sdesc(sB);  // stage s, k step k: + (s * bytes + 32 k) >> 4
         int it = 0, lu = 0;
         for (int u = u0; u < uend; u += ustride, ++lu) {
             const int acc = lu & 1;
@@ -443,17 +549,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
                 bar_wait(&full[s], ph);
+                if (it == 0 && lane == 0) TL(3);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    const uint64_t a = sdesc(sA + s * A_BYTES + k * 32);
-                    const uint64_t b = sdesc(sB + s * B_BYTES + k * 32);
-                    mma_bf16(tacc, a, b, idesc, (i | k) != 0 ? 1u : 0u);
-                }
-                mma_commit(&empty[s]);
+                mma_kblock_commit(tacc, da0 + static_cast<uint64_t>((s * A_BYTES) >> 4),
+                                  db0 + static_cast<uint64_t>((s * B_BYTES) >> 4), idesc, i != 0 ? 1u : 0u, &empty[s]);
             }
-            mma_commit(&tfull[acc]);
+            mma_commit_elect(&tfull[acc]);
         }
+        // every MMA of this CTA is issued: let the next kernel of the stream start launching
+        // (its CTAs take SMs as ours exit, and its weight TMA overlaps our epilogues)
+        if (ADX_TC_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     } else if (warp >= 2) {
         // --------------------------------------------------------- epilogue
         const int q = warp & 3;             // TMEM lane quadrant this warp may access
@@ -471,7 +576,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 __syncwarp();
             }
+            // while the mainloop runs: (1) the residual chunks of this warp's share arrive by TMA
+            // straight into its staging blocks (the output is written over them in place);
+            // (2) the tile's bias / per-image channel-add columns are staged in SMEM -- no
+            // dependent global load is left inside the chunk loop
+            int rcb = 0, rce = 0;
+            if (S == 1 && p.act != 2) epi_chunks(BN / 16, part, rcb, rce);
+            if (p.tma_res && S == 1 && p.act != 2 && lane == 0 && rcb < rce) {
+                bar_expect(&rbar[warp - 2], (rce - rcb) / 16 * 1024);
+                for (int c = rcb; c < rce; c += 16) {
+                    uint8_t* dst = stage + ((c - rcb) >> 4) * 1024;
+                    if constexpr (CONV)
+                        tma4d(dst, &tmR, n0 + c, w0 + (q * 32) % p.box_w, h0 + (q * 32) / p.box_w, img, &rbar[warp - 2]);
+                    else
+                        tma2d(dst, &tmR, n0 + c, tile_m * BM + q * 32, &rbar[warp - 2]);
+                }
+            }
+            float* sb = sepi + acc * 2 * BN;
+            const bool stage_cols = S == 1 && p.act != 2 && !p.chan_add_rows;
+            if (stage_cols) {
+                const float* car = p.chan_add ? p.chan_add + static_cast<long long>(p.chan_add_shared ? 0 : img) * p.N
+                                              : nullptr;
+                for (int cidx = threadIdx.x - 64; cidx < BN; cidx += 32 * EPW) {
+                    const int n = n0 + cidx;
+                    sb[cidx] = p.bias && n < p.N ? p.bias[n] : 0.f;
+                    sb[BN + cidx] = car && n < p.N ? car[n] : 0.f;
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * EPW) : "memory");  // the epilogue warps
+            }
             bar_wait(&tfull[acc], (lu >> 1) & 1);
+            if (lu == 0 && threadIdx.x == 64) TL(4);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t trow = tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16);
             if (S > 1) {
@@ -503,36 +637,70 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                     // the residual of chunk c+16 is requested before chunk c's TMEM read and
                     // epilogue, so its L2 latency overlaps instead of stalling every chunk
                     const int nlim = p.n_store ? p.n_store : p.N;
-                    const bool pre = valid && p.residual && (((p.ldo | p.ldr) & 7) == 0);
-                    int cb, ce;
-                    epi_chunks(BN / 16, part, cb, ce);
+#if defined(ADX_EPI_DBG) && ADX_EPI_DBG == 1  // diagnostics: no residual traffic
+                    TcArgs pnr = p;
+                    pnr.residual = nullptr;
+                    const TcArgs& pe = pnr;
+#else
+                    const TcArgs& pe = p;
+#endif
+                    // residual: TMA-staged (tma_res), else register-prefetched one chunk ahead
+                    const bool tres = p.tma_res != 0;
+                    const bool pre = !tres && valid && pe.residual && (((p.ldo | p.ldr) & 7) == 0);
+                    const int cb = rcb, ce = rce;
                     uint4 rnext[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
                     if (pre && cb < ce && n0 + cb + 16 <= nlim) {
                         const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + cb);
                         rnext[0] = rp[0], rnext[1] = rp[1];
                     }
-                    const float* ca = valid ? chan_row(p, m, img) : nullptr;
+                    const float* ca = !valid ? nullptr : stage_cols ? (p.chan_add ? sb + BN - n0 : nullptr)
+                                                                    : chan_row(p, m, img);
+                    const float* bb = stage_cols ? (p.bias ? sb - n0 : nullptr) : p.bias;
+                    if (tres && cb < ce) bar_wait(&rbar[warp - 2], lu & 1);
                     for (int c = cb; c < ce; c += 16) {
+                        const uint4* stg_res = tres ? reinterpret_cast<const uint4*>(stage + ((c - cb) >> 4) * 1024 +
+                                                                                      lane * 32)
+                                                    : nullptr;
                         const uint4 rcur[2] = {rnext[0], rnext[1]};
-                        const bool have = pre && n0 + c + 16 <= nlim;
+                        const bool have = tres ? pe.residual != nullptr : pre && n0 + c + 16 <= nlim;
                         if (pre && c + 16 < ce && n0 + c + 32 <= nlim) {
                             const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + c + 16);
                             rnext[0] = rp[0], rnext[1] = rp[1];
                         }
                         float v[16];
+#ifdef ADX_TL_CHUNK
+                        if (c == cb && lu == 0 && threadIdx.x == 64) TL(5);
+#endif
                         tmem_ld16(trow + c, v);
+#ifdef ADX_TL_CHUNK
+                        if (c == cb && lu == 0 && threadIdx.x == 64) TL(6);
+#endif
+#if defined(ADX_EPI_DBG) && ADX_EPI_DBG == 2  // diagnostics: TMEM drain only
+                        if (v[0] == 12345.f && valid) p.out_bf16[m * p.ldo] = __float2bfloat16(v[1]);
+                        continue;
+#endif
                         if (p.tma_store) {
                             // rows past M are clipped by the TMA; their staging content is unused
                             uint4* sd = reinterpret_cast<uint4*>(stage + ((c - cb) >> 4) * 1024 + lane * 32);
-                            if (valid) epi16(p, m, ca, n0 + c, v, have ? rcur : nullptr, sd);
+                            uint4 rr[2] = {rcur[0], rcur[1]};
+                            if (tres) rr[0] = stg_res[0], rr[1] = stg_res[1];  // (registers: no local copy)
+                            if (valid) epi16(pe, m, ca, n0 + c, v, have ? rr : nullptr, sd, bb);
+#ifdef ADX_TL_CHUNK
+                            if (c == cb && lu == 0 && threadIdx.x == 64) TL(7);
+#endif
                             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                             __syncwarp();
                             if (lane == 0) {
-                                tma_store2d(&tmC, stage + ((c - cb) >> 4) * 1024, n0 + c, tile_m * BM + q * 32);
+                                if constexpr (CONV) {  // tile rows 32q.. = 32 pixels of the box (32 | bw or bw | 32)
+                                    tma_store4d(&tmC, stage + ((c - cb) >> 4) * 1024, n0 + c, w0 + (q * 32) % p.box_w,
+                                                h0 + (q * 32) / p.box_w, img);
+                                } else {
+                                    tma_store2d(&tmC, stage + ((c - cb) >> 4) * 1024, n0 + c, tile_m * BM + q * 32);
+                                }
                                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                             }
                         } else if (valid) {
-                            epi16(p, m, ca, n0 + c, v, have ? rcur : nullptr);
+                            epi16(pe, m, ca, n0 + c, v, have ? rcur : nullptr, nullptr, bb);
                         }
                     }
                 }
@@ -542,7 +710,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             __syncwarp();
             if (lane == 0) bar_arrive1(&tempty[acc]);
         }
+#ifndef ADX_TL_CHUNK
+        if (threadIdx.x == 64) TL(5);
+#endif
         if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#ifndef ADX_TL_CHUNK
+        if (threadIdx.x == 64) TL(6);
+#endif
     }
     if (S > 1) {
         // split-K reduction: CTA `split` owns tile rows [r0, r1) and sums the S staged
@@ -594,6 +768,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * ACC_COLS)
                      : "memory");
+#ifndef ADX_TL_CHUNK
+    if (threadIdx.x == 0) TL(7);
+#endif
 }
 
 // --------------------------------------------------------- tensor maps
@@ -627,11 +804,12 @@ CUtensorMap make_map(const void* base, int rank, const cuuint64_t* dims, const c
 }
 
 template <int BN, bool CONV>
-void launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcArgs& p, dim3 grid,
-              cudaStream_t st) {
-    constexpr size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256 + EPW * kStageChunks<BN>() * 1024;
-    static_assert(static_cast<size_t>(BM) * (BN + 4) * 4 <= STAGES * (BM * BK * 2 + BN * BK * 2),
+void launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& r, const TcArgs& p,
+              dim3 grid, cudaStream_t st) {
+    constexpr size_t smem = kGemmSmem<BN>();
+    static_assert(static_cast<size_t>(BM) * (BN + 4) * 4 <= kStages<BN>() * (BM * BK * 2 + BN * BK * 2),
                   "split-K staging must fit in the pipeline buffers");
+    static_assert(smem <= 227 * 1024, "tc_gemm: SMEM over the per-CTA limit");
     static bool attr[64] = {};
     int dev = 0;
     CKT(cudaGetDevice(&dev));
@@ -640,21 +818,21 @@ void launch_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, 
         attr[dev] = true;
     }
     CKT(launch_pdl(tc_gemm_kernel<BN, CONV>, grid, dim3(kGemmThreads), smem, st, static_cast<unsigned>(p.splits), a,
-                   b, c, p));
+                   b, c, r, p));
 }
 
 template <bool CONV>
-void dispatch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcArgs& p, dim3 grid, int bn,
-              cudaStream_t st) {
+void dispatch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& r, const TcArgs& p,
+              dim3 grid, int bn, cudaStream_t st) {
     switch (bn) {
-        case 32: launch_t<32, CONV>(a, b, c, p, grid, st); break;
-        case 64: launch_t<64, CONV>(a, b, c, p, grid, st); break;
-        case 80: launch_t<80, CONV>(a, b, c, p, grid, st); break;
-        case 96: launch_t<96, CONV>(a, b, c, p, grid, st); break;
-        case 128: launch_t<128, CONV>(a, b, c, p, grid, st); break;
-        case 160: launch_t<160, CONV>(a, b, c, p, grid, st); break;
-        case 192: launch_t<192, CONV>(a, b, c, p, grid, st); break;
-        case 256: launch_t<256, CONV>(a, b, c, p, grid, st); break;
+        case 32: launch_t<32, CONV>(a, b, c, r, p, grid, st); break;
+        case 64: launch_t<64, CONV>(a, b, c, r, p, grid, st); break;
+        case 80: launch_t<80, CONV>(a, b, c, r, p, grid, st); break;
+        case 96: launch_t<96, CONV>(a, b, c, r, p, grid, st); break;
+        case 128: launch_t<128, CONV>(a, b, c, r, p, grid, st); break;
+        case 160: launch_t<160, CONV>(a, b, c, r, p, grid, st); break;
+        case 192: launch_t<192, CONV>(a, b, c, r, p, grid, st); break;
+        case 256: launch_t<256, CONV>(a, b, c, r, p, grid, st); break;
         default: throw std::invalid_argument("tc_gemm: BN must be 32/64/80/96/128/160/192/256");
     }
 }
@@ -682,7 +860,7 @@ int cluster_capacity_t(int S) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find({dev, S});
     if (it != cache.end()) return it->second;
-    constexpr size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256 + EPW * kStageChunks<BN>() * 1024;
+    constexpr size_t smem = kGemmSmem<BN>();
     CKT(cudaFuncSetAttribute(tc_gemm_kernel<BN, CONV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(S * 64, 1, 1);
@@ -844,6 +1022,15 @@ void tc_profile_collect(double out[3][3]) {
     g_prof.clear();
 }
 
+// the conditions under which epi16 takes its vectorised path (16-byte residual loads / stores);
+// the TMA-store epilogue is only enabled when they hold (the scalar path stages too, but the
+// launcher keeps the fast path the only one the bulk stores see)
+static bool vec_epilogue(const TcArgs& p) {
+    if (p.residual_f32) return false;
+    if (p.residual && ((p.ldr & 7) || (reinterpret_cast<uintptr_t>(p.residual) & 15))) return false;
+    return true;
+}
+
 // D = A[M x K] . B[N x K]^T ; A, B bf16 row-major (K contiguous), K % 64 == 0
 void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn) {
     tc_gemm_strided(A, K, B, K, M, N, K, p, st, bn);
@@ -890,18 +1077,28 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     CUtensorMap mc = ma;
     p.tma_store = 0;
     if (tma_store_enabled() && S == 1 && bn <= 192 && p.act != 2 && p.out_bf16 && !p.out_f32 && !p.n_store &&
-        N % 16 == 0 && p.ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(p.out_bf16) & 15) == 0) {
+        N % 16 == 0 && p.ldo % 8 == 0 && (reinterpret_cast<uintptr_t>(p.out_bf16) & 15) == 0 && vec_epilogue(p)) {
         const cuuint64_t dc[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
         const cuuint64_t sc[1] = {static_cast<cuuint64_t>(p.ldo) * 2};
         const cuuint32_t bc[2] = {16, 32};
         mc = make_map(p.out_bf16, 2, dc, sc, bc, CU_TENSOR_MAP_SWIZZLE_NONE);
         p.tma_store = 1;
     }
+    CUtensorMap mr = ma;
+    p.tma_res = 0;
+    if (p.tma_store && p.residual && tma_res_enabled()) {
+        const cuuint64_t dr[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+        const cuuint64_t sr[1] = {static_cast<cuuint64_t>(p.ldr) * 2};
+        const cuuint32_t br[2] = {16, 32};
+        mr = make_map(p.residual, 2, dr, sr, br, CU_TENSOR_MAP_SWIZZLE_NONE);
+        p.tma_res = 1;
+    }
     const dim3 grid = launch_grid<false>(p, bn);
     if (tc_trace_on())
         fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d act=%d grid=%ux%u\n", M, N, K, bn, S, p.act, grid.x, grid.y);
-    dispatch<false>(ma, mb, mc, p, grid, bn, st);
-    tc_profile_measure(st, 1, 2.0 * M * N * K, [&](cudaStream_t s2) { dispatch<false>(ma, mb, mc, p, grid, bn, s2); });
+    dispatch<false>(ma, mb, mc, mr, p, grid, bn, st);
+    tc_profile_measure(st, 1, 2.0 * M * N * K,
+                       [&](cudaStream_t s2) { dispatch<false>(ma, mb, mc, mr, p, grid, bn, s2); });
 }
 
 // 3x3 conv, stride 1, pad 1, as an implicit GEMM over NHWC bf16:
@@ -961,22 +1158,70 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     p.n_tiles = (Cout + bn - 1) / bn;
     p.batch = batch;
     p.n_fast = S == 1 && p.n_tiles > 1 && n_fast_order(2LL * batch * H * W * Cin);
+    // bf16 NHWC output through SMEM + 4-D TMA bulk stores when a warp's 32 tile rows are one
+    // box of pixels (32 | bw or bw | 32, full 128-pixel boxes): the row-per-thread epilogue
+    // otherwise issues 32 row-scattered 16-byte stores per warp instruction
+    CUtensorMap mc = ma;
+    p.tma_store = 0;
+    if (tma_store_enabled() && S == 1 && bn <= 192 && p.out_bf16 && !p.out_f32 && !p.n_store && !p.sub2 &&
+        bw * bh == BM && (bw % 32 == 0 || 32 % bw == 0) && Cout % 16 == 0 && p.ldo % 8 == 0 &&
+        (reinterpret_cast<uintptr_t>(p.out_bf16) & 15) == 0 && vec_epilogue(p)) {
+        const int bx = bw < 32 ? bw : 32;
+        const cuuint64_t dc[4] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(W),
+                                  static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(batch)};
+        const cuuint64_t sc[3] = {static_cast<cuuint64_t>(p.ldo) * 2, static_cast<cuuint64_t>(W) * p.ldo * 2,
+                                  static_cast<cuuint64_t>(H) * W * p.ldo * 2};
+        const cuuint32_t bc[4] = {16, static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(32 / bx), 1};
+        mc = make_map(p.out_bf16, 4, dc, sc, bc, CU_TENSOR_MAP_SWIZZLE_NONE);
+        p.tma_store = 1;
+    }
+    CUtensorMap mr = ma;
+    p.tma_res = 0;
+    if (p.tma_store && p.residual && tma_res_enabled()) {
+        const int bx = bw < 32 ? bw : 32;
+        const cuuint64_t dr[4] = {static_cast<cuuint64_t>(Cout), static_cast<cuuint64_t>(W),
+                                  static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(batch)};
+        const cuuint64_t sr[3] = {static_cast<cuuint64_t>(p.ldr) * 2, static_cast<cuuint64_t>(W) * p.ldr * 2,
+                                  static_cast<cuuint64_t>(H) * W * p.ldr * 2};
+        const cuuint32_t br[4] = {16, static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(32 / bx), 1};
+        mr = make_map(p.residual, 4, dr, sr, br, CU_TENSOR_MAP_SWIZZLE_NONE);
+        p.tma_res = 1;
+    }
     const dim3 grid = launch_grid<true>(p, bn);
     if (tc_trace_on())
-        fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u\n", H, W, Cin, Cout, bw, bh, bn, S,
-                grid.x, grid.y, grid.z);
-    dispatch<true>(ma, mb, ma, p, grid, bn, st);  // (no TMA store for convs: tmC unused)
+        fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u tma_store=%d\n", H, W, Cin, Cout, bw,
+                bh, bn, S, grid.x, grid.y, grid.z, p.tma_store);
+    dispatch<true>(ma, mb, mc, mr, p, grid, bn, st);
     // algorithmic FLOPs (a stride-2 conv does a quarter of the work it launches)
     tc_profile_measure(st, 0, 2.0 * batch * H * W * Cout * 9.0 * Cin / (p.sub2 ? 4.0 : 1.0),
-                       [&](cudaStream_t s2) { dispatch<true>(ma, mb, ma, p, grid, bn, s2); });
+                       [&](cudaStream_t s2) { dispatch<true>(ma, mb, mc, mr, p, grid, bn, s2); });
 }
 
 bool tc_trace() { return tc_trace_on(); }
+
+// copy the per-CTA timeline stamps of the last launch (-DADX_TC_TIMELINE builds; else zeros)
+void tc_timeline(unsigned long long* out, int n_ctas) {
+#ifdef ADX_TC_TIMELINE
+    CKT(cudaDeviceSynchronize());
+    CKT(cudaMemcpyFromSymbol(out, g_tl, static_cast<size_t>(std::min(n_ctas, 2048)) * 8 * 8));
+#else
+    std::memset(out, 0, static_cast<size_t>(n_ctas) * 8 * 8);
+#endif
+}
 
 // ADX_TC_TMA_STORE=0: the GEMM epilogue stores straight from registers
 bool tma_store_enabled() {
     static const bool on = [] {
         const char* e = getenv("ADX_TC_TMA_STORE");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
+// ADX_TC_TMA_RES=0: the residual is register-prefetched from global one chunk ahead instead
+bool tma_res_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("ADX_TC_TMA_RES");
         return !(e && *e == '0');
     }();
     return on;

@@ -37,10 +37,14 @@ struct TcArgs {
     int splits = 1;                       // filled by the launcher: split-K factor (cluster size)
     int tma_store = 0;                    // filled by the launcher: bf16 output written per 32x16
                                           //   chunk from SMEM by the TMA (GEMM, S = 1, BN <= 192)
+    int tma_res = 0;                      // filled by the launcher: the bf16 residual arrives by TMA in
+                                          //   the TMA-store staging blocks (with tma_store)
     int n_fast = 0;                       // filled by the launcher: persistent tile order n-fastest
                                           //   (A tiles reused while L2-hot when A is the big operand)
 };
 
+// per-CTA %globaltimer stamps of the last launch (ADX_TC_TIMELINE builds; zeros otherwise)
+void tc_timeline(unsigned long long* out, int n_ctas);
 // force (bn, splits) for every following launch (tuning); (0, 0) restores the plan table / model
 void tc_plan_override(int bn, int splits);
 // ADX_TC_TRACE=1: print every launch's shape / plan (and, when profiling, its isolated time)

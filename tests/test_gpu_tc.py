@@ -99,11 +99,24 @@ def test_tc_conv3x3_matches_fp32_reference(batch, H, W, Cin, Cout):
 @pytest.mark.parametrize("L,Lk,C", [(256, 256, 64), (9216 // 16, 576, 128), (144, 144, 320), (300, 77, 128),
                                      (1024, 1024, 640),
                                      # split-KV (ticketed combine of partial O / max / sum): level-1 shape, ragged Lk
-                                     (2304, 2304, 640), (700, 1000, 320)])
+                                     (2304, 2304, 640), (700, 1000, 320),
+                                     # the c2 level-0 self-attention exactly (split-KV S=2, 1.0 ms of a c2 pass)
+                                     (9216, 9216, 320)])
 def test_tc_attention_matches_fp32_reference(L, Lk, C):
+    check_attention(L, Lk, C, 1.0)
+
+
+@pytest.mark.parametrize("L,Lk,C,scale", [(1024, 1024, 128, 3.0), (512, 700, 64, 6.0)])
+def test_tc_attention_large_logits_rescale(L, Lk, C, scale):
+    """score spreads of hundreds: the running max grows by > 2^8 across KV blocks, so the
+    lazy O / row-sum rescale path runs"""
+    check_attention(L, Lk, C, scale)
+
+
+def check_attention(L, Lk, C, scale):
     rng = np.random.default_rng(L + Lk + C)
-    Q = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
-    K = bf16_bits(rng.standard_normal((Lk, C)).astype(np.float32))
+    Q = bf16_bits((scale * rng.standard_normal((L, C))).astype(np.float32))
+    K = bf16_bits((scale * rng.standard_normal((Lk, C))).astype(np.float32))
     Vb = bf16_bits(rng.standard_normal((Lk, C)).astype(np.float32))
     out = np.zeros((L, C), np.uint16)
     _lib.check(adx.lib().adx_tc_attention(0, L, Lk, C, Q.ctypes.data_as(P16), K.ctypes.data_as(P16),
@@ -147,3 +160,57 @@ def test_temporal_attention_matches_fp32_reference(frames, HW, C):
     got = bits_f32(out)
     err = np.abs(got - ref.numpy()).max() / np.abs(ref.numpy()).max()
     assert err < 1e-2, err  # one bf16 rounding of the output
+
+
+def rne_bf16(x):
+    return bf16_bits(np.asarray(x, np.float32))
+
+
+@pytest.mark.parametrize("M,N,K,ldo,bn,S", [(300, 160, 128, 160, 160, 1),   # M % 128 != 0, BN 160
+                                            (1000, 320, 192, 336, 80, 1),   # ldo > N, more tiles than CTAs? (BN 80)
+                                            (2048, 192, 64, 192, 192, 1),   # BN 192
+                                            (4608, 96, 128, 104, 96, 1),    # BN 96, 36 tiles/CTA pass
+                                            (600, 256, 128, 256, 0, 0)])    # launcher's plan
+def test_tc_gemm_bf16_epilogue_bit_exact(M, N, K, ldo, bn, S):
+    """the bf16 epilogue (TMA-store staging, residual, ldo > N) equals the fp32 epilogue's
+    accumulator + bias + residual rounded once to bf16, bit for bit"""
+    rng = np.random.default_rng(M + N)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    res = rne_bf16(rng.standard_normal((M, ldo)))
+    out = np.full((M, ldo), 0x7fc0, np.uint16)  # NaN sentinel: columns past N must stay untouched
+    ab, bb = bf16_bits(A), bf16_bits(B)
+    _lib.check(adx.lib().adx_tc_gemm_bf16(0, M, N, K, ab.ctypes.data_as(P16), bb.ctypes.data_as(P16),
+                                          bias.ctypes.data_as(PF), res.ctypes.data_as(P16), ldo,
+                                          out.ctypes.data_as(P16), ldo, bn, S, 0, None))
+    f32 = np.zeros((M, N), np.float32)
+    _lib.check(adx.lib().adx_tc_plan_override(bn, S))  # the same tile plan (summation order)
+    try:
+        _lib.check(adx.lib().adx_tc_gemm(0, M, N, K, ab.ctypes.data_as(P16), bb.ctypes.data_as(P16),
+                                         bias.ctypes.data_as(PF), 0, f32.ctypes.data_as(PF), 0, 0, None))
+    finally:
+        _lib.check(adx.lib().adx_tc_plan_override(0, 0))
+    want = rne_bf16(f32 + bits_f32(res[:, :N]))
+    assert np.array_equal(out[:, :N], want)
+    assert np.all(out[:, N:] == 0x7fc0)
+
+
+@pytest.mark.parametrize("b,H,W,Ci,Co", [(1, 32, 32, 64, 160),    # box 32x4: 4-D TMA-store epilogue
+                                          (2, 16, 16, 128, 96),   # box 16x8, two images
+                                          (1, 24, 24, 64, 64),    # box 24x5: register epilogue
+                                          (1, 8, 8, 64, 32)])
+def test_tc_conv3x3_bf16_epilogue_bit_exact(b, H, W, Ci, Co):
+    rng = np.random.default_rng(H * Ci + Co)
+    X = bf16_bits(rng.standard_normal((b, H, W, Ci)).astype(np.float32))
+    Wt = bf16_bits((0.1 * rng.standard_normal((Co, 9 * Ci))).astype(np.float32))
+    bias = rng.standard_normal(Co).astype(np.float32)
+    res = rne_bf16(rng.standard_normal((b, H, W, Co)))
+    out = np.zeros((b, H, W, Co), np.uint16)
+    _lib.check(adx.lib().adx_tc_conv3x3_bf16(0, b, H, W, Ci, Co, X.ctypes.data_as(P16), Wt.ctypes.data_as(P16),
+                                             bias.ctypes.data_as(PF), res.ctypes.data_as(P16),
+                                             out.ctypes.data_as(P16), 0, 0, 0, None))
+    f32 = np.zeros((b, H, W, Co), np.float32)
+    _lib.check(adx.lib().adx_tc_conv3x3(0, b, H, W, Ci, Co, X.ctypes.data_as(P16), Wt.ctypes.data_as(P16),
+                                        bias.ctypes.data_as(PF), f32.ctypes.data_as(PF), 0, None))
+    assert np.array_equal(out, rne_bf16(f32 + bits_f32(res)))
