@@ -481,6 +481,8 @@ void Session::release() {
             destroy_ev(v.read_done[s]);
             destroy_ev(v.xfer_done[s]);
         }
+        for (auto& kv : v.stage_done) destroy_ev(kv.second);
+        v.stage_done.clear();
         if (v.comp) cudaStreamDestroy(v.comp);
         if (v.comm) cudaStreamDestroy(v.comm);
         v.comp = v.comm = nullptr;
@@ -544,6 +546,11 @@ void Session::alloc_buffers() {
             for (int i = seg_first_[seg]; i <= seg_last_[seg]; ++i) {
                 E_->stage_on(v.idx, i);
                 if (i < L) need.insert(i);
+                if (!v.stage_done.count(i)) {
+                    cudaEvent_t e;
+                    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    v.stage_done[i] = e;
+                }
                 void* h = nullptr;
                 CK(cudaMalloc(&h, static_cast<size_t>(std::max(m.widths[i], 1)) * E_->stage_bytes()));
                 v.H[i] = h;
@@ -631,6 +638,7 @@ void Session::enqueue_segment_eval(VDev& v, int seg, int embed_t, int wslot, int
         void* y = i == m.L ? eps_out : v.Y.at(i)[wslot];
         enq_kernels_ += E_->enqueue_stage(v.idx, i, in, embed_t, v.H.at(i), y, v.bad, seq * kKeyStride + i, v.comp,
                                           true);
+        if (mode_ == kParallel) CK(cudaEventRecord(v.stage_done.at(i), v.comp));  // its copies may start
     }
 }
 
@@ -655,10 +663,13 @@ void Session::enqueue_transfers(VDev& v, int seg, int slot, int eps_step) {
     const bool eps_xfer = eps_step >= 0 && v.v != 0;
     if (xfers.empty() && !eps_xfer) return;
     setdev(v.ordinal);
-    CK(cudaStreamWaitEvent(v.comm, v.eval_done, 0));
+    // each output leaves as soon as the stage that produced it finished (a crossing skip made
+    // early in the segment travels while the segment computes on); eps after the whole eval
     std::set<int> waited;
+    std::sort(xfers.begin(), xfers.end());
     for (auto& [p, c] : xfers) {
         VDev& cv = vd_[c];
+        if (waited.insert(-1 - p).second) CK(cudaStreamWaitEvent(v.comm, v.stage_done.at(p), 0));
         if (cv.read_rec[slot] && waited.insert(c).second) CK(cudaStreamWaitEvent(v.comm, cv.read_done[slot], 0));
         const size_t bytes = static_cast<size_t>(m.widths[p]) * E_->stage_bytes();
         if (cv.ordinal == v.ordinal)
@@ -667,6 +678,7 @@ void Session::enqueue_transfers(VDev& v, int seg, int slot, int eps_step) {
             CK(cudaMemcpyPeerAsync(cv.Y.at(p)[slot], cv.ordinal, v.Y.at(p)[slot], v.ordinal, bytes, v.comm));
     }
     if (eps_xfer) {
+        CK(cudaStreamWaitEvent(v.comm, v.eval_done, 0));
         const size_t bytes = static_cast<size_t>(d_) * ab_bytes_;
         void* dst = offset(traj_eps_, static_cast<size_t>(eps_step) * bytes);
         if (vd_[0].ordinal == v.ordinal)

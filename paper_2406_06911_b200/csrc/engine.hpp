@@ -147,6 +147,7 @@ private:
         std::array<void*, 2> EPS{nullptr, nullptr};
         // sync events
         cudaEvent_t eval_done = nullptr;
+        std::map<int, cudaEvent_t> stage_done;  // per stage it evaluates: its sends may start
         std::array<cudaEvent_t, 2> read_done{}, xfer_done{};
         std::array<bool, 2> read_rec{}, xfer_rec{};
         cudaEvent_t join = nullptr;

@@ -467,10 +467,15 @@ std::vector<long long> round_exchange_bytes(const Plan& plan, const Partition& p
     std::vector<long long> out(plan.rounds.size(), 0);
     const int traj = precision == 0 ? 8 : 4;                           // kF64 : kF32 / kBF16 trajectory
     const int stage = m.kind == 1 ? (precision == 1 ? 4 : 2) : traj;  // UNet f32 : bf16 stage outputs
-    const int base = plan.w * plan.N;  // warm-up exchange points come first
-    for (int r = 0; r < plan.D; ++r)
-        for (const RankOp& op : rank_program(plan, part, m, r))
-            if (op.kind == kOpSend && op.point >= base) out[op.point - base] += op.elems * (op.stage < 0 ? traj : stage);
+    // exchange points carry their round (group op `step`; warm-up steps are negative)
+    for (int r = 0; r < plan.D; ++r) {
+        int round = -1;
+        for (const RankOp& op : rank_program(plan, part, m, r)) {
+            if (op.kind == kOpGroup) round = op.step;
+            if (op.kind == kOpSend && round >= 0 && round < static_cast<int>(out.size()))
+                out[round] += op.elems * (op.stage < 0 ? traj : stage);
+        }
+    }
     return out;
 }
 

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <set>
 
 namespace adx {
 
@@ -139,8 +140,10 @@ public:
         cudaFree(traj_eps_);
         cudaFree(xT_);
         cudaFree(bad_);
-        for (cudaEvent_t ev : {ev_eval_, ev_group_, ev_fork_, ev_join_, t0_, t1_})
-            if (ev) cudaEventDestroy(ev);
+        for (cudaEvent_t e : {ev_eval_, ev_group_, ev_fork_, ev_join_, t0_, t1_, ev_eps_})
+            if (e) cudaEventDestroy(e);
+        for (auto* pool : {&ev_stage_, &ev_deliver_, &ev_sent_, &ev_read_})
+            for (auto& kv : *pool) cudaEventDestroy(kv.second);
         if (comp_) cudaStreamDestroy(comp_);
         if (cstr_) cudaStreamDestroy(cstr_);
     }
@@ -216,8 +219,8 @@ private:
         CKR(cudaMalloc(&bad_, 2 * sizeof(int)));
         CKR(cudaStreamCreateWithFlags(&comp_, cudaStreamNonBlocking));
         CKR(cudaStreamCreateWithFlags(&cstr_, cudaStreamNonBlocking));
-        for (cudaEvent_t* ev : {&ev_eval_, &ev_group_, &ev_fork_, &ev_join_})
-            CKR(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+        for (cudaEvent_t* e : {&ev_eval_, &ev_group_, &ev_fork_, &ev_join_, &ev_eps_})
+            CKR(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         CKR(cudaEventCreate(&t0_));
         CKR(cudaEventCreate(&t1_));
     }
@@ -245,8 +248,21 @@ private:
                 in.push_back({Y_.at(l.first)[stage_seg_[l.first] == seg ? op.wslot : op.rslot], m.widths[l.first]});
             void* y = i == m.L ? eps_out : Y_.at(i)[op.wslot];
             kernels_ += E_->enqueue_stage(0, i, in, op.t, H_.at(i), y, bad_, seq * 1024 + i, comp_, true);
+            CKR(cudaEventRecord(ev(ev_stage_, i), comp_));  // its sends may start now
         }
     }
+
+    // one event per key, created on first use (capture-time dependencies: a wait binds to the
+    // most recent record of the event when it is issued)
+    cudaEvent_t ev(std::map<long long, cudaEvent_t>& pool, long long key) {
+        auto it = pool.find(key);
+        if (it != pool.end()) return it->second;
+        cudaEvent_t e;
+        CKR(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        pool[key] = e;
+        return e;
+    }
+    static long long key(int stage, int slot) { return static_cast<long long>(stage) * 4 + slot + 8; }
 
     void build_graph() {
         CKR(cudaStreamBeginCapture(comp_, cudaStreamCaptureModeRelaxed));
@@ -258,21 +274,49 @@ private:
         CKR(cudaMemsetAsync(bad_, 0x7f, 2 * sizeof(int), comp_));
         CKR(cudaEventRecord(ev_fork_, comp_));
         CKR(cudaStreamWaitEvent(cstr_, ev_fork_, 0));
-        bool have_eval = false, have_group = false;
+        // Dependencies are per exchange point (schedule.hpp): a point's sends wait for the stage
+        // that produced them, its receives for the last local eval that read the slot they
+        // overwrite; an eval waits for the points that delivered its inputs and for the earlier
+        // sends out of the slots it overwrites; the sampler waits for the eps delivery.
         int seq = 0;
         const size_t row = static_cast<size_t>(d_) * ab_bytes_;
-        for (const RankOp& op : ops_) {
+        const Model& mdl = E_->model();
+        bool have_eps = false;
+        for (size_t oi = 0; oi < ops_.size(); ++oi) {
+            const RankOp& op = ops_[oi];
             switch (op.kind) {
-                case kOpEval:
-                    if (have_group) CKR(cudaStreamWaitEvent(comp_, ev_group_, 0));
+                case kOpEval: {
+                    // inputs received from other ranks (this slot), and earlier sends out of the
+                    // slots this eval overwrites
+                    const int seg = op.seg;
+                    std::set<int> reads;
+                    if (seg > 1) reads.insert(seg_last_[seg - 1]);
+                    for (int i = seg_first_[seg]; i <= seg_last_[seg]; ++i)
+                        for (auto& l : mdl.links_into(i))
+                            if (stage_seg_[l.first] != seg) reads.insert(l.first);
+                    for (int p : reads)
+                        if (ev_deliver_.count(key(p, op.rslot))) CKR(cudaStreamWaitEvent(comp_, ev_deliver_.at(key(p, op.rslot)), 0));
+                    for (int i = seg_first_[seg]; i <= seg_last_[seg]; ++i)
+                        if (ev_sent_.count(key(i, op.wslot))) CKR(cudaStreamWaitEvent(comp_, ev_sent_.at(key(i, op.wslot)), 0));
+                    if (seg == plan_.N && ev_sent_.count(key(-1, op.wslot)))
+                        CKR(cudaStreamWaitEvent(comp_, ev_sent_.at(key(-1, op.wslot)), 0));
                     eval(op, seq++);
                     CKR(cudaEventRecord(ev_eval_, comp_));
-                    have_eval = true;
+                    CKR(cudaEventRecord(ev(ev_read_, op.rslot), comp_));  // last reader of slot rslot
                     break;
-                case kOpGroup:
-                    if (have_eval) CKR(cudaStreamWaitEvent(cstr_, ev_eval_, 0));
+                }
+                case kOpGroup: {
+                    bool sends = false, recvs = false;
+                    int rslot = 0;
+                    for (size_t k = oi + 1; k < ops_.size() && ops_[k].kind != kOpEnd; ++k) {
+                        sends |= ops_[k].kind == kOpSend;
+                        if (ops_[k].kind == kOpRecv && ops_[k].stage >= 0) recvs = true, rslot = ops_[k].slot;
+                    }
+                    if (sends) CKR(cudaStreamWaitEvent(cstr_, op.stage >= 0 ? ev(ev_stage_, op.stage) : ev_eval_, 0));
+                    if (recvs && ev_read_.count(rslot)) CKR(cudaStreamWaitEvent(cstr_, ev_read_.at(rslot), 0));
                     CKN(nccl().GroupStart(), "ncclGroupStart");
                     break;
+                }
                 case kOpSend: {
                     const void* src = op.stage < 0 ? EPS_[op.slot] : Y_.at(op.stage)[op.slot];
                     CKN(nccl().Send(src, op.elems * (op.stage < 0 ? ab_bytes_ : E_->stage_bytes()), ncclInt8,
@@ -287,13 +331,28 @@ private:
                         "ncclRecv");
                     break;
                 }
-                case kOpEnd:
+                case kOpEnd: {
                     CKN(nccl().GroupEnd(), "ncclGroupEnd");
-                    CKR(cudaEventRecord(ev_group_, cstr_));
-                    have_group = true;
+                    // what this point moved: register the delivery / send-completion events
+                    size_t g = oi;
+                    while (g > 0 && ops_[g].kind != kOpGroup) --g;
+                    for (size_t k = g + 1; k < oi; ++k) {
+                        const RankOp& x = ops_[k];
+                        if (x.kind == kOpRecv && x.stage < 0) {
+                            CKR(cudaEventRecord(ev_eps_, cstr_));
+                            have_eps = true;
+                        } else if (x.kind == kOpRecv) {
+                            cudaEvent_t e = ev(ev_deliver_, key(x.stage, x.slot));
+                            CKR(cudaEventRecord(e, cstr_));
+                        } else if (x.kind == kOpSend) {
+                            cudaEvent_t e = ev(ev_sent_, key(x.stage, x.slot));
+                            CKR(cudaEventRecord(e, cstr_));
+                        }
+                    }
                     break;
+                }
                 case kOpDdim: {
-                    if (have_group) CKR(cudaStreamWaitEvent(comp_, ev_group_, 0));
+                    if (have_eps) CKR(cudaStreamWaitEvent(comp_, ev_eps_, 0));
                     DdimArgs a = {};
                     a.x = off_c(traj_lat_, op.step * row);
                     a.eps = off_c(traj_eps_, op.step * row);
@@ -335,7 +394,8 @@ private:
     int* bad_ = nullptr;
     cudaStream_t comp_ = nullptr, cstr_ = nullptr;
     cudaEvent_t ev_eval_ = nullptr, ev_group_ = nullptr, ev_fork_ = nullptr, ev_join_ = nullptr, t0_ = nullptr,
-                t1_ = nullptr;
+                t1_ = nullptr, ev_eps_ = nullptr;
+    std::map<long long, cudaEvent_t> ev_stage_, ev_deliver_, ev_sent_, ev_read_;
     ncclComm_t comm_ = nullptr;
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t gexec_ = nullptr;

@@ -71,11 +71,14 @@ std::vector<RankOp> rank_program(const Plan& plan, const Partition& part, const 
     std::vector<RankOp> ops;
     int point = 0;
 
-    auto emit_point = [&](std::vector<RankOp>& xs) {
+    // one exchange point: group op (carrying the produced stage and the round), its transfers, end
+    auto emit_point = [&](std::vector<RankOp>& xs, int stage, int round) {
         if (!xs.empty()) {
             RankOp g;
             g.kind = kOpGroup;
             g.point = point;
+            g.stage = stage;
+            g.step = round;
             ops.push_back(g);
             for (auto& x : xs) {
                 x.point = point;
@@ -84,29 +87,31 @@ std::vector<RankOp> rank_program(const Plan& plan, const Partition& part, const 
             RankOp e;
             e.kind = kOpEnd;
             e.point = point;
+            e.stage = stage;
+            e.step = round;
             ops.push_back(e);
         }
         ++point;
     };
-    // transfers of segment `seg`'s outputs (evaluated by `owner`) into `slot`
-    auto stage_xfers = [&](int seg, int owner, int slot, std::vector<RankOp>& xs) {
+    // transfers of segment `seg`'s stage p output (evaluated by `owner`) into `slot`
+    auto stage_xfers = [&](int seg, int p, int owner, int slot, std::vector<RankOp>& xs) {
         if (seg >= N) return;
         for (int cr : all_ranks) {
             if (cr == owner) continue;
-            for (int p : c.xfer(seg, cr)) {
-                RankOp o;
-                o.stage = p;
-                o.slot = slot;
-                o.elems = m.widths[p];
-                if (owner == v) {
-                    o.kind = kOpSend;
-                    o.peer = cr;
-                    xs.push_back(o);
-                } else if (cr == v) {
-                    o.kind = kOpRecv;
-                    o.peer = owner;
-                    xs.push_back(o);
-                }
+            const std::set<int> st = c.xfer(seg, cr);
+            if (!st.count(p)) continue;
+            RankOp o;
+            o.stage = p;
+            o.slot = slot;
+            o.elems = m.widths[p];
+            if (owner == v) {
+                o.kind = kOpSend;
+                o.peer = cr;
+                xs.push_back(o);
+            } else if (cr == v) {
+                o.kind = kOpRecv;
+                o.peer = owner;
+                xs.push_back(o);
             }
         }
     };
@@ -127,6 +132,17 @@ std::vector<RankOp> rank_program(const Plan& plan, const Partition& part, const 
             xs.push_back(o);
         }
     };
+    // every stage output of `evals` (segment, owner) that another rank reads: one point per stage,
+    // in stage order (the order each producer computes them)
+    auto stage_points = [&](const std::vector<std::pair<int, int>>& evals, int slot, int round) {
+        for (int p = 1; p < m.L; ++p)
+            for (auto& [seg, owner] : evals)
+                if (p >= c.first[seg] && p <= c.last[seg]) {
+                    std::vector<RankOp> xs;
+                    stage_xfers(seg, p, owner, slot, xs);
+                    emit_point(xs, p, round);
+                }
+    };
 
     // warm-up: w sequential cascades (executor.cpp:168-202), slot 1
     for (int k = 0; k < plan.w; ++k) {
@@ -141,28 +157,34 @@ std::vector<RankOp> rank_program(const Plan& plan, const Partition& part, const 
                 e.wslot = e.rslot = 1;
                 e.step = k;
                 e.eps_step = n == N ? k : -1;
+                e.point = -1 - k;  // (eval ops: the round, -1 - k for warm-up step k)
                 ops.push_back(e);
             }
-            std::vector<RankOp> xs;
-            stage_xfers(n, owner, 1, xs);
-            if (n == N) eps_xfer(owner, 1, k, xs);
-            emit_point(xs);
+            stage_points({{n, owner}}, 1, -1 - k);
+            if (n == N) {
+                std::vector<RankOp> xs;
+                eps_xfer(owner, 1, k, xs);
+                emit_point(xs, -1, -1 - k);
+            }
         }
         if (v == 0) {
             RankOp dd;
             dd.kind = kOpDdim;
             dd.step = k;
             dd.t = t;
+            dd.point = -1 - k;
             ops.push_back(dd);
         }
     }
-    // rounds (executor.cpp:289-318): evals against the round-start snapshot,
-    // then one exchange point, then the sampler on rank 0
+    // rounds (executor.cpp:289-318): evals against the round-start snapshot, then the round's
+    // exchange points (per produced stage, then eps), then the sampler on rank 0
     for (auto& rd : plan.rounds) {
         const int r = rd.index;
         const int wslot = (r + 2) % 2, rslot = (r + 1) % 2;
         const int step0 = T - rd.sampler_steps.front();
+        std::vector<std::pair<int, int>> evs;
         for (auto& e : rd.evals) {
+            evs.emplace_back(e.segment, e.device);
             if (e.device != v) continue;
             RankOp o;
             o.kind = kOpEval;
@@ -172,20 +194,23 @@ std::vector<RankOp> rank_program(const Plan& plan, const Partition& part, const 
             o.rslot = rslot;
             o.step = step0;
             o.eps_step = e.emits_eps_for ? T - *e.emits_eps_for : -1;
+            o.point = r;  // (eval ops: the round index)
             ops.push_back(o);
         }
-        std::vector<RankOp> xs;
-        for (auto& e : rd.evals) {
-            if (rd.broadcast) stage_xfers(e.segment, e.device, wslot, xs);  // last round: nobody reads
-            if (e.emits_eps_for) eps_xfer(e.device, wslot, T - *e.emits_eps_for, xs);
-        }
-        emit_point(xs);
+        if (rd.broadcast) stage_points(evs, wslot, r);  // last round: nobody reads its bundles
+        for (auto& e : rd.evals)
+            if (e.emits_eps_for) {
+                std::vector<RankOp> xs;
+                eps_xfer(e.device, wslot, T - *e.emits_eps_for, xs);
+                emit_point(xs, -1, r);
+            }
         if (v == 0)
             for (int t : rd.sampler_steps) {
                 RankOp dd;
                 dd.kind = kOpDdim;
                 dd.step = T - t;
                 dd.t = t;
+                dd.point = r;
                 ops.push_back(dd);
             }
     }

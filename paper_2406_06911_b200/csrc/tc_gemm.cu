@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                 }
             }
             float* sb = sepi + acc * 2 * BN;
-            const bool stage_cols = S == 1 && p.act != 2 && !p.chan_add_rows;
+            const bool stage_cols = p.act != 2 && !p.chan_add_rows;  // (S > 1: one tile, acc 0)
             if (stage_cols) {
                 const float* car = p.chan_add ? p.chan_add + static_cast<long long>(p.chan_add_shared ? 0 : img) * p.N
                                               : nullptr;
@@ -710,11 +710,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             __syncwarp();
             if (lane == 0) bar_arrive1(&tempty[acc]);
         }
-#ifndef ADX_TL_CHUNK
+#if !defined(ADX_TL_CHUNK) && !defined(ADX_TL_SPLIT)
         if (threadIdx.x == 64) TL(5);
 #endif
         if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-#ifndef ADX_TL_CHUNK
+#if !defined(ADX_TL_CHUNK) && !defined(ADX_TL_SPLIT)
         if (threadIdx.x == 64) TL(6);
 #endif
     }
@@ -722,7 +722,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
         // split-K reduction: CTA `split` owns tile rows [r0, r1) and sums the S staged
         // partials in split order 0..S-1 over DSMEM (fixed order: deterministic)
         __syncwarp();
+#ifdef ADX_TL_SPLIT
+        if (threadIdx.x == 64) TL(5);
+#endif
         cluster_sync_all();
+#ifdef ADX_TL_SPLIT
+        if (threadIdx.x == 64) TL(6);
+#endif
         if (warp >= 2) {
             int tile_m, tile_n, img, h0, w0;
             coords(u0, tile_m, tile_n, img, h0, w0);
@@ -731,16 +737,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             const uint32_t base = sa(smem);
             const int et = threadIdx.x - 64;  // 0 .. 32 EPW - 1
             const int cols = p.act == 2 ? BN / 2 : BN, chunks = cols / 16;
+            // the S ranks' staging bases (mapa is linear in the offset); bias / channel-add come
+            // from this CTA's SMEM copy, the residual is requested with the partials
+            uint32_t rb[kMaxSplitsDev];
+#pragma unroll
+            for (int r = 0; r < kMaxSplitsDev; ++r) rb[r] = mapa(base, r < S ? r : 0);
+            const bool sc = p.act != 2 && !p.chan_add_rows;
+            const float* bb = sc && p.bias ? sepi - n0 : p.bias;
             for (int it = et; it < (r1 - r0) * chunks; it += 32 * EPW) {
                 const int row = r0 + it / chunks, c = (it % chunks) * 16;
                 long long m;
                 const bool valid = row_to_m<CONV>(p, tile_m, img, h0, w0, row, m);
                 if (!valid) continue;
+                const bool rv = p.act != 2 && p.residual && !p.residual_f32 && (((p.ldo | p.ldr) & 7) == 0) &&
+                                n0 + c + 16 <= (p.n_store ? p.n_store : p.N);
+                uint4 res[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+                if (rv) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + c);
+                    res[0] = rp[0], res[1] = rp[1];
+                }
                 float v[16], g[16];
                 uint32_t a[kMaxSplitsDev];
+                const uint32_t off = static_cast<uint32_t>((row * (BN + 4) + c) * 4);
 #pragma unroll
-                for (int r = 0; r < kMaxSplitsDev; ++r)
-                    a[r] = mapa(base + static_cast<uint32_t>((row * (BN + 4) + c) * 4), r < S ? r : 0);
+                for (int r = 0; r < kMaxSplitsDev; ++r) a[r] = rb[r] + off;
 #pragma unroll
                 for (int j = 0; j < 16; j += 4) {
                     const float4 x = reduce_dsmem4(a, S, j * 4);
@@ -756,10 +776,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                 if (p.act == 2)
                     epi_geglu16(p, m, n0, c, v, g);
                 else
-                    epi16(p, m, chan_row(p, m, img), n0 + c, v);
+                    epi16(p, m, sc ? (p.chan_add ? sepi + BN - n0 : nullptr) : chan_row(p, m, img), n0 + c, v,
+                          rv ? res : nullptr, nullptr, bb);
             }
         }
         __syncwarp();
+#ifdef ADX_TL_SPLIT
+        if (threadIdx.x == 64) TL(7);
+#endif
         cluster_sync_all();  // keep every CTA's SMEM alive until all slices are reduced
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -768,7 +792,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * ACC_COLS)
                      : "memory");
-#ifndef ADX_TL_CHUNK
+#if !defined(ADX_TL_CHUNK) && !defined(ADX_TL_SPLIT)
     if (threadIdx.x == 0) TL(7);
 #endif
 }
