@@ -172,6 +172,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
 template <int BN>
 constexpr uint32_t idesc_bf16() {
     return (1u << 4)                               // D = f32
@@ -657,50 +665,58 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                                                                     : chan_row(p, m, img);
                     const float* bb = stage_cols ? (p.bias ? sb - n0 : nullptr) : p.bias;
                     if (tres && cb < ce) bar_wait(&rbar[warp - 2], lu & 1);
-                    for (int c = cb; c < ce; c += 16) {
-                        const uint4* stg_res = tres ? reinterpret_cast<const uint4*>(stage + ((c - cb) >> 4) * 1024 +
-                                                                                      lane * 32)
-                                                    : nullptr;
-                        const uint4 rcur[2] = {rnext[0], rnext[1]};
-                        const bool have = tres ? pe.residual != nullptr : pre && n0 + c + 16 <= nlim;
-                        if (pre && c + 16 < ce && n0 + c + 32 <= nlim) {
-                            const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + c + 16);
-                            rnext[0] = rp[0], rnext[1] = rp[1];
+                    if (p.tma_store) {
+                        // staged epilogue: TMEM chunks in pairs (two loads, one wait), the math written
+                        // over the (TMA-loaded) residual in the staging blocks, then ONE proxy fence and
+                        // warp sync, and lane 0 issues every bulk store of the share in one group
+                        for (int c = cb; c < ce; c += 32) {
+                            const bool two = c + 16 < ce;
+                            uint32_t r0[16], r1[16];
+                            tmem_ld16_nowait(trow + c, r0);
+                            if (two) tmem_ld16_nowait(trow + c + 16, r1);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                if (h == 1 && !two) break;
+                                const int cc = c + 16 * h;
+                                float v[16];
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(h ? r1[i] : r0[i]);
+                                uint4* sd = reinterpret_cast<uint4*>(stage + ((cc - cb) >> 4) * 1024 + lane * 32);
+                                // the residual (used only when pe.residual): TMA-staged in sd, or from global
+                                uint4 rr[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+                                if (tres) {
+                                    rr[0] = sd[0], rr[1] = sd[1];
+                                } else if (pre) {
+                                    const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + cc);
+                                    rr[0] = rp[0], rr[1] = rp[1];
+                                }
+                                if (valid) epi16(pe, m, ca, n0 + cc, v, rr, sd, bb);
+                            }
                         }
-                        float v[16];
-#ifdef ADX_TL_CHUNK
-                        if (c == cb && lu == 0 && threadIdx.x == 64) TL(5);
-#endif
-                        tmem_ld16(trow + c, v);
-#ifdef ADX_TL_CHUNK
-                        if (c == cb && lu == 0 && threadIdx.x == 64) TL(6);
-#endif
-#if defined(ADX_EPI_DBG) && ADX_EPI_DBG == 2  // diagnostics: TMEM drain only
-                        if (v[0] == 12345.f && valid) p.out_bf16[m * p.ldo] = __float2bfloat16(v[1]);
-                        continue;
-#endif
-                        if (p.tma_store) {
-                            // rows past M are clipped by the TMA; their staging content is unused
-                            uint4* sd = reinterpret_cast<uint4*>(stage + ((c - cb) >> 4) * 1024 + lane * 32);
-                            uint4 rr[2] = {rcur[0], rcur[1]};
-                            if (tres) rr[0] = stg_res[0], rr[1] = stg_res[1];  // (registers: no local copy)
-                            if (valid) epi16(pe, m, ca, n0 + c, v, have ? rr : nullptr, sd, bb);
-#ifdef ADX_TL_CHUNK
-                            if (c == cb && lu == 0 && threadIdx.x == 64) TL(7);
-#endif
-                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                            __syncwarp();
-                            if (lane == 0) {
-                                if constexpr (CONV) {  // tile rows 32q.. = 32 pixels of the box (32 | bw or bw | 32)
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0 && cb < ce) {
+                            for (int c = cb; c < ce; c += 16) {
+                                if constexpr (CONV)  // tile rows 32q.. = 32 pixels of the box (32 | bw or bw | 32)
                                     tma_store4d(&tmC, stage + ((c - cb) >> 4) * 1024, n0 + c, w0 + (q * 32) % p.box_w,
                                                 h0 + (q * 32) / p.box_w, img);
-                                } else {
+                                else
                                     tma_store2d(&tmC, stage + ((c - cb) >> 4) * 1024, n0 + c, tile_m * BM + q * 32);
-                                }
-                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                             }
-                        } else if (valid) {
-                            epi16(pe, m, ca, n0 + c, v, have ? rcur : nullptr, nullptr, bb);
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                    } else {
+                        for (int c = cb; c < ce; c += 16) {
+                            const uint4 rcur[2] = {rnext[0], rnext[1]};
+                            const bool have = pre && n0 + c + 16 <= nlim;
+                            if (pre && c + 16 < ce && n0 + c + 32 <= nlim) {
+                                const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + c + 16);
+                                rnext[0] = rp[0], rnext[1] = rp[1];
+                            }
+                            float v[16];
+                            tmem_ld16(trow + c, v);
+                            if (valid) epi16(pe, m, ca, n0 + c, v, have ? rcur : nullptr, nullptr, bb);
                         }
                     }
                 }
