@@ -348,6 +348,13 @@ int adx_tc_gemm_bf16(int ordinal, int M, int N, int K, const uint16_t* A, const 
 int adx_tc_conv3x3_bf16(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X,
                         const uint16_t* Wt, const float* bias, const uint16_t* residual, uint16_t* out, int bn,
                         int splits, int iters, double* ms_per_iter);
+/* GroupNorm(+SiLU) of bf16 NHWC images over a channel concat [x0 (c0) | x1 (c1)] (x1 NULL when
+ * c1 == 0): the UNet pass's norm kernels (cooperative one-launch path for one image, stats +
+ * apply for batches); iters > 0 also times it (graph of `iters` launches) */
+int adx_group_norm_bf16(int ordinal, int batch, int HW, int c0, int c1, int groups, const uint16_t* x0,
+                        const uint16_t* x1, const float* gamma, const float* beta, float eps, int act,
+                        uint16_t* out, int iters, double* ms_per_iter);
+int adx_gn_timeline(unsigned long long* out, int n);
 /* per-CTA %globaltimer stamps (8 per CTA) of the last tc_gemm / conv launch: diagnostics of
  * -DADX_TC_TIMELINE builds (tools/tools_tc_timeline.py); zeros in the product build */
 int adx_tc_timeline(unsigned long long* out, int n_ctas);

@@ -102,7 +102,7 @@ EXPORTS = [
     "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes", "adx_tc_gemm", "adx_tc_conv3x3",
     "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context", "adx_tc_attention", "adx_temporal_attention",
     "adx_engine_profile_pass", "adx_tc_plan_override", "adx_engine_stage_times", "adx_partition_by_cost",
-    "adx_tc_timeline", "adx_tc_gemm_bf16", "adx_tc_conv3x3_bf16",
+    "adx_tc_timeline", "adx_tc_gemm_bf16", "adx_tc_conv3x3_bf16", "adx_group_norm_bf16", "adx_gn_timeline",
 ]
 
 
@@ -222,6 +222,9 @@ def lib():
                                P(d)]),
         "adx_tc_plan_override": (i, [i, i]),
         "adx_tc_timeline": (i, [P(C.c_ulonglong), i]),
+        "adx_gn_timeline": (i, [P(C.c_ulonglong), i]),
+        "adx_group_norm_bf16": (i, [i, i, i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_float),
+                                    C.c_float, i, P(C.c_uint16), i, P(d)]),
         "adx_tc_gemm_bf16": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_uint16), i,
                                  P(C.c_uint16), i, i, i, i, P(d)]),
         "adx_tc_conv3x3_bf16": (i, [i, i, i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_uint16),

@@ -1094,6 +1094,42 @@ int adx_tc_conv3x3_bf16(int ordinal, int batch, int H, int W, int Cin, int Cout,
     });
 }
 
+// GroupNorm(+SiLU) over a (one- or two-segment) channel concat of bf16 NHWC images:
+// x0 [batch][HW][c0], x1 [batch][HW][c1] (NULL when c1 == 0) -> out [batch][HW][c0 + c1]
+int adx_group_norm_bf16(int ordinal, int batch, int HW, int c0, int c1, int groups, const uint16_t* x0,
+                        const uint16_t* x1, const float* gamma, const float* beta, float eps, int act, uint16_t* out,
+                        int iters, double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        const int C = c0 + c1;
+        const size_t n0 = static_cast<size_t>(batch) * HW * c0, n1 = static_cast<size_t>(batch) * HW * c1,
+                     no = static_cast<size_t>(batch) * HW * C;
+        DevBuf a(n0 * 2), b(std::max<size_t>(n1, 8) * 2), o(no * 2), g(static_cast<size_t>(C) * 4),
+            be(static_cast<size_t>(C) * 4);
+        const size_t sb = adx::group_norm_scratch_bytes(batch, HW, groups, C);
+        DevBuf sc(sb);
+        CKC(cudaMemset(sc.p, 0, sb));
+        CKC(cudaMemcpy(a.p, x0, n0 * 2, cudaMemcpyHostToDevice));
+        if (c1) CKC(cudaMemcpy(b.p, x1, n1 * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(g.p, gamma, static_cast<size_t>(C) * 4, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(be.p, beta, static_cast<size_t>(C) * 4, cudaMemcpyHostToDevice));
+        adx::Cat2 xc{static_cast<const __nv_bfloat16*>(a.p), c0, c1 ? static_cast<const __nv_bfloat16*>(b.p) : nullptr,
+                     c1};
+        auto run = [&](cudaStream_t st) {
+            adx::group_norm(xc, batch, HW, groups, static_cast<const float*>(g.p), static_cast<const float*>(be.p),
+                            eps, act, static_cast<__nv_bfloat16*>(o.p), static_cast<float2*>(sc.p), st);
+        };
+        run(0);
+        CKC(cudaDeviceSynchronize());
+        if (iters > 0 && ms_per_iter) *ms_per_iter = time_graph_ms(run, iters);
+        CKC(cudaMemcpy(out, o.p, no * 2, cudaMemcpyDeviceToHost));
+    });
+}
+
+int adx_gn_timeline(unsigned long long* out, int n) {
+    return guard([&] { adx::gn_timeline(out, n); });
+}
+
 int adx_tc_timeline(unsigned long long* out, int n_ctas) {
     return guard([&] { adx::tc_timeline(out, n_ctas); });
 }

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 #include <utility>
 #include <string>
@@ -29,7 +30,9 @@ namespace {
 
 using bf16 = __nv_bfloat16;
 
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+// x * sigmoid(x) with the MUFU reciprocal: an IEEE division here was a branchy ~15-instruction
+// sequence per element (the GroupNorm apply phase's bottleneck); 1 / (1 + e^-x) -> 0 as x -> -inf
+__device__ __forceinline__ float silu(float x) { return x * __fdividef(1.0f, 1.0f + __expf(-x)); }
 __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -299,11 +302,26 @@ __global__ void gn_apply(Cat2T<T> x, int pixels, int HW, const float2* __restric
 // publishes its group partials; after a grid barrier every CTA folds all G partials
 // in the same fixed fp64 order (identical statistics everywhere, deterministic),
 // builds per-channel (a, b) and normalises its SMEM copy: one HBM read of x.
+#ifdef ADX_GN_TIMELINE  // %globaltimer stamps per CTA (diagnostics; adx_gn_timeline)
+__device__ unsigned long long g_gn_tl[256][8];
+__device__ __forceinline__ void gn_stamp(int k) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        g_gn_tl[blockIdx.x][k] = t;
+    }
+}
+#else
+__device__ __forceinline__ void gn_stamp(int) {}
+#endif
+
 template <typename T>
 __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const float* gamma, const float* beta,
                          float eps, int act, float2* scratch, T* out) {
     extern __shared__ __align__(16) uint8_t gsm[];
+    gn_stamp(0);
     pdl_wait();
+    gn_stamp(1);
     const int G = gridDim.x, cta = blockIdx.x;
     const int C = x.c0 + x.c1, nv = C / 8, cpg = C / groups;
     const int rpb = blockDim.x / nv, r = threadIdx.x / nv, v = threadIdx.x % nv;
@@ -348,6 +366,7 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
         w1[1] = make_float4(ss[4], ss[5], ss[6], ss[7]);
     }
     __syncthreads();
+    gn_stamp(2);
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
         float a = 0.f, b = 0.f;
         for (int rr = 0; rr < rpb; ++rr) {
@@ -366,6 +385,7 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
         }
         part[static_cast<long long>(cta) * groups + g] = make_float2(a, b);
     }
+    gn_stamp(3);
     // grid barrier (co-residency guaranteed by the cooperative launch): arrival count +
     // generation; the last CTA to arrive re-arms the count and bumps the generation, so
     // consecutive launches with different grid sizes reuse the same two words
@@ -389,6 +409,7 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
         }
     }
     __syncthreads();
+    gn_stamp(4);
     // statistics: nsub threads per group over a fixed strided subset of the G partials
     const int nsub = max(1, static_cast<int>(blockDim.x) / groups);
     if (threadIdx.x < nsub * groups) {
@@ -432,6 +453,7 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
         ab[c] = make_float2(static_cast<float>(rs * gamma[c]), static_cast<float>(beta[c] - st[2 * g] * rs * gamma[c]));
     }
     __syncthreads();
+    gn_stamp(5);
     // normalise the SMEM copy, 16-byte coalesced stores.  blockDim.x = rpb * nv, so the
     // vector index i % nv of a thread is the same every iteration: its 8 (a, b) pairs are
     // read from SMEM once (per-iteration reads at a 64-byte thread stride were 16-way
@@ -457,6 +479,7 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
         }
         Vec8<T>::store(o + static_cast<long long>(i) * 8, Vec8<T>::pack(f));
     }
+    gn_stamp(6);
 }
 
 // LayerNorm over C per token, one warp per token, row held in registers (C <= 2048)
@@ -1111,6 +1134,15 @@ void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma
 void group_norm(const Cat2F& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
                 int silu_act, float* out, float2* scratch, cudaStream_t st) {
     group_norm_t(x, batch, HW, groups, gamma, beta, eps, silu_act, out, scratch, st);
+}
+
+void gn_timeline(unsigned long long* out, int n) {
+#ifdef ADX_GN_TIMELINE
+    CKU(cudaDeviceSynchronize());
+    CKU(cudaMemcpyFromSymbol(out, g_gn_tl, static_cast<size_t>(std::min(n, 256)) * 64));
+#else
+    std::memset(out, 0, static_cast<size_t>(n) * 64);
+#endif
 }
 
 size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C) {

@@ -48,6 +48,8 @@ void temporal_attention(const float* qkv, int frames, int HW, int C, float* out,
 void cfg_combine(const float* e, long long n, float scale, float* out, cudaStream_t st);
 // latent (fp32 / fp64, HWC) -> fp32 NHWC with cpad channels
 void pack_latent_f32(const void* x, bool f64, long long pixels, int c_lat, int cpad, float* out, cudaStream_t st);
+// per-CTA %globaltimer stamps of the last gn_fused launch (ADX_GN_TIMELINE builds; zeros otherwise)
+void gn_timeline(unsigned long long* out, int n);
 // scratch for group_norm; must be zeroed once at allocation (holds a self-resetting ticket counter)
 size_t group_norm_scratch_bytes(int batch, int HW, int groups, int C);
 void layer_norm(const __nv_bfloat16* x, int tokens, int C, const float* gamma, const float* beta, float eps,

@@ -214,3 +214,33 @@ def test_tc_conv3x3_bf16_epilogue_bit_exact(b, H, W, Ci, Co):
     _lib.check(adx.lib().adx_tc_conv3x3(0, b, H, W, Ci, Co, X.ctypes.data_as(P16), Wt.ctypes.data_as(P16),
                                         bias.ctypes.data_as(PF), f32.ctypes.data_as(PF), 0, None))
     assert np.array_equal(out, rne_bf16(f32 + bits_f32(res)))
+
+
+@pytest.mark.parametrize("batch,HW,c0,c1,groups,act", [(1, 9216, 320, 0, 32, 1),   # c2 level 0 (cooperative)
+                                                       (1, 2304, 640, 640, 32, 1),  # decoder concat input
+                                                       (1, 144, 1280, 1280, 32, 0),
+                                                       (2, 576, 640, 0, 32, 1),     # CFG batch (stats + apply)
+                                                       (16, 256, 320, 320, 32, 1)])  # video frames
+def test_group_norm_matches_fp32_reference(batch, HW, c0, c1, groups, act):
+    """GroupNorm(+SiLU) over a channel concat vs torch fp32 on the same bf16 inputs (one bf16
+    rounding of the output)"""
+    rng = np.random.default_rng(HW + c0 + c1)
+    x0 = bf16_bits((2.0 * rng.standard_normal((batch, HW, c0)) + 0.5).astype(np.float32))
+    x1 = bf16_bits(rng.standard_normal((batch, HW, max(c1, 1))).astype(np.float32)) if c1 else None
+    C = c0 + c1
+    gamma = (1 + 0.1 * rng.standard_normal(C)).astype(np.float32)
+    beta = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    out = np.zeros((batch, HW, C), np.uint16)
+    _lib.check(adx.lib().adx_group_norm_bf16(0, batch, HW, c0, c1, groups, x0.ctypes.data_as(P16),
+                                             x1.ctypes.data_as(P16) if c1 else None, gamma.ctypes.data_as(PF),
+                                             beta.ctypes.data_as(PF), 1e-5, act, out.ctypes.data_as(P16), 0, None))
+    x = torch.from_numpy(bits_f32(x0))
+    if c1:
+        x = torch.cat([x, torch.from_numpy(bits_f32(x1))], dim=2)
+    ref = torch.nn.functional.group_norm(x.permute(0, 2, 1), groups, torch.from_numpy(gamma), torch.from_numpy(beta),
+                                         1e-5).permute(0, 2, 1)
+    if act:
+        ref = torch.nn.functional.silu(ref)
+    got = bits_f32(out)
+    err = np.abs(got - ref.numpy()).max() / np.abs(ref.numpy()).max()
+    assert err < 1e-2, err
