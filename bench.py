@@ -203,12 +203,17 @@ def config_block(args, cfg, N):
 
 def measured_traffic(cfg, prec, kernel, launches):
     """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel's launches over one
-    pass, from the committed ncu capture profiles/r01_<config>_dram_traffic.json
+    pass, from the newest committed ncu capture profiles/r0N_<config>_dram_traffic.json
     (tools/tools_ncu_traffic.py; same per-pass basis as `achieved`).  None when this config /
     precision has no capture."""
     name = next((k for k, v in CONFIGS.items() if v is cfg), None)
-    path = os.path.join(ROOT, "profiles", f"r01_{name}_dram_traffic.json")
-    if prec != "bf16" or not os.path.exists(path):
+    path = None
+    for rnd in ("r02", "r01"):  # the newest capture of this config
+        cand = os.path.join(ROOT, "profiles", f"{rnd}_{name}_dram_traffic.json")
+        if os.path.exists(cand):
+            path = cand
+            break
+    if prec != "bf16" or path is None:
         return None, None
     fam = json.load(open(path))["families"].get(kernel)
     if not fam:
