@@ -1039,6 +1039,158 @@ void check_vec8(const Cat2T<T>& x, const char* who) {
         throw std::invalid_argument(std::string(who) + ": channel segments must be multiples of 8");
 }
 
+
+// GroupNorm(+SiLU) with one thread-block CLUSTER per (image, group): CTA r of the CS-CTA cluster
+// owns pixels [r*chunk, (r+1)*chunk) of the group's channels (cpg of the concat, read as pairs
+// from whichever segment holds them), keeps them in SMEM while summing (fp32 per thread, fixed
+// xor-butterfly per warp, fp64 across warps), the CTAs exchange their (sum, sumsq) over DSMEM
+// after one cluster barrier and every CTA folds them in rank order (identical statistics in the
+// cluster, deterministic), then applies from SMEM.  No grid-wide barrier and no partials in
+// global memory: the cooperative kernel spent ~4 of its ~9 us (level 0) in the grid barrier and
+// the fold of 147 CTA partials.
+template <typename T>
+struct Pair2;
+template <>
+struct Pair2<bf16> {
+    using raw = uint32_t;
+    __device__ static raw load(const bf16* p) { return __ldg(reinterpret_cast<const unsigned int*>(p)); }
+    __device__ static float2 unpack(raw u) {
+        return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+    }
+    __device__ static void store(bf16* p, float2 f) {
+        *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(f.x, f.y);
+    }
+};
+template <>
+struct Pair2<float> {
+    using raw = float2;
+    __device__ static raw load(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+    __device__ static float2 unpack(raw u) { return u; }
+    __device__ static void store(float* p, float2 f) { *reinterpret_cast<float2*>(p) = f; }
+};
+
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gn_cluster(Cat2T<T> x, int HW, int groups, int chunk, const float* gamma,
+                                                  const float* beta, float eps, int act, T* out) {
+    extern __shared__ __align__(16) uint8_t gsm[];
+    using P2 = Pair2<T>;
+    using Raw = typename P2::raw;
+    pdl_wait();
+    const int CS = gridDim.x, r = blockIdx.x, g = blockIdx.y, n = blockIdx.z;
+    const int C = x.c0 + x.c1, cpg = C / groups, np2 = cpg / 2;
+    const int p0 = r * chunk, p1 = min(HW, p0 + chunk), npx = max(0, p1 - p0);
+    Raw* tile = reinterpret_cast<Raw*>(gsm);  // [npx][np2]
+    double* red = reinterpret_cast<double*>(gsm + ((static_cast<size_t>(chunk) * np2 * sizeof(Raw) + 15) & ~size_t(15)));
+    float2* ab = reinterpret_cast<float2*>(red + 24);  // [cpg] (scale, shift)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long base = static_cast<long long>(n) * HW + p0;
+    float s = 0.f, ss = 0.f;
+    const int total = npx * np2;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int pl = e / np2, j = e - pl * np2;
+        const int c = g * cpg + 2 * j;
+        const long long pix = base + pl;
+        const Raw v = c < x.c0 ? P2::load(x.p0 + pix * x.c0 + c) : P2::load(x.p1 + pix * x.c1 + (c - x.c0));
+        tile[e] = v;
+        const float2 f = P2::unpack(v);
+        s += f.x + f.y;
+        ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+    }
+    s = warp_sum(s);
+    ss = warp_sum(ss);
+    if (lane == 0) red[2 * warp] = s, red[2 * warp + 1] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) a += red[2 * w], b += red[2 * w + 1];
+        red[16] = a;
+        red[17] = b;
+    }
+    cluster_barrier();  // every CTA's (sum, sumsq) is published in its SMEM
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        const uint32_t mine = static_cast<uint32_t>(__cvta_generic_to_shared(red + 16));
+        for (int q = 0; q < CS; ++q) {
+            uint32_t addr;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(addr) : "r"(mine), "r"(q));
+            double da, db;
+            asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(da) : "r"(addr));
+            asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(db) : "r"(addr + 8));
+            a += da;
+            b += db;
+        }
+        const double cnt = static_cast<double>(HW) * cpg;
+        const double mu = a / cnt;
+        red[18] = mu;
+        red[19] = 1.0 / sqrt(fmax(b / cnt - mu * mu, 0.0) + static_cast<double>(eps));
+    }
+    __syncthreads();
+    if (threadIdx.x < cpg) {
+        const int c = g * cpg + threadIdx.x;
+        const double rs = red[19];
+        ab[threadIdx.x] = make_float2(static_cast<float>(rs * gamma[c]), static_cast<float>(beta[c] - red[18] * rs * gamma[c]));
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int pl = e / np2, j = e - pl * np2;
+        const float2 q0 = ab[2 * j], q1 = ab[2 * j + 1];
+        float2 f = P2::unpack(tile[e]);
+        f.x = fmaf(f.x, q0.x, q0.y);
+        f.y = fmaf(f.y, q1.x, q1.y);
+        if (act) f.x = silu(f.x), f.y = silu(f.y);
+        P2::store(out + (base + pl) * C + g * cpg + 2 * j, f);
+    }
+    cluster_barrier();  // peers may still read this CTA's partial
+}
+
+// cluster GroupNorm (gn_cluster): CS CTAs per (image, group), CS = 4 (8 when a CTA's share of
+// the group would not fit in 200 KB of SMEM); returns false (nothing launched) when it cannot run.
+// ADX_GN_CLUSTER=0 disables it, =2 uses it for every size.
+template <typename T>
+bool group_norm_cluster(const Cat2T<T>& x, int batch, int HW, int groups, const float* gamma, const float* beta,
+                        float eps, int act, T* out, cudaStream_t st) {
+    static const int mode = [] {
+        const char* e = getenv("ADX_GN_CLUSTER");
+        return e ? atoi(e) : 1;
+    }();
+    if (!mode || batch > 65535) return false;
+    // measured (tools/tools_gn_bench.py): a cluster per group wins on the small low-resolution maps
+    // (576 px: 7.8 vs 9.1 us, 144 px x 2560 ch: 5.6 vs 11.8) and loses on the big ones, where 128
+    // CTAs reading 20-40-byte channel runs cannot match 147 CTAs streaming whole pixels
+    // (9216 px x 320 ch: 20.8 vs 9.9 us) -- so it takes the maps of <= 1024 pixels
+    if (mode == 1 && (HW > 1024 || batch > 1)) return false;  // (batches: the stats + apply path measured faster)
+    const int C = x.c0 + x.c1, cpg = C / groups;
+    if (cpg % 2 || (x.c0 % 2) || cpg > 256) return false;
+    const size_t pair = sizeof(T) * 2;
+    int CS = 0;
+    size_t smem = 0;
+    for (int cs : {4, 8}) {
+        const int chunk = (HW + cs - 1) / cs;
+        const size_t sm = ((static_cast<size_t>(chunk) * (cpg / 2) * pair + 15) & ~size_t(15)) + 24 * 8 + cpg * 8 + 64;
+        if (sm <= 200 * 1024) {
+            CS = cs;
+            smem = sm;
+            break;
+        }
+    }
+    if (!CS) return false;
+    const int chunk = (HW + CS - 1) / CS;
+    int dev = 0;
+    CKU(cudaGetDevice(&dev));
+    static bool attr[64] = {};
+    if (!attr[dev]) {
+        CKU(cudaFuncSetAttribute(gn_cluster<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr[dev] = true;
+    }
+    CKU(launch_pdl(gn_cluster<T>, dim3(CS, groups, batch), dim3(256), smem, st, static_cast<unsigned>(CS), x, HW,
+                   groups, chunk, gamma, beta, eps, act, out));
+    return true;
+}
+
 // one-launch cooperative GroupNorm when the chunk of every SM fits in SMEM (see gn_fused);
 // returns false (nothing launched) otherwise.  ADX_GN_FUSED=0 disables it.
 template <typename T>
@@ -1100,6 +1252,12 @@ void group_norm_t(const Cat2T<T>& x, int batch, int HW, int groups, const float*
     check_vec8(x, "group_norm");
     const int nv = C / 8;
     if (nv > 1024) throw std::invalid_argument("group_norm: more than 8192 channels");
+    if (group_norm_cluster(x, batch, HW, groups, gamma, beta, eps, silu_act, out, st)) {
+        tc_profile_measure(st, 3, 2.0 * batch * HW * (x.c0 + x.c1) * sizeof(T), [&](cudaStream_t s2) {
+            group_norm_cluster(x, batch, HW, groups, gamma, beta, eps, silu_act, out, s2);
+        });
+        return;
+    }
     if (batch == 1 && group_norm_fused(x, HW, groups, gamma, beta, eps, silu_act, out, scratch, st)) {
         tc_profile_measure(st, 3, 2.0 * HW * (x.c0 + x.c1) * sizeof(T), [&](cudaStream_t s2) {
             group_norm_fused(x, HW, groups, gamma, beta, eps, silu_act, out, scratch, s2);
