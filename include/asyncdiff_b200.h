@@ -328,6 +328,11 @@ int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint1
  * K [Lk x C] and V [Lk x ldv] (row-major, ldv >= C, multiple of 8) */
 int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K,
                      const uint16_t* V, int ldv, uint16_t* out, int iters, double* ms_per_iter);
+/* the ADX_F32 mode's fused attention: fp32 Q [batch][L][C], K and V [batch][Lk][C] split on
+ * the device into bf16 hi / lo planes, S and O as three split products each on the tensor
+ * cores (fp32 accumulation), fp32 softmax; out [batch][L][C] fp32 */
+int adx_tc_attention_f32(int ordinal, int batch, int L, int Lk, int C, const float* Q, const float* K,
+                         const float* V, float* out, int iters, double* ms_per_iter);
 /* video motion-module temporal attention: for every (pixel, 64-wide head) the frames
  * attend to each other; qkv frame-major [frames][HW][3C] bf16 (q | k | v), out
  * [frames][HW][C] bf16; 2 <= frames <= 32 */

@@ -1161,6 +1161,36 @@ int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const
     });
 }
 
+int adx_tc_attention_f32(int ordinal, int batch, int L, int Lk, int C, const float* Q, const float* K,
+                         const float* V, float* out, int iters, double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        const size_t nq = static_cast<size_t>(batch) * L * C, nk = static_cast<size_t>(batch) * Lk * C;
+        if ((nq | nk) % 8) throw std::invalid_argument("tc_attention_f32: element counts must be multiples of 8");
+        DevBuf q(nq * 4), k(nk * 4), v(nk * 4), o(nq * 4), qs(nq * 4), ks(nk * 4), vs(nk * 4);
+        CKC(cudaMemcpy(q.p, Q, nq * 4, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(k.p, K, nk * 4, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(v.p, V, nk * 4, cudaMemcpyHostToDevice));
+        const size_t wsb = adx::tc_attention_ws_bytes(L, Lk, C, batch);
+        DevBuf ws(std::max<size_t>(wsb, 256));
+        CKC(cudaMemset(ws.p, 0, std::max<size_t>(wsb, 256)));
+        auto* qh = static_cast<__nv_bfloat16*>(qs.p);
+        auto* kh = static_cast<__nv_bfloat16*>(ks.p);
+        auto* vh = static_cast<__nv_bfloat16*>(vs.p);
+        auto run = [&](cudaStream_t st) {  // the ADX_F32 transformer's sequence: split, then the fused kernel
+            adx::split2(static_cast<const float*>(q.p), static_cast<long long>(nq), qh, qh + nq, st);
+            adx::split2(static_cast<const float*>(k.p), static_cast<long long>(nk), kh, kh + nk, st);
+            adx::split2(static_cast<const float*>(v.p), static_cast<long long>(nk), vh, vh + nk, st);
+            adx::tc_attention_x(qh, qh + nq, C, kh, kh + nk, C, vh, vh + nk, C, L, Lk, C,
+                                static_cast<float*>(o.p), C, st, ws.p, wsb, batch);
+        };
+        run(0);
+        CKC(cudaDeviceSynchronize());
+        if (iters > 0 && ms_per_iter) *ms_per_iter = time_graph_ms(run, iters);
+        if (out) CKC(cudaMemcpy(out, o.p, nq * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
 int adx_temporal_attention(int ordinal, int frames, int HW, int C, const uint16_t* qkv, uint16_t* out, int iters,
                            double* ms_per_iter) {
     return guard([&] {

@@ -46,6 +46,9 @@ namespace {
 #define ADX_ATTN_STG 3
 #endif
 constexpr int QT = 128, KT = 64, HD = 64, STG = ADX_ATTN_STG;
+// the split-operand kernel carries hi and lo planes of Q, K and V (2x the SMEM per stage):
+// a 2-deep KV ring keeps it at two CTAs per SM
+constexpr int XSTG = 2;
 constexpr int HK = KT / 2;                            // keys per softmax warp (two warps per row)
 // V tiles are [KT keys][64 dims] straight from the V rows (SW128, dims contiguous) and feed
 // the PV MMA as an MN-major B operand (idesc bit 16; a K=16 step = 16 key rows = 2048 B,
@@ -227,6 +230,7 @@ struct AttnArgs {
     // last CTA of the item (ticket in `counters`) combines them in split order
     int nsplit = 1;
     float* part = nullptr;         // [item][split] records of kRecFloats
+    float* out_f32 = nullptr;      // split-operand (fp32-exact) kernel: fp32 output instead of `out`
     unsigned* counters = nullptr;  // [item], zero at allocation, re-armed by the combiner
 };
 constexpr int kRecFloats = QT * HD + 2 * QT;  // O [128][64] fp32, then m[128], l[128]
@@ -513,21 +517,27 @@ __global__ void __launch_bounds__(320, TM_COLS == 256 ? 2 : 1) attn_kernel(const
 // the half's own S_j columns (TMEM budget: S[2] 128 + O[2] 128 = 256 columns).  S_{j+2}
 // reuses that buffer: the MMA warp issues it after PV_j (tcgen05.mma from one thread
 // execute in issue order), and after the softmax has read S_j (p_full_j precedes PV_j).
+template <bool X>
 __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__ CUtensorMap tmQ,
                                                          const __grid_constant__ CUtensorMap tmK,
-                                                         const __grid_constant__ CUtensorMap tmV, const AttnArgs p) {
+                                                         const __grid_constant__ CUtensorMap tmV,
+                                                         const __grid_constant__ CUtensorMap tmQl,
+                                                         const __grid_constant__ CUtensorMap tmKl,
+                                                         const __grid_constant__ CUtensorMap tmVl, const AttnArgs p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
     constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2;
-    constexpr int XCH_OFF = Q_B + STG * (K_B + V_B) + 256;
-    uint8_t* sQ = smem;
-    uint8_t* sK = sQ + Q_B;
-    uint8_t* sV = sK + STG * K_B;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + STG * V_B);
+    constexpr int XS = X ? 2 : 1;            // operand planes: hi (+ lo)
+    constexpr int NS = X ? XSTG : STG;       // KV ring depth
+    constexpr int XCH_OFF = XS * Q_B + NS * XS * (K_B + V_B) + 256;
+    uint8_t* sQ = smem;                      // [hi | lo]
+    uint8_t* sK = sQ + XS * Q_B;             // stage s: [hi | lo] at s * XS * K_B
+    uint8_t* sV = sK + NS * XS * K_B;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NS * XS * V_B);
     uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;        // [STG]
-    uint64_t* kv_empty = kv_full + STG;  // [STG]
-    uint64_t* s_full = kv_empty + STG;   // [2]
+    uint64_t* kv_full = bars + 1;       // [NS]
+    uint64_t* kv_empty = kv_full + NS;  // [NS]
+    uint64_t* s_full = kv_empty + NS;   // [2]
     uint64_t* p_full = s_full + 2;       // [2 buffers][2 halves]
     uint64_t* pv_done = p_full + 4;      // [2 buffers][2 halves]
     uint32_t* tptr = reinterpret_cast<uint32_t*>(pv_done + 4);
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__
 
     if (warp == 0 && lane == 0) {
         bar_init(q_full, 1);
-        for (int s = 0; s < STG; ++s) {
+        for (int s = 0; s < NS; ++s) {
             bar_init(&kv_full[s], 1);
             bar_init(&kv_empty[s], 1);
         }
@@ -564,38 +574,56 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__
     const uint32_t tmem = *tptr;
 
     if (warp == 0 && lane == 0) {
-        bar_expect(q_full, Q_B);
+        bar_expect(q_full, XS * Q_B);
         tma2d(sQ, &tmQ, head * HD, img * p.L + qt * QT, q_full);
+        if constexpr (X) tma2d(sQ + Q_B, &tmQl, head * HD, img * p.L + qt * QT, q_full);
         for (int j = 0; j < nkv; ++j) {
-            const int s = j % STG;
-            bar_wait(&kv_empty[s], ((j / STG) & 1) ^ 1);
-            bar_expect(&kv_full[s], K_B + V_B);
-            tma2d(sK + s * K_B, &tmK, head * HD, img * p.Lk + (j0 + j) * KT, &kv_full[s]);
-            tma2d(sV + s * V_B, &tmV, head * HD, img * p.Lk + (j0 + j) * KT, &kv_full[s]);
+            const int s = j % NS, row = img * p.Lk + (j0 + j) * KT;
+            bar_wait(&kv_empty[s], ((j / NS) & 1) ^ 1);
+            bar_expect(&kv_full[s], XS * (K_B + V_B));
+            tma2d(sK + s * XS * K_B, &tmK, head * HD, row, &kv_full[s]);
+            tma2d(sV + s * XS * V_B, &tmV, head * HD, row, &kv_full[s]);
+            if constexpr (X) {
+                tma2d(sK + s * XS * K_B + K_B, &tmKl, head * HD, row, &kv_full[s]);
+                tma2d(sV + s * XS * V_B + V_B, &tmVl, head * HD, row, &kv_full[s]);
+            }
         }
     } else if (warp == 1 && lane == 0) {
         auto issue_s = [&](int j) {
-            const int s = j % STG, b = j & 1;
-            bar_wait(&kv_full[s], (j / STG) & 1);
+            const int s = j % NS, b = j & 1;
+            bar_wait(&kv_full[s], (j / NS) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint8_t* kh = sK + s * XS * K_B;
 #pragma unroll
-            for (int k = 0; k < HD / 16; ++k)
-                mma(tmem + b * KT, sdesc(sQ + k * 32), sdesc(sK + s * K_B + k * 32), idesc(QT, KT), k > 0);
+            for (int k = 0; k < HD / 16; ++k) {
+                mma(tmem + b * KT, sdesc(sQ + k * 32), sdesc(kh + k * 32), idesc(QT, KT), k > 0);
+                if constexpr (X) {  // S = Qh Kh^T + Qh Kl^T + Ql Kh^T (fp32 in TMEM)
+                    mma(tmem + b * KT, sdesc(sQ + k * 32), sdesc(kh + K_B + k * 32), idesc(QT, KT), 1u);
+                    mma(tmem + b * KT, sdesc(sQ + Q_B + k * 32), sdesc(kh + k * 32), idesc(QT, KT), 1u);
+                }
+            }
             commit(&s_full[b]);
         };
         bar_wait(q_full, 0);
         issue_s(0);
         for (int j = 1; j <= nkv; ++j) {
             if (j < nkv) issue_s(j);  // after PV_{j-2} in issue order: S_j may overwrite P_{j-2}
-            const int jj = j - 1, s = jj % STG, b = jj & 1;
+            const int jj = j - 1, s = jj % NS, b = jj & 1;
+            const uint8_t* vh = sV + s * XS * V_B;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 bar_wait(&p_full[b * 2 + h], (jj >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-                for (int k = 2 * h; k < 2 * h + 2; ++k)  // keys [16k, 16k + 16) of the block
-                    mma_ts(tmem + 2 * KT + h * HD, tmem + b * KT + h * HK + (k & 1) * 8,
-                           sdesc(sV + s * V_B + k * 2048), idesc(QT, HD) | (1u << 16), (jj > 0 || (k & 1)) ? 1u : 0u);
+                for (int k = 2 * h; k < 2 * h + 2; ++k) {  // keys [16k, 16k + 16) of the block
+                    const uint32_t ph = tmem + b * KT + h * HK + (k & 1) * 8, od = tmem + 2 * KT + h * HD;
+                    constexpr uint32_t id = idesc(QT, HD) | (1u << 16);
+                    mma_ts(od, ph, sdesc(vh + k * 2048), id, (jj > 0 || (k & 1)) ? 1u : 0u);
+                    if constexpr (X) {  // O += Ph Vl + Pl Vh (P lo 16 columns after P hi)
+                        mma_ts(od, ph, sdesc(vh + V_B + k * 2048), id, 1u);
+                        mma_ts(od, ph + HK / 2, sdesc(vh + k * 2048), id, 1u);
+                    }
+                }
                 commit(&pv_done[b * 2 + h]);
             }
             commit(&kv_empty[s]);
@@ -651,7 +679,7 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__
             }
             const float off = m == -INFINITY ? 0.f : -m * sl2;  // (a fully masked half: P = 0)
             float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            uint32_t pk[HK / 2];
+            uint32_t pk[HK / 2], pl[X ? HK / 2 : 1];
 #pragma unroll
             for (int c = 0; c < HK; c += 2) {
                 const float v0 = ex2_mix(fmaf(__uint_as_float(sr[c]), sl2, off), c);
@@ -660,8 +688,13 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__
                 sp[(c + 1) & 7] += v1;
                 __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
                 pk[c / 2] = *reinterpret_cast<uint32_t*>(&h2);
+                if constexpr (X) {  // P = hi + lo to ~2^-17
+                    __nv_bfloat162 l2 = __floats2bfloat162_rn(v0 - __low2float(h2), v1 - __high2float(h2));
+                    pl[c / 2] = *reinterpret_cast<uint32_t*>(&l2);
+                }
             }
             tst_u32<HK / 2>(tS, pk);  // P_j,h over the S_j,h columns just read
+            if constexpr (X) tst_u32<HK / 2>(tS + HK / 2, pl);
             tst_wait();
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -735,7 +768,14 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__
                 if (threadIdx.x == 64) p.counters[item] = 0u;
             }
         }
-        if (write_out && row < p.L) {
+        if (X && write_out && row < p.L) {
+            const float inv = 1.0f / lt;
+            float* dst = p.out_f32 + (static_cast<long long>(img) * p.L + row) * p.ldo + head * HD + half * (HD / 2);
+#pragma unroll
+            for (int c = 0; c < HD / 2; c += 4)
+                *reinterpret_cast<float4*>(dst + c) =
+                    make_float4(ov[c] * inv, ov[c + 1] * inv, ov[c + 2] * inv, ov[c + 3] * inv);
+        } else if (write_out && row < p.L) {
             const float inv = 1.0f / lt;
             __nv_bfloat16* dst = p.out + (static_cast<long long>(img) * p.L + row) * p.ldo + head * HD + half * (HD / 2);
 #pragma unroll
@@ -864,20 +904,62 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
     }
     static bool attr2[64] = {};
     if (!attr2[dev]) {
-        CKA(cudaFuncSetAttribute(attn_kernel_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CKA(cudaFuncSetAttribute(attn_kernel_v2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr2[dev] = true;
     }
     static const int ver = [] {  // ADX_ATTN_V=1: the round-1 kernel (per-block max exchange)
         const char* e = getenv("ADX_ATTN_V");
         return e && *e == '1' ? 1 : 2;
     }();
-    auto kern = ver == 1 ? attn_kernel : attn_kernel_v2;
     dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD, batch);
     if (tc_trace()) fprintf(stderr, "tc_attention L=%d Lk=%d C=%d batch=%d S=%d v%d\n", L, Lk, C, batch, a.nsplit, ver);
-    CKA(launch_pdl(kern, grid, dim3(320), smem, st, 1, mq, mk, mv, a));
-    tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, [&](cudaStream_t s2) {
-        CKA(launch_pdl(kern, grid, dim3(320), smem, s2, 1, mq, mk, mv, a));
-    });
+    auto launch = [&](cudaStream_t s2) {
+        if (ver == 1)
+            CKA(launch_pdl(attn_kernel, grid, dim3(320), smem, s2, 1, mq, mk, mv, a));
+        else
+            CKA(launch_pdl(attn_kernel_v2<false>, grid, dim3(320), smem, s2, 1, mq, mk, mv, mq, mk, mv, a));
+    };
+    launch(st);
+    tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, launch);
+    CKA(cudaGetLastError());
+}
+
+void tc_attention_x(const void* Qh, const void* Ql, long long ldq, const void* Kh, const void* Kl, long long ldk,
+                    const void* Vh, const void* Vl, long long ldv, int L, int Lk, int C, float* out, long long ldo,
+                    cudaStream_t st, void* ws, size_t ws_bytes, int batch) {
+    if (C % HD) throw std::invalid_argument("attention: C must be a multiple of 64");
+    if ((ldq | ldk | ldv) % 8 || ldo % 4) throw std::invalid_argument("attention: bad strides");
+    if (batch < 1 || batch > 65535) throw std::invalid_argument("attention: batch must be in 1..65535");
+    const long long rq = static_cast<long long>(batch) * L, rk = static_cast<long long>(batch) * Lk;
+    const CUtensorMap mqh = map2d(Qh, rq, C, ldq, QT), mql = map2d(Ql, rq, C, ldq, QT);
+    const CUtensorMap mkh = map2d(Kh, rk, C, ldk, KT), mkl = map2d(Kl, rk, C, ldk, KT);
+    const CUtensorMap mvh = map2d(Vh, rk, C, ldv, KT), mvl = map2d(Vl, rk, C, ldv, KT);
+    AttnArgs a{L, Lk, C, nullptr, ldo};
+    a.out_f32 = out;
+    const int S = attn_splits(L, Lk, C, device_sms(), batch);
+    const size_t need = tc_attention_ws_bytes(L, Lk, C, batch);
+    if (S > 1 && ws && ws_bytes >= need) {
+        const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD) * batch;
+        a.nsplit = S;
+        a.counters = static_cast<unsigned*>(ws);
+        a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * ((items * 4 + 255) / 256));
+    }
+    constexpr size_t smem =
+        1024 + 2 * QT * HD * 2 + XSTG * 2 * (KT * HD * 2 + HD * KT * 2) + 256 + 6 * QT * sizeof(float);
+    static bool attr[64] = {};
+    int dev = 0;
+    CKA(cudaGetDevice(&dev));
+    if (!attr[dev]) {
+        CKA(cudaFuncSetAttribute(attn_kernel_v2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr[dev] = true;
+    }
+    dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD, batch);
+    if (tc_trace()) fprintf(stderr, "tc_attention_x L=%d Lk=%d C=%d batch=%d S=%d\n", L, Lk, C, batch, a.nsplit);
+    auto launch = [&](cudaStream_t s2) {
+        CKA(launch_pdl(attn_kernel_v2<true>, grid, dim3(320), smem, s2, 1, mqh, mkh, mvh, mql, mkl, mvl, a));
+    };
+    launch(st);
+    tc_profile_measure(st, 2, 3 * 4.0 * L * Lk * C * batch, launch);
     CKA(cudaGetLastError());
 }
 

@@ -20,4 +20,12 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
                   size_t ws_bytes = 0, int batch = 1);
 size_t tc_attention_ws_bytes(int L, int Lk, int C, int batch = 1);
 
+// the ADX_F32 mode's attention: every operand as bf16 hi and lo planes (x = hi + lo, same
+// layout and strides each), S = Qh Kh^T + Qh Kl^T + Ql Kh^T and O = Ph Vh + Ph Vl + Pl Vh with
+// fp32 accumulation in TMEM, fp32 softmax, P split in registers; fp32 output (ldo floats).
+// Same grid, split-KV workspace and batching rules as tc_attention.
+void tc_attention_x(const void* Qh, const void* Ql, long long ldq, const void* Kh, const void* Kl, long long ldk,
+                    const void* Vh, const void* Vl, long long ldv, int L, int Lk, int C, float* out, long long ldo,
+                    cudaStream_t st, void* ws = nullptr, size_t ws_bytes = 0, int batch = 1);
+
 }  // namespace adx

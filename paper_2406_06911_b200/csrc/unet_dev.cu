@@ -140,6 +140,7 @@ UNetDevice::~UNetDevice() {
         cudaFree(s.chan_add);
         for (auto* q : s.k2) cudaFree(q);
         for (auto* q : s.vt2) cudaFree(q);
+        for (auto* q : s.kv2x) cudaFree(q);
         for (auto* q : s.pe_proj) cudaFree(q);
     }
     for (auto& kv : scratch_) {
@@ -245,6 +246,19 @@ void UNetDevice::ensure_stage(int stage) {
                         }
                     ds.k2.push_back(static_cast<bf16*>(upload_u16(split_b(k2, Lp, C, 64))));
                     ds.vt2.push_back(static_cast<bf16*>(upload_u16(split_b(vt2, C, Lp, Lp))));
+                    const size_t pl = static_cast<size_t>(Lp) * C;
+                    std::vector<uint16_t> x4(4 * pl);
+                    for (int l = 0; l < Lp; ++l)
+                        for (int c = 0; c < C; ++c) {
+                            const size_t i = static_cast<size_t>(l) * C + c;
+                            const float kv[2] = {k2[i], vt2[static_cast<size_t>(c) * Lp + l]};
+                            for (int w = 0; w < 2; ++w) {
+                                const uint16_t hb = to_bf16_bits(kv[w]);
+                                x4[2 * w * pl + i] = hb;
+                                x4[(2 * w + 1) * pl + i] = to_bf16_bits(kv[w] - bf16_to_float(hb));
+                            }
+                        }
+                    ds.kv2x.push_back(static_cast<bf16*>(upload_u16(x4)));
                 } else {  // bf16 on the tensor cores: two GEMMs (SDXL: 10 blocks x 2 contexts per stage)
                     ds.k2.push_back(static_cast<bf16*>(device_zeros(static_cast<size_t>(Lp) * C * 2)));
                     ds.vt2.push_back(static_cast<bf16*>(device_zeros(static_cast<size_t>(Lp) * C * 2)));
@@ -791,6 +805,10 @@ void UNetDevice::transformer_exact(int stage, const float* x, int H, int W, int 
     const UNetSpec& sp = d_.spec;
     const int L = H * W, B = sp.batch(), BL = B * L, depth = d_.st[stage - 1].attn;
     const long long img = static_cast<long long>(L) * C;
+    static const bool fused = [] {  // ADX_F32_ATTN=unfused: S through HBM, one head at a time (A/B)
+        const char* e = getenv("ADX_F32_ATTN");
+        return !(e && std::string(e) == "unfused");
+    }();
     gn_images(Cat2F{x, C, nullptr, 0}, L, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"), 1e-6f, 0, s.fa, s, st);
     TcArgs pi;
     pi.bias = F(stage, "tf.proj_in.b");
@@ -807,10 +825,17 @@ void UNetDevice::transformer_exact(int stage, const float* x, int H, int W, int 
         qk.out_f32 = s.fqkv;
         qk.ldo = 3 * C;
         gemm_x(s, s.fa, BL, C, n_qkv.c_str(), stage, 3 * C, qk, st);
-        for (int b = 0; b < B; ++b) {
-            const float* q = s.fqkv + b * 3 * img;
-            split3(q + C, L, C, 3LL * C, 64, 1, s.sk, st);
-            attention_exact(s, q, 3LL * C, s.sk, q + 2 * C, 3LL * C, nullptr, L, L, C, s.fatt + b * img, st);
+        if (fused) {  // hi / lo planes of q | k | v, then every image and head in one launch
+            bf16 *hi = s.sa, *lo = s.sa + 3 * BL * static_cast<long long>(C);
+            split2(s.fqkv, 3LL * BL * C, hi, lo, st);
+            tc_attention_x(hi, lo, 3LL * C, hi + C, lo + C, 3LL * C, hi + 2 * C, lo + 2 * C, 3LL * C, L, L, C, s.fatt,
+                           C, st, s.attn_ws, s.attn_ws_bytes, B);
+        } else {
+            for (int b = 0; b < B; ++b) {
+                const float* q = s.fqkv + b * 3 * img;
+                split3(q + C, L, C, 3LL * C, 64, 1, s.sk, st);
+                attention_exact(s, q, 3LL * C, s.sk, q + 2 * C, 3LL * C, nullptr, L, L, C, s.fatt + b * img, st);
+            }
         }
         TcArgs o1;
         o1.bias = Fn("o1.b");
@@ -824,10 +849,23 @@ void UNetDevice::transformer_exact(int stage, const float* x, int H, int W, int 
         q2.out_f32 = s.fqkv;
         q2.ldo = C;
         gemm_x(s, s.fa, BL, C, n_q2.c_str(), stage, C, q2, st);
-        for (int b = 0; b < B; ++b) {
-            const int ci = sp.contexts() == 1 ? blk : blk * B + b;  // video frames share one context
-            attention_exact(s, s.fqkv + b * img, C, st_[stage].k2[ci], nullptr, 0, st_[stage].vt2[ci], L, sp.ctx_len,
-                            C, s.fatt + b * img, st);
+        if (fused) {
+            bf16 *hi = s.sa, *lo = s.sa + BL * static_cast<long long>(C);
+            split2(s.fqkv, static_cast<long long>(BL) * C, hi, lo, st);
+            const long long pl = static_cast<long long>(pad64(sp.ctx_len)) * C;
+            const int nimg = sp.contexts() == 1 ? 1 : B;  // one shared context: all B * L queries at once
+            for (int b = 0; b < nimg; ++b) {
+                const bf16* kv = st_[stage].kv2x[sp.contexts() == 1 ? blk : blk * B + b];
+                tc_attention_x(hi + b * img, lo + b * img, C, kv, kv + pl, C, kv + 2 * pl, kv + 3 * pl, C,
+                               nimg == 1 ? BL : L, sp.ctx_len, C, s.fatt + b * img, C, st, s.attn_ws,
+                               s.attn_ws_bytes, 1);
+            }
+        } else {
+            for (int b = 0; b < B; ++b) {
+                const int ci = sp.contexts() == 1 ? blk : blk * B + b;  // video frames share one context
+                attention_exact(s, s.fqkv + b * img, C, st_[stage].k2[ci], nullptr, 0, st_[stage].vt2[ci], L,
+                                sp.ctx_len, C, s.fatt + b * img, st);
+            }
         }
         TcArgs o2;
         o2.bias = Fn("o2.b");

@@ -24,6 +24,9 @@ struct UDevStage {
     // block * contexts + context; values row-major [ctx_pad][C] (bf16 mode) or V^T split
     // along the keys [C][3 ctx_pad] (ADX_F32 mode)
     std::vector<__nv_bfloat16*> k2, vt2;
+    // ADX_F32 mode, fused attention: per (block, context) the planes [Kh | Kl | Vh | Vl], each
+    // [ctx_pad][C] bf16 row-major (x = hi + lo)
+    std::vector<__nv_bfloat16*> kv2x;
     // video motion module: per temporal attention, the frame positional encoding through the
     // QKV projection, PE . Wqkv^T [frames][3C] fp32 (added per frame in the GEMM epilogue)
     std::vector<float*> pe_proj;

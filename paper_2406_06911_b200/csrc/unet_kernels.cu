@@ -682,6 +682,23 @@ __global__ void split3_k(const float* x, long long rows, int cols, long long ldx
     }
 }
 
+// hi / lo planes of the fused split-operand attention (see split2 in unet_kernels.cuh)
+__global__ void split2_k(const float* x, long long n8, bf16* hi, bf16* lo) {
+    pdl_wait();
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float f[8], h[8], l[8];
+        Vec8<float>::unpack(Vec8<float>::load(x + 8 * i), f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            h[k] = __bfloat162float(__float2bfloat16(f[k]));
+            l[k] = f[k] - h[k];
+        }
+        *reinterpret_cast<uint4*>(hi + 8 * i) = pack8(h);
+        *reinterpret_cast<uint4*>(lo + 8 * i) = pack8(l);
+    }
+}
+
 // fp32 row softmax, in place (the ADX_F32 mode's unfused attention)
 __global__ void softmax_rows_f32_k(float* S, long long lds, int valid, int padded) {
     pdl_wait();
@@ -1335,6 +1352,12 @@ void split3(const float* x, long long rows, int cols, long long ldx, int g, int 
     if (cols % g || g % 8) throw std::invalid_argument("split3: group width must divide cols and be a multiple of 8");
     CKU(launch_pdl(split3_k, dim3(grid_for(rows * cols / 8)), dim3(256), 0, st, 1, x, rows, cols, ldx, g, pattern,
                    out));
+    CKU(cudaGetLastError());
+}
+
+void split2(const float* x, long long n, __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t st) {
+    if (n % 8) throw std::invalid_argument("split2: element count must be a multiple of 8");
+    CKU(launch_pdl(split2_k, dim3(grid_for(n / 8)), dim3(256), 0, st, 1, x, n / 8, hi, lo));
     CKU(cudaGetLastError());
 }
 

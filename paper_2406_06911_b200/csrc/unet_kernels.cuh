@@ -32,6 +32,8 @@ void layer_norm(const float* x, int tokens, int C, const float* gamma, const flo
 // A'.B'^T = hi.hi + hi.lo + lo.hi (the lo.lo term is ~2^-16 relative)
 void split3(const float* x, long long rows, int cols, long long ldx, int g, int pattern, __nv_bfloat16* out,
             cudaStream_t st);
+// x (n contiguous fp32) -> hi = bf16(x), lo = bf16(x - hi), same layout (tc_attention_x planes)
+void split2(const float* x, long long n, __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t st);
 // fp32 row softmax over the first `valid` columns written as the split-bf16 A operand
 // [hi | hi | lo] (3 x padded per row; split3 pattern 0 with g = padded); S is not modified
 void softmax_split_rows(const float* S, long long lds, int rows, int valid, int padded, __nv_bfloat16* out,

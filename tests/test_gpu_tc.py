@@ -131,6 +131,30 @@ def check_attention(L, Lk, C, scale):
     assert err < 2e-2, err
 
 
+@pytest.mark.parametrize("batch,L,Lk,C,scale", [(1, 1024, 1024, 128, 1.0), (2, 700, 1000, 320, 1.0),
+                                                (1, 2304, 77, 640, 1.0), (2, 9216, 9216, 320, 1.0),
+                                                (1, 512, 700, 64, 6.0)])
+def test_tc_attention_f32_matches_fp64(batch, L, Lk, C, scale):
+    """the ADX_F32 mode's fused split-operand attention vs torch fp64: S and P V as three
+    bf16 split products each (error ~2^-16 relative), far inside the mode's 1e-3 budget"""
+    rng = np.random.default_rng(batch * 7 + L + Lk + C)
+    Q = (scale * rng.standard_normal((batch, L, C))).astype(np.float32)
+    K = (scale * rng.standard_normal((batch, Lk, C))).astype(np.float32)
+    V = rng.standard_normal((batch, Lk, C)).astype(np.float32)
+    out = np.zeros((batch, L, C), np.float32)
+    _lib.check(adx.lib().adx_tc_attention_f32(0, batch, L, Lk, C, Q.ctypes.data_as(PF), K.ctypes.data_as(PF),
+                                              V.ctypes.data_as(PF), out.ctypes.data_as(PF), 0, None))
+    heads = lambda x, n: torch.from_numpy(x).double().view(batch, n, C // 64, 64).transpose(1, 2)
+    q, k, v = heads(Q, L), heads(K, Lk), heads(V, Lk)
+    ref = (torch.softmax(q @ k.transpose(-1, -2) / 8.0, dim=-1) @ v).transpose(1, 2).reshape(batch, L, C).numpy()
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    # the split products lose ~2^-16 |q||k| per logit: 3.6e-5 at scale 1 and 1.1e-3 at scale 6
+    # (|S| ~ 36), 1.0e-5 / 1.4e-4 in the output by a numpy emulation of the same split scheme
+    tol = 1e-4 if scale <= 1 else 5e-4
+    print(f"f32 attention batch={batch} L={L} Lk={Lk} C={C} scale={scale}: max rel err {err:.2e}")
+    assert err < tol, err
+
+
 def test_tc_attention_split_kv_is_deterministic():
     rng = np.random.default_rng(9)
     L, C = 1024, 640  # 80 (query tile, head) items -> split over KV
