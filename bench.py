@@ -27,6 +27,8 @@ import sys
 import tempfile
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -243,9 +245,11 @@ def roofline(m, cfg, prec, dev):
         cg_ms = prof["conv3x3"]["ms"] + prof["gemm"]["ms"]
         cg_fl = prof["conv3x3"]["flops"] + prof["gemm"]["flops"]
         ach = cg_fl / (cg_ms * 1e-3) / 1e12
+        recs = prof.pop("records")
         fam = {k: dict(v, tflops=v["flops"] / (v["ms"] * 1e-3) / 1e12 if v["ms"] else 0.0,
                        frac_burst=(v["flops"] / (v["ms"] * 1e-3) / 1e12) / peak if v["ms"] else 0.0)
                for k, v in prof.items()}
+        sol = per_launch_sol(recs, peak)
         # the whole pass (every kernel, gaps included) inside the long timed step -> sustained peak
         whole = 2.0 * sum(st.cost_macs for st in m.stages) / (pass_ms * 1e-3) / 1e12
         traffic, tnote = measured_traffic(cfg, prec, "tc_gemm_kernel", prof["conv3x3"]["launches"] + prof["gemm"]["launches"])
@@ -256,7 +260,7 @@ def roofline(m, cfg, prec, dev):
                 "achieved_basis": ("algorithmic conv+GEMM FLOPs of one pass / the sum of their per-launch device "
                                    "times, each launch replayed alone from a CUDA graph (CUDA events on its "
                                    "stream) -> compared with the BURST peak"),
-                "families": fam, "ms_per_pass": pass_ms, "whole_pass_tflops": whole,
+                "families": fam, "per_launch_sol": sol, "ms_per_pass": pass_ms, "whole_pass_tflops": whole,
                 "whole_pass_frac_sustained": whole / sus, "sustained_peak": sus, "sustained_peak_source": sus_src,
                 "stage_launches_per_pass": launches}
     peak, src = load_peak("hbm")
@@ -264,6 +268,32 @@ def roofline(m, cfg, prec, dev):
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
             "peak_source": src, "kernel": "gemv_tma_kernel (stage W1/W2 GEMV)", "bytes_per_pass": pass_bytes,
             "ms_per_pass": pass_ms, "launches_per_pass": launches}
+
+
+def per_launch_sol(recs, tc_peak):
+    """speed of light per launch = max(algorithmic FLOPs / tensor peak, compulsory HBM bytes / HBM
+    peak) (both burst: each launch is timed alone); frac = sum(SOL) / sum(measured) per family.
+    Small-K GEMMs (K = 320..1280 against M = 18432) move more bytes than they compute: their
+    ceiling is the HBM line, which the tensor-peak `frac` above does not show."""
+    hbm, _ = load_peak("hbm")
+    names = {0: "conv3x3", 1: "gemm", 2: "attention", 3: "group_norm", 4: "layer_norm"}
+    out = {}
+    for kind, name in names.items():
+        r = recs[recs[:, 0] == kind]
+        if not len(r):
+            continue
+        t_tc = r[:, 1] / (tc_peak * 1e12) * 1e3
+        t_hbm = r[:, 2] / (hbm * 1e9) * 1e3
+        sol = np.maximum(t_tc, t_hbm)
+        out[name] = {"launches": int(len(r)), "ms": float(r[:, 3].sum()), "sol_ms": float(sol.sum()),
+                     "sol_frac": float(sol.sum() / r[:, 3].sum()),
+                     "hbm_bound_launches": int((t_hbm > t_tc).sum()),
+                     "gbs": float(r[:, 2].sum() / (r[:, 3].sum() * 1e-3) / 1e9)}
+    tot_ms = sum(v["ms"] for v in out.values())
+    out["all"] = {"ms": tot_ms, "sol_ms": sum(v["sol_ms"] for v in out.values()),
+                  "sol_frac": sum(v["sol_ms"] for v in out.values()) / tot_ms if tot_ms else 0.0,
+                  "hbm_peak_gbs": hbm, "tensor_peak_tflops": tc_peak}
+    return out
 
 
 def cpu_baseline(cfg, n_components, steps=1):

@@ -178,6 +178,10 @@ int adx_bench_gemv(int ordinal, int precision, int n, int chain, int iters, int 
 /* One eager full-model pass with CUDA events around every tensor-core launch:
  * out9 = {launches, ms, algorithmic FLOPs} for conv3x3, GEMM, attention. */
 int adx_engine_profile_pass(adx_engine* e, int t_embed, double* out9);
+/* the per-launch records of the last adx_engine_profile_pass: 4 doubles per launch
+ * (kind 0 conv3x3 / 1 GEMM / 2 attention / 3 GroupNorm / 4 LayerNorm, algorithmic FLOPs,
+ * compulsory HBM bytes, device ms); *n = the record count (at most `cap` are written) */
+int adx_profile_records(double* out, int cap, int* n);
 
 /* eval_full: denoiser.hpp:79, denoiser.cpp:222-233 (on ordinals[0]) */
 int adx_eval_full(adx_engine* e, const double* x, int t_embed, double* eps_out);
@@ -324,6 +328,13 @@ int adx_unet_context(const adx_model* m, float* out /* batch x ctx_len x ctx_dim
  * act 0 none, 1 SiLU, 2 GEGLU over 256-row tiles of [128 hidden | 128 gate] rows (C is M x N/2) */
 int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B,
                 const float* bias, int act, float* C, int bn, int iters, double* ms_per_iter);
+/* the bf16 mode's LayerNorm-folded GEMM (kernel test): y = rstd_m (H . W1'^T - mean_m colsum1) +
+ * bias1 with the row statistics of H [M x C] (bf16) reduced inside the GEMM, W1' [N x C] =
+ * W1 diag(gamma) and bias1 = b + W1 beta folded by the caller (geglu: N = 2H rows tile-
+ * interleaved, y [M x H]); bn forces the N tile (0: the launcher's plan) */
+int adx_tc_ln_fold_bf16(int ordinal, int M, int C, int N, const uint16_t* H, const uint16_t* W1, const float* bias1,
+                        const float* colsum1, int geglu, float eps, uint16_t* y_out, int bn, int iters,
+                        double* ms_per_iter);
 /* fused multi-head attention (64-wide heads, scale 1/8): out[L x C] bf16 from Q [L x C],
  * K [Lk x C] and V [Lk x ldv] (row-major, ldv >= C, multiple of 8) */
 int adx_tc_attention(int ordinal, int L, int Lk, int C, const uint16_t* Q, const uint16_t* K,

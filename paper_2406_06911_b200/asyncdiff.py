@@ -1127,8 +1127,14 @@ def profile_model_pass(m: LayeredDenoiser, t_embed: int, precision: Optional[str
     events per launch) and algorithmic FLOPs."""
     out = np.zeros(9)
     check(lib().adx_engine_profile_pass(m.engine(precision, devices)._h, t_embed, _dp(out)))
-    return {k: dict(launches=int(out[3 * i]), ms=float(out[3 * i + 1]), flops=float(out[3 * i + 2]))
-            for i, k in enumerate(("conv3x3", "gemm", "attention"))}
+    res = {k: dict(launches=int(out[3 * i]), ms=float(out[3 * i + 1]), flops=float(out[3 * i + 2]))
+           for i, k in enumerate(("conv3x3", "gemm", "attention"))}
+    n = C.c_int()
+    check(lib().adx_profile_records(None, 0, C.byref(n)))
+    rec = np.zeros(4 * max(n.value, 1))
+    check(lib().adx_profile_records(_dp(rec), n.value, C.byref(n)))
+    res["records"] = rec[:4 * n.value].reshape(-1, 4)  # (kind, flops, compulsory bytes, ms) per launch
+    return res
 
 
 def stage_times(m: LayeredDenoiser, t_embed: int, iters: int = 10, precision: Optional[str] = None,

@@ -669,6 +669,13 @@ int adx_engine_profile_pass(adx_engine* e, int t_embed, double* out9) {
     });
 }
 
+int adx_profile_records(double* out, int cap, int* n) {
+    return guard([&] {
+        if (!n) throw std::invalid_argument("profile_records: n is null");
+        *n = adx::tc_profile_records(out, out ? cap : 0);
+    });
+}
+
 int adx_eval_full(adx_engine* e, const double* x, int t_embed, double* eps_out) {
     return guard([&] {
         need(e, "eval_full");
@@ -1057,6 +1064,41 @@ int adx_tc_gemm_bf16(int ordinal, int M, int N, int K, const uint16_t* A, const 
         }
         if (bn) adx::tc_plan_override(0, 0);
         CKC(cudaMemcpy(out, o.p, static_cast<size_t>(M) * ldo * 2, cudaMemcpyDeviceToHost));
+    });
+}
+
+int adx_tc_ln_fold_bf16(int ordinal, int M, int C, int N, const uint16_t* H, const uint16_t* W1, const float* bias1,
+                        const float* colsum1, int geglu, float eps, uint16_t* y_out, int bn, int iters,
+                        double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        const int No = geglu ? N / 2 : N;
+        const size_t mc = static_cast<size_t>(M) * C;
+        DevBuf h(mc * 2), w1(static_cast<size_t>(N) * C * 2), b1(static_cast<size_t>(N) * 4),
+            cs(static_cast<size_t>(N) * 4), y(static_cast<size_t>(M) * No * 2);
+        CKC(cudaMemcpy(h.p, H, mc * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(w1.p, W1, static_cast<size_t>(N) * C * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(b1.p, bias1, static_cast<size_t>(N) * 4, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(cs.p, colsum1, static_cast<size_t>(N) * 4, cudaMemcpyHostToDevice));
+        adx::TcArgs p1;
+        p1.bias = static_cast<const float*>(b1.p);
+        p1.act = geglu ? 2 : 0;
+        p1.out_bf16 = static_cast<__nv_bfloat16*>(y.p);
+        p1.ldo = No;
+        p1.ln_colsum = static_cast<const float*>(cs.p);
+        p1.ln_eps = eps;
+        if (bn) adx::tc_plan_override(bn, 1);
+        try {
+            adx::tc_gemm(h.p, w1.p, M, N, C, p1, 0, 0);
+            CKC(cudaDeviceSynchronize());
+            if (iters > 0 && ms_per_iter)
+                *ms_per_iter = time_graph_ms([&](cudaStream_t st) { adx::tc_gemm(h.p, w1.p, M, N, C, p1, st, 0); }, iters);
+        } catch (...) {
+            adx::tc_plan_override(0, 0);
+            throw;
+        }
+        if (bn) adx::tc_plan_override(0, 0);
+        if (y_out) CKC(cudaMemcpy(y_out, y.p, static_cast<size_t>(M) * No * 2, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -920,7 +920,7 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
             CKA(launch_pdl(attn_kernel_v2<false>, grid, dim3(320), smem, s2, 1, mq, mk, mv, mq, mk, mv, a));
     };
     launch(st);
-    tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, launch);
+    tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, 2.0 * batch * C * (2.0 * L + 2.0 * Lk), launch);
     CKA(cudaGetLastError());
 }
 
@@ -959,7 +959,8 @@ void tc_attention_x(const void* Qh, const void* Ql, long long ldq, const void* K
         CKA(launch_pdl(attn_kernel_v2<true>, grid, dim3(320), smem, s2, 1, mqh, mkh, mvh, mql, mkl, mvl, a));
     };
     launch(st);
-    tc_profile_measure(st, 2, 3 * 4.0 * L * Lk * C * batch, launch);
+    tc_profile_measure(st, 2, 3 * 4.0 * L * Lk * C * batch, 2.0 * batch * C * (2.0 * L + 4.0 * Lk + 2.0 * L),
+                       launch);
     CKA(cudaGetLastError());
 }
 

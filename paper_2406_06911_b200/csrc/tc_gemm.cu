@@ -244,9 +244,18 @@ __device__ __forceinline__ const float* chan_row(const TcArgs& p, long long m, i
 // bias_base: column-indexed bias (p.bias, or the tile's SMEM-staged copy offset by -n0)
 __device__ __forceinline__ void epi16(const TcArgs& p, long long m, const float* ca, int nb, float* v,
                                       const uint4* rpre = nullptr, uint4* sdst = nullptr,
-                                      const float* bias_base = nullptr) {
+                                      const float* bias_base = nullptr, const float* lncs = nullptr,
+                                      float2 ln = make_float2(0.f, 1.f)) {
     const int nlim = p.n_store ? p.n_store : p.N;
     const float* bias = bias_base ? bias_base : p.bias;
+    if (lncs) {  // LayerNorm fold: rstd (acc - mean colsum)
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+            const float4 c = *reinterpret_cast<const float4*>(lncs + nb + j);
+            v[j] = ln.y * fmaf(-ln.x, c.x, v[j]), v[j + 1] = ln.y * fmaf(-ln.x, c.y, v[j + 1]);
+            v[j + 2] = ln.y * fmaf(-ln.x, c.z, v[j + 2]), v[j + 3] = ln.y * fmaf(-ln.x, c.w, v[j + 3]);
+        }
+    }
     if ((((p.ldo | p.ldr) & 7) == 0) && nb + 16 <= nlim && !p.residual_f32) {
         // vectorised: 16-byte loads / stores
 #pragma unroll
@@ -311,14 +320,42 @@ __device__ __forceinline__ void epi16(const TcArgs& p, long long m, const float*
     }
 }
 
-// GEGLU epilogue: the host interleaved the weight rows per 256-wide tile, so tile
-// columns [0, 128) are hidden units n0/2 + c and [128, 256) their gates;
-// out[m][n0/2 + c] = (h + bh) * gelu(g + bg)  (the 2x-wide product never reaches HBM)
-__device__ __forceinline__ void epi_geglu16(const TcArgs& p, long long m, int n0, int c, float* v, float* g) {
+// packed fp32 pairs (FADD2 / FFMA2): the LayerNorm-fold statistics warps
+__device__ __forceinline__ unsigned long long f2add(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ float f2lo(unsigned long long a) { return __uint_as_float(static_cast<uint32_t>(a)); }
+__device__ __forceinline__ float f2hi(unsigned long long a) { return __uint_as_float(static_cast<uint32_t>(a >> 32)); }
+// a bf16 pair word -> the packed fp32 pair (lo, hi)
+__device__ __forceinline__ unsigned long long bf2_to_f2(uint32_t w) {
+    return static_cast<unsigned long long>(w << 16) | (static_cast<unsigned long long>(w & 0xffff0000u) << 32);
+}
+
+// bias / cs: column-indexed bases (the tile's SMEM-staged copies offset by -n0)
+__device__ __forceinline__ void epi_geglu16(const TcArgs& p, long long m, int n0, int c, float* v, float* g,
+                                            const float* bias, const float* cs, float2 ln = make_float2(0.f, 1.f)) {
+    if (cs) {  // LayerNorm fold on both halves
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+            const float4 ch = *reinterpret_cast<const float4*>(cs + n0 + c + j);
+            const float4 cg = *reinterpret_cast<const float4*>(cs + n0 + 128 + c + j);
+            v[j] = ln.y * fmaf(-ln.x, ch.x, v[j]), v[j + 1] = ln.y * fmaf(-ln.x, ch.y, v[j + 1]);
+            v[j + 2] = ln.y * fmaf(-ln.x, ch.z, v[j + 2]), v[j + 3] = ln.y * fmaf(-ln.x, ch.w, v[j + 3]);
+            g[j] = ln.y * fmaf(-ln.x, cg.x, g[j]), g[j + 1] = ln.y * fmaf(-ln.x, cg.y, g[j + 1]);
+            g[j + 2] = ln.y * fmaf(-ln.x, cg.z, g[j + 2]), g[j + 3] = ln.y * fmaf(-ln.x, cg.w, g[j + 3]);
+        }
+    }
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
-        const float4 bh = *reinterpret_cast<const float4*>(p.bias + n0 + c + j);
-        const float4 bg = *reinterpret_cast<const float4*>(p.bias + n0 + 128 + c + j);
+        const float4 bh = *reinterpret_cast<const float4*>(bias + n0 + c + j);
+        const float4 bg = *reinterpret_cast<const float4*>(bias + n0 + 128 + c + j);
         v[j] += bh.x, v[j + 1] += bh.y, v[j + 2] += bh.z, v[j + 3] += bh.w;
         g[j] += bg.x, g[j + 1] += bg.y, g[j + 2] += bg.z, g[j + 3] += bg.w;
     }
@@ -388,7 +425,7 @@ constexpr int kStageChunks() { return BN > 192 ? 0 : (BN / 16 + 1) / 2; }
 #endif
 template <int BN>
 constexpr int kStages() {
-    constexpr int fixed = 1024 + 256 + EPW_ * kStageChunks<BN>() * 1024 + 16 * BN;
+    constexpr int fixed = 1024 + 256 + EPW_ * kStageChunks<BN>() * 1024 + 16 * BN + 2 * BM * 8;
     constexpr int per = BM * BK * 2 + BN * BK * 2;
     constexpr int fit = (227 * 1024 - fixed) / per;
     return fit < ADX_TC_STAGES ? fit : ADX_TC_STAGES;
@@ -396,14 +433,15 @@ constexpr int kStages() {
 template <int BN>
 constexpr size_t kGemmSmem() {
     return 1024 + static_cast<size_t>(kStages<BN>()) * (BM * BK * 2 + BN * BK * 2) + 256 +
-           static_cast<size_t>(EPW_) * kStageChunks<BN>() * 1024 + 16 * BN;
+           static_cast<size_t>(EPW_) * kStageChunks<BN>() * 1024 + 16 * BN + 2 * BM * 8;
 }
 
 // ------------------------------------------------------------------ kernel
 // epilogue warps: EPW / 4 per TMEM lane quadrant, each over its share of the tile's
 // 16-column chunks (more loads / stores in flight for the 1-tile-per-CTA small GEMMs)
 constexpr int EPW = EPW_;
-constexpr int kGemmThreads = 64 + 32 * EPW;
+constexpr int kStatWarps = 2;  // LayerNorm-fold statistics warps (idle otherwise); 384 threads keep 168 regs
+constexpr int kGemmThreads = 64 + 32 * EPW + 32 * kStatWarps;
 __device__ __forceinline__ void epi_chunks(int nch, int part, int& c0, int& c1) {
     constexpr int P = EPW / 4;
     c0 = (nch * part) / P * 16;
@@ -430,9 +468,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
     uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
     uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
     uint64_t* rbar = tempty + 2;       // [EPW] residual chunks landed in an epilogue warp's staging
-    uint32_t* tptr = reinterpret_cast<uint32_t*>(rbar + EPW);
+    uint64_t* sfull = rbar + EPW;      // [2] LayerNorm-fold row statistics of an accumulator's tile ready
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(sfull + 2);  // (barrier block: <= 244 of 256 B)
     // per accumulator: [bias | chan_add] of the tile's BN columns, staged by the epilogue warps
     float* sepi = reinterpret_cast<float*>(sB + STAGES * B_BYTES + 256 + EPW * kStageChunks<BN>() * 1024);
+    float2* sstat = reinterpret_cast<float2*>(sepi + 4 * BN);  // [2 accumulators][BM rows] (mean, rstd)
+    const bool lnf = !CONV && p.ln_colsum != nullptr;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // Work units.  S == 1: persistent -- CTA b takes output tiles b, b + G, ... (m fastest,
@@ -477,11 +518,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             bar_init(&full[s], 1);
-            bar_init(&empty[s], 1);
+            bar_init(&empty[s], lnf ? 1 + kStatWarps : 1);  // + the statistics warps' reads
         }
         for (int a = 0; a < 2; ++a) {
             bar_init(&tfull[a], 1);
             bar_init(&tempty[a], EPW);  // one arrival per epilogue warp
+            bar_init(&sfull[a], kStatWarps);
         }
         for (int w = 0; w < EPW; ++w) bar_init(&rbar[w], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -569,7 +611,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
         // every MMA of this CTA is issued: let the next kernel of the stream start launching
         // (its CTAs take SMs as ours exit, and its weight TMA overlaps our epilogues)
         if (ADX_TC_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    } else if (warp >= 2) {
+    } else if (warp >= 2 && warp < 2 + EPW) {
         // --------------------------------------------------------- epilogue
         const int q = warp & 3;             // TMEM lane quadrant this warp may access
         const int part = (warp - 2) >> 2;   // which share of the tile's column chunks
@@ -582,6 +624,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             coords(u, tile_m, tile_n, img, h0, w0);
             const int n0 = tile_n * BN;
             const int acc = lu & 1;
+            float2 lnr = make_float2(0.f, 1.f);
             if (p.tma_store && lu > 0) {  // the previous tile's stores have read their staging blocks
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 __syncwarp();
@@ -603,19 +646,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                 }
             }
             float* sb = sepi + acc * 2 * BN;
-            const bool stage_cols = p.act != 2 && !p.chan_add_rows;  // (S > 1: one tile, acc 0)
+            const bool stage_cols = (!CONV || p.act != 2) && !p.chan_add_rows;  // (S > 1: one tile, acc 0)
             if (stage_cols) {
                 const float* car = p.chan_add ? p.chan_add + static_cast<long long>(p.chan_add_shared ? 0 : img) * p.N
                                               : nullptr;
                 for (int cidx = threadIdx.x - 64; cidx < BN; cidx += 32 * EPW) {
                     const int n = n0 + cidx;
                     sb[cidx] = p.bias && n < p.N ? p.bias[n] : 0.f;
-                    sb[BN + cidx] = car && n < p.N ? car[n] : 0.f;
+                    // LayerNorm-fold consumer: colsum(W') in the channel-add slot (never both)
+                    sb[BN + cidx] = n >= p.N ? 0.f : !CONV && p.ln_colsum ? p.ln_colsum[n] : car ? car[n] : 0.f;
                 }
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * EPW) : "memory");  // the epilogue warps
             }
             bar_wait(&tfull[acc], (lu >> 1) & 1);
             if (lu == 0 && threadIdx.x == 64) TL(4);
+            if (lnf) {  // this row's LayerNorm statistics from the statistics warps
+                bar_wait(&sfull[acc], (lu >> 1) & 1);
+                lnr = sstat[acc * BM + row];
+            }
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t trow = tmem + acc * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16);
             if (S > 1) {
@@ -634,14 +682,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             } else {
                 long long m;
                 const bool valid = row_to_m<CONV>(p, tile_m, img, h0, w0, row, m);
-                if (p.act == 2) {
+                const float2 ln = lnr;
+                if (!CONV && p.act == 2) {
                     int cb, ce;
                     epi_chunks(BN / 32, part, cb, ce);
                     for (int c = cb; c < ce; c += 16) {
                         float v[16], g[16];
                         tmem_ld16(trow + c, v);
                         tmem_ld16(trow + BN / 2 + c, g);
-                        if (valid) epi_geglu16(p, m, n0, c, v, g);
+                        if (valid) epi_geglu16(p, m, n0, c, v, g, sb - n0, p.ln_colsum ? sb + BN - n0 : nullptr, ln);
                     }
                 } else {
                     // the residual of chunk c+16 is requested before chunk c's TMEM read and
@@ -666,6 +715,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                     const float* ca = !valid ? nullptr : stage_cols ? (p.chan_add ? sb + BN - n0 : nullptr)
                                                                     : chan_row(p, m, img);
                     const float* bb = stage_cols ? (p.bias ? sb - n0 : nullptr) : p.bias;
+                    const float* lncs = CONV || !p.ln_colsum ? nullptr : stage_cols ? sb + BN - n0 : p.ln_colsum;
+                    if (!CONV && p.ln_colsum) ca = nullptr;
                     if (tres && cb < ce) bar_wait(&rbar[warp - 2], lu & 1);
                     if (p.tma_store) {
                         // staged epilogue: TMEM chunks in pairs (two loads, one wait), the math written
@@ -693,7 +744,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                                     const uint4* rp = reinterpret_cast<const uint4*>(p.residual + m * p.ldr + n0 + cc);
                                     rr[0] = rp[0], rr[1] = rp[1];
                                 }
-                                if (valid) epi16(pe, m, ca, n0 + cc, v, rr, sd, bb);
+                                if (valid) epi16(pe, m, ca, n0 + cc, v, rr, sd, bb, lncs, ln);
                             }
                         }
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -718,7 +769,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                             }
                             float v[16];
                             tmem_ld16(trow + c, v);
-                            if (valid) epi16(pe, m, ca, n0 + c, v, have ? rcur : nullptr, nullptr, bb);
+                            if (valid) epi16(pe, m, ca, n0 + c, v, have ? rcur : nullptr, nullptr, bb, lncs, ln);
                         }
                     }
                 }
@@ -735,6 +786,58 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
 #if !defined(ADX_TL_CHUNK) && !defined(ADX_TL_SPLIT)
         if (threadIdx.x == 64) TL(6);
 #endif
+    } else if (lnf && warp >= 2 + EPW) {
+        // ------------------------------------------- LayerNorm-fold statistics (2 warps)
+        // thread t owns tile rows t and t + 64: every A k-block of the tile is read from the ring
+        // (the 128 B of a row, swizzle order irrelevant to a sum) as soon as it lands, then
+        // released; sum x and sum (x - c)^2 with c = a value of the row (shift against
+        // cancellation) in packed fp32 pairs; (mean, rstd) per row to sstat[acc]
+        const int t = threadIdx.x - (64 + 32 * EPW);
+        const float inv_k = 1.f / static_cast<float>(p.k_blocks * BK);
+        int it = 0, lu = 0;
+        for (int u = u0; u < uend; u += ustride, ++lu) {
+            const int acc = lu & 1;
+            bar_wait(&tempty[acc], ((lu >> 1) & 1) ^ 1);  // the epilogue read sstat[acc] two tiles ago
+            unsigned long long s1[2] = {0ull, 0ull}, s2[2] = {0ull, 0ull}, c2[2] = {0ull, 0ull};
+            for (int i = 0; i < nkb; ++i, ++it) {
+                const int s = it % STAGES;
+                bar_wait(&full[s], (it / STAGES) & 1);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(sA + s * A_BYTES + (t + 64 * h) * 128);
+                    uint4 q[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) q[j] = rp[j];
+                    if (i == 0) {  // shift: the row's first stored pair's low value, in both halves
+                        const float c = __uint_as_float(q[0].x << 16);
+                        c2[h] = static_cast<unsigned long long>(__float_as_uint(-c)) |
+                                (static_cast<unsigned long long>(__float_as_uint(-c)) << 32);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const unsigned long long x = bf2_to_f2(w4[k]);
+                            const unsigned long long d = f2add(x, c2[h]);
+                            s1[h] = f2add(s1[h], x);
+                            s2[h] = f2fma(d, d, s2[h]);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive1(&empty[s]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float mean = (f2lo(s1[h]) + f2hi(s1[h])) * inv_k;
+                const float dm = mean + f2lo(c2[h]);  // mean - c
+                const float var = fmaxf((f2lo(s2[h]) + f2hi(s2[h])) * inv_k - dm * dm, 0.f);
+                sstat[acc * BM + t + 64 * h] = make_float2(mean, rsqrtf(var + p.ln_eps));
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive1(&sfull[acc]);
+        }
     }
     if (S > 1) {
         // split-K reduction: CTA `split` owns tile rows [r0, r1) and sums the S staged
@@ -747,7 +850,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
 #ifdef ADX_TL_SPLIT
         if (threadIdx.x == 64) TL(6);
 #endif
-        if (warp >= 2) {
+        if (warp >= 2 && warp < 2 + EPW) {
             int tile_m, tile_n, img, h0, w0;
             coords(u0, tile_m, tile_n, img, h0, w0);
             const int n0 = tile_n * BN;
@@ -760,7 +863,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
             uint32_t rb[kMaxSplitsDev];
 #pragma unroll
             for (int r = 0; r < kMaxSplitsDev; ++r) rb[r] = mapa(base, r < S ? r : 0);
-            const bool sc = p.act != 2 && !p.chan_add_rows;
+            const bool sc = (!CONV || p.act != 2) && !p.chan_add_rows;
             const float* bb = sc && p.bias ? sepi - n0 : p.bias;
             for (int it = et; it < (r1 - r0) * chunks; it += 32 * EPW) {
                 const int row = r0 + it / chunks, c = (it % chunks) * 16;
@@ -784,18 +887,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                     const float4 x = reduce_dsmem4(a, S, j * 4);
                     v[j] = x.x, v[j + 1] = x.y, v[j + 2] = x.z, v[j + 3] = x.w;
                 }
-                if (p.act == 2) {
+                if (!CONV && p.act == 2) {
 #pragma unroll
                     for (int j = 0; j < 16; j += 4) {
                         const float4 x = reduce_dsmem4(a, S, (BN / 2 + j) * 4);
                         g[j] = x.x, g[j + 1] = x.y, g[j + 2] = x.z, g[j + 3] = x.w;
                     }
                 }
-                if (p.act == 2)
-                    epi_geglu16(p, m, n0, c, v, g);
-                else
-                    epi16(p, m, sc ? (p.chan_add ? sepi + BN - n0 : nullptr) : chan_row(p, m, img), n0 + c, v,
-                          rv ? res : nullptr, nullptr, bb);
+                const float2 ln = make_float2(0.f, 1.f);  // (LayerNorm-fold GEMMs run unsplit)
+                if (!CONV && p.act == 2) {
+                    epi_geglu16(p, m, n0, c, v, g, sc ? sepi - n0 : p.bias, nullptr, ln);
+                } else {
+                    const float* ca = sc ? (p.chan_add ? sepi + BN - n0 : nullptr) : chan_row(p, m, img);
+                    epi16(p, m, ca, n0 + c, v, rv ? res : nullptr, nullptr, bb, nullptr, ln);
+                }
             }
         }
         __syncwarp();
@@ -999,10 +1104,10 @@ void tile_plan(int m_tiles, int N, int batch, int k_blocks, int bn_fixed, int& b
 
 struct ProfRec {
     int kind;
-    double flops, ms;
+    double flops, bytes, ms;  // bytes: compulsory HBM traffic (every operand read once, output written once)
 };
 bool g_prof_on = false;
-std::vector<ProfRec> g_prof;
+std::vector<ProfRec> g_prof, g_prof_last;
 
 }  // namespace
 
@@ -1021,6 +1126,10 @@ void tc_plan_override(int bn, int splits) {
 // from a CUDA graph on a side stream and timed with events around the replay -- device time
 // per launch, warm inputs (as in the pass), no host gaps, no event nodes between kernels.
 void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::function<void(cudaStream_t)>& launch) {
+    tc_profile_measure(st, kind, flops, kind > 2 ? flops : 0.0, launch);
+}
+void tc_profile_measure(cudaStream_t st, int kind, double flops, double bytes,
+                        const std::function<void(cudaStream_t)>& launch) {
     if (!g_prof_on) return;
     constexpr int kRep = 10;
     CKT(cudaStreamSynchronize(st));
@@ -1042,7 +1151,7 @@ void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::func
     CKT(cudaEventSynchronize(b));
     float ms = 0.f;
     CKT(cudaEventElapsedTime(&ms, a, b));
-    g_prof.push_back({kind, flops, ms / kRep});
+    g_prof.push_back({kind, flops, bytes, ms / kRep});
     if (tc_trace_on())
         fprintf(stderr, "  prof kind=%d %.1f us %.1f %s\n", kind, 1e3 * ms / kRep, flops / (ms / kRep) / 1e9,
                 kind > 2 ? "GB/s" : "TFLOP/s");
@@ -1061,7 +1170,28 @@ void tc_profile_collect(double out[3][3]) {
         out[r.kind][1] += r.ms;
         out[r.kind][2] += r.flops;
     }
+    g_prof_last.swap(g_prof);
     g_prof.clear();
+}
+
+int tc_profile_records(double* out, int cap) {
+    const int n = static_cast<int>(g_prof_last.size());
+    for (int i = 0; i < n && i < cap; ++i) {
+        out[4 * i] = g_prof_last[i].kind;
+        out[4 * i + 1] = g_prof_last[i].flops;
+        out[4 * i + 2] = g_prof_last[i].bytes;
+        out[4 * i + 3] = g_prof_last[i].ms;
+    }
+    return n;
+}
+
+// compulsory HBM bytes of one launch: A and B read once, the stored columns of every output
+// row written once (+ the residual read); bias / per-channel adds are negligible
+static double compulsory_bytes(const TcArgs& p, double a_bytes, double b_bytes, double out_rows) {
+    const int cols = p.n_store ? p.n_store : (p.act == 2 ? p.N / 2 : p.N);
+    const double ob = p.out_f32 ? 4.0 : 2.0;
+    const double rb = p.residual_f32 ? 4.0 : (p.residual ? 2.0 : 0.0);
+    return a_bytes + b_bytes + out_rows * cols * (ob + rb);
 }
 
 // the conditions under which epi16 takes its vectorised path (16-byte residual loads / stores);
@@ -1074,6 +1204,19 @@ static bool vec_epilogue(const TcArgs& p) {
 }
 
 // D = A[M x K] . B[N x K]^T ; A, B bf16 row-major (K contiguous), K % 64 == 0
+// (bn, S) of a GEMM launch: the tuning override, else the measured plan table, else the model
+static void gemm_plan(int M, int N, int K, bool geglu, int& bn, int& S) {
+    S = 1;
+    if (!geglu && bn == 0 && g_override_bn) {
+        bn = g_override_bn;
+        S = std::max(1, g_override_splits);
+    } else if (!(bn == 0 && !geglu && plan_lookup(0, M, N, K, 0, bn, S))) {
+        tile_plan<false>((M + BM - 1) / BM, N, 1, K / BK, bn, bn, S);
+    }
+    if (geglu && g_override_splits) S = g_override_splits;  // the GEGLU tile width stays 256
+    if (S > 1 && (K / BK) / S < 1) S = std::max(1, K / BK);
+}
+
 void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn) {
     tc_gemm_strided(A, K, B, K, M, N, K, p, st, bn);
 }
@@ -1090,15 +1233,8 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
         bn = 256;
     }
     int S = 1;
-    const bool geglu = p.act == 2;
-    if (!geglu && bn == 0 && g_override_bn) {
-        bn = g_override_bn;
-        S = std::max(1, g_override_splits);
-    } else if (!(bn == 0 && !geglu && plan_lookup(0, M, N, K, 0, bn, S))) {
-        tile_plan<false>((M + BM - 1) / BM, N, 1, K / BK, bn, bn, S);
-    }
-    if (geglu && g_override_splits) S = g_override_splits;  // the GEGLU tile width stays 256
-    if (S > 1 && (K / BK) / S < 1) S = std::max(1, K / BK);
+    gemm_plan(M, N, K, p.act == 2, bn, S);
+    if (p.ln_colsum) S = 1;  // LayerNorm fold: the statistics warps see whole rows of A
     const cuuint64_t da[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
     const cuuint64_t sa_[1] = {static_cast<cuuint64_t>(lda) * 2};
     const cuuint64_t sb_[1] = {static_cast<cuuint64_t>(ldb) * 2};
@@ -1135,11 +1271,13 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
         mr = make_map(p.residual, 2, dr, sr, br, CU_TENSOR_MAP_SWIZZLE_NONE);
         p.tma_res = 1;
     }
+    if (p.ln_colsum && (p.chan_add || N % 16 || S != 1))
+        throw std::invalid_argument("tc_gemm: the LayerNorm fold needs an unsplit plan and no chan_add");
     const dim3 grid = launch_grid<false>(p, bn);
     if (tc_trace_on())
         fprintf(stderr, "tc_gemm M=%d N=%d K=%d bn=%d S=%d act=%d grid=%ux%u\n", M, N, K, bn, S, p.act, grid.x, grid.y);
     dispatch<false>(ma, mb, mc, mr, p, grid, bn, st);
-    tc_profile_measure(st, 1, 2.0 * M * N * K,
+    tc_profile_measure(st, 1, 2.0 * M * N * K, compulsory_bytes(p, 2.0 * M * K, 2.0 * N * K, M),
                        [&](cudaStream_t s2) { dispatch<false>(ma, mb, mc, mr, p, grid, bn, s2); });
 }
 
@@ -1150,6 +1288,8 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
 void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin, int Cout, TcArgs p,
                 cudaStream_t st, int bn) {
     if (Cin % BK) throw std::invalid_argument("tc_conv3x3: Cin must be a multiple of 64");
+    if (p.ln_colsum || p.act == 2)
+        throw std::invalid_argument("tc_conv3x3: the LayerNorm fold and GEGLU are GEMM-only");
     // box = bw columns x bh rows of output pixels, bw | W, bw * bh <= 128 and a multiple
     // of 8 (whole 1024-byte swizzle atoms); minimise the MMA rows computed per image
     // (e.g. 24 x 24 -> 24 x 5 boxes: 640 rows, not 768 with 8 x 16)
@@ -1236,6 +1376,8 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     dispatch<true>(ma, mb, mc, mr, p, grid, bn, st);
     // algorithmic FLOPs (a stride-2 conv does a quarter of the work it launches)
     tc_profile_measure(st, 0, 2.0 * batch * H * W * Cout * 9.0 * Cin / (p.sub2 ? 4.0 : 1.0),
+                       compulsory_bytes(p, 2.0 * batch * H * W * Cin, 2.0 * 9 * Cin * Cout,
+                                        static_cast<double>(batch) * H * W / (p.sub2 ? 4.0 : 1.0)),
                        [&](cudaStream_t s2) { dispatch<true>(ma, mb, mc, mr, p, grid, bn, s2); });
 }
 

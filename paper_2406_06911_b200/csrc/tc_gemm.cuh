@@ -41,6 +41,13 @@ struct TcArgs {
                                           //   the TMA-store staging blocks (with tma_store)
     int n_fast = 0;                       // filled by the launcher: persistent tile order n-fastest
                                           //   (A tiles reused while L2-hot when A is the big operand)
+    // LayerNorm fold (GEMM, unsplit, K = the LayerNorm width): A is the RAW LayerNorm input h and
+    // the weights carry the gain (W' = W diag(gamma)).  Two statistics warps read every A tile
+    // from the SMEM ring as the MMAs consume it and reduce each row's sum and (shifted) sum of
+    // squares -> (mean, rstd) per row; the epilogue computes rstd (acc - mean colsum(W')_n) +
+    // bias'_n with bias' = bias + W beta (host-folded).  No producer involvement, no extra pass.
+    const float* ln_colsum = nullptr;     // [N], indexed like bias; non-null enables the fold
+    float ln_eps = 1e-5f;
 };
 
 // per-CTA %globaltimer stamps of the last launch (ADX_TC_TIMELINE builds; zeros otherwise)
@@ -56,6 +63,10 @@ bool tc_trace();
 // (LayerNorm) with their algorithmic bytes are only traced (ADX_TC_TRACE=1).
 void tc_profile_enable(bool on);
 void tc_profile_measure(cudaStream_t st, int kind, double flops, const std::function<void(cudaStream_t)>& launch);
+void tc_profile_measure(cudaStream_t st, int kind, double flops, double bytes,
+                        const std::function<void(cudaStream_t)>& launch);
+// the records of the last collected pass: (kind, flops, compulsory bytes, ms) x n; returns n
+int tc_profile_records(double* out, int cap);
 // per kind: {launches, total ms, total flops}; clears the records
 void tc_profile_collect(double out[3][3]);
 

@@ -85,6 +85,38 @@ bool ends_with(const std::string& s, const char* suf) {
     return s.size() >= n && s.compare(s.size() - n, n, suf) == 0;
 }
 
+// bf16 mode, ADX_LN_FOLD=1: LayerNorm folded into the GEMM that consumes it (statistics warps
+// in the GEMM, gain in the weights).  Off by default: measured slower at c2 / c4
+// than the standalone layernorm_k pass -- the statistics of a tile finish after its MMAs.
+bool ln_fold() {
+    static const bool on = [] {
+        const char* e = getenv("ADX_LN_FOLD");
+        return e && *e == '1';
+    }();
+    return on;
+}
+
+// LN(h) W^T + b = rstd (h W'^T - mean colsum(W')) + (b + W beta) with W' = W diag(gamma):
+// rewrites the consumer weight `w` [rows][K] into W', its bias into b + W beta (created when the
+// layer has none) and returns colsum(W') over the bf16-rounded W' the tensor cores multiply by
+std::vector<float> fold_layer_norm(std::vector<float>& w, int rows, int K, const std::vector<float>& gamma,
+                                   const std::vector<float>& beta, std::vector<float>& bias) {
+    if (bias.empty()) bias.assign(rows, 0.f);
+    std::vector<float> colsum(rows);
+    for (int n = 0; n < rows; ++n) {
+        double b = 0.0, cs = 0.0;
+        float* r = w.data() + static_cast<size_t>(n) * K;
+        for (int k = 0; k < K; ++k) {
+            b += static_cast<double>(r[k]) * beta[k];
+            r[k] *= gamma[k];
+            cs += bf16_to_float(to_bf16_bits(r[k]));
+        }
+        bias[n] = static_cast<float>(bias[n] + b);
+        colsum[n] = static_cast<float>(cs);
+    }
+    return colsum;
+}
+
 void* device_zeros(size_t bytes) {
     void* d = nullptr;
     CKD(cudaMalloc(&d, std::max<size_t>(bytes, 16)));
@@ -170,6 +202,43 @@ void UNetDevice::ensure_stage(int stage) {
     CKD(cudaSetDevice(ordinal_));
     const UNetSpec& sp = d_.spec;
     auto ps = unet_stage_params(d_, stage);
+    if (!exact_ && ln_fold()) {
+        // LayerNorm fold of the transformer blocks: qkv <- ln1, q2 <- ln2, ff1 <- ln3 (weights,
+        // bias and colsum; ff1's GEGLU row interleave below then applies to all three alike)
+        std::map<std::string, UParam*> by;
+        for (auto& p : ps) by[p.name] = &p;
+        std::vector<UParam> extra;
+        for (auto& p : ps) {
+            if (p.name.rfind("tf.", 0) != 0) continue;
+            const char* sufs[3][2] = {{"qkv.w", "ln1"}, {"q2.w", "ln2"}, {"ff1.w", "ln3"}};
+            for (auto& sf : sufs) {
+                if (!ends_with(p.name, sf[0])) continue;
+                const std::string pre = p.name.substr(0, p.name.size() - std::strlen(sf[0]));
+                const std::string layer = p.name.substr(0, p.name.size() - 2);  // drop ".w"
+                auto g = by.find(pre + sf[1] + ".gamma"), b = by.find(pre + sf[1] + ".beta");
+                if (g == by.end() || b == by.end()) throw std::logic_error("unet: missing LayerNorm of " + p.name);
+                const int rows = p.shape[0], K = p.shape[1];
+                auto bi = by.find(layer + ".b");
+                std::vector<float> bias = bi != by.end() ? bi->second->data : std::vector<float>();
+                std::vector<float> cs = fold_layer_norm(p.data, rows, K, g->second->data, b->second->data, bias);
+                if (bi != by.end())
+                    bi->second->data = bias;
+                else
+                    extra.push_back(UParam{layer + ".b", {rows}, bias});
+                extra.push_back(UParam{layer + ".lncs", {rows}, cs});
+            }
+        }
+        for (auto& e : extra) {
+            if (ends_with(e.name, "ff1.lncs")) {  // GEGLU interleave, as for ff1's weight rows and bias
+                const int H = static_cast<int>(e.data.size()) / 2;
+                std::vector<float> perm(e.data.size());
+                for (int t = 0; t < H / 128; ++t)
+                    for (int i = 0; i < 256; ++i) perm[256 * t + i] = e.data[i < 128 ? 128 * t + i : H + 128 * t + i - 128];
+                e.data = perm;
+            }
+            ps.push_back(std::move(e));
+        }
+    }
     for (auto& p : ps) {
         const bool matrix = p.shape.size() == 2;
         const bool ctx_proj = ends_with(p.name, ".k2.w") || ends_with(p.name, ".v2.w");  // precomputed below
@@ -593,6 +662,10 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
     const int L = H * W, B = sp.batch(), BL = B * L, depth = d_.st[stage - 1].attn;
     const long long img = static_cast<long long>(L) * C;
     gn_images(Cat2{x, C, nullptr, 0}, L, F(stage, "tf.gn.gamma"), F(stage, "tf.gn.beta"), 1e-6f, 0, s.a, s, st);
+    // LayerNorm fold: the GEMM reading LN(h) (qkv, q2, ff1) takes h itself, reduces each token's
+    // statistics from its A tiles and has the gain folded into its weights: no standalone
+    // LayerNorm pass, no normalised copy of h
+    const bool fold = ln_fold();
     TcArgs pi;
     pi.bias = F(stage, "tf.proj_in.b");
     pi.out_bf16 = s.b;
@@ -602,12 +675,24 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
         const std::string pre = blk == 0 ? "tf." : "tf.b" + std::to_string(blk) + ".";
         auto Pn = [&](const char* n) { return P(stage, (pre + n).c_str()); };
         auto Fn = [&](const char* n) { return F(stage, (pre + n).c_str()); };
+        // the consumer side: A = h (raw) with the fold, else the normalised copy in s.a
+        auto consume = [&](TcArgs& a, const char* layer, const char* ln) -> const bf16* {
+            if (!fold) {
+                layer_norm(s.b, BL, C, Fn((std::string(ln) + ".gamma").c_str()),
+                           Fn((std::string(ln) + ".beta").c_str()), 1e-5f, s.a, st);
+                return s.a;
+            }
+            a.ln_eps = 1e-5f;
+            a.ln_colsum = Fn((std::string(layer) + ".lncs").c_str());
+            a.bias = Fn((std::string(layer) + ".b").c_str());
+            return s.b;
+        };
         // self attention
-        layer_norm(s.b, BL, C, Fn("ln1.gamma"), Fn("ln1.beta"), 1e-5f, s.a, st);
         TcArgs qk;
         qk.out_bf16 = s.qkv;
         qk.ldo = 3 * C;
-        tc_gemm(s.a, Pn("qkv.w"), BL, 3 * C, C, qk, st);
+        const bf16* a1 = consume(qk, "qkv", "ln1");
+        tc_gemm(a1, Pn("qkv.w"), BL, 3 * C, C, qk, st);
         // self attention of every image in one launch (stacked rows)
         attention(s, s.qkv, 3 * C, s.qkv + C, 3 * C, s.qkv + 2 * C, 3 * C, L, L, C, s.att, st, B);
         TcArgs o1;
@@ -618,11 +703,11 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
         o1.ldo = C;
         tc_gemm(s.att, Pn("o1.w"), BL, C, C, o1, st);
         // cross attention against the fixed context(s)
-        layer_norm(s.b, BL, C, Fn("ln2.gamma"), Fn("ln2.beta"), 1e-5f, s.a, st);
         TcArgs q2;
         q2.out_bf16 = s.qkv;
         q2.ldo = C;
-        tc_gemm(s.a, Pn("q2.w"), BL, C, C, q2, st);
+        const bf16* a2 = consume(q2, "q2", "ln2");
+        tc_gemm(a2, Pn("q2.w"), BL, C, C, q2, st);
         if (sp.contexts() == 1)  // one shared context: every image's queries in one launch
             attention(s, s.qkv, C, st_[stage].k2[blk], C, st_[stage].vt2[blk], C, BL, sp.ctx_len, C, s.att, st);
         else
@@ -637,13 +722,13 @@ void UNetDevice::transformer(int stage, const bf16* x, int H, int W, int C, bf16
         o2.ldo = C;
         tc_gemm(s.att, Pn("o2.w"), BL, C, C, o2, st);
         // GEGLU feed-forward
-        layer_norm(s.b, BL, C, Fn("ln3.gamma"), Fn("ln3.beta"), 1e-5f, s.a, st);
         TcArgs f1;
         f1.bias = Fn("ff1.b");
         f1.act = 2;  // GEGLU in the epilogue: s.ff2 = hidden * gelu(gate), 4C wide
         f1.out_bf16 = s.ff2;
         f1.ldo = 4 * C;
-        tc_gemm(s.a, Pn("ff1.w"), BL, 8 * C, C, f1, st);
+        const bf16* a3 = consume(f1, "ff1", "ln3");
+        tc_gemm(a3, Pn("ff1.w"), BL, 8 * C, C, f1, st);
         TcArgs f2;
         f2.bias = Fn("ff2.b");
         f2.residual = s.b;

@@ -3,6 +3,7 @@ fp32 PyTorch reference on the same bf16-representable inputs.  The kernel
 accumulates in fp32 (TMEM), so only summation order differs: tolerance 2e-3
 relative to the output scale."""
 import ctypes as C
+import math
 
 import numpy as np
 import pytest
@@ -267,4 +268,60 @@ def test_group_norm_matches_fp32_reference(batch, HW, c0, c1, groups, act):
         ref = torch.nn.functional.silu(ref)
     got = bits_f32(out)
     err = np.abs(got - ref.numpy()).max() / np.abs(ref.numpy()).max()
+    assert err < 1e-2, err
+
+
+def geglu_rows(x):
+    """the GEGLU weight-row interleave of csrc/unet_dev.cu: tile t = hidden rows [128t, 128t+128)
+    then their gates H + same"""
+    H = x.shape[0] // 2
+    idx = [128 * t + i if i < 128 else H + 128 * t + i - 128 for t in range(H // 128) for i in range(256)]
+    return x[idx]
+
+
+@pytest.mark.parametrize("M,C,N,geglu,bn", [
+    (1000, 320, 960, 0, 0),       # ragged last m-tile, launcher plan (qkv at level 0)
+    (1000, 320, 960, 0, 160),     # TMA-store epilogue, several tiles per CTA
+    (576, 1280, 1280, 0, 64),     # K = 1280: 20 k-blocks through the ring (q2 at level 2)
+    (4000, 640, 1920, 0, 256),    # register-store epilogue, many tiles per CTA
+    (2304, 640, 5120, 1, 0),      # GEGLU consumer (ff1)
+    (144, 1280, 10240, 1, 0)])    # one partial m-tile
+def test_layer_norm_fold(M, C, N, geglu, bn):
+    """the bf16 mode's LayerNorm-folded GEMM: row statistics reduced from the A tiles in the
+    SMEM ring by the statistics warps, gamma folded into the weights, rstd (acc - mean colsum) +
+    b' in the epilogue -- against LayerNorm(h) W^T + b in fp64; rows with a mean far from zero
+    (the shifted sums); bit-identical across runs"""
+    rng = np.random.default_rng(M + C + N)
+    mu_rows = 3.0 * rng.standard_normal((M, 1))
+    h = bf16_bits((mu_rows + rng.standard_normal((M, C)) * (0.5 + rng.random((M, 1)))).astype(np.float32))
+    gamma = (1 + 0.1 * rng.standard_normal(C)).astype(np.float32)
+    beta = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    W1 = (rng.standard_normal((N, C)) / np.sqrt(C)).astype(np.float32)
+    b1 = (0.1 * rng.standard_normal(N)).astype(np.float32)
+    W1f = bf16_bits(W1 * gamma[None, :])
+    cs = bits_f32(W1f).astype(np.float64).sum(axis=1).astype(np.float32)
+    b1f = (b1 + W1.astype(np.float64) @ beta).astype(np.float32)
+    if geglu:
+        W1f, b1f, cs = geglu_rows(W1f), geglu_rows(b1f), geglu_rows(cs)
+    No = N // 2 if geglu else N
+    outs = []
+    for _ in range(2):
+        y = np.zeros((M, No), np.uint16)
+        _lib.check(adx.lib().adx_tc_ln_fold_bf16(
+            0, M, C, N, h.ctypes.data_as(P16), np.ascontiguousarray(W1f).ctypes.data_as(P16),
+            np.ascontiguousarray(b1f).ctypes.data_as(PF), np.ascontiguousarray(cs).ctypes.data_as(PF), geglu, 1e-5,
+            y.ctypes.data_as(P16), bn, 0, None))
+        outs.append(y)
+    assert np.array_equal(outs[0], outs[1])
+    hf = bits_f32(h).astype(np.float64)
+    mu = hf.mean(axis=1, keepdims=True)
+    ln = (hf - mu) / np.sqrt(((hf - mu) ** 2).mean(axis=1, keepdims=True) + 1e-5) * gamma + beta
+    ref = ln @ W1.astype(np.float64).T + b1
+    if geglu:
+        H = N // 2
+        g = ref[:, H:]
+        ref = ref[:, :H] * 0.5 * g * (1 + np.vectorize(math.erf)(g / math.sqrt(2)))
+    got = bits_f32(outs[0]).astype(np.float64)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    print(f"LN fold M={M} C={C} N={N} geglu={geglu} bn={bn}: rel-L2 {err:.2e}")
     assert err < 1e-2, err
