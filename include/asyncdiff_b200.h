@@ -328,6 +328,10 @@ int adx_unet_context(const adx_model* m, float* out /* batch x ctx_len x ctx_dim
  * act 0 none, 1 SiLU, 2 GEGLU over 256-row tiles of [128 hidden | 128 gate] rows (C is M x N/2) */
 int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B,
                 const float* bias, int act, float* C, int bn, int iters, double* ms_per_iter);
+/* C [M x N] bf16 = [A1 | A2] . B^T + bias with A1 [M x K1], A2 [M x K2] read in place (the
+ * UNet skip concatenation; K1, K2 multiples of 64); bn / splits force the tile plan */
+int adx_tc_gemm_cat_bf16(int ordinal, int M, int N, int K1, int K2, const uint16_t* A1, const uint16_t* A2,
+                         const uint16_t* B, const float* bias, uint16_t* out, int bn, int splits);
 /* the bf16 mode's LayerNorm-folded GEMM (kernel test): y = rstd_m (H . W1'^T - mean_m colsum1) +
  * bias1 with the row statistics of H [M x C] (bf16) reduced inside the GEMM, W1' [N x C] =
  * W1 diag(gamma) and bias1 = b + W1 beta folded by the caller (geglu: N = 2H rows tile-

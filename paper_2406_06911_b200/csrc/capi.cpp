@@ -1067,6 +1067,34 @@ int adx_tc_gemm_bf16(int ordinal, int M, int N, int K, const uint16_t* A, const 
     });
 }
 
+int adx_tc_gemm_cat_bf16(int ordinal, int M, int N, int K1, int K2, const uint16_t* A1, const uint16_t* A2,
+                         const uint16_t* B, const float* bias, uint16_t* out, int bn, int splits) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        const int K = K1 + K2;
+        DevBuf a1(static_cast<size_t>(M) * K1 * 2), a2(static_cast<size_t>(M) * K2 * 2),
+            b(static_cast<size_t>(N) * K * 2), o(static_cast<size_t>(M) * N * 2), bi(static_cast<size_t>(N) * 4);
+        CKC(cudaMemcpy(a1.p, A1, static_cast<size_t>(M) * K1 * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(a2.p, A2, static_cast<size_t>(M) * K2 * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(b.p, B, static_cast<size_t>(N) * K * 2, cudaMemcpyHostToDevice));
+        if (bias) CKC(cudaMemcpy(bi.p, bias, static_cast<size_t>(N) * 4, cudaMemcpyHostToDevice));
+        adx::TcArgs p;
+        p.bias = bias ? static_cast<const float*>(bi.p) : nullptr;
+        p.out_bf16 = static_cast<__nv_bfloat16*>(o.p);
+        p.ldo = N;
+        if (bn) adx::tc_plan_override(bn, std::max(1, splits));
+        try {
+            adx::tc_gemm_cat(a1.p, K1, a2.p, K2, b.p, M, N, p, 0, 0);
+            CKC(cudaDeviceSynchronize());
+        } catch (...) {
+            adx::tc_plan_override(0, 0);
+            throw;
+        }
+        if (bn) adx::tc_plan_override(0, 0);
+        CKC(cudaMemcpy(out, o.p, static_cast<size_t>(M) * N * 2, cudaMemcpyDeviceToHost));
+    });
+}
+
 int adx_tc_ln_fold_bf16(int ordinal, int M, int C, int N, const uint16_t* H, const uint16_t* W1, const float* bias1,
                         const float* colsum1, int geglu, float eps, uint16_t* y_out, int bn, int iters,
                         double* ms_per_iter) {

@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        if (p.k_split) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmR)) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tptr)),
@@ -579,6 +580,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                     const int tap = kb / cpb, cb = kb - tap * cpb;
                     const int dr = tap / 3 - 1, ds = tap % 3 - 1;
                     tma4d(sA + s * A_BYTES, &tmA, cb * BK, w0 + ds, h0 + dr, img, &full[s]);
+                } else if (p.k_split && kb * BK >= p.k_split) {  // A = [A1 | A2] along K: A2 rides in tmR
+                    tma2d(sA + s * A_BYTES, &tmR, kb * BK - p.k_split, tile_m * BM, &full[s]);
                 } else {
                     tma2d(sA + s * A_BYTES, &tmA, kb * BK, tile_m * BM, &full[s]);
                 }
@@ -1221,9 +1224,26 @@ void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaSt
     tc_gemm_strided(A, K, B, K, M, N, K, p, st, bn);
 }
 
+static void gemm_impl(const void* A, long long lda, const void* A2, long long lda2, int k_split, const void* B,
+                      long long ldb, int M, int N, int K, TcArgs p, cudaStream_t st, int bn);
+
 void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,
                      cudaStream_t st, int bn) {
+    gemm_impl(A, lda, nullptr, 0, 0, B, ldb, M, N, K, p, st, bn);
+}
+
+void tc_gemm_cat(const void* A1, int K1, const void* A2, int K2, const void* B, int M, int N, TcArgs p,
+                 cudaStream_t st, int bn) {
+    gemm_impl(A1, K1, A2, K2, K1, B, K1 + K2, M, N, K1 + K2, p, st, bn);
+}
+
+// A2 != nullptr: the A operand is [A1 | A2] concatenated along K at column k_split (A1 rows of
+// lda elements, A2 rows of lda2); the A2 tensor map takes the residual map's slot (no residual)
+static void gemm_impl(const void* A, long long lda, const void* A2, long long lda2, int k_split, const void* B,
+                      long long ldb, int M, int N, int K, TcArgs p, cudaStream_t st, int bn) {
     if (K % BK) throw std::invalid_argument("tc_gemm: K must be a multiple of 64");
+    if (A2 && (k_split % BK || k_split <= 0 || k_split >= K || lda2 % 8 || p.residual || p.residual_f32))
+        throw std::invalid_argument("tc_gemm_cat: K1, K2 must be multiples of 64 and the GEMM has no residual");
     if ((lda | ldb) % 8) throw std::invalid_argument("tc_gemm: row strides must be multiples of 8 elements");
     if (p.act == 2) {  // fused GEGLU (see the epilogue): fixed 256-wide tiles of [128 hidden | 128 gate]
         if (bn && bn != 256) throw std::invalid_argument("tc_gemm: GEGLU epilogue needs 256-wide N tiles");
@@ -1241,7 +1261,9 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
     const cuuint32_t ba[2] = {BK, BM};
     const cuuint64_t db[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N)};
     const cuuint32_t bb[2] = {BK, static_cast<cuuint32_t>(bn)};
-    const CUtensorMap ma = make_map(A, 2, da, sa_, ba), mb = make_map(B, 2, db, sb_, bb);
+    const cuuint64_t da1[2] = {static_cast<cuuint64_t>(A2 ? k_split : K), static_cast<cuuint64_t>(M)};
+    const CUtensorMap ma = make_map(A, 2, da1, sa_, ba), mb = make_map(B, 2, db, sb_, bb);
+    p.k_split = A2 ? k_split : 0;
     p.M = M;
     p.N = N;
     p.k_blocks = K / BK;
@@ -1270,6 +1292,11 @@ void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb,
         const cuuint32_t br[2] = {16, 32};
         mr = make_map(p.residual, 2, dr, sr, br, CU_TENSOR_MAP_SWIZZLE_NONE);
         p.tma_res = 1;
+    }
+    if (A2) {  // (no residual: the map slot is free)
+        const cuuint64_t da2[2] = {static_cast<cuuint64_t>(K - k_split), static_cast<cuuint64_t>(M)};
+        const cuuint64_t sa2[1] = {static_cast<cuuint64_t>(lda2) * 2};
+        mr = make_map(A2, 2, da2, sa2, ba);
     }
     if (p.ln_colsum && (p.chan_add || N % 16 || S != 1))
         throw std::invalid_argument("tc_gemm: the LayerNorm fold needs an unsplit plan and no chan_add");

@@ -39,6 +39,7 @@ struct TcArgs {
                                           //   chunk from SMEM by the TMA (GEMM, S = 1, BN <= 192)
     int tma_res = 0;                      // filled by the launcher: the bf16 residual arrives by TMA in
                                           //   the TMA-store staging blocks (with tma_store)
+    int k_split = 0;                      // filled by tc_gemm_cat: A = [A1 | A2] along K, A2 from column k_split
     int n_fast = 0;                       // filled by the launcher: persistent tile order n-fastest
                                           //   (A tiles reused while L2-hot when A is the big operand)
     // LayerNorm fold (GEMM, unsplit, K = the LayerNorm width): A is the RAW LayerNorm input h and
@@ -75,6 +76,10 @@ void tc_profile_collect(double out[3][3]);
 // thread-block cluster and reduced deterministically over DSMEM
 void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaStream_t st, int bn = 0);
 // same with explicit row strides (elements; multiples of 8) -- e.g. one head's slice of a packed QKV
+// C = [A1 | A2] . B^T with A1 [M x K1] and A2 [M x K2] (dense rows) read in place: the channel
+// concatenation of a UNet skip never materialised (K1, K2 multiples of 64; no residual)
+void tc_gemm_cat(const void* A1, int K1, const void* A2, int K2, const void* B, int M, int N, TcArgs p,
+                 cudaStream_t st, int bn = 0);
 void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,
                      cudaStream_t st, int bn = 0);
 // conv3x3 / stride 1 / pad 1 over NHWC bf16 X [batch][H][W][Cin], weights Wt [Cout][3*3*Cin]

@@ -814,16 +814,18 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
             gn_images(Cat2{sc.b, C, nullptr, 0}, HW, F(stage, "gn2.gamma"), F(stage, "gn2.beta"), 1e-5f, 1, sc.a, sc, st);
             const bf16* res = x0;
             if (cin != C) {
-                const bf16* xin = x0;
-                if (s.cskip) {
-                    concat_channels(Cat2{x0, s.cin, x1, s.cskip}, static_cast<long long>(B) * HW, sc.c, st);
-                    xin = sc.c;
-                }
                 TcArgs sh;
                 sh.bias = F(stage, "short.b");
                 sh.out_bf16 = sc.r;
                 sh.ldo = C;
-                tc_gemm(xin, P(stage, "short.w"), B * HW, C, cin, sh, st);
+                if (s.cskip && s.cin % 64 == 0 && s.cskip % 64 == 0)  // [x | skip] read in place along K
+                    tc_gemm_cat(x0, s.cin, x1, s.cskip, P(stage, "short.w"), B * HW, C, sh, st);
+                else if (s.cskip) {
+                    concat_channels(Cat2{x0, s.cin, x1, s.cskip}, static_cast<long long>(B) * HW, sc.c, st);
+                    tc_gemm(sc.c, P(stage, "short.w"), B * HW, C, cin, sh, st);
+                } else {
+                    tc_gemm(x0, P(stage, "short.w"), B * HW, C, cin, sh, st);
+                }
                 res = sc.r;
             }
             TcArgs c2;

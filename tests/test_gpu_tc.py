@@ -325,3 +325,25 @@ def test_layer_norm_fold(M, C, N, geglu, bn):
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     print(f"LN fold M={M} C={C} N={N} geglu={geglu} bn={bn}: rel-L2 {err:.2e}")
     assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("M,N,K1,K2,bn,S", [(2304, 640, 640, 640, 0, 0), (9216, 320, 320, 320, 160, 1),
+                                          (576, 1280, 1280, 1280, 64, 4), (1000, 320, 640, 320, 80, 2)])
+def test_tc_gemm_cat_equals_concatenated(M, N, K1, K2, bn, S):
+    """the skip concatenation read in place along K (A2 by its own tensor map) is bit-identical to
+    the GEMM over the materialised [A1 | A2] (same k-block order, split-K included)"""
+    rng = np.random.default_rng(M + N + K1 + K2)
+    A1 = bf16_bits(rng.standard_normal((M, K1)).astype(np.float32))
+    A2 = bf16_bits(rng.standard_normal((M, K2)).astype(np.float32))
+    B = bf16_bits((rng.standard_normal((N, K1 + K2)) / 30).astype(np.float32))
+    bias = rng.standard_normal(N).astype(np.float32)
+    out = np.zeros((M, N), np.uint16)
+    _lib.check(adx.lib().adx_tc_gemm_cat_bf16(0, M, N, K1, K2, A1.ctypes.data_as(P16), A2.ctypes.data_as(P16),
+                                              B.ctypes.data_as(P16), bias.ctypes.data_as(PF), out.ctypes.data_as(P16),
+                                              bn, S))
+    A = np.ascontiguousarray(np.concatenate([A1, A2], axis=1))
+    ref = np.zeros((M, N), np.uint16)
+    _lib.check(adx.lib().adx_tc_gemm_bf16(0, M, N, K1 + K2, A.ctypes.data_as(P16), B.ctypes.data_as(P16),
+                                          bias.ctypes.data_as(PF), None, 0, ref.ctypes.data_as(P16), N, bn, S, 0,
+                                          None))
+    assert np.array_equal(out, ref)
