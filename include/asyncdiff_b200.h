@@ -328,6 +328,11 @@ int adx_unet_context(const adx_model* m, float* out /* batch x ctx_len x ctx_dim
  * act 0 none, 1 SiLU, 2 GEGLU over 256-row tiles of [128 hidden | 128 gate] rows (C is M x N/2) */
 int adx_tc_gemm(int ordinal, int M, int N, int K, const uint16_t* A, const uint16_t* B,
                 const float* bias, int act, float* C, int bn, int iters, double* ms_per_iter);
+/* stride-2 conv3x3 (pad 1), NHWC bf16: out [batch][H/2][W/2][Cout] from X [batch][H][W][Cin] (H, W
+ * even); the A boxes are read with TMA element strides of 2 (no discarded output rows) */
+int adx_tc_conv3x3_s2_bf16(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X,
+                           const uint16_t* Wt, const float* bias, uint16_t* out, int bn, int splits, int iters,
+                           double* ms_per_iter);
 /* C [M x N] bf16 = [A1 | A2] . B^T + bias with A1 [M x K1], A2 [M x K2] read in place (the
  * UNet skip concatenation; K1, K2 multiples of 64); bn / splits force the tile plan */
 int adx_tc_gemm_cat_bf16(int ordinal, int M, int N, int K1, int K2, const uint16_t* A1, const uint16_t* A2,

@@ -1164,6 +1164,38 @@ int adx_tc_conv3x3_bf16(int ordinal, int batch, int H, int W, int Cin, int Cout,
     });
 }
 
+int adx_tc_conv3x3_s2_bf16(int ordinal, int batch, int H, int W, int Cin, int Cout, const uint16_t* X,
+                           const uint16_t* Wt, const float* bias, uint16_t* out, int bn, int splits, int iters,
+                           double* ms_per_iter) {
+    return guard([&] {
+        CKC(cudaSetDevice(ordinal));
+        const size_t nx = static_cast<size_t>(batch) * H * W * Cin, nw = static_cast<size_t>(Cout) * 9 * Cin,
+                     no = static_cast<size_t>(batch) * (H / 2) * (W / 2) * Cout;
+        DevBuf x(nx * 2), w(nw * 2), o(no * 2), bi(static_cast<size_t>(Cout) * 4);
+        CKC(cudaMemcpy(x.p, X, nx * 2, cudaMemcpyHostToDevice));
+        CKC(cudaMemcpy(w.p, Wt, nw * 2, cudaMemcpyHostToDevice));
+        if (bias) CKC(cudaMemcpy(bi.p, bias, static_cast<size_t>(Cout) * 4, cudaMemcpyHostToDevice));
+        adx::TcArgs p;
+        p.bias = bias ? static_cast<const float*>(bi.p) : nullptr;
+        p.out_bf16 = static_cast<__nv_bfloat16*>(o.p);
+        p.ldo = Cout;
+        p.sub2 = 1;
+        if (bn) adx::tc_plan_override(bn, std::max(1, splits));
+        try {
+            adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, 0);
+            CKC(cudaDeviceSynchronize());
+            if (iters > 0 && ms_per_iter)
+                *ms_per_iter = time_graph_ms(
+                    [&](cudaStream_t st) { adx::tc_conv3x3(x.p, w.p, batch, H, W, Cin, Cout, p, st); }, iters);
+        } catch (...) {
+            adx::tc_plan_override(0, 0);
+            throw;
+        }
+        if (bn) adx::tc_plan_override(0, 0);
+        CKC(cudaMemcpy(out, o.p, no * 2, cudaMemcpyDeviceToHost));
+    });
+}
+
 // GroupNorm(+SiLU) over a (one- or two-segment) channel concat of bf16 NHWC images:
 // x0 [batch][HW][c0], x1 [batch][HW][c1] (NULL when c1 == 0) -> out [batch][HW][c0 + c1]
 int adx_group_norm_bf16(int ordinal, int batch, int HW, int c0, int c1, int groups, const uint16_t* x0,

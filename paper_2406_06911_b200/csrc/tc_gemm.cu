@@ -209,12 +209,9 @@ __device__ __forceinline__ bool row_to_m(const TcArgs& p, int tile_m, int img, i
     if constexpr (CONV) {
         const int hh = h0 + row / p.box_w, ww = w0 + row % p.box_w;
         // rows past the box (box_w * box_h < 128) hold stale SMEM: computed, never stored
-        bool valid = row < p.box_w * p.box_h && hh < p.H && ww < p.W;
+        // (stride-2 convs: H, W are the output grid's; the TMA box already skipped the odd pixels)
+        const bool valid = row < p.box_w * p.box_h && hh < p.H && ww < p.W;
         m = (static_cast<long long>(img) * p.H + hh) * p.W + ww;
-        if (p.sub2) {  // stride-2 conv: keep even pixels, write the half-resolution grid
-            valid = valid && !(hh & 1) && !(ww & 1);
-            m = (static_cast<long long>(img) * (p.H / 2) + hh / 2) * (p.W / 2) + ww / 2;
-        }
         return valid;
     } else {
         m = static_cast<long long>(tile_m) * BM + row;
@@ -579,7 +576,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                     const int cpb = p.cin / BK;
                     const int tap = kb / cpb, cb = kb - tap * cpb;
                     const int dr = tap / 3 - 1, ds = tap % 3 - 1;
-                    tma4d(sA + s * A_BYTES, &tmA, cb * BK, w0 + ds, h0 + dr, img, &full[s]);
+                    const int st2 = p.sub2 ? 2 : 1;  // stride 2: input pixel (2h + dr, 2w + ds)
+                    tma4d(sA + s * A_BYTES, &tmA, cb * BK, st2 * w0 + ds, st2 * h0 + dr, img, &full[s]);
                 } else if (p.k_split && kb * BK >= p.k_split) {  // A = [A1 | A2] along K: A2 rides in tmR
                     tma2d(sA + s * A_BYTES, &tmR, kb * BK - p.k_split, tile_m * BM, &full[s]);
                 } else {
@@ -943,9 +941,12 @@ EncodeTiledFn encode_fn() {
 }
 
 CUtensorMap make_map(const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-                     const cuuint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                     const cuuint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                     const cuuint32_t* elem_strides = nullptr) {
     CUtensorMap m;
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (elem_strides)
+        for (int i = 0; i < rank; ++i) es[i] = elem_strides[i];
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims,
                                    strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1317,6 +1318,14 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     if (Cin % BK) throw std::invalid_argument("tc_conv3x3: Cin must be a multiple of 64");
     if (p.ln_colsum || p.act == 2)
         throw std::invalid_argument("tc_conv3x3: the LayerNorm fold and GEGLU are GEMM-only");
+    // stride 2 (p.sub2): the output grid is (H/2, W/2) and the A boxes are read with TMA element
+    // strides of 2 along W and H from input pixel (2 h + dr, 2 w + ds): no discarded rows
+    const int Hi = H, Wi = W;
+    if (p.sub2) {
+        if ((H | W) & 1) throw std::invalid_argument("tc_conv3x3: stride 2 needs even H and W");
+        H /= 2;
+        W /= 2;
+    }
     // box = bw columns x bh rows of output pixels, bw | W, bw * bh <= 128 and a multiple
     // of 8 (whole 1024-byte swizzle atoms); minimise the MMA rows computed per image
     // (e.g. 24 x 24 -> 24 x 5 boxes: 640 rows, not 768 with 8 x 16)
@@ -1341,19 +1350,21 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     if (bn == 0 && g_override_bn) {
         bn = g_override_bn;
         S = std::max(1, g_override_splits);
-    } else if (!(bn == 0 && batch == 1 && plan_lookup(1, H, W, Cin, Cout, bn, S))) {
+    } else if (!(bn == 0 && batch == 1 && plan_lookup(p.sub2 ? 2 : 1, Hi, Wi, Cin, Cout, bn, S))) {
         tile_plan<true>(m_tiles, Cout, batch, 9 * Cin / BK, bn, bn, S);
     }
-    const cuuint64_t dx[4] = {static_cast<cuuint64_t>(Cin), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+    const cuuint64_t dx[4] = {static_cast<cuuint64_t>(Cin), static_cast<cuuint64_t>(Wi), static_cast<cuuint64_t>(Hi),
                               static_cast<cuuint64_t>(batch)};
-    const cuuint64_t sx[3] = {static_cast<cuuint64_t>(Cin) * 2, static_cast<cuuint64_t>(W) * Cin * 2,
-                              static_cast<cuuint64_t>(H) * W * Cin * 2};
-    const cuuint32_t bx[4] = {BK, static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh), 1};
+    const cuuint64_t sx[3] = {static_cast<cuuint64_t>(Cin) * 2, static_cast<cuuint64_t>(Wi) * Cin * 2,
+                              static_cast<cuuint64_t>(Hi) * Wi * Cin * 2};
+    const cuuint32_t f2 = p.sub2 ? 2 : 1;  // box traversal spans f2 x the loaded pixels
+    const cuuint32_t bx[4] = {BK, static_cast<cuuint32_t>(bw) * f2, static_cast<cuuint32_t>(bh) * f2, 1};
+    const cuuint32_t ex[4] = {1, f2, f2, 1};
     const int K = 9 * Cin;
     const cuuint64_t dw[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(Cout)};
     const cuuint64_t sw[1] = {static_cast<cuuint64_t>(K) * 2};
     const cuuint32_t bwb[2] = {BK, static_cast<cuuint32_t>(bn)};
-    const CUtensorMap ma = make_map(X, 4, dx, sx, bx), mb = make_map(Wt, 2, dw, sw, bwb);
+    const CUtensorMap ma = make_map(X, 4, dx, sx, bx, CU_TENSOR_MAP_SWIZZLE_128B, ex), mb = make_map(Wt, 2, dw, sw, bwb);
     p.M = batch * H * W;
     p.N = Cout;
     p.k_blocks = K / BK;
@@ -1366,13 +1377,13 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     p.m_tiles = m_tiles;
     p.n_tiles = (Cout + bn - 1) / bn;
     p.batch = batch;
-    p.n_fast = S == 1 && p.n_tiles > 1 && n_fast_order(2LL * batch * H * W * Cin);
+    p.n_fast = S == 1 && p.n_tiles > 1 && n_fast_order(2LL * batch * Hi * Wi * Cin);
     // bf16 NHWC output through SMEM + 4-D TMA bulk stores when a warp's 32 tile rows are one
     // box of pixels (32 | bw or bw | 32, full 128-pixel boxes): the row-per-thread epilogue
     // otherwise issues 32 row-scattered 16-byte stores per warp instruction
     CUtensorMap mc = ma;
     p.tma_store = 0;
-    if (tma_store_enabled() && S == 1 && bn <= 192 && p.out_bf16 && !p.out_f32 && !p.n_store && !p.sub2 &&
+    if (tma_store_enabled() && S == 1 && bn <= 192 && p.out_bf16 && !p.out_f32 && !p.n_store &&
         bw * bh == BM && (bw % 32 == 0 || 32 % bw == 0) && Cout % 16 == 0 && p.ldo % 8 == 0 &&
         (reinterpret_cast<uintptr_t>(p.out_bf16) & 15) == 0 && vec_epilogue(p)) {
         const int bx = bw < 32 ? bw : 32;
@@ -1401,10 +1412,10 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
         fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u tma_store=%d\n", H, W, Cin, Cout, bw,
                 bh, bn, S, grid.x, grid.y, grid.z, p.tma_store);
     dispatch<true>(ma, mb, mc, mr, p, grid, bn, st);
-    // algorithmic FLOPs (a stride-2 conv does a quarter of the work it launches)
-    tc_profile_measure(st, 0, 2.0 * batch * H * W * Cout * 9.0 * Cin / (p.sub2 ? 4.0 : 1.0),
-                       compulsory_bytes(p, 2.0 * batch * H * W * Cin, 2.0 * 9 * Cin * Cout,
-                                        static_cast<double>(batch) * H * W / (p.sub2 ? 4.0 : 1.0)),
+    // algorithmic FLOPs and compulsory bytes (H, W: the output grid; the input is Hi x Wi)
+    tc_profile_measure(st, 0, 2.0 * batch * H * W * Cout * 9.0 * Cin,
+                       compulsory_bytes(p, 2.0 * batch * Hi * Wi * Cin, 2.0 * 9 * Cin * Cout,
+                                        static_cast<double>(batch) * H * W),
                        [&](cudaStream_t s2) { dispatch<true>(ma, mb, mc, mr, p, grid, bn, s2); });
 }
 

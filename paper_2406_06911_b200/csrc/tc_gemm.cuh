@@ -32,7 +32,7 @@ struct TcArgs {
     __nv_bfloat16* out_bf16 = nullptr;    // exactly one of out_bf16 / out_f32
     float* out_f32 = nullptr;
     long long ldo = 0;
-    int sub2 = 0;                         // conv: write only even (h, w) at (h/2, w/2) -> stride-2 conv
+    int sub2 = 0;                         // conv: stride 2 (output H/2 x W/2; A read with TMA element strides)
     int n_store = 0;                      // store only the first n_store columns (0: all N)
     int splits = 1;                       // filled by the launcher: split-K factor (cluster size)
     int tma_store = 0;                    // filled by the launcher: bf16 output written per 32x16

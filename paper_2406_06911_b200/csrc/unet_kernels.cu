@@ -334,6 +334,8 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
     // header words 18-19 (bytes 72-79): clear of gn_stats' ticket counters (words 0-15)
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(scratch + 9);
     float2* part = scratch + 16;
+    // (gamma, beta) staged now: their loads overlap the statistics instead of following the fold
+    for (int c = threadIdx.x; c < C; c += blockDim.x) ab[c] = make_float2(__ldg(gamma + c), __ldg(beta + c));
     if (r < rpb) {
         float s[8], ss[8];
 #pragma unroll
@@ -450,7 +452,8 @@ __global__ void gn_fused(Cat2T<T> x, int HW, int groups, int chunk_pix, const fl
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
         const int g = c / cpg;
         const double rs = st[2 * g + 1];
-        ab[c] = make_float2(static_cast<float>(rs * gamma[c]), static_cast<float>(beta[c] - st[2 * g] * rs * gamma[c]));
+        const float2 gb = ab[c];
+        ab[c] = make_float2(static_cast<float>(rs * gb.x), static_cast<float>(gb.y - st[2 * g] * rs * gb.x));
     }
     __syncthreads();
     gn_stamp(5);
@@ -1105,6 +1108,9 @@ __global__ void __launch_bounds__(256) gn_cluster(Cat2T<T> x, int HW, int groups
     float2* ab = reinterpret_cast<float2*>(red + 24);  // [cpg] (scale, shift)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long base = static_cast<long long>(n) * HW + p0;
+    // this thread's (gamma, beta), requested before the statistics (not after the cluster fold)
+    const float gm = threadIdx.x < cpg ? __ldg(gamma + g * cpg + threadIdx.x) : 0.f;
+    const float bt = threadIdx.x < cpg ? __ldg(beta + g * cpg + threadIdx.x) : 0.f;
     float s = 0.f, ss = 0.f;
     const int total = npx * np2;
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
@@ -1147,9 +1153,8 @@ __global__ void __launch_bounds__(256) gn_cluster(Cat2T<T> x, int HW, int groups
     }
     __syncthreads();
     if (threadIdx.x < cpg) {
-        const int c = g * cpg + threadIdx.x;
         const double rs = red[19];
-        ab[threadIdx.x] = make_float2(static_cast<float>(rs * gamma[c]), static_cast<float>(beta[c] - red[18] * rs * gamma[c]));
+        ab[threadIdx.x] = make_float2(static_cast<float>(rs * gm), static_cast<float>(bt - red[18] * rs * gm));
     }
     __syncthreads();
     for (int e = threadIdx.x; e < total; e += blockDim.x) {

@@ -347,3 +347,23 @@ def test_tc_gemm_cat_equals_concatenated(M, N, K1, K2, bn, S):
                                           bias.ctypes.data_as(PF), None, 0, ref.ctypes.data_as(P16), N, bn, S, 0,
                                           None))
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("b,H,W,Ci,Co,bn,S", [(1, 96, 96, 320, 320, 0, 0), (1, 48, 48, 640, 640, 0, 0),
+                                             (1, 24, 24, 1280, 1280, 0, 0), (2, 16, 40, 64, 128, 64, 2),
+                                             (1, 12, 12, 128, 64, 32, 1)])
+def test_tc_conv3x3_stride2_matches_fp32_reference(b, H, W, Ci, Co, bn, S):
+    """the stride-2 conv (UNet downsample) with strided TMA boxes vs torch conv2d(stride 2, pad 1)"""
+    rng = np.random.default_rng(b * H * W + Ci + Co)
+    X = bf16_bits(rng.standard_normal((b, H, W, Ci)).astype(np.float32))
+    Wt = bf16_bits((rng.standard_normal((Co, 3, 3, Ci)) / np.sqrt(9 * Ci)).astype(np.float32))
+    bias = rng.standard_normal(Co).astype(np.float32)
+    out = np.zeros((b, H // 2, W // 2, Co), np.uint16)
+    _lib.check(adx.lib().adx_tc_conv3x3_s2_bf16(0, b, H, W, Ci, Co, X.ctypes.data_as(P16), Wt.ctypes.data_as(P16),
+                                                bias.ctypes.data_as(PF), out.ctypes.data_as(P16), bn, S, 0, None))
+    x = torch.from_numpy(bits_f32(X)).permute(0, 3, 1, 2)
+    w = torch.from_numpy(bits_f32(Wt)).permute(0, 3, 1, 2)
+    ref = torch.nn.functional.conv2d(x, w, torch.from_numpy(bias), stride=2, padding=1).permute(0, 2, 3, 1).numpy()
+    got = bits_f32(out)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 1e-2, err
