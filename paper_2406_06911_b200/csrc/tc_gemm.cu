@@ -437,7 +437,13 @@ constexpr size_t kGemmSmem() {
 // epilogue warps: EPW / 4 per TMEM lane quadrant, each over its share of the tile's
 // 16-column chunks (more loads / stores in flight for the 1-tile-per-CTA small GEMMs)
 constexpr int EPW = EPW_;
-constexpr int kStatWarps = 2;  // LayerNorm-fold statistics warps (idle otherwise); 384 threads keep 168 regs
+// LayerNorm-fold statistics warps: compiled in only with -DADX_TC_STATW=2 (384 threads, still 168
+// registers).  The default build has none: the fold measured slower than the standalone LayerNorm
+// and the two idle warps alone cost 0.2-0.5% of a pass
+#ifndef ADX_TC_STATW
+#define ADX_TC_STATW 0
+#endif
+constexpr int kStatWarps = ADX_TC_STATW;
 constexpr int kGemmThreads = 64 + 32 * EPW + 32 * kStatWarps;
 __device__ __forceinline__ void epi_chunks(int nch, int part, int& c0, int& c1) {
     constexpr int P = EPW / 4;
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
     // per accumulator: [bias | chan_add] of the tile's BN columns, staged by the epilogue warps
     float* sepi = reinterpret_cast<float*>(sB + STAGES * B_BYTES + 256 + EPW * kStageChunks<BN>() * 1024);
     float2* sstat = reinterpret_cast<float2*>(sepi + 4 * BN);  // [2 accumulators][BM rows] (mean, rstd)
-    const bool lnf = !CONV && p.ln_colsum != nullptr;
+    const bool lnf = !CONV && kStatWarps > 0 && p.ln_colsum != nullptr;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // Work units.  S == 1: persistent -- CTA b takes output tiles b, b + G, ... (m fastest,
@@ -647,7 +653,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                 }
             }
             float* sb = sepi + acc * 2 * BN;
-            const bool stage_cols = (!CONV || p.act != 2) && !p.chan_add_rows;  // (S > 1: one tile, acc 0)
+#ifndef ADX_TC_GEGLU_STAGE
+#define ADX_TC_GEGLU_STAGE 1
+#endif
+            const bool stage_cols = (ADX_TC_GEGLU_STAGE ? (!CONV || p.act != 2) : p.act != 2) &&
+                                    !p.chan_add_rows;  // (S > 1: one tile, acc 0)
             if (stage_cols) {
                 const float* car = p.chan_add ? p.chan_add + static_cast<long long>(p.chan_add_shared ? 0 : img) * p.N
                                               : nullptr;
@@ -688,10 +698,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                     int cb, ce;
                     epi_chunks(BN / 32, part, cb, ce);
                     for (int c = cb; c < ce; c += 16) {
+                        // hidden and gate columns: two TMEM loads, one wait
+                        uint32_t rv[16], rg[16];
+                        tmem_ld16_nowait(trow + c, rv);
+                        tmem_ld16_nowait(trow + BN / 2 + c, rg);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                         float v[16], g[16];
-                        tmem_ld16(trow + c, v);
-                        tmem_ld16(trow + BN / 2 + c, g);
-                        if (valid) epi_geglu16(p, m, n0, c, v, g, sb - n0, p.ln_colsum ? sb + BN - n0 : nullptr, ln);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(rv[i]), g[i] = __uint_as_float(rg[i]);
+                        if (valid)
+                            epi_geglu16(p, m, n0, c, v, g, stage_cols ? sb - n0 : p.bias,
+                                        p.ln_colsum ? (stage_cols ? sb + BN - n0 : p.ln_colsum) : nullptr, ln);
                     }
                 } else {
                     // the residual of chunk c+16 is requested before chunk c's TMEM read and
@@ -1228,6 +1245,8 @@ void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaSt
 static void gemm_impl(const void* A, long long lda, const void* A2, long long lda2, int k_split, const void* B,
                       long long ldb, int M, int N, int K, TcArgs p, cudaStream_t st, int bn);
 
+bool tc_ln_fold_supported() { return kStatWarps > 0; }
+
 void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,
                      cudaStream_t st, int bn) {
     gemm_impl(A, lda, nullptr, 0, 0, B, ldb, M, N, K, p, st, bn);
@@ -1299,6 +1318,8 @@ static void gemm_impl(const void* A, long long lda, const void* A2, long long ld
         const cuuint64_t sa2[1] = {static_cast<cuuint64_t>(lda2) * 2};
         mr = make_map(A2, 2, da2, sa2, ba);
     }
+    if (p.ln_colsum && !tc_ln_fold_supported())
+        throw std::invalid_argument("tc_gemm: the LayerNorm fold needs a build with -DADX_TC_STATW=2");
     if (p.ln_colsum && (p.chan_add || N % 16 || S != 1))
         throw std::invalid_argument("tc_gemm: the LayerNorm fold needs an unsplit plan and no chan_add");
     const dim3 grid = launch_grid<false>(p, bn);

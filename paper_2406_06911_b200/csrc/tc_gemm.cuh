@@ -78,6 +78,8 @@ void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaSt
 // same with explicit row strides (elements; multiples of 8) -- e.g. one head's slice of a packed QKV
 // C = [A1 | A2] . B^T with A1 [M x K1] and A2 [M x K2] (dense rows) read in place: the channel
 // concatenation of a UNet skip never materialised (K1, K2 multiples of 64; no residual)
+// whether this build has the LayerNorm-fold statistics warps (-DADX_TC_STATW=2)
+bool tc_ln_fold_supported();
 void tc_gemm_cat(const void* A1, int K1, const void* A2, int K2, const void* B, int M, int N, TcArgs p,
                  cudaStream_t st, int bn = 0);
 void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,

@@ -85,13 +85,14 @@ bool ends_with(const std::string& s, const char* suf) {
     return s.size() >= n && s.compare(s.size() - n, n, suf) == 0;
 }
 
-// bf16 mode, ADX_LN_FOLD=1: LayerNorm folded into the GEMM that consumes it (statistics warps
-// in the GEMM, gain in the weights).  Off by default: measured slower at c2 / c4
-// than the standalone layernorm_k pass -- the statistics of a tile finish after its MMAs.
+// bf16 mode, ADX_LN_FOLD=1 on a -DADX_TC_STATW=2 build: LayerNorm folded into the GEMM that
+// consumes it (statistics warps in the GEMM, gain in the weights).  Off by default: measured
+// slower at c2 / c4 than the standalone layernorm_k pass -- the statistics of a
+// tile finish after its MMAs.
 bool ln_fold() {
     static const bool on = [] {
         const char* e = getenv("ADX_LN_FOLD");
-        return e && *e == '1';
+        return e && *e == '1' && tc_ln_fold_supported();
     }();
     return on;
 }
@@ -818,7 +819,11 @@ void UNetDevice::enqueue(int stage, const std::vector<Seg>& in, int t, void* y, 
                 sh.bias = F(stage, "short.b");
                 sh.out_bf16 = sc.r;
                 sh.ldo = C;
-                if (s.cskip && s.cin % 64 == 0 && s.cskip % 64 == 0)  // [x | skip] read in place along K
+                static const bool cat_gemm = [] {  // ADX_CAT_GEMM=0: materialise the concat (A/B)
+                    const char* e = getenv("ADX_CAT_GEMM");
+                    return !(e && *e == '0');
+                }();
+                if (cat_gemm && s.cskip && s.cin % 64 == 0 && s.cskip % 64 == 0)  // [x | skip] in place along K
                     tc_gemm_cat(x0, s.cin, x1, s.cskip, P(stage, "short.w"), B * HW, C, sh, st);
                 else if (s.cskip) {
                     concat_channels(Cat2{x0, s.cin, x1, s.cskip}, static_cast<long long>(B) * HW, sc.c, st);
