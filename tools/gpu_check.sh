@@ -1,2 +1,1 @@
-python tools/tools_pass_ab.py --configs c2,c4,c5 nogs - nogs - 
-timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+for v in pre -; do if [ "$v" = "-" ]; then unset ADX_LIB_VARIANT; else export ADX_LIB_VARIANT=$v; fi; python tools/tools_shape_profile.py c2 bf16 > gpurun_out/shape_$v.txt 2>&1; done

@@ -21,3 +21,6 @@ python tools/tools_unet_layer0.py > gpurun_out/plain3.log 2>&1 && \
 ncu --set full --import-source on --clock-control none -k regex:"tc_gemm_kernel|attn_kernel" -c 2 \
     -o gpurun_out/r02_layer0 python tools/tools_unet_layer0.py > gpurun_out/r02_ncu_full.log 2>&1
 python tools/tools_ncu_summary.py gpurun_out/r02_layer0.ncu-rep > gpurun_out/r02_layer0_ncu_full_summary.txt
+python tools/tools_sol.py c2 bf16 > gpurun_out/r02_c2_sol_bf16.txt 2>&1
+python tools/tools_sol.py c2 f32 > gpurun_out/r02_c2_sol_f32.txt 2>&1
+python tools/tools_shape_profile.py c2 bf16 > gpurun_out/r02_c2_shape_profile.txt 2>&1
