@@ -1295,16 +1295,24 @@ void group_norm_t(const Cat2T<T>& x, int batch, int HW, int groups, const float*
     if (batch <= kGnImageTickets)  // per-image merge (gn_stats): nsub over one image's groups
         smem = std::max(smem, static_cast<size_t>(std::max(1, threads / groups) + 1) * groups * 2 * sizeof(double));
     if (smem > 48 * 1024) throw std::invalid_argument("group_norm: statistics tile exceeds 48 KB shared memory");
-    CKU(launch_pdl(gn_stats<T>, dim3(chunks, batch), dim3(threads), smem, st, 1, x, HW, groups, chunk_pix, chunks, gamma,
-                   beta, eps, scratch));
+    auto stats = [&](cudaStream_t s2) {
+        CKU(launch_pdl(gn_stats<T>, dim3(chunks, batch), dim3(threads), smem, s2, 1, x, HW, groups, chunk_pix, chunks,
+                       gamma, beta, eps, scratch));
+    };
+    stats(st);
     CKU(cudaGetLastError());
+    tc_profile_measure(st, 3, 1.0 * batch * HW * C * sizeof(T), stats);  // reads x once
     const GnLayout L = gn_layout(scratch, batch, C);
     const int pixels = batch * HW;
     const int arpb = std::max(1, 256 / nv);
     const int ablocks = static_cast<int>(std::min<long long>(148LL * 8, (pixels + 4LL * arpb - 1) / (4LL * arpb)));
-    CKU(launch_pdl(gn_apply<T>, dim3(ablocks), dim3(arpb * nv), 0, st, 1, x, pixels, HW,
-                   static_cast<const float2*>(L.ab), silu_act, out));
+    auto apply = [&](cudaStream_t s2) {
+        CKU(launch_pdl(gn_apply<T>, dim3(ablocks), dim3(arpb * nv), 0, s2, 1, x, pixels, HW,
+                       static_cast<const float2*>(L.ab), silu_act, out));
+    };
+    apply(st);
     CKU(cudaGetLastError());
+    tc_profile_measure(st, 3, 2.0 * batch * HW * C * sizeof(T), apply);  // reads x, writes y
 }
 
 void group_norm(const Cat2& x, int batch, int HW, int groups, const float* gamma, const float* beta, float eps,
