@@ -166,14 +166,13 @@ def init_dist(ws):
 
 def build_model(cfg):
     import paper_2406_06911_b200 as adx
-    from oracle import oracle as O  # x_T drawn with the reference RNG restatement (input generation only)
     if cfg["family"] == "unet":
         m = adx.build_unet_denoiser(seed=cfg["seed"], **cfg["unet"])
     else:
         m = adx.build_toy_denoiser(cfg["L"], cfg["widths"], cfg["skip"], cfg["seed"], cfg["E"])
     s = adx.build_schedule(cfg["T"], cfg["beta"][0], cfg["beta"][1], "linear")
     d = m.data_dim()
-    x = adx.Latent(O.random_normals(cfg["x_seed"], d), cfg["T"])
+    x = adx.Latent(adx.random_normals(cfg["x_seed"], d), cfg["T"])  # the library's own Rng
     return m, s, x, d
 
 

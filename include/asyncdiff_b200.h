@@ -51,6 +51,9 @@ typedef enum {
  * build_schedule: proj/include/asyncdiff/diffusion.hpp:36-37,
  *                 proj/src/diffusion.cpp:39-77.  kind 0=linear 1=scaled-linear.
  * betas/alphas: T doubles, alpha_bars: T+1 doubles (caller-owned). */
+/* n standard normals from Rng(seed) (mt19937_64 + the reference's normal(), rng.hpp; the
+ * draw of x_T in draw_x_T, experiment.cpp:131-136, with the seed already mixed) */
+int adx_random_normals(uint64_t seed, long long n, double* out);
 int adx_build_schedule(int T, double beta_start, double beta_end, int kind, double* betas,
                        double* alphas, double* alpha_bars);
 

@@ -84,7 +84,7 @@ class adx_plan_counts_t(C.Structure):
 
 # every symbol the header declares (checked by tests/test_capi_symbols.py)
 EXPORTS = [
-    "adx_last_error", "adx_version", "adx_device_count", "adx_build_schedule", "adx_ddim_step",
+    "adx_last_error", "adx_version", "adx_device_count", "adx_random_normals", "adx_build_schedule", "adx_ddim_step",
     "adx_model_build_toy", "adx_model_shell", "adx_model_destroy", "adx_model_info", "adx_model_widths",
     "adx_model_links", "adx_model_stage_shape", "adx_model_set_stage_macs", "adx_model_tensor", "adx_sinusoid",
     "adx_partition_balanced", "adx_partition_create", "adx_partition_destroy", "adx_partition_num_segments",
@@ -143,6 +143,7 @@ def lib():
         "adx_last_error": (C.c_char_p, []),
         "adx_version": (i, []),
         "adx_device_count": (i, []),
+        "adx_random_normals": (i, [u64, ll, P(d)]),
         "adx_build_schedule": (i, [i, d, d, i, P(d), P(d), P(d)]),
         "adx_ddim_step": (i, [i, i, P(d), P(d), i, i, P(d), i, P(d)]),
         "adx_model_build_toy": (i, [i, P(i), i, i, u64, i, P(vp)]),

@@ -30,7 +30,7 @@ __all__ = [
     "Round", "ExecutionPlan", "plan_async", "validate_plan", "PlanCounts", "plan_counts", "shift_embeddings",
     "render_plan", "RunOptions", "RunStats", "InstrumentedDenoiser", "inject_delay", "run_serial",
     "run_parallel", "DivergenceReport", "compare_trajectories", "kWarmupRound", "set_default_precision",
-    "PRECISIONS", "Session", "time_model_pass", "profile_model_pass", "stage_times", "partition_by_cost",
+    "PRECISIONS", "random_normals", "Session", "time_model_pass", "profile_model_pass", "stage_times", "partition_by_cost",
     "RankSession", "nccl_unique_id", "save_checkpoint",
     "load_checkpoint", "plan_to_json", "plan_from_json", "CostModel", "LatencyReport", "predict_sequential",
     "predict_async", "CostComparison", "calibrate_and_compare", "round_exchange_bytes", "SimilarityProfile",
@@ -93,6 +93,14 @@ class NoiseSchedule:
     def alpha_bar(self, t: int) -> float:
         self._chk(t, 0, "alpha_bar")
         return float(self.alpha_bars[t])
+
+
+def random_normals(seed: int, n: int) -> np.ndarray:
+    """n standard normals from the library's Rng(seed) (the reference's draw_x_T,
+    experiment.cpp:131-136, with the seed already mixed)"""
+    out = np.empty(n, np.float64)
+    check(lib().adx_random_normals(C.c_uint64(seed), n, _dp(out)))
+    return out
 
 
 def build_schedule(T: int, beta_start: float, beta_end: float, kind: str = "linear") -> NoiseSchedule:

@@ -300,6 +300,14 @@ int adx_device_count(void) {
     return n;
 }
 
+int adx_random_normals(uint64_t seed, long long n, double* out) {
+    return guard([&] {
+        if (n < 0 || (n > 0 && !out)) throw std::invalid_argument("random_normals: bad output");
+        adx::Rng r(seed);
+        for (long long i = 0; i < n; ++i) out[i] = r.normal();
+    });
+}
+
 int adx_build_schedule(int T, double beta_start, double beta_end, int kind, double* betas, double* alphas,
                        double* alpha_bars) {
     return guard([&] {

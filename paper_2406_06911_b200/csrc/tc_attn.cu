@@ -1,18 +1,21 @@
 // tc_attn.cu -- fused multi-head attention on tcgen05 (flash style) for the
 // UNet-shaped family: out = softmax(Q K^T / sqrt(64)) V per 64-wide head.
 //
-// One CTA per (128-query tile, head), 6 warps:
-//   warp 0    TMA: Q tile once; K tile [128 keys x 64] and V^T tile
-//             [64 dims x 128 keys] per KV block into a 2-stage ring (SW128);
-//   warp 1    TMEM alloc + single-thread MMA issue: S = Q K^T (M128 N128 K64)
-//             into TMEM cols [0,128), then O_blk = P V (M128 N64 K128) into
-//             cols [128,192);
-//   warps 2-5 softmax / epilogue, thread = query row: tcgen05.ld its S row,
-//             online softmax (running max / sum in registers, exp2), P (bf16)
-//             written straight into the 128B-swizzled SMEM layout the PV MMA
-//             reads as its A operand, O accumulated in registers with the
-//             softmax rescale, normalised and stored as bf16 at the end.
-// S never touches HBM (the unfused path wrote an L x L fp32 matrix per head).
+// attn_kernel_v2 (default): one CTA per (128-query tile, head, KV split), 10 warps, two CTAs
+// per SM (64-key KV blocks, 256 TMEM columns per CTA):
+//   warp 0     TMA: the Q tile once; K and V [64 keys x 64 dims] per KV block, straight from
+//              the row-major projection output, into a 3-stage SW128 ring;
+//   warp 1     TMEM alloc + MMA issue: S = Q K^T (M128 N64 K64) into one of two TMEM S
+//              buffers; O_h += P_h V_h with the A operand P read from TMEM (P written over
+//              the half's own S columns) and V as an MN-major B operand (no V^T pass);
+//   warps 2-9  softmax, two warps per TMEM lane quadrant, each owning half of every block's
+//              keys with its own running max / sum and O accumulator (O_0, O_1 in TMEM),
+//              merged once after the last block; lazy O rescale (row max grows by > 2^8).
+// A (tile, head) grid with a wave tail is split over KV; the last split (ticket) combines
+// the partial O / max / sum in split order.  attn_kernel_v2<true> is the f32 mode's
+// split-operand variant: Q, K, V as bf16 hi / lo planes, three MMAs per product, P split
+// into hi / lo in registers, fp32 output.  attn_kernel (ADX_ATTN_V=1) is the round-1 kernel.
+// S never touches HBM.
 #include "tc_attn.cuh"
 
 #include "pdl.cuh"

@@ -50,3 +50,13 @@ def test_status_codes_map_to_reference_exception_classes():
         adx.plan_async(50, 0, 2, 1)
     with pytest.raises(ValueError):  # std::invalid_argument is a ValueError here
         adx.build_schedule(0, 0.1, 0.2)
+
+
+def test_random_normals_match_the_oracle_rng():
+    """x_T comes from the library's own Rng (host code, no GPU): bit-identical to the oracle's
+    restatement of the reference's mt19937_64 + normal()"""
+    import numpy as np
+    import paper_2406_06911_b200 as adx
+    from oracle import oracle as O
+    for seed, n in [(12, 1000), (0, 7), (2**63 + 5, 4096)]:
+        assert np.array_equal(adx.random_normals(seed, n), O.random_normals(seed, n))

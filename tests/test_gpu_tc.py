@@ -370,3 +370,22 @@ def test_tc_conv3x3_stride2_matches_fp32_reference(b, H, W, Ci, Co, bn, S):
     got = bits_f32(out)
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("M,K,H", [(1000, 320, 512), (2304, 640, 1280), (144, 1280, 2560)])
+def test_tc_gemm_geglu_epilogue(M, K, H):
+    """the fused GEGLU epilogue (ff1): weight rows tile-interleaved [128 hidden | 128 gate],
+    out = (x Wh^T + bh) * gelu(x Wg^T + bg) with the exact (erf) GELU, vs torch fp64"""
+    rng = np.random.default_rng(M + K + H)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = (rng.standard_normal((2 * H, K)) / np.sqrt(K)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(2 * H)).astype(np.float32)
+    Ab, Wb = bf16_bits(A), bf16_bits(W)
+    Wi, bi = np.ascontiguousarray(geglu_rows(Wb)), np.ascontiguousarray(geglu_rows(b))
+    out = np.zeros((M, H), np.float32)
+    _lib.check(adx.lib().adx_tc_gemm(0, M, 2 * H, K, Ab.ctypes.data_as(P16), Wi.ctypes.data_as(P16),
+                                     bi.ctypes.data_as(PF), 2, out.ctypes.data_as(PF), 0, 0, None))
+    f = torch.from_numpy(bits_f32(Ab)).double() @ torch.from_numpy(bits_f32(Wb)).double().T + torch.from_numpy(b).double()
+    ref = (f[:, :H] * torch.nn.functional.gelu(f[:, H:])).numpy()
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    assert err < 1e-4, err  # fp32 accumulation and epilogue: summation order only
