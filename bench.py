@@ -295,7 +295,7 @@ def per_launch_sol(recs, tc_peak):
     return out
 
 
-def cpu_baseline(cfg, n_components, steps=1):
+def cpu_baseline(cfg, n_components, steps=1, warmup=0):
     """The reference's CPU path on this host.  MLP family: oracle port of
     run_parallel (executor.cpp:501-601, D worker threads, fp64), one full image
     per step.  UNet family (no reference CPU implementation exists): the numpy
@@ -313,6 +313,8 @@ def cpu_baseline(cfg, n_components, steps=1):
             om.params(st)
         orc = UNetOracle(om)
         x = O.random_normals(cfg["x_seed"], om.data_dim()).astype(np.float32)
+        for _ in range(warmup):  # untimed (page-in, BLAS / thread-pool start-up)
+            orc.eval_full(x, cfg["T"])
         evals = []
         for _ in range(steps):
             t0 = time.perf_counter()
@@ -331,6 +333,8 @@ def cpu_baseline(cfg, n_components, steps=1):
     N = n_components
     ss, _ = O.partition_balanced(om.costs(), N)
     pf = O.plan_async_flat(cfg["T"], cfg["w"] if N > 1 else cfg["T"], N, cfg["S"])
+    for _ in range(warmup):
+        O.run_parallel(om, ss, N, pf, s.alpha_bars, x)
     walls = []
     for _ in range(steps):
         _, _, wall = O.run_parallel(om, ss, N, pf, s.alpha_bars, x)
@@ -345,16 +349,16 @@ def run_reference(args, cfg):
         return
     N = args.gpus if args.gpus > 1 else 1
     t0 = time.time()
-    # MLP configs: every step is one full x_T -> x_0 run (the GPU arm's step).  UNet configs:
-    # every step is ONE full denoiser evaluation (1/T of an image, ~40-60 s on the host), at
-    # most 2 timed after 1 untimed, so the arm ends within a few minutes; value = median x T
+    # MLP configs: every step is one full x_T -> x_0 run (the GPU arm's step), after W untimed
+    # runs.  UNet configs: every step is ONE full denoiser evaluation (1/T of an image, ~15 s on
+    # 16 host cores), at most 2 timed after 1 untimed, so the arm ends within a few minutes;
+    # value = median x T
     steps = args.steps if cfg["family"] == "mlp" else min(args.steps, 2)
-    if cfg["family"] == "mlp":
-        cpu_baseline(cfg, N, 1)  # warm-up (caches, page-in)
-    ms, cores, sample = cpu_baseline(cfg, N, steps)
+    warm = max(1, args.warmup) if cfg["family"] == "mlp" else 1
+    ms, cores, sample = cpu_baseline(cfg, N, steps, warm)
     line = {
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": steps,
-        "warmup": 1, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if cfg["family"] == "mlp" else "f32", "data": "synthetic",
         "config": config_block(args, cfg, N),
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port", "sample": sample},
