@@ -235,6 +235,11 @@ struct AttnArgs {
     float* part = nullptr;         // [item][split] records of kRecFloats
     float* out_f32 = nullptr;      // split-operand (fp32-exact) kernel: fp32 output instead of `out`
     unsigned* counters = nullptr;  // [item], zero at allocation, re-armed by the combiner
+    // stream-K (attn_kernel_sk): the items' KV blocks laid end to end (item = (query tile, head,
+    // image), nkv blocks each) and cut into gridDim.x equal ranges, one per CTA; an item cut
+    // across ranges is combined like a split-KV item (nsplit = record slots per item)
+    int qtiles = 0, heads = 0;
+    long long total_blocks = 0;
 };
 constexpr int kRecFloats = QT * HD + 2 * QT;  // O [128][64] fp32, then m[128], l[128]
 
@@ -802,6 +807,326 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256) : "memory");
 }
 
+
+// ---------------------------------------------------------------------- stream-K
+// attn_kernel_v2's CTA (10 warps, two per SM, same TMEM / SMEM plan) run persistently over a
+// contiguous range of the (item, KV block) sequence instead of one item: every CTA gets the
+// same number of KV blocks (+-1), so a grid of items that does not fill the SMs evenly (level 0:
+// 360 items over 296 slots; SDXL level 2: 320) has no wave tail.  Per segment (the part of
+// one item inside the range): Q is loaded into one of two Q buffers (the next segment's Q
+// overlaps this one's MMAs), the softmax state restarts, and at its end the output is written
+// (whole item) or published as a partial record whose last-arriving segment combines all of
+// them in segment order (deterministic).  Barrier phases run on the CTA's global block count.
+// (block counts fit 32 bits: the launcher checks total < 2^31 / G)
+__device__ __forceinline__ int sk_b0(int c, int total, int G) {
+    return static_cast<int>(static_cast<long long>(c) * total / G);
+}
+// the CTA whose range holds block x
+__device__ __forceinline__ int sk_cta(int x, int total, int G) {
+    int c = static_cast<int>(static_cast<long long>(x) * G / total);
+    while (c + 1 < G && sk_b0(c + 1, total, G) <= x) ++c;
+    while (c > 0 && sk_b0(c, total, G) > x) --c;
+    return c;
+}
+
+__global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__ CUtensorMap tmQ,
+                                                         const __grid_constant__ CUtensorMap tmK,
+                                                         const __grid_constant__ CUtensorMap tmV, const AttnArgs p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
+    constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2;
+    constexpr int XCH_OFF = 2 * Q_B + STG * (K_B + V_B) + 256;
+    uint8_t* sQ = smem;  // [2] Q buffers
+    uint8_t* sK = sQ + 2 * Q_B;
+    uint8_t* sV = sK + STG * K_B;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + STG * V_B);
+    uint64_t* q_full = bars;              // [2]
+    uint64_t* q_empty = q_full + 2;       // [2] the S MMAs of the buffer's segment are done
+    uint64_t* kv_full = q_empty + 2;      // [STG]
+    uint64_t* kv_empty = kv_full + STG;   // [STG]
+    uint64_t* s_full = kv_empty + STG;    // [2]
+    uint64_t* p_full = s_full + 2;        // [2 buffers][2 halves]
+    uint64_t* pv_done = p_full + 4;       // [2 buffers][2 halves]
+    uint32_t* tptr = reinterpret_cast<uint32_t*>(pv_done + 4);
+    float* xml = reinterpret_cast<float*>(smem + XCH_OFF);  // [2 segment parities][2 halves][2][128]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = gridDim.x, cta = blockIdx.x;
+    const int nkv = (p.Lk + KT - 1) / KT;
+    const int total = static_cast<int>(p.total_blocks);
+    const int b_lo = sk_b0(cta, total, G), b_hi = sk_b0(cta + 1, total, G);
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < 2; ++i) {
+            bar_init(&q_full[i], 1);
+            bar_init(&q_empty[i], 1);
+        }
+        for (int s = 0; s < STG; ++s) {
+            bar_init(&kv_full[s], 1);
+            bar_init(&kv_empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) bar_init(&s_full[b], 1);
+        for (int i = 0; i < 4; ++i) {
+            bar_init(&p_full[i], 4);
+            bar_init(&pv_done[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa(tptr)), "n"(256)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    pdl_wait();
+    const uint32_t tmem = *tptr;
+    // item -> (query tile, head, image)
+    auto decode = [&](int it, int& qt, int& head, int& img) {
+        qt = it % p.qtiles;
+        const int r = it / p.qtiles;
+        head = r % p.heads;
+        img = r / p.heads;
+    };
+
+    if (warp == 0 && lane == 0) {
+        int g = 0;  // the CTA's KV block count
+        int q = 0;        // segment count
+        for (int b = b_lo; b < b_hi; ++q) {
+            const int it = b / nkv, kb0 = b - it * nkv, end = min(b_hi, (it + 1) * nkv);
+            int qt, head, img;
+            decode(it, qt, head, img);
+            const int qb = q & 1;
+            bar_wait(&q_empty[qb], ((q >> 1) & 1) ^ 1);
+            bar_expect(&q_full[qb], Q_B);
+            tma2d(sQ + qb * Q_B, &tmQ, head * HD, img * p.L + qt * QT, &q_full[qb]);
+            for (int kb = kb0; kb < kb0 + (end - b); ++kb, ++g) {
+                const int s = g % STG;
+                bar_wait(&kv_empty[s], ((g / STG) & 1) ^ 1);
+                bar_expect(&kv_full[s], K_B + V_B);
+                const int row = img * p.Lk + kb * KT;
+                tma2d(sK + s * K_B, &tmK, head * HD, row, &kv_full[s]);
+                tma2d(sV + s * V_B, &tmV, head * HD, row, &kv_full[s]);
+            }
+            b = end;
+        }
+    } else if (warp == 1 && lane == 0) {
+        int g = 0;
+        int q = 0;
+        auto issue_s = [&](int gg, int qb) {
+            const int s = gg % STG, b = gg & 1;
+            bar_wait(&kv_full[s], (gg / STG) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < HD / 16; ++k)
+                mma(tmem + b * KT, sdesc(sQ + qb * Q_B + k * 32), sdesc(sK + s * K_B + k * 32), idesc(QT, KT), k > 0);
+            commit(&s_full[b]);
+        };
+        for (int b = b_lo; b < b_hi; ++q) {
+            const int it = b / nkv, end = min(b_hi, (it + 1) * nkv);
+            const int n = end - b, qb = q & 1;
+            bar_wait(&q_full[qb], (q >> 1) & 1);
+            issue_s(g, qb);
+            if (n == 1) commit(&q_empty[qb]);
+            for (int j = 1; j <= n; ++j) {
+                if (j < n) {
+                    issue_s(g + j, qb);
+                    if (j == n - 1) commit(&q_empty[qb]);  // every S of this segment issued
+                }
+                const int jj = g + j - 1;
+                const int s = jj % STG, bb = jj & 1;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    bar_wait(&p_full[bb * 2 + h], (jj >> 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                    for (int k = 2 * h; k < 2 * h + 2; ++k)
+                        mma_ts(tmem + 2 * KT + h * HD, tmem + bb * KT + h * HK + (k & 1) * 8,
+                               sdesc(sV + s * V_B + k * 2048), idesc(QT, HD) | (1u << 16),
+                               (j > 1 || (k & 1)) ? 1u : 0u);
+                    commit(&pv_done[bb * 2 + h]);
+                }
+                commit(&kv_empty[s]);
+            }
+            g += n;
+            b = end;
+        }
+    } else if (warp >= 2) {
+        const int qq = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int r = qq * 32 + lane;
+        const uint32_t lrow = static_cast<uint32_t>(qq * 32) << 16;
+        const float sl2 = 0.125f * 1.4426950408889634f;
+        int g = 0;
+        int q = 0;
+        for (int b = b_lo; b < b_hi; ++q) {
+            const int it = b / nkv, kb0 = b - it * nkv, end = min(b_hi, (it + 1) * nkv);
+            const int n = end - b;
+            int qt, head, img;
+            decode(it, qt, head, img);
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < n; ++j) {
+                const int gg = g + j;
+                const int bb = gg & 1;
+                const uint32_t tS = tmem + bb * KT + half * HK + lrow;
+                bar_wait(&s_full[bb], (gg >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                uint32_t sr[HK];
+                tld_hk_nowait(tS, sr);
+                tld_wait();
+                const int valid = min(KT, p.Lk - (kb0 + j) * KT) - half * HK;
+                if (valid < HK) {
+#pragma unroll
+                    for (int i = 0; i < HK; ++i)
+                        if (i >= valid) sr[i] = 0xff800000u;
+                }
+                float mp[8];
+#pragma unroll
+                for (int a = 0; a < 8; ++a) mp[a] = __uint_as_float(sr[a]);
+#pragma unroll
+                for (int i = 8; i < HK; ++i) mp[i & 7] = fmaxf(mp[i & 7], __uint_as_float(sr[i]));
+                const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                                       fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+                const bool need = mx > m && (m == -INFINITY || (mx - m) * sl2 > 8.f);
+                if (__any_sync(0xffffffffu, need)) {
+                    if (j > 0) {  // O_h must hold PV_{j-1},h of this segment
+                        const int gp = gg - 1;
+                        bar_wait(&pv_done[(gp & 1) * 2 + half], (gp >> 1) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const float alpha = need ? (m == -INFINITY ? 0.f : ex2((m - mx) * sl2)) : 1.f;
+                        const uint32_t tO = tmem + 2 * KT + half * HD + lrow;
+#pragma unroll
+                        for (int c = 0; c < HD; c += 16) {
+                            float ov[16];
+                            tld16(tO + c, ov);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) ov[i] *= alpha;
+                            tst16(tO + c, ov);
+                        }
+                        tst_wait();
+                        l *= alpha;
+                    }
+                    if (need) m = mx;
+                }
+                const float off = m == -INFINITY ? 0.f : -m * sl2;
+                float sp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                uint32_t pk[HK / 2];
+#pragma unroll
+                for (int c = 0; c < HK; c += 2) {
+                    const float v0 = ex2(fmaf(__uint_as_float(sr[c]), sl2, off));
+                    const float v1 = ex2(fmaf(__uint_as_float(sr[c + 1]), sl2, off));
+                    sp[c & 7] += v0;
+                    sp[(c + 1) & 7] += v1;
+                    __nv_bfloat162 h2 = __floats2bfloat162_rn(v0, v1);
+                    pk[c / 2] = *reinterpret_cast<uint32_t*>(&h2);
+                }
+                tst_u32<HK / 2>(tS, pk);
+                tst_wait();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) bar_arrive(&p_full[bb * 2 + half]);
+                l += ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
+            }
+            // merge the halves (xml double-buffered by segment parity: the partner warp may still
+            // read the previous segment's values)
+            float* xm = xml + (q & 1) * 4 * QT;
+            xm[(half * 2 + 0) * QT + r] = m;
+            xm[(half * 2 + 1) * QT + r] = l;
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + qq) : "memory");
+            const float m0 = xm[0 * QT + r], l0 = xm[1 * QT + r], m1 = xm[2 * QT + r], l1 = xm[3 * QT + r];
+            const float M = fmaxf(m0, m1);
+            const float w0 = m0 == -INFINITY ? 0.f : ex2((m0 - M) * sl2);
+            const float w1 = m1 == -INFINITY ? 0.f : ex2((m1 - M) * sl2);
+            float lt = w0 * l0 + w1 * l1;
+            const int gl = g + n - 1;
+            const int lb = gl & 1;
+            bar_wait(&pv_done[lb * 2 + 0], (gl >> 1) & 1);
+            bar_wait(&pv_done[lb * 2 + 1], (gl >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            float ov[HD / 2], o1[HD / 2];
+            const uint32_t tO0 = tmem + 2 * KT + lrow + half * (HD / 2);
+            tld16(tO0, ov);
+            tld16(tO0 + 16, ov + 16);
+            tld16(tO0 + HD, o1);
+            tld16(tO0 + HD + 16, o1 + 16);
+#pragma unroll
+            for (int c = 0; c < HD / 2; ++c) ov[c] = w0 * ov[c] + w1 * o1[c];
+            const long long row = static_cast<long long>(qt) * QT + r;
+            // segments of this item: CTAs sk_cta(first block) .. sk_cta(last block)
+            const int c_first = sk_cta(it * nkv, total, G);
+            const int nseg = sk_cta((it + 1) * nkv - 1, total, G) - c_first + 1;
+            bool write_out = true;
+            if (nseg > 1) {
+                const int seg = cta - c_first;
+                float* rec = p.part + (static_cast<long long>(it) * p.nsplit + seg) * kRecFloats;
+#pragma unroll
+                for (int c = 0; c < HD / 2; c += 4)
+                    *reinterpret_cast<float4*>(rec + r * HD + half * (HD / 2) + c) =
+                        make_float4(ov[c], ov[c + 1], ov[c + 2], ov[c + 3]);
+                if (half == 0) rec[QT * HD + r] = M, rec[QT * HD + QT + r] = lt;
+                __threadfence();
+                __shared__ unsigned last_sk;
+                asm volatile("bar.sync 5, 256;" ::: "memory");
+                if (threadIdx.x == 64)
+                    last_sk = atomicAdd(p.counters + it, 1u) == static_cast<unsigned>(nseg - 1);
+                asm volatile("bar.sync 5, 256;" ::: "memory");
+                write_out = last_sk != 0u;
+                if (write_out) {
+                    __threadfence();
+                    const float* base = p.part + static_cast<long long>(it) * p.nsplit * kRecFloats;
+                    float MM = -INFINITY;
+                    for (int s2 = 0; s2 < nseg; ++s2) MM = fmaxf(MM, __ldcg(base + s2 * kRecFloats + QT * HD + r));
+                    float acc[HD / 2], den = 0.f;
+#pragma unroll
+                    for (int c = 0; c < HD / 2; ++c) acc[c] = 0.f;
+                    for (int s2 = 0; s2 < nseg; ++s2) {
+                        const float* rs = base + s2 * kRecFloats;
+                        const float ms = __ldcg(rs + QT * HD + r);
+                        const float w = ms == -INFINITY ? 0.f : ex2((ms - MM) * sl2);
+                        den = fmaf(w, __ldcg(rs + QT * HD + QT + r), den);
+#pragma unroll
+                        for (int c = 0; c < HD / 2; c += 4) {
+                            const float4 o4 =
+                                __ldcg(reinterpret_cast<const float4*>(rs + r * HD + half * (HD / 2) + c));
+                            acc[c] = fmaf(w, o4.x, acc[c]), acc[c + 1] = fmaf(w, o4.y, acc[c + 1]);
+                            acc[c + 2] = fmaf(w, o4.z, acc[c + 2]), acc[c + 3] = fmaf(w, o4.w, acc[c + 3]);
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < HD / 2; ++c) ov[c] = acc[c];
+                    lt = den;
+                    if (threadIdx.x == 64) p.counters[it] = 0u;
+                }
+            }
+            if (write_out && row < p.L) {
+                const float inv = 1.0f / lt;
+                __nv_bfloat16* dst =
+                    p.out + (static_cast<long long>(img) * p.L + row) * p.ldo + head * HD + half * (HD / 2);
+#pragma unroll
+                for (int c = 0; c < HD / 2; c += 8) {
+                    uint4 v;
+                    __nv_bfloat162 b0 = __floats2bfloat162_rn(ov[c] * inv, ov[c + 1] * inv);
+                    __nv_bfloat162 b1 = __floats2bfloat162_rn(ov[c + 2] * inv, ov[c + 3] * inv);
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(ov[c + 4] * inv, ov[c + 5] * inv);
+                    __nv_bfloat162 b3 = __floats2bfloat162_rn(ov[c + 6] * inv, ov[c + 7] * inv);
+                    v.x = *reinterpret_cast<uint32_t*>(&b0);
+                    v.y = *reinterpret_cast<uint32_t*>(&b1);
+                    v.z = *reinterpret_cast<uint32_t*>(&b2);
+                    v.w = *reinterpret_cast<uint32_t*>(&b3);
+                    *reinterpret_cast<uint4*>(dst + c) = v;
+                }
+            }
+            g += n;
+            b = end;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(256) : "memory");
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -870,12 +1195,45 @@ int device_sms() {
     CKA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     return sms;
 }
+// stream-K plan: grid G (0 = use the per-item grid of attn_splits) and the record slots per item.
+// Modelled in KV-block times like attn_splits: ceil(total / G) + 3 per CTA, + 10 when items are
+// cut (partial publish + ticket + combine, as for split-KV); taken only when it beats the best
+// split plan by 15% (measured: c2 level 0, 360 items x 144 blocks, 188.9 -> 183.7 us; level 1,
+// 180 x 36, 38.3 -> 43.8 us -- the cut items' combine costs more than the model says).
+// ADX_ATTN_SK=0 / 1 disables / forces it.
+int attn_sk_plan(int L, int Lk, int C, int sms, int batch, int& slots) {
+    static const int mode = [] {
+        const char* e = getenv("ADX_ATTN_SK");
+        return e ? atoi(e) : -1;
+    }();
+    slots = 0;
+    if (mode == 0) return 0;
+    const long long items = static_cast<long long>((L + QT - 1) / QT) * (C / HD) * batch;
+    const int nkv = (Lk + KT - 1) / KT;
+    const long long total = items * nkv;
+    const int G = static_cast<int>(std::min<long long>(2LL * sms, total));
+    const long long rmin = total / G;
+    if (rmin < 1 || total >= (1LL << 31) / G) return 0;
+    const int S = attn_splits(L, Lk, C, sms, batch);
+    const long long rounds = (items * S + 2LL * sms - 1) / (2LL * sms);
+    const double t_split = static_cast<double>(rounds) * ((nkv + S - 1) / S + 3 + (S > 1 ? 10 : 0));
+    const bool cut = total % G != 0 || (total / G) % nkv != 0;
+    const double t_sk = static_cast<double>((total + G - 1) / G) + 3 + (cut ? 10 : 0);
+    // long items only (a combine per cut item is amortised over >= 96 blocks): measured gains
+    // at c2 level 0 (144 blocks per item), losses at SDXL's L = 1024 (16) and the cross attention
+    if (mode != 1 && (t_sk > 0.85 * t_split || nkv < 96)) return 0;
+    slots = static_cast<int>((nkv + rmin - 1) / rmin) + 1;
+    return G;
+}
 }  // namespace
 
 size_t tc_attention_ws_bytes(int L, int Lk, int C, int batch) {
+    const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD) * batch;
+    int slots = 0;
+    if (attn_sk_plan(L, Lk, C, device_sms(), batch, slots) > 0)
+        return 256 * ((items * 4 + 255) / 256) + items * slots * kRecFloats * sizeof(float);
     const int S = attn_splits(L, Lk, C, device_sms(), batch);
     if (S == 1) return 0;
-    const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD) * batch;
     return 256 * ((items * 4 + 255) / 256) + items * S * kRecFloats * sizeof(float);
 }
 
@@ -889,10 +1247,43 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
     const CUtensorMap mk = map2d(K, static_cast<long long>(batch) * Lk, C, ldk, KT);
     const CUtensorMap mv = map2d(V, static_cast<long long>(batch) * Lk, C, ldv, KT);  // rows = keys, like K
     AttnArgs a{L, Lk, C, out, ldo};
-    const int S = attn_splits(L, Lk, C, device_sms(), batch);
     const size_t need = tc_attention_ws_bytes(L, Lk, C, batch);
+    const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD) * batch;
+    int sk_slots = 0;
+    const int sk_grid = ws && ws_bytes >= need ? attn_sk_plan(L, Lk, C, device_sms(), batch, sk_slots) : 0;
+    static const int ver = [] {  // ADX_ATTN_V=1: the round-1 kernel (per-block max exchange)
+        const char* e = getenv("ADX_ATTN_V");
+        return e && *e == '1' ? 1 : 2;
+    }();
+    if (sk_grid > 0 && ver == 2) {  // stream-K over the items' KV blocks (see attn_kernel_sk)
+        a.nsplit = sk_slots;
+        a.counters = static_cast<unsigned*>(ws);
+        a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * ((items * 4 + 255) / 256));
+        a.qtiles = (L + QT - 1) / QT;
+        a.heads = C / HD;
+        a.total_blocks = static_cast<long long>(items) * ((Lk + KT - 1) / KT);
+        constexpr size_t smem_sk =
+            1024 + 2 * QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + 256 + 8 * QT * sizeof(float);
+        static bool attr_sk[64] = {};
+        int dev = 0;
+        CKA(cudaGetDevice(&dev));
+        if (!attr_sk[dev]) {
+            CKA(cudaFuncSetAttribute(attn_kernel_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_sk));
+            attr_sk[dev] = true;
+        }
+        if (tc_trace())
+            fprintf(stderr, "tc_attention L=%d Lk=%d C=%d batch=%d stream-K grid=%d slots=%d\n", L, Lk, C, batch,
+                    sk_grid, sk_slots);
+        auto launch = [&](cudaStream_t s2) {
+            CKA(launch_pdl(attn_kernel_sk, dim3(sk_grid), dim3(320), smem_sk, s2, 1, mq, mk, mv, a));
+        };
+        launch(st);
+        tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, 2.0 * batch * C * (2.0 * L + 2.0 * Lk), launch);
+        CKA(cudaGetLastError());
+        return;
+    }
+    const int S = attn_splits(L, Lk, C, device_sms(), batch);
     if (S > 1 && ws && ws_bytes >= need) {  // without a (large enough) workspace: unsplit
-        const size_t items = static_cast<size_t>((L + QT - 1) / QT) * (C / HD) * batch;
         a.nsplit = S;
         a.counters = static_cast<unsigned*>(ws);
         a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256 * ((items * 4 + 255) / 256));
@@ -910,10 +1301,6 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
         CKA(cudaFuncSetAttribute(attn_kernel_v2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr2[dev] = true;
     }
-    static const int ver = [] {  // ADX_ATTN_V=1: the round-1 kernel (per-block max exchange)
-        const char* e = getenv("ADX_ATTN_V");
-        return e && *e == '1' ? 1 : 2;
-    }();
     dim3 grid(((L + QT - 1) / QT) * a.nsplit, C / HD, batch);
     if (tc_trace()) fprintf(stderr, "tc_attention L=%d Lk=%d C=%d batch=%d S=%d v%d\n", L, Lk, C, batch, a.nsplit, ver);
     auto launch = [&](cudaStream_t s2) {

@@ -156,9 +156,10 @@ def test_tc_attention_f32_matches_fp64(batch, L, Lk, C, scale):
     assert err < tol, err
 
 
-def test_tc_attention_split_kv_is_deterministic():
+@pytest.mark.parametrize("L,C", [(1024, 640),    # 80 (query tile, head) items
+                                 (9216, 320)])   # c2 level 0: the stream-K grid (items cut across CTAs)
+def test_tc_attention_split_kv_is_deterministic(L, C):
     rng = np.random.default_rng(9)
-    L, C = 1024, 640  # 80 (query tile, head) items -> split over KV
     Q = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
     V = bf16_bits(rng.standard_normal((L, C)).astype(np.float32))
     outs = []

@@ -1,3 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python bench.py 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['roofline']['frac'], d.get('gpu_launches'), d['clocks'])"
+timeout 300 python -m pytest tests/test_gpu_tc.py -q -x -k "deterministic" 2>&1 | tail -2
