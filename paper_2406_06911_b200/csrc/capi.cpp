@@ -1103,6 +1103,8 @@ int adx_tc_gemm_cat_bf16(int ordinal, int M, int N, int K1, int K2, const uint16
     });
 }
 
+int adx_tc_geglu_group(void) { return adx::tc_geglu_group(); }
+
 int adx_tc_ln_fold_supported(void) { return adx::tc_ln_fold_supported() ? 1 : 0; }
 
 int adx_tc_ln_fold_bf16(int ordinal, int M, int C, int N, const uint16_t* H, const uint16_t* W1, const float* bias1,

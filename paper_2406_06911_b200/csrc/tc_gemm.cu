@@ -336,13 +336,14 @@ __device__ __forceinline__ unsigned long long bf2_to_f2(uint32_t w) {
 }
 
 // bias / cs: column-indexed bases (the tile's SMEM-staged copies offset by -n0)
-__device__ __forceinline__ void epi_geglu16(const TcArgs& p, long long m, int n0, int c, float* v, float* g,
+// (hb: hidden columns per tile, BN / 2; the gate column of hidden column c is c + hb)
+__device__ __forceinline__ void epi_geglu16(const TcArgs& p, long long m, int n0, int c, int hb, float* v, float* g,
                                             const float* bias, const float* cs, float2 ln = make_float2(0.f, 1.f)) {
     if (cs) {  // LayerNorm fold on both halves
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
             const float4 ch = *reinterpret_cast<const float4*>(cs + n0 + c + j);
-            const float4 cg = *reinterpret_cast<const float4*>(cs + n0 + 128 + c + j);
+            const float4 cg = *reinterpret_cast<const float4*>(cs + n0 + hb + c + j);
             v[j] = ln.y * fmaf(-ln.x, ch.x, v[j]), v[j + 1] = ln.y * fmaf(-ln.x, ch.y, v[j + 1]);
             v[j + 2] = ln.y * fmaf(-ln.x, ch.z, v[j + 2]), v[j + 3] = ln.y * fmaf(-ln.x, ch.w, v[j + 3]);
             g[j] = ln.y * fmaf(-ln.x, cg.x, g[j]), g[j + 1] = ln.y * fmaf(-ln.x, cg.y, g[j + 1]);
@@ -352,7 +353,7 @@ __device__ __forceinline__ void epi_geglu16(const TcArgs& p, long long m, int n0
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
         const float4 bh = *reinterpret_cast<const float4*>(bias + n0 + c + j);
-        const float4 bg = *reinterpret_cast<const float4*>(bias + n0 + 128 + c + j);
+        const float4 bg = *reinterpret_cast<const float4*>(bias + n0 + hb + c + j);
         v[j] += bh.x, v[j + 1] += bh.y, v[j + 2] += bh.z, v[j + 3] += bh.w;
         g[j] += bg.x, g[j + 1] += bg.y, g[j + 2] += bg.z, g[j + 3] += bg.w;
     }
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
 #pragma unroll
                         for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(rv[i]), g[i] = __uint_as_float(rg[i]);
                         if (valid)
-                            epi_geglu16(p, m, n0, c, v, g, stage_cols ? sb - n0 : p.bias,
+                            epi_geglu16(p, m, n0, c, BN / 2, v, g, stage_cols ? sb - n0 : p.bias,
                                         p.ln_colsum ? (stage_cols ? sb + BN - n0 : p.ln_colsum) : nullptr, ln);
                     }
                 } else {
@@ -914,7 +915,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                 }
                 const float2 ln = make_float2(0.f, 1.f);  // (LayerNorm-fold GEMMs run unsplit)
                 if (!CONV && p.act == 2) {
-                    epi_geglu16(p, m, n0, c, v, g, sc ? sepi - n0 : p.bias, nullptr, ln);
+                    epi_geglu16(p, m, n0, c, BN / 2, v, g, sc ? sepi - n0 : p.bias, nullptr, ln);
                 } else {
                     const float* ca = sc ? (p.chan_add ? sepi + BN - n0 : nullptr) : chan_row(p, m, img);
                     epi16(p, m, ca, n0 + c, v, rv ? res : nullptr, nullptr, bb, nullptr, ln);
@@ -1247,6 +1248,12 @@ static void gemm_impl(const void* A, long long lda, const void* A2, long long ld
 
 bool tc_ln_fold_supported() { return kStatWarps > 0; }
 
+// GEGLU weight-row interleave group (hidden rows per N tile): the N tile is twice this
+#ifndef ADX_GEGLU_BN
+#define ADX_GEGLU_BN 256
+#endif
+int tc_geglu_group() { return ADX_GEGLU_BN / 2; }
+
 void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,
                      cudaStream_t st, int bn) {
     gemm_impl(A, lda, nullptr, 0, 0, B, ldb, M, N, K, p, st, bn);
@@ -1265,12 +1272,13 @@ static void gemm_impl(const void* A, long long lda, const void* A2, long long ld
     if (A2 && (k_split % BK || k_split <= 0 || k_split >= K || lda2 % 8 || p.residual || p.residual_f32))
         throw std::invalid_argument("tc_gemm_cat: K1, K2 must be multiples of 64 and the GEMM has no residual");
     if ((lda | ldb) % 8) throw std::invalid_argument("tc_gemm: row strides must be multiples of 8 elements");
-    if (p.act == 2) {  // fused GEGLU (see the epilogue): fixed 256-wide tiles of [128 hidden | 128 gate]
-        if (bn && bn != 256) throw std::invalid_argument("tc_gemm: GEGLU epilogue needs 256-wide N tiles");
-        if (N % 256 || !(p.out_bf16 || p.out_f32) || !p.bias || p.residual || p.residual_f32 || p.chan_add ||
+    if (p.act == 2) {  // fused GEGLU (see the epilogue): fixed tiles of [G hidden | G gate], G = tc_geglu_group()
+        const int gbn = 2 * tc_geglu_group();
+        if (bn && bn != gbn) throw std::invalid_argument("tc_gemm: GEGLU epilogue needs its fixed N tile");
+        if (N % gbn || !(p.out_bf16 || p.out_f32) || !p.bias || p.residual || p.residual_f32 || p.chan_add ||
             (p.ldo % 8))
-            throw std::invalid_argument("tc_gemm: GEGLU epilogue needs N % 256 == 0, bias, no residual, ldo % 8 == 0");
-        bn = 256;
+            throw std::invalid_argument("tc_gemm: GEGLU epilogue needs N % tile == 0, bias, no residual, ldo % 8 == 0");
+        bn = gbn;
     }
     int S = 1;
     gemm_plan(M, N, K, p.act == 2, bn, S);

@@ -80,6 +80,9 @@ void tc_gemm(const void* A, const void* B, int M, int N, int K, TcArgs p, cudaSt
 // concatenation of a UNet skip never materialised (K1, K2 multiples of 64; no residual)
 // whether this build has the LayerNorm-fold statistics warps (-DADX_TC_STATW=2)
 bool tc_ln_fold_supported();
+// the fused GEGLU epilogue's weight-row group: N tile t holds hidden rows [G t, G t + G) and then
+// their gate rows H + the same (the host interleaves ff1's rows and bias this way)
+int tc_geglu_group();
 void tc_gemm_cat(const void* A1, int K1, const void* A2, int K2, const void* B, int M, int N, TcArgs p,
                  cudaStream_t st, int bn = 0);
 void tc_gemm_strided(const void* A, long long lda, const void* B, long long ldb, int M, int N, int K, TcArgs p,

@@ -231,10 +231,10 @@ void UNetDevice::ensure_stage(int stage) {
         }
         for (auto& e : extra) {
             if (ends_with(e.name, "ff1.lncs")) {  // GEGLU interleave, as for ff1's weight rows and bias
-                const int H = static_cast<int>(e.data.size()) / 2;
+                const int H = static_cast<int>(e.data.size()) / 2, G = tc_geglu_group();
                 std::vector<float> perm(e.data.size());
-                for (int t = 0; t < H / 128; ++t)
-                    for (int i = 0; i < 256; ++i) perm[256 * t + i] = e.data[i < 128 ? 128 * t + i : H + 128 * t + i - 128];
+                for (int t = 0; t < H / G; ++t)
+                    for (int i = 0; i < 2 * G; ++i) perm[2 * G * t + i] = e.data[i < G ? G * t + i : H + G * t + i - G];
                 e.data = perm;
             }
             ps.push_back(std::move(e));
@@ -250,13 +250,13 @@ void UNetDevice::ensure_stage(int stage) {
             const int rows = p.shape[0], K = p.shape[1];
             std::vector<float> w = p.data;
             if (ff1) {
-                const int H = rows / 2;
-                if (H % 128) throw std::invalid_argument("unet: GEGLU width must be a multiple of 128");
-                for (int t = 0; t < H / 128; ++t)
-                    for (int i = 0; i < 256; ++i) {
-                        const int src = i < 128 ? 128 * t + i : H + 128 * t + (i - 128);
+                const int H = rows / 2, G = tc_geglu_group();
+                if (H % G) throw std::invalid_argument("unet: GEGLU width must be a multiple of the tile group");
+                for (int t = 0; t < H / G; ++t)
+                    for (int i = 0; i < 2 * G; ++i) {
+                        const int src = i < G ? G * t + i : H + G * t + (i - G);
                         std::copy_n(p.data.begin() + static_cast<size_t>(src) * K, K,
-                                    w.begin() + static_cast<size_t>(256 * t + i) * K);
+                                    w.begin() + static_cast<size_t>(2 * G * t + i) * K);
                     }
             }
             const bool conv = p.name.rfind("conv", 0) == 0;
@@ -266,15 +266,15 @@ void UNetDevice::ensure_stage(int stage) {
         }
         if (ff1) {
             // GEGLU fused into the ff1 GEMM epilogue: rows [hidden | gate] interleaved per
-            // 256-wide N tile: tile t = hidden rows [128t, 128t+128) then gate rows 4C + same
-            const int rows = p.shape[0], cols = matrix ? p.shape[1] : 1, H = rows / 2;
-            if (H % 128) throw std::invalid_argument("unet: GEGLU width must be a multiple of 128");
+            // N tile of 2G: tile t = hidden rows [Gt, Gt+G) then gate rows 4C + same (G = tc_geglu_group())
+            const int rows = p.shape[0], cols = matrix ? p.shape[1] : 1, H = rows / 2, G = tc_geglu_group();
+            if (H % G) throw std::invalid_argument("unet: GEGLU width must be a multiple of the tile group");
             std::vector<float> perm(p.data.size());
-            for (int t = 0; t < H / 128; ++t)
-                for (int i = 0; i < 256; ++i) {
-                    const int src = i < 128 ? 128 * t + i : H + 128 * t + (i - 128);
+            for (int t = 0; t < H / G; ++t)
+                for (int i = 0; i < 2 * G; ++i) {
+                    const int src = i < G ? G * t + i : H + G * t + (i - G);
                     std::copy_n(p.data.begin() + static_cast<size_t>(src) * cols, cols,
-                                perm.begin() + static_cast<size_t>(256 * t + i) * cols);
+                                perm.begin() + static_cast<size_t>(2 * G * t + i) * cols);
                 }
             ds.p[p.name] = matrix ? upload_bf16(perm) : upload_f32(perm);
             ds.bytes[p.name] = static_cast<long long>(p.data.size()) * (matrix ? 2 : 4);

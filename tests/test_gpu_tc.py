@@ -273,10 +273,10 @@ def test_group_norm_matches_fp32_reference(batch, HW, c0, c1, groups, act):
 
 
 def geglu_rows(x):
-    """the GEGLU weight-row interleave of csrc/unet_dev.cu: tile t = hidden rows [128t, 128t+128)
-    then their gates H + same"""
-    H = x.shape[0] // 2
-    idx = [128 * t + i if i < 128 else H + 128 * t + i - 128 for t in range(H // 128) for i in range(256)]
+    """the GEGLU weight-row interleave of csrc/unet_dev.cu: tile t = hidden rows [Gt, Gt+G) then
+    their gates H + same (G = adx_tc_geglu_group())"""
+    H, G = x.shape[0] // 2, adx.lib().adx_tc_geglu_group()
+    idx = [G * t + i if i < G else H + G * t + i - G for t in range(H // G) for i in range(2 * G)]
     return x[idx]
 
 
