@@ -1232,10 +1232,16 @@ static void gemm_plan(int M, int N, int K, bool geglu, int& bn, int& S) {
     if (!geglu && bn == 0 && g_override_bn) {
         bn = g_override_bn;
         S = std::max(1, g_override_splits);
-    } else if (!(bn == 0 && !geglu && plan_lookup(0, M, N, K, 0, bn, S))) {
+    } else if (geglu) {  // fixed N tile: the measured split (rows {3, ...}), else the model's
+        int tbn = 0, ts = 1;
+        if (plan_lookup(3, M, N, K, 0, tbn, ts) && tbn == bn)
+            S = ts;
+        else
+            tile_plan<false>((M + BM - 1) / BM, N, 1, K / BK, bn, bn, S);
+    } else if (!(bn == 0 && plan_lookup(0, M, N, K, 0, bn, S))) {
         tile_plan<false>((M + BM - 1) / BM, N, 1, K / BK, bn, bn, S);
     }
-    if (geglu && g_override_splits) S = g_override_splits;  // the GEGLU tile width stays 256
+    if (geglu && g_override_splits) S = g_override_splits;  // the GEGLU tile width stays fixed
     if (S > 1 && (K / BK) / S < 1) S = std::max(1, K / BK);
 }
 

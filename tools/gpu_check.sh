@@ -1,1 +1,3 @@
-for v in g128 -; do for c in c2 c4 c5; do if [ "$v" = "-" ]; then unset ADX_LIB_VARIANT; else export ADX_LIB_VARIANT=$v; fi; echo "== $v $c"; python tools/tools_shape_profile.py $c bf16 2>&1 | grep "act=2"; done; done
+ADX_TC_TRACE=1 python tools/tools_unet_pass.py c2 2>&1 | grep "M=144 N=10240"
+timeout 300 python -m pytest tests/test_gpu_tc.py -q -x -k "geglu" 2>&1 | tail -1
+python tools/tools_pass_ab.py --configs c2 - - -
