@@ -1,3 +1,4 @@
-ADX_TC_TRACE=1 python tools/tools_unet_pass.py c2 2>&1 | grep "M=144 N=10240"
-timeout 300 python -m pytest tests/test_gpu_tc.py -q -x -k "geglu" 2>&1 | tail -1
-python tools/tools_pass_ab.py --configs c2 - - -
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+python bench.py --steps 10 --warmup 3 > gpurun_out/r02_bench_c2.json 2> gpurun_out/r02_bench_c2.err
+python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/r02_bench_c2_reference.json 2> gpurun_out/r02_ref.err
