@@ -1,4 +1,8 @@
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -2
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-python bench.py --steps 10 --warmup 3 > gpurun_out/r02_bench_c2.json 2> gpurun_out/r02_bench_c2.err
-python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/r02_bench_c2_reference.json 2> gpurun_out/r02_ref.err
+python tools/tools_unet_layer0.py > gpurun_out/p1.log 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:"attn_kernel" -c 1 \
+    -o gpurun_out/r02_attn_sk python tools/tools_unet_layer0.py > gpurun_out/ncu_sk.log 2>&1
+python tools/tools_ncu_summary.py gpurun_out/r02_attn_sk.ncu-rep > gpurun_out/r02_attn_sk_ncu_full_summary.txt
+python tools/tools_attn_f32_one.py > gpurun_out/p2.log 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:"attn_kernel" -c 1 \
+    -o gpurun_out/r02_attn_f32 python tools/tools_attn_f32_one.py > gpurun_out/ncu_f32.log 2>&1
+python tools/tools_ncu_summary.py gpurun_out/r02_attn_f32.ncu-rep > gpurun_out/r02_attn_f32_ncu_full_summary.txt
