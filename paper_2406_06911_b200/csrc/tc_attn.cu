@@ -1065,15 +1065,19 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
                     *reinterpret_cast<float4*>(rec + r * HD + half * (HD / 2) + c) =
                         make_float4(ov[c], ov[c + 1], ov[c + 2], ov[c + 3]);
                 if (half == 0) rec[QT * HD + r] = M, rec[QT * HD + QT + r] = lt;
-                __threadfence();
+                // release: the barrier orders every softmax thread's record stores before thread 64's
+                // gpu-scope fence and ticket (one fence per CTA, not one per thread); acquire: the
+                // last arrival fences again before the barrier that releases the combine reads
                 __shared__ unsigned last_sk;
                 asm volatile("bar.sync 5, 256;" ::: "memory");
-                if (threadIdx.x == 64)
+                if (threadIdx.x == 64) {
+                    __threadfence();
                     last_sk = atomicAdd(p.counters + it, 1u) == static_cast<unsigned>(nseg - 1);
+                    __threadfence();
+                }
                 asm volatile("bar.sync 5, 256;" ::: "memory");
                 write_out = last_sk != 0u;
                 if (write_out) {
-                    __threadfence();
                     const float* base = p.part + static_cast<long long>(it) * p.nsplit * kRecFloats;
                     float MM = -INFINITY;
                     for (int s2 = 0; s2 < nseg; ++s2) MM = fmaxf(MM, __ldcg(base + s2 * kRecFloats + QT * HD + r));

@@ -1,8 +1,3 @@
-python tools/tools_unet_layer0.py > gpurun_out/p1.log 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:"attn_kernel" -c 1 \
-    -o gpurun_out/r02_attn_sk python tools/tools_unet_layer0.py > gpurun_out/ncu_sk.log 2>&1
-python tools/tools_ncu_summary.py gpurun_out/r02_attn_sk.ncu-rep > gpurun_out/r02_attn_sk_ncu_full_summary.txt
-python tools/tools_attn_f32_one.py > gpurun_out/p2.log 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:"attn_kernel" -c 1 \
-    -o gpurun_out/r02_attn_f32 python tools/tools_attn_f32_one.py > gpurun_out/ncu_f32.log 2>&1
-python tools/tools_ncu_summary.py gpurun_out/r02_attn_f32.ncu-rep > gpurun_out/r02_attn_f32_ncu_full_summary.txt
+timeout 300 python -m pytest tests/test_gpu_tc.py -q -x -k "attention and not f32 and not temporal" 2>&1 | tail -1
+ADX_ATTN_SK=1 timeout 300 python -m pytest tests/test_gpu_tc.py -q -x -k "attention and not f32 and not temporal" 2>&1 | tail -1
+for sk in 0 1; do echo "== SK=$sk"; ADX_ATTN_SK=$sk python tools/tools_attn_bench.py; done
