@@ -347,7 +347,10 @@ int adx_tc_gemm_cat_bf16(int ordinal, int M, int N, int K1, int K2, const uint16
 int adx_tc_ln_fold_supported(void);
 /* the fused GEGLU epilogue's weight-row group G: N tile t = hidden rows [G t, G t + G), then their
  * gate rows H + the same (callers of adx_tc_gemm with act 2 interleave W and bias this way) */
-int adx_tc_geglu_group(void); /* 1 when built with -DADX_TC_STATW=2 (else the fold is rejected) */
+int adx_tc_geglu_group(void);
+/* per-CTA %globaltimer stamps (16 per CTA) of the last stream-K attention launch; zeros unless
+ * built with -DADX_SK_TIMELINE (diagnostics) */
+int adx_sk_timeline(unsigned long long* out, int n_ctas); /* 1 when built with -DADX_TC_STATW=2 (else the fold is rejected) */
 int adx_tc_ln_fold_bf16(int ordinal, int M, int C, int N, const uint16_t* H, const uint16_t* W1, const float* bias1,
                         const float* colsum1, int geglu, float eps, uint16_t* y_out, int bn, int iters,
                         double* ms_per_iter);

@@ -100,7 +100,7 @@ EXPORTS = [
     "adx_rank_session_destroy", "adx_rank_session_run", "adx_rank_session_time", "adx_rank_session_kernel_count",
     "adx_model_save_checkpoint", "adx_model_load_checkpoint", "adx_plan_to_json", "adx_plan_from_json",
     "adx_predict_async", "adx_calibrate_and_compare", "adx_round_exchange_bytes", "adx_tc_gemm", "adx_tc_conv3x3",
-    "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context", "adx_tc_attention", "adx_tc_attention_f32", "adx_tc_ln_fold_bf16", "adx_tc_ln_fold_supported", "adx_tc_geglu_group", "adx_tc_gemm_cat_bf16", "adx_tc_conv3x3_s2_bf16", "adx_temporal_attention",
+    "adx_model_build_unet", "adx_unet_stage_info", "adx_unet_stage_params", "adx_unet_context", "adx_tc_attention", "adx_tc_attention_f32", "adx_tc_ln_fold_bf16", "adx_tc_ln_fold_supported", "adx_tc_geglu_group", "adx_sk_timeline", "adx_tc_gemm_cat_bf16", "adx_tc_conv3x3_s2_bf16", "adx_temporal_attention",
     "adx_engine_profile_pass", "adx_profile_records", "adx_tc_plan_override", "adx_engine_stage_times", "adx_partition_by_cost",
     "adx_tc_timeline", "adx_tc_gemm_bf16", "adx_tc_conv3x3_bf16", "adx_group_norm_bf16", "adx_gn_timeline",
 ]
@@ -223,6 +223,7 @@ def lib():
                                        i, i, i, P(d)]),
         "adx_tc_ln_fold_supported": (i, []),
         "adx_tc_geglu_group": (i, []),
+        "adx_sk_timeline": (i, [P(C.c_ulonglong), i]),
         "adx_tc_gemm_cat_bf16": (i, [i, i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_uint16), P(C.c_float),
                                      P(C.c_uint16), i, i]),
         "adx_tc_ln_fold_bf16": (i, [i, i, i, i, P(C.c_uint16), P(C.c_uint16), P(C.c_float), P(C.c_float), i,

@@ -1103,6 +1103,10 @@ int adx_tc_gemm_cat_bf16(int ordinal, int M, int N, int K1, int K2, const uint16
     });
 }
 
+int adx_sk_timeline(unsigned long long* out, int n_ctas) {
+    return guard([&] { adx::tc_sk_timeline(out, n_ctas); });
+}
+
 int adx_tc_geglu_group(void) { return adx::tc_geglu_group(); }
 
 int adx_tc_ln_fold_supported(void) { return adx::tc_ln_fold_supported() ? 1 : 0; }

@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -809,6 +810,19 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__
 
 
 // ---------------------------------------------------------------------- stream-K
+// -DADX_SK_TIMELINE: %globaltimer stamps of the first softmax thread of every CTA (diagnostics)
+#ifdef ADX_SK_TIMELINE
+__device__ unsigned long long g_sk_tl[512 * 16];
+__device__ __forceinline__ void sk_stamp(int i) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (i < 16) g_sk_tl[blockIdx.x * 16 + i] = t;
+}
+#define SK_TL(i) \
+    if (threadIdx.x == 64) sk_stamp(i)
+#else
+#define SK_TL(i)
+#endif
 // attn_kernel_v2's CTA (10 warps, two per SM, same TMEM / SMEM plan) run persistently over a
 // contiguous range of the (item, KV block) sequence instead of one item: every CTA gets the
 // same number of KV blocks (+-1), so a grid of items that does not fill the SMs evenly (level 0:
@@ -960,6 +974,7 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
         const float sl2 = 0.125f * 1.4426950408889634f;
         int g = 0;
         int q = 0;
+        SK_TL(0);
         for (int b = b_lo; b < b_hi; ++q) {
             const int it = b / nkv, kb0 = b - it * nkv, end = min(b_hi, (it + 1) * nkv);
             const int n = end - b;
@@ -971,6 +986,7 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
                 const int bb = gg & 1;
                 const uint32_t tS = tmem + bb * KT + half * HK + lrow;
                 bar_wait(&s_full[bb], (gg >> 1) & 1);
+                if (j == 0) SK_TL(1 + 3 * q);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 uint32_t sr[HK];
                 tld_hk_nowait(tS, sr);
@@ -1028,6 +1044,7 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
                 if (lane == 0) bar_arrive(&p_full[bb * 2 + half]);
                 l += ((sp[0] + sp[1]) + (sp[2] + sp[3])) + ((sp[4] + sp[5]) + (sp[6] + sp[7]));
             }
+            SK_TL(2 + 3 * q);
             // merge the halves (xml double-buffered by segment parity: the partner warp may still
             // read the previous segment's values)
             float* xm = xml + (q & 1) * 4 * QT;
@@ -1121,6 +1138,7 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
                     *reinterpret_cast<uint4*>(dst + c) = v;
                 }
             }
+            SK_TL(3 + 3 * q);
             g += n;
             b = end;
         }
@@ -1316,6 +1334,16 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
     launch(st);
     tc_profile_measure(st, 2, 4.0 * L * Lk * C * batch, 2.0 * batch * C * (2.0 * L + 2.0 * Lk), launch);
     CKA(cudaGetLastError());
+}
+
+// the stream-K kernel's per-CTA stamps of the last launch (-DADX_SK_TIMELINE builds; else zeros)
+void tc_sk_timeline(unsigned long long* out, int n_ctas) {
+#ifdef ADX_SK_TIMELINE
+    CKA(cudaDeviceSynchronize());
+    CKA(cudaMemcpyFromSymbol(out, g_sk_tl, static_cast<size_t>(std::min(n_ctas, 512)) * 16 * 8));
+#else
+    std::fill(out, out + static_cast<size_t>(n_ctas) * 16, 0ull);
+#endif
 }
 
 void tc_attention_x(const void* Qh, const void* Ql, long long ldq, const void* Kh, const void* Kl, long long ldk,

@@ -19,6 +19,8 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
                   int Lk, int C, __nv_bfloat16* out, long long ldo, cudaStream_t st, void* ws = nullptr,
                   size_t ws_bytes = 0, int batch = 1);
 size_t tc_attention_ws_bytes(int L, int Lk, int C, int batch = 1);
+// per-CTA %globaltimer stamps of the last stream-K launch (16 per CTA; -DADX_SK_TIMELINE builds)
+void tc_sk_timeline(unsigned long long* out, int n_ctas);
 
 // the ADX_F32 mode's attention: every operand as bf16 hi and lo planes (x = hi + lo, same
 // layout and strides each), S = Qh Kh^T + Qh Kl^T + Ql Kh^T and O = Ph Vh + Ph Vl + Pl Vh with
