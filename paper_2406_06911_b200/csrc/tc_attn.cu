@@ -724,14 +724,16 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_v2(const __grid_constant__
         bar_wait(&pv_done[lb * 2 + 0], ((nkv - 1) >> 1) & 1);
         bar_wait(&pv_done[lb * 2 + 1], ((nkv - 1) >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float ov[HD / 2], o1[HD / 2];
+        float ov[HD / 2];
         const uint32_t tO0 = tmem + 2 * KT + lrow + half * (HD / 2);
-        tld16(tO0, ov);
-        tld16(tO0 + 16, ov + 16);
-        tld16(tO0 + HD, o1);
-        tld16(tO0 + HD + 16, o1 + 16);
+        {  // both halves' O columns: two TMEM loads, one wait
+            uint32_t r0[HD / 2], r1[HD / 2];
+            tld32_nowait(tO0, r0);
+            tld32_nowait(tO0 + HD, r1);
+            tld_wait();
 #pragma unroll
-        for (int c = 0; c < HD / 2; ++c) ov[c] = w0 * ov[c] + w1 * o1[c];
+            for (int c = 0; c < HD / 2; ++c) ov[c] = w0 * __uint_as_float(r0[c]) + w1 * __uint_as_float(r1[c]);
+        }
         const float mrow = M;
         const long long row = static_cast<long long>(qt) * QT + r;
         bool write_out = true;
