@@ -400,6 +400,36 @@ __device__ __forceinline__ float4 reduce_dsmem4(const uint32_t* a, int S, int of
     return acc;
 }
 
+// 16 consecutive floats of the staged row chunk at byte offset `off`, summed over the S CTAs in
+// split order 0..S-1 (the same order and rounding as reduce_dsmem4); two splits' 4 float4 loads
+// are issued together, so a chunk costs ceil(S / 2) DSMEM round trips instead of 4 ceil(S / 2)
+__device__ __forceinline__ void reduce_dsmem16(const uint32_t* a, int S, uint32_t off, float* v) {
+    float4 acc[4];
+#pragma unroll
+    for (int r = 0; r < kMaxSplitsDev; r += 2) {
+        if (r >= S) break;
+        const bool two = r + 1 < S;
+        float4 xa[4], xb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xa[j] = ld_dsmem4(a[r] + off + 16 * j);
+        if (two) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xb[j] = ld_dsmem4(a[r + 1] + off + 16 * j);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (r == 0) {
+                acc[j] = xa[j];
+            } else {
+                acc[j].x += xa[j].x, acc[j].y += xa[j].y, acc[j].z += xa[j].z, acc[j].w += xa[j].w;
+            }
+            if (two) acc[j].x += xb[j].x, acc[j].y += xb[j].y, acc[j].z += xb[j].z, acc[j].w += xb[j].w;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[4 * j] = acc[j].x, v[4 * j + 1] = acc[j].y, v[4 * j + 2] = acc[j].z, v[4 * j + 3] = acc[j].w;
+}
+
 // TMA-store staging chunks per epilogue warp (its share of the BN / 16 column chunks);
 // BN = 256 tiles do not use the TMA store (no SMEM left beside their pipeline)
 template <int BN>
@@ -901,6 +931,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                 const uint32_t off = static_cast<uint32_t>((row * (BN + 4) + c) * 4);
 #pragma unroll
                 for (int r = 0; r < kMaxSplitsDev; ++r) a[r] = rb[r] + off;
+#ifdef ADX_TC_REDUCE4  // (A/B: the per-float4 reduction)
 #pragma unroll
                 for (int j = 0; j < 16; j += 4) {
                     const float4 x = reduce_dsmem4(a, S, j * 4);
@@ -913,6 +944,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) tc_gemm_kernel(const __grid_c
                         g[j] = x.x, g[j + 1] = x.y, g[j + 2] = x.z, g[j + 3] = x.w;
                     }
                 }
+#else
+                reduce_dsmem16(a, S, 0, v);
+                if (!CONV && p.act == 2) reduce_dsmem16(a, S, (BN / 2) * 4, g);
+#endif
                 const float2 ln = make_float2(0.f, 1.f);  // (LayerNorm-fold GEMMs run unsplit)
                 if (!CONV && p.act == 2) {
                     epi_geglu16(p, m, n0, c, BN / 2, v, g, sc ? sepi - n0 : p.bias, nullptr, ln);

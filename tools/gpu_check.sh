@@ -1,2 +1,4 @@
-timeout 300 python -m pytest tests/test_gpu_tc.py -q -x -k "attention" 2>&1 | tail -1
-for sk in 0 1; do ADX_ATTN_SK=$sk python tools/tools_attn_bench.py | head -3; done
+ADX_LIB_VARIANT=tls python tools/tools_tc_timeline.py 2>&1 | grep conv
+timeout 600 python -m pytest tests/test_gpu_tc.py -q -x 2>&1 | tail -1
+python tools/tools_pass_ab.py --configs c2,c4,c5 r4 - r4 -
+timeout 900 python -m pytest tests/test_gpu_unet_full.py -q -x 2>&1 | tail -1
