@@ -1479,8 +1479,8 @@ void tc_conv3x3(const void* X, const void* Wt, int batch, int H, int W, int Cin,
     }
     const dim3 grid = launch_grid<true>(p, bn);
     if (tc_trace_on())
-        fprintf(stderr, "tc_conv3x3 %dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u tma_store=%d\n", H, W, Cin, Cout, bw,
-                bh, bn, S, grid.x, grid.y, grid.z, p.tma_store);
+        fprintf(stderr, "tc_conv3x3 %s%dx%dx%d->%d box=%dx%d bn=%d S=%d grid=%ux%ux%u tma_store=%d\n",
+                p.sub2 ? "stride2 " : "", H, W, Cin, Cout, bw, bh, bn, S, grid.x, grid.y, grid.z, p.tma_store);
     dispatch<true>(ma, mb, mc, mr, p, grid, bn, st);
     // algorithmic FLOPs and compulsory bytes (H, W: the output grid; the input is Hi x Wi)
     tc_profile_measure(st, 0, 2.0 * batch * H * W * Cout * 9.0 * Cin,
