@@ -833,6 +833,11 @@ __device__ __forceinline__ void sk_stamp(int i) {
 // overlaps this one's MMAs), the softmax state restarts, and at its end the output is written
 // (whole item) or published as a partial record whose last-arriving segment combines all of
 // them in segment order (deterministic).  Barrier phases run on the CTA's global block count.
+// K/V ring depth of the stream-K kernel (ADX_ATTN_SKSTG for A/B)
+#ifndef ADX_ATTN_SKSTG
+#define ADX_ATTN_SKSTG 3
+#endif
+constexpr int SKSTG = ADX_ATTN_SKSTG;
 // (block counts fit 32 bits: the launcher checks total < 2^31 / G)
 __device__ __forceinline__ int sk_b0(int c, int total, int G) {
     return static_cast<int>(static_cast<long long>(c) * total / G);
@@ -851,16 +856,16 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
     constexpr int Q_B = QT * HD * 2, K_B = KT * HD * 2, V_B = HD * KT * 2;
-    constexpr int XCH_OFF = 2 * Q_B + STG * (K_B + V_B) + 256;
+    constexpr int XCH_OFF = 2 * Q_B + SKSTG * (K_B + V_B) + 256;
     uint8_t* sQ = smem;  // [2] Q buffers
     uint8_t* sK = sQ + 2 * Q_B;
-    uint8_t* sV = sK + STG * K_B;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + STG * V_B);
+    uint8_t* sV = sK + SKSTG * K_B;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + SKSTG * V_B);
     uint64_t* q_full = bars;              // [2]
     uint64_t* q_empty = q_full + 2;       // [2] the S MMAs of the buffer's segment are done
-    uint64_t* kv_full = q_empty + 2;      // [STG]
-    uint64_t* kv_empty = kv_full + STG;   // [STG]
-    uint64_t* s_full = kv_empty + STG;    // [2]
+    uint64_t* kv_full = q_empty + 2;      // [SKSTG]
+    uint64_t* kv_empty = kv_full + SKSTG;   // [SKSTG]
+    uint64_t* s_full = kv_empty + SKSTG;    // [2]
     uint64_t* p_full = s_full + 2;        // [2 buffers][2 halves]
     uint64_t* pv_done = p_full + 4;       // [2 buffers][2 halves]
     uint32_t* tptr = reinterpret_cast<uint32_t*>(pv_done + 4);
@@ -877,7 +882,7 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
             bar_init(&q_full[i], 1);
             bar_init(&q_empty[i], 1);
         }
-        for (int s = 0; s < STG; ++s) {
+        for (int s = 0; s < SKSTG; ++s) {
             bar_init(&kv_full[s], 1);
             bar_init(&kv_empty[s], 1);
         }
@@ -918,8 +923,8 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
             bar_expect(&q_full[qb], Q_B);
             tma2d(sQ + qb * Q_B, &tmQ, head * HD, img * p.L + qt * QT, &q_full[qb]);
             for (int kb = kb0; kb < kb0 + (end - b); ++kb, ++g) {
-                const int s = g % STG;
-                bar_wait(&kv_empty[s], ((g / STG) & 1) ^ 1);
+                const int s = g % SKSTG;
+                bar_wait(&kv_empty[s], ((g / SKSTG) & 1) ^ 1);
                 bar_expect(&kv_full[s], K_B + V_B);
                 const int row = img * p.Lk + kb * KT;
                 tma2d(sK + s * K_B, &tmK, head * HD, row, &kv_full[s]);
@@ -931,8 +936,8 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
         int g = 0;
         int q = 0;
         auto issue_s = [&](int gg, int qb) {
-            const int s = gg % STG, b = gg & 1;
-            bar_wait(&kv_full[s], (gg / STG) & 1);
+            const int s = gg % SKSTG, b = gg & 1;
+            bar_wait(&kv_full[s], (gg / SKSTG) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < HD / 16; ++k)
@@ -951,7 +956,7 @@ __global__ void __launch_bounds__(320, 2) attn_kernel_sk(const __grid_constant__
                     if (j == n - 1) commit(&q_empty[qb]);  // every S of this segment issued
                 }
                 const int jj = g + j - 1;
-                const int s = jj % STG, bb = jj & 1;
+                const int s = jj % SKSTG, bb = jj & 1;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     bar_wait(&p_full[bb * 2 + h], (jj >> 1) & 1);
@@ -1287,7 +1292,7 @@ void tc_attention(const void* Q, long long ldq, const void* K, long long ldk, co
         a.heads = C / HD;
         a.total_blocks = static_cast<long long>(items) * ((Lk + KT - 1) / KT);
         constexpr size_t smem_sk =
-            1024 + 2 * QT * HD * 2 + STG * (KT * HD * 2 + HD * KT * 2) + 256 + 8 * QT * sizeof(float);
+            1024 + 2 * QT * HD * 2 + SKSTG * (KT * HD * 2 + HD * KT * 2) + 256 + 8 * QT * sizeof(float);
         static bool attr_sk[64] = {};
         int dev = 0;
         CKA(cudaGetDevice(&dev));
