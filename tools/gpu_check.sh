@@ -1,3 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -2
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-python tools/tools_pass_ab.py --configs c2,c4,c5 -
+python bench.py --config c1b --steps 10 --warmup 3 > gpurun_out/r02_bench_c1b.json 2> gpurun_out/r02_bench_c1b.err
+python bench.py --config c1b --precision f64 --steps 10 --warmup 3 > gpurun_out/r02_bench_c1b_f64.json 2> gpurun_out/r02_bench_c1b_f64.err
